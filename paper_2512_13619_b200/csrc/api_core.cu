@@ -1,0 +1,181 @@
+// C ABI: context management and the batched dense kernels (A0-A2 of SURVEY.md section 8a).
+#include <climits>
+
+#include "kernels.cuh"
+
+using namespace hdgb;
+
+extern "C" {
+
+const char* hdgb_version(void) { return "hdgb200 0.1 (sm_100a)"; }
+
+hdgb_status hdgb_ctx_create(int device, hdgb_ctx** out) {
+    if (!out) return HDGB_ERR_GENERIC;
+    *out = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0 || device < 0 || device >= count) {
+        cudaGetLastError();
+        // No CPU fallback by design: the hot path exists only as sm_100a kernels.
+        fprintf(stderr, "hdgb200: no usable CUDA device (requested %d of %d); there is no CPU fallback\n", device, count);
+        return HDGB_ERR_CUDA;
+    }
+    hdgb_ctx* c = new hdgb_ctx();
+    hdgb_status st = guarded(c, [&] {
+        HDGB_CUDA(cudaSetDevice(device));
+        c->device = device;
+        cudaDeviceProp prop{};
+        HDGB_CUDA(cudaGetDeviceProperties(&prop, device));
+        c->sm_count = prop.multiProcessorCount;
+        HDGB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->owns_stream = true;
+        c->pinned_doubles = 1 << 16;
+        HDGB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&c->pinned), c->pinned_doubles * sizeof(double)));
+        HDGB_CUDA(cudaMalloc(reinterpret_cast<void**>(&c->d_flags), 4 * sizeof(int)));
+        for (auto& e : c->ev) HDGB_CUDA(cudaEventCreate(&e));
+    });
+    if (st != HDGB_OK) {
+        fprintf(stderr, "hdgb200: context creation failed: %s\n", c->err.c_str());
+        delete c;
+        return st;
+    }
+    *out = c;
+    return HDGB_OK;
+}
+
+void hdgb_ctx_destroy(hdgb_ctx* c) {
+    if (!c) return;
+    cudaStreamSynchronize(c->stream);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    if (c->d_flags) cudaFree(c->d_flags);
+    if (c->pinned) cudaFreeHost(c->pinned);
+    if (c->owns_stream && c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+const char* hdgb_last_error(const hdgb_ctx* c) { return c ? c->err.c_str() : "null context"; }
+int64_t hdgb_last_error_index(const hdgb_ctx* c) { return c ? c->err_index : -1; }
+
+hdgb_status hdgb_ctx_set_stream(hdgb_ctx* c, void* s) {
+    return guarded(c, [&] {
+        HDGB_CUDA(cudaStreamSynchronize(c->stream));
+        if (c->owns_stream && c->stream) cudaStreamDestroy(c->stream);
+        c->stream = static_cast<cudaStream_t>(s);
+        c->owns_stream = false;
+    });
+}
+void* hdgb_ctx_stream(hdgb_ctx* c) { return c->stream; }
+
+hdgb_status hdgb_ctx_synchronize(hdgb_ctx* c) {
+    return guarded(c, [&] { HDGB_CUDA(cudaStreamSynchronize(c->stream)); });
+}
+
+int64_t hdgb_ctx_launch_count(const hdgb_ctx* c) { return c->launches; }
+void hdgb_ctx_reset_launch_count(hdgb_ctx* c) { c->launches = 0; }
+void hdgb_ctx_enable_phase_timing(hdgb_ctx* c, int on) { c->phase_timing = on != 0; }
+
+hdgb_status hdgb_device_alloc(hdgb_ctx* c, int64_t n, double** out) {
+    return guarded(c, [&] {
+        *out = nullptr;
+        HDGB_CUDA(cudaMalloc(reinterpret_cast<void**>(out), static_cast<size_t>(n) * sizeof(double)));
+    });
+}
+void hdgb_device_free(hdgb_ctx*, double* p) {
+    if (p) cudaFree(p);
+}
+hdgb_status hdgb_copy(hdgb_ctx* c, double* dst, const double* src, int64_t n) {
+    return guarded(c, [&] {
+        HDGB_CUDA(cudaMemcpyAsync(dst, src, static_cast<size_t>(n) * sizeof(double), cudaMemcpyDefault, c->stream));
+        HDGB_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+}  // extern "C"
+
+namespace hdgb {
+
+// Resets the device error words, returns after `fn` the lowest singular batch index (or -1).
+void reset_flags(hdgb_ctx* c) {
+    const int init[4] = {INT_MAX, 0, 0, 0};
+    HDGB_CUDA(cudaMemcpyAsync(c->d_flags, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+}
+
+void read_flags(hdgb_ctx* c, int* singular_index, int* nonfinite) {
+    int h[4];
+    HDGB_CUDA(cudaMemcpyAsync(h, c->d_flags, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    HDGB_CUDA(cudaStreamSynchronize(c->stream));
+    if (singular_index) *singular_index = (h[0] == INT_MAX) ? -1 : h[0];
+    if (nonfinite) *nonfinite = h[1];
+}
+
+// lu_invert_batch on device pointers with the reference's error convention.
+void device_lu_invert(hdgb_ctx* c, int n, int64_t batch, const double* a, double* inv, const char* context,
+                      hdgb_status code) {
+    reset_flags(c);
+    launch_lu_invert_batch(c, n, batch, a, inv, c->d_flags);
+    int bad = -1;
+    read_flags(c, &bad, nullptr);
+    if (bad >= 0) {
+        std::string msg;
+        if (code == HDGB_ERR_SINGULAR_MASS) msg = "singular mass matrix in element " + std::to_string(bad);
+        else if (code == HDGB_ERR_SINGULAR_LOCAL_SOLVE) msg = "singular local solve in element " + std::to_string(bad);
+        else msg = std::string(context) + ": singular block at batch index " + std::to_string(bad);
+        throw Failure(code, msg, bad);
+    }
+}
+
+}  // namespace hdgb
+
+extern "C" {
+
+hdgb_status hdgb_lu_invert_batch(hdgb_ctx* c, int n, int batch, const double* a, double* inv) {
+    return guarded(c, [&] {
+        if (n < 1) throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: lu_invert_batch requires square blocks with n >= 1");
+        const size_t total = static_cast<size_t>(n) * n * batch;
+        InArg A(c, a, total);
+        OutArg X(c, inv, total);
+        device_lu_invert(c, n, batch, A.dev, X.dev, "lu_invert_batch", HDGB_ERR_SINGULAR_BLOCK);
+        X.commit();
+    });
+}
+
+hdgb_status hdgb_gemm_batch(hdgb_ctx* c, int a_rows, int a_cols, int a_batch, const double* a, int b_rows,
+                            int b_cols, int b_batch, const double* b, int transpose_a, double* out) {
+    return guarded(c, [&] {
+        const int m = transpose_a ? a_cols : a_rows;
+        const int k = transpose_a ? a_rows : a_cols;
+        if (k != b_rows)
+            throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: gemm_batch inner dimensions " +
+                                                           std::to_string(k) + " vs " + std::to_string(b_rows));
+        if (a_batch != b_batch && a_batch != 1 && b_batch != 1)
+            throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: gemm_batch batch counts " +
+                                                           std::to_string(a_batch) + " vs " + std::to_string(b_batch));
+        const int nb = a_batch > b_batch ? a_batch : b_batch;
+        InArg A(c, a, static_cast<size_t>(a_rows) * a_cols * a_batch);
+        InArg B(c, b, static_cast<size_t>(b_rows) * b_cols * b_batch);
+        OutArg Cc(c, out, static_cast<size_t>(m) * b_cols * nb);
+        launch_gemm_batch(c, m, b_cols, k, A.dev, a_batch == 1 ? 0 : static_cast<int64_t>(a_rows) * a_cols,
+                          transpose_a != 0, B.dev, b_batch == 1 ? 0 : static_cast<int64_t>(b_rows) * b_cols, Cc.dev,
+                          static_cast<int64_t>(m) * b_cols, nb, 1.0, 0.0);
+        Cc.commit();
+        HDGB_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+hdgb_status hdgb_gemv_strided_batch(hdgb_ctx* c, int rows, int cols, int batch, const double* a, const double* x,
+                                    double* y, int accumulate) {
+    return guarded(c, [&] {
+        InArg A(c, a, static_cast<size_t>(rows) * cols * batch);
+        InArg X(c, x, static_cast<size_t>(cols) * batch);
+        OutArg Y(c, y, static_cast<size_t>(rows) * batch, accumulate != 0);
+        GemvArgs g;
+        g.a = A.dev; g.x = X.dev; g.y = Y.dev;
+        g.rows = rows; g.cols = cols; g.batch = batch;
+        if (accumulate) { g.z = Y.dev; g.beta = 1.0; }
+        launch_team_gemv(c, g);
+        Y.commit();
+        HDGB_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,517 @@
+// C ABI: the global face-block operator (A7-A8) and the preconditioners (A9-A12).
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <random>
+
+#include "host/ritz.hpp"
+#include "solver.cuh"
+
+using namespace hdgb;
+
+namespace hdgb {
+
+void matvec_device(hdgb_matrix* k, const double* x, double* y) {
+    // block_matvec (face_matrix.cpp:83-107) with gather_extended (:63-81) fused into the GEMV:
+    // the nb neighbour slices are staged in shared memory, the block row is streamed once.
+    GemvArgs g;
+    g.a = k->blocks.p;
+    g.x = x;
+    g.y = y;
+    g.rows = k->mpf();
+    g.cols = k->mpf() * k->nb();
+    g.batch = k->nf;
+    g.idx = k->nbr32.p;
+    g.width = k->mpf();
+    g.comp = 1;
+    launch_team_gemv(k->ctx, g);
+}
+
+void apply_base_device(hdgb_precond* p, const double* y, double* z) {
+    hdgb_ctx* c = p->ctx;
+    const int64_t n = static_cast<int64_t>(p->mpf) * p->nf;
+    switch (p->kind) {
+        case HDGB_PC_IDENTITY:
+            if (y != z) HDGB_CUDA(cudaMemcpyAsync(z, y, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+            break;
+        case HDGB_PC_BJ: {
+            // apply_bj (preconditioner.cpp:48-52)
+            GemvArgs g;
+            g.a = p->bj_inv.p; g.x = y; g.y = z;
+            g.rows = p->mpf; g.cols = p->mpf; g.batch = p->nf;
+            launch_team_gemv(c, g);
+            break;
+        }
+        default: {
+            // apply_asm (preconditioner.cpp:86-105): gather_element_trace fused into the element
+            // solve, then the scatter-add written as an atomics-free face gather (side 0 first).
+            const DiscView& v = p->disc->view;
+            GemvArgs g;
+            g.a = p->asm_inv.p; g.x = y; g.y = p->ze.p;
+            g.rows = v.nfl; g.cols = v.nfl; g.batch = v.ne;
+            g.idx = v.elem_faces; g.width = v.mpf; g.comp = 1;
+            launch_team_gemv(c, g);
+            launch_face_sum(c, p->ze.p, v.face_elems, v.face_lidx, v.nf, v.mpf, v.n_lfe, z,
+                            p->kind == HDGB_PC_RAS ? 1 : 2);
+            break;
+        }
+    }
+}
+
+// apply_poly (preconditioner.cpp:246-283); op = v -> base(K v).
+static void apply_poly_device(hdgb_precond* p, hdgb_matrix* k, const double* y, double* z) {
+    hdgb_ctx* c = p->ctx;
+    const int64_t n = static_cast<int64_t>(p->mpf) * p->nf;
+    double *q = p->wq.p, *t = p->wt.p, *s = p->ws.p, *kv = p->wkv.p;
+    double* w = z;
+    apply_base_device(p, y, q);
+    launch_fill(c, w, 0.0, n);
+    auto op = [&](const double* in, double* out) {
+        matvec_device(k, in, kv);
+        apply_base_device(p, kv, out);
+        ++p->inner_ops;
+    };
+    const size_t cnt = p->ritz.size() / 2;
+    size_t i = 0;
+    while (i < cnt) {
+        const double re = p->ritz[2 * i], im = p->ritz[2 * i + 1];
+        if (im == 0.0) {
+            const double inv = 1.0 / re;
+            launch_axpby(c, inv, q, 1.0, w, n);   // w += inv q
+            op(q, t);
+            launch_axpby(c, -inv, t, 1.0, q, n);  // q -= inv t
+            i += 1;
+        } else {
+            const double inv = 1.0 / (re * re + im * im);
+            op(q, t);
+            launch_poly_pair_mid(c, 2.0 * re, inv, q, t, s, w, n);  // s = 2a q - t ; w += inv s
+            op(s, t);
+            launch_axpby(c, -inv, t, 1.0, q, n);
+            i += 2;
+        }
+    }
+}
+
+void apply_precond_device(hdgb_precond* p, hdgb_matrix* k, const double* y, double* z) {
+    if (!p) {
+        if (y != z)
+            HDGB_CUDA(cudaMemcpyAsync(z, y, k->n_dof() * sizeof(double), cudaMemcpyDeviceToDevice, k->ctx->stream));
+        return;
+    }
+    if (p->poly_degree == 0 || p->ritz.empty()) apply_base_device(p, y, z);
+    else apply_poly_device(p, k, y, z);
+}
+
+// compute_harmonic_ritz (preconditioner.cpp:119-205): seeded start vector, MGS Arnoldi on the
+// device, small eigen-solve and Leja ordering on the host.
+static std::vector<std::complex<double>> harmonic_ritz_device(hdgb_precond* p, hdgb_matrix* k, int degree,
+                                                              uint64_t seed, bool* breakdown_out) {
+    hdgb_ctx* c = p->ctx;
+    const int64_t n = k->n_dof();
+    if (degree < 1) throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: polynomial degree must be >= 1");
+    if (degree > n) throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: polynomial degree exceeds the operator dimension");
+    std::mt19937_64 rng(seed);
+    std::vector<double> v0(n);
+    for (double& x : v0) x = 2.0 * (static_cast<double>(rng() >> 11) * 0x1p-53) - 1.0;
+    double acc = 0.0;
+    for (double x : v0) acc += x * x;  // same ascending order as the reference's dot
+    const double nv = std::sqrt(acc);
+    for (double& x : v0) x /= nv;
+
+    const int pmax = degree;
+    DevBuf<double> basis(static_cast<size_t>(pmax) * n), w(n), kv(n), sc(4);
+    DevBuf<double> partial(multi_dot_workspace_doubles(n, 1));
+    HDGB_CUDA(cudaMemcpyAsync(basis.p, v0.data(), n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    std::vector<double> hess(static_cast<size_t>(pmax + 1) * pmax, 0.0);
+    auto h = [&](int i, int j) -> double& { return hess[static_cast<size_t>(j) * (pmax + 1) + i]; };
+    auto fetch = [&](const double* dev) {
+        double v;
+        HDGB_CUDA(cudaMemcpyAsync(&v, dev, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        HDGB_CUDA(cudaStreamSynchronize(c->stream));
+        return v;
+    };
+    int p_eff = 0;
+    double scale = 1.0;
+    for (int j = 0; j < pmax; ++j) {
+        matvec_device(k, basis.p + static_cast<size_t>(j) * n, kv.p);
+        apply_base_device(p, kv.p, w.p);
+        if (j == 0) {
+            launch_sumsq(c, w.p, n, sc.p, partial.p);
+            scale = std::max(1.0, std::sqrt(fetch(sc.p)));
+        }
+        for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt (preconditioner.cpp:146-150)
+            const double* vi = basis.p + static_cast<size_t>(i) * n;
+            launch_multi_dot(c, vi, n, 1, w.p, n, sc.p, partial.p);
+            launch_multi_axpy(c, vi, n, 1, sc.p, -1.0, w.p, n, nullptr, partial.p);
+            h(i, j) = fetch(sc.p);
+        }
+        launch_sumsq(c, w.p, n, sc.p + 1, partial.p);
+        const double hn = std::sqrt(fetch(sc.p + 1));
+        h(j + 1, j) = hn;
+        p_eff = j + 1;
+        if (!std::isfinite(hn)) throw Failure(HDGB_ERR_NAN_DETECTED, "NaN detected in harmonic Ritz Arnoldi");
+        if (hn < 1e-14 * scale) break;
+        if (j + 1 < pmax) launch_scale_dev(c, w.p, sc.p + 1, 0, basis.p + static_cast<size_t>(j + 1) * n, n);
+    }
+    HDGB_CUDA(cudaStreamSynchronize(c->stream));
+    if (breakdown_out) *breakdown_out = p_eff < pmax;
+    return harmonic_ritz_from_hessenberg(hess.data(), pmax, p_eff);
+}
+
+// Chebyshev nodes of the real interval covering the Ritz estimates, Leja-ordered.
+static std::vector<std::complex<double>> chebyshev_nodes(const std::vector<std::complex<double>>& ritz, int degree) {
+    double lo = INFINITY, hi = -INFINITY;
+    for (const auto& t : ritz) {
+        lo = std::min(lo, t.real());
+        hi = std::max(hi, t.real());
+    }
+    if (!(lo > 0.0)) lo = hi / 30.0;  // indefinite / tiny estimate: fall back to a fixed ratio
+    if (hi <= lo) hi = lo * (1.0 + 1e-8);
+    const double kPi = 3.14159265358979323846;
+    std::vector<std::complex<double>> nodes;
+    for (int j = 0; j < degree; ++j) {
+        const double x = std::cos(kPi * (2.0 * j + 1.0) / (2.0 * degree));
+        nodes.emplace_back(0.5 * (hi + lo) + 0.5 * (hi - lo) * x, 0.0);
+    }
+    return leja_order(nodes);
+}
+
+hdgb_precond* build_preconditioner_spec(hdgb_matrix* k, const hdgb_ops* o, hdgb_disc* d, const hdgb_precond_spec& spec) {
+    hdgb_ctx* c = k->ctx;
+    std::unique_ptr<hdgb_precond> p(new hdgb_precond());
+    p->ctx = c;
+    p->kind = spec.kind;
+    p->mpf = k->mpf();
+    p->nf = k->nf;
+    p->n_lfe = k->n_lfe;
+    const int64_t n = k->n_dof();
+    switch (spec.kind) {
+        case HDGB_PC_IDENTITY: break;
+        case HDGB_PC_BJ: {
+            // build_bj (preconditioner.cpp:30-46)
+            const int mpf = p->mpf;
+            p->bj_inv.alloc(static_cast<size_t>(mpf) * mpf * k->nf);
+            launch_extract_diag(c, k->blocks.p, k->nf, mpf, k->nb(), p->bj_inv.p);
+            device_lu_invert(c, mpf, k->nf, p->bj_inv.p, p->bj_inv.p, "build_bj (face block)", HDGB_ERR_SINGULAR_BLOCK);
+            break;
+        }
+        case HDGB_PC_ASM:
+        case HDGB_PC_RAS: {
+            // build_asm (preconditioner.cpp:54-84)
+            if (!o || !d) throw Failure(HDGB_ERR_GENERIC, "build_asm needs the element operators and the discretisation");
+            const DiscView& v = d->view;
+            if (v.mpf != p->mpf || v.nf != p->nf)
+                throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: build_asm matrix / mesh");
+            p->disc = d;
+            p->ne = v.ne;
+            p->asm_inv.alloc(static_cast<size_t>(v.nfl) * v.nfl * v.ne);
+            launch_asm_enrich(c, v, o->kbar.p, p->asm_inv.p);
+            device_lu_invert(c, v.nfl, v.ne, p->asm_inv.p, p->asm_inv.p, "build_asm (element block)", HDGB_ERR_SINGULAR_BLOCK);
+            p->ze.alloc(static_cast<size_t>(v.nfl) * v.ne);
+            break;
+        }
+        default: throw Failure(HDGB_ERR_UNSUPPORTED, "unknown preconditioner kind");
+    }
+    if (spec.poly_degree > 0) {
+        const int degree = static_cast<int>(std::min<int64_t>(spec.poly_degree, n));  // newton.cpp:41
+        p->wq.alloc(n); p->wt.alloc(n); p->ws.alloc(n); p->wkv.alloc(n);
+        bool breakdown = false;
+        std::vector<std::complex<double>> th = harmonic_ritz_device(p.get(), k, degree, spec.ritz_seed, &breakdown);
+        p->poly_kind = spec.poly_kind;
+        if (spec.poly_kind == HDGB_POLY_CHEBYSHEV && !th.empty()) th = chebyshev_nodes(th, degree);
+        p->ritz.clear();
+        for (const auto& t : th) { p->ritz.push_back(t.real()); p->ritz.push_back(t.imag()); }
+        p->poly_degree = degree;
+    }
+    return p.release();
+}
+
+hdgb_matrix* assemble_global_device(hdgb_disc* d, const hdgb_ops* o) {
+    hdgb_ctx* c = d->ctx;
+    const DiscView& v = d->view;
+    std::unique_ptr<hdgb_matrix> k(new hdgb_matrix());
+    k->ctx = c;
+    k->m = v.M;  // the reference leaves m = 1 (face_matrix.hpp:27); identical for its scalar models
+    k->pf = v.pf;
+    k->n_lfe = v.n_lfe;
+    k->nf = v.nf;
+    const size_t row = static_cast<size_t>(v.mpf) * v.mpf * k->nb();
+    k->blocks.alloc(row * v.nf);
+    k->rhs.alloc(static_cast<size_t>(v.mpf) * v.nf);
+    k->nbr32.alloc(static_cast<size_t>(v.nf) * k->nb());
+    launch_fill_neighbors(c, v, k->nbr32.p);
+    launch_assemble_global(c, v, o->kbar.p, o->rbar.p, k->blocks.p, k->rhs.p);
+    return k.release();
+}
+
+static void ensure_host_neighbors(hdgb_matrix* k) {
+    if (k->neighbor_valid) return;
+    std::vector<int> h = k->nbr32.to_host(k->ctx->stream);
+    k->neighbor.resize(h.size());
+    for (size_t i = 0; i < h.size(); ++i) k->neighbor[i] = h[i];  // kNoFace = -1 widens unchanged
+    k->neighbor_valid = true;
+}
+
+}  // namespace hdgb
+
+extern "C" {
+
+void hdgb_precond_spec_default(hdgb_precond_spec* s) {
+    s->kind = HDGB_PC_BJ;
+    s->poly_degree = 0;
+    s->ritz_seed = 12345;
+    s->ritz_per_restart = 0;
+    s->poly_kind = HDGB_POLY_GMRES;
+}
+
+hdgb_status hdgb_assemble_global(hdgb_disc* d, const hdgb_ops* o, hdgb_matrix** out, double* rhs) {
+    *out = nullptr;
+    hdgb_ctx* c = d->ctx;
+    return guarded(c, [&] {
+        if (o->ne != d->view.ne || o->nfl != d->view.nfl)
+            throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: assemble_global operators / mesh");
+        std::unique_ptr<hdgb_matrix> k(assemble_global_device(d, o));
+        if (rhs) HDGB_CUDA(cudaMemcpyAsync(rhs, k->rhs.p, k->rhs.n * sizeof(double), cudaMemcpyDefault, c->stream));
+        HDGB_CUDA(cudaStreamSynchronize(c->stream));
+        *out = k.release();
+    });
+}
+
+hdgb_status hdgb_matrix_create(hdgb_ctx* c, int m, int pf, int n_lfe, int nf, const int64_t* neighbor,
+                               const double* blocks, hdgb_matrix** out) {
+    *out = nullptr;
+    return guarded(c, [&] {
+        if (m < 1 || pf < 1 || n_lfe < 1 || nf < 0)
+            throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: invalid face-block matrix dimensions");
+        std::unique_ptr<hdgb_matrix> k(new hdgb_matrix());
+        k->ctx = c; k->m = m; k->pf = pf; k->n_lfe = n_lfe; k->nf = nf;
+        const size_t nn = static_cast<size_t>(nf) * k->nb();
+        k->neighbor.assign(neighbor, neighbor + nn);
+        std::vector<int> h32(nn);
+        for (size_t i = 0; i < nn; ++i) {
+            const int64_t g = neighbor[i];
+            if (g < -1 || g >= nf) throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: neighbour id out of range", static_cast<int64_t>(i / k->nb()));
+            h32[i] = static_cast<int>(g);
+        }
+        k->neighbor_valid = true;
+        k->nbr32.from_host(h32, c->stream);
+        const size_t total = static_cast<size_t>(k->mpf()) * k->mpf() * k->nb() * nf;
+        k->blocks.alloc(total);
+        if (blocks) HDGB_CUDA(cudaMemcpyAsync(k->blocks.p, blocks, total * sizeof(double), cudaMemcpyDefault, c->stream));
+        HDGB_CUDA(cudaStreamSynchronize(c->stream));
+        *out = k.release();
+    });
+}
+
+void hdgb_matrix_destroy(hdgb_matrix* k) { delete k; }
+
+hdgb_status hdgb_matrix_dims(const hdgb_matrix* k, int* out4) {
+    out4[0] = k->m; out4[1] = k->pf; out4[2] = k->n_lfe; out4[3] = k->nf;
+    return HDGB_OK;
+}
+
+hdgb_status hdgb_matrix_get_neighbor(const hdgb_matrix* kc, int64_t* out) {
+    hdgb_matrix* k = const_cast<hdgb_matrix*>(kc);
+    return guarded(k->ctx, [&] {
+        ensure_host_neighbors(k);
+        std::memcpy(out, k->neighbor.data(), k->neighbor.size() * sizeof(int64_t));
+    });
+}
+
+hdgb_status hdgb_matrix_get_blocks(const hdgb_matrix* k, double* out) {
+    return guarded(k->ctx, [&] {
+        HDGB_CUDA(cudaMemcpyAsync(out, k->blocks.p, k->blocks.n * sizeof(double), cudaMemcpyDefault, k->ctx->stream));
+        HDGB_CUDA(cudaStreamSynchronize(k->ctx->stream));
+    });
+}
+
+double* hdgb_matrix_blocks_ptr(hdgb_matrix* k) { return k->blocks.p; }
+double* hdgb_matrix_rhs(hdgb_matrix* k) { return k->rhs.p; }
+
+hdgb_status hdgb_block_matvec(hdgb_matrix* k, const double* x, double* y) {
+    hdgb_ctx* c = k->ctx;
+    return guarded(c, [&] {
+        const size_t n = k->n_dof();
+        InArg X(c, x, n);
+        OutArg Y(c, y, n);
+        matvec_device(k, X.dev, Y.dev);
+        Y.commit();
+        if (!X.tmp.p && !Y.host) return;  // fully device-resident call stays asynchronous
+        HDGB_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+hdgb_status hdgb_gather_extended(hdgb_matrix* k, const double* x, double* out) {
+    hdgb_ctx* c = k->ctx;
+    return guarded(c, [&] {
+        const size_t n = k->n_dof();
+        InArg X(c, x, n);
+        OutArg Y(c, out, n * k->nb());
+        launch_gather_extended(c, X.dev, k->nbr32.p, k->nf, k->nb(), k->mpf(), Y.dev);
+        Y.commit();
+        HDGB_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+hdgb_status hdgb_matrix_write(hdgb_matrix* k, const double* rhs, const char* path) {
+    hdgb_ctx* c = k->ctx;
+    return guarded(c, [&] {
+        ensure_host_neighbors(k);
+        std::vector<double> blocks = k->blocks.to_host(c->stream);
+        std::vector<double> r(k->n_dof(), 0.0);
+        const double* src = rhs ? rhs : k->rhs.p;
+        if (src) {
+            HDGB_CUDA(cudaMemcpyAsync(r.data(), src, r.size() * sizeof(double), cudaMemcpyDefault, c->stream));
+            HDGB_CUDA(cudaStreamSynchronize(c->stream));
+        }
+        const std::string p = path;
+        std::FILE* fp = std::fopen(path, "wb");
+        if (!fp) throw Failure(HDGB_ERR_IO, "cannot open " + p + " for writing");
+        const uint32_t header[5] = {1u, static_cast<uint32_t>(k->m), static_cast<uint32_t>(k->pf),
+                                    static_cast<uint32_t>(k->n_lfe), static_cast<uint32_t>(k->nf)};
+        bool ok = std::fwrite("HDGK", 1, 4, fp) == 4;
+        ok = ok && std::fwrite(header, 1, sizeof(header), fp) == sizeof(header);
+        ok = ok && std::fwrite(k->neighbor.data(), sizeof(int64_t), k->neighbor.size(), fp) == k->neighbor.size();
+        ok = ok && std::fwrite(blocks.data(), sizeof(double), blocks.size(), fp) == blocks.size();
+        ok = ok && std::fwrite(r.data(), sizeof(double), r.size(), fp) == r.size();
+        std::fclose(fp);
+        if (!ok) throw Failure(HDGB_ERR_IO, "short write to " + p);
+    });
+}
+
+hdgb_status hdgb_matrix_read(hdgb_ctx* c, const char* path, hdgb_matrix** out, double* rhs) {
+    *out = nullptr;
+    return guarded(c, [&] {
+        const std::string p = path;
+        std::FILE* fp = std::fopen(path, "rb");
+        if (!fp) throw Failure(HDGB_ERR_IO, "cannot open " + p);
+        struct Closer { std::FILE* f; ~Closer() { std::fclose(f); } } closer{fp};
+        char magic[4];
+        if (std::fread(magic, 1, 4, fp) != 4) throw Failure(HDGB_ERR_IO, "short read from " + p);
+        if (std::memcmp(magic, "HDGK", 4) != 0) throw Failure(HDGB_ERR_IO, p + " is not a matrix dump");
+        uint32_t header[5];
+        if (std::fread(header, 1, sizeof(header), fp) != sizeof(header)) throw Failure(HDGB_ERR_IO, "short read from " + p);
+        if (header[0] != 1u) throw Failure(HDGB_ERR_IO, p + ": unsupported format version");
+        const int m = static_cast<int>(header[1]), pf = static_cast<int>(header[2]);
+        const int n_lfe = static_cast<int>(header[3]), nf = static_cast<int>(header[4]);
+        const int nb = 2 * n_lfe - 1;
+        std::vector<int64_t> nbr(static_cast<size_t>(nf) * nb);
+        if (std::fread(nbr.data(), sizeof(int64_t), nbr.size(), fp) != nbr.size()) throw Failure(HDGB_ERR_IO, "short read from " + p);
+        std::vector<double> blocks(static_cast<size_t>(m) * pf * m * pf * nb * nf);
+        if (std::fread(blocks.data(), sizeof(double), blocks.size(), fp) != blocks.size()) throw Failure(HDGB_ERR_IO, "short read from " + p);
+        std::vector<double> r(static_cast<size_t>(m) * pf * nf);
+        if (std::fread(r.data(), sizeof(double), r.size(), fp) != r.size()) throw Failure(HDGB_ERR_IO, "short read from " + p);
+        hdgb_matrix* k = nullptr;
+        hdgb_status st = hdgb_matrix_create(c, m, pf, n_lfe, nf, nbr.data(), blocks.data(), &k);
+        if (st != HDGB_OK) throw Failure(st, c->err, c->err_index);
+        k->rhs.alloc(r.size());
+        k->rhs.upload(r.data(), r.size(), c->stream);
+        HDGB_CUDA(cudaStreamSynchronize(c->stream));
+        if (rhs) std::memcpy(rhs, r.data(), r.size() * sizeof(double));
+        *out = k;
+    });
+}
+
+// ---- preconditioners -----------------------------------------------------------------------------------
+hdgb_status hdgb_build_preconditioner(hdgb_matrix* k, const hdgb_ops* o, hdgb_disc* d, const hdgb_precond_spec* spec,
+                                      hdgb_precond** out) {
+    *out = nullptr;
+    return guarded(k->ctx, [&] {
+        hdgb_precond_spec s;
+        hdgb_precond_spec_default(&s);
+        if (spec) s = *spec;
+        *out = build_preconditioner_spec(k, o, d, s);
+        HDGB_CUDA(cudaStreamSynchronize(k->ctx->stream));
+    });
+}
+
+void hdgb_precond_destroy(hdgb_precond* p) { delete p; }
+
+hdgb_status hdgb_precond_get(const hdgb_precond* p, const char* name, double* dst, int64_t cap, int64_t* n) {
+    return guarded(p->ctx, [&] {
+        const std::string s = name;
+        if (s == "ritz") {
+            if (n) *n = static_cast<int64_t>(p->ritz.size());
+            if (dst) {
+                if (cap < static_cast<int64_t>(p->ritz.size())) throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "destination too small");
+                std::memcpy(dst, p->ritz.data(), p->ritz.size() * sizeof(double));
+            }
+            return;
+        }
+        const DevBuf<double>* b = nullptr;
+        if (s == "bj_inv") b = &p->bj_inv;
+        else if (s == "asm_inv") b = &p->asm_inv;
+        else throw Failure(HDGB_ERR_GENERIC, "unknown preconditioner field " + s);
+        if (n) *n = static_cast<int64_t>(b->n);
+        if (dst) {
+            if (cap < static_cast<int64_t>(b->n)) throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "destination too small");
+            HDGB_CUDA(cudaMemcpyAsync(dst, b->p, b->n * sizeof(double), cudaMemcpyDeviceToHost, p->ctx->stream));
+            HDGB_CUDA(cudaStreamSynchronize(p->ctx->stream));
+        }
+    });
+}
+
+hdgb_status hdgb_precond_set_ritz(hdgb_precond* p, const double* reim, int count) {
+    return guarded(p->ctx, [&] {
+        p->ritz.assign(reim, reim + 2 * static_cast<size_t>(count));
+        p->poly_degree = count;
+        const size_t n = static_cast<size_t>(p->mpf) * p->nf;
+        if (count > 0 && p->wq.n != n) { p->wq.alloc(n); p->wt.alloc(n); p->ws.alloc(n); p->wkv.alloc(n); }
+    });
+}
+
+hdgb_status hdgb_precond_apply_base(hdgb_precond* p, const double* y, double* z) {
+    hdgb_ctx* c = p->ctx;
+    return guarded(c, [&] {
+        const size_t n = static_cast<size_t>(p->mpf) * p->nf;
+        InArg Y(c, y, n);
+        OutArg Z(c, z, n);
+        apply_base_device(p, Y.dev, Z.dev);
+        Z.commit();
+        if (!Y.tmp.p && !Z.host) return;
+        HDGB_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+hdgb_status hdgb_precond_apply(hdgb_precond* p, hdgb_matrix* k, const double* y, double* z) {
+    hdgb_ctx* c = p->ctx;
+    return guarded(c, [&] {
+        const size_t n = static_cast<size_t>(p->mpf) * p->nf;
+        InArg Y(c, y, n);
+        OutArg Z(c, z, n);
+        apply_precond_device(p, k, Y.dev, Z.dev);
+        Z.commit();
+        if (!Y.tmp.p && !Z.host) return;
+        HDGB_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int64_t hdgb_precond_inner_ops(const hdgb_precond* p) { return p->inner_ops; }
+
+hdgb_status hdgb_leja_order(const double* reim, int n, double* out_reim, int* n_out) {
+    try {
+        std::vector<std::complex<double>> th(n);
+        for (int i = 0; i < n; ++i) th[i] = {reim[2 * i], reim[2 * i + 1]};
+        const auto o = leja_order(th);
+        for (size_t i = 0; i < o.size(); ++i) { out_reim[2 * i] = o[i].real(); out_reim[2 * i + 1] = o[i].imag(); }
+        *n_out = static_cast<int>(o.size());
+        return HDGB_OK;
+    } catch (...) {
+        return HDGB_ERR_GENERIC;
+    }
+}
+
+hdgb_status hdgb_harmonic_ritz_from_hessenberg(const double* hess, int pmax, int p_eff, double* out_reim, int* n_out) {
+    try {
+        const auto o = harmonic_ritz_from_hessenberg(hess, pmax, p_eff);
+        for (size_t i = 0; i < o.size(); ++i) { out_reim[2 * i] = o[i].real(); out_reim[2 * i + 1] = o[i].imag(); }
+        *n_out = static_cast<int>(o.size());
+        return HDGB_OK;
+    } catch (...) {
+        return HDGB_ERR_GENERIC;
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,430 @@
+// C ABI: restarted GMRES (A13) and the Newton / time-marching drivers (A14).
+//
+// The Krylov basis, the operator and the preconditioner live on the device.  Per Arnoldi step the
+// host sees exactly one small transfer (the Hessenberg column: projection coefficients of both
+// Gram-Schmidt passes and the squared norm) -- Givens rotations, the convergence test and the
+// back-substitution are host scalars like in the reference (gmres.cpp:135-166,188-193).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "solver.cuh"
+
+using namespace hdgb;
+
+namespace hdgb {
+
+namespace {
+
+GmresWork& gmres_work(hdgb_matrix* k, int restart) {
+    const int64_t n = k->n_dof();
+    if (!k->work || k->work->restart < restart || k->work->n != n) {
+        k->work.reset(new GmresWork());
+        GmresWork& w = *k->work;
+        w.restart = restart;
+        w.n = n;
+        w.basis.alloc(static_cast<size_t>(restart + 1) * n);
+        w.kv.alloc(n);
+        w.r.alloc(n);
+        w.coef.alloc(2 * static_cast<size_t>(restart + 1) + 2);
+        w.partial.alloc(multi_dot_workspace_doubles(n, restart + 1));
+        w.ycoef.alloc(restart + 1);
+    }
+    return *k->work;
+}
+
+// orthogonalize (gmres.cpp:28-59) of w against V[0..nvec); h (host) gets nvec + 1 entries.
+// CGS mode: both projection passes are batched (c = V^T w; w -= V c; d = V^T w; w -= V d) with the
+// norm fused into the second update; the reference's second pass interleaves dot and update, which
+// differs at O(eps^2) relative.  MGS mode follows the reference sequence exactly.
+void orthogonalize_device(hdgb_ctx* c, const double* V, int nvec, int64_t n, double* w, int orth, double* coef,
+                          double* partial, double* h) {
+    double* dc = coef;
+    double* dd = coef + nvec;
+    double* dn = coef + 2 * nvec;
+    if (orth == 1) {
+        for (int i = 0; i < nvec; ++i) {
+            const double* vi = V + static_cast<size_t>(i) * n;
+            launch_multi_dot(c, vi, n, 1, w, n, dc + i, partial);
+            launch_multi_axpy(c, vi, n, 1, dc + i, -1.0, w, n, nullptr, partial);
+        }
+        launch_sumsq(c, w, n, dn, partial);
+        HDGB_CUDA(cudaMemsetAsync(dd, 0, nvec * sizeof(double), c->stream));
+    } else {
+        launch_multi_dot(c, V, n, nvec, w, n, dc, partial);
+        launch_multi_axpy(c, V, n, nvec, dc, -1.0, w, n, nullptr, partial);
+        launch_multi_dot(c, V, n, nvec, w, n, dd, partial);
+        launch_multi_axpy(c, V, n, nvec, dd, -1.0, w, n, dn, partial);
+    }
+    // normalise on the device (no-op when the norm is zero, gmres.cpp:54-57) while the column
+    // travels to the host
+    double* stage = c->pinned;
+    HDGB_CUDA(cudaMemcpyAsync(stage, coef, (2 * nvec + 1) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    launch_scale_dev(c, w, dn, 0, w, n);
+    HDGB_CUDA(cudaStreamSynchronize(c->stream));
+    for (int i = 0; i < nvec; ++i) h[i] = stage[i] + stage[nvec + i];
+    h[nvec] = std::sqrt(stage[2 * nvec]);
+}
+
+}  // namespace
+
+void gmres_device(hdgb_matrix* k, hdgb_precond* p, const double* rhs, double* x, const hdgb_gmres_config& cfg,
+                  hdgb_gmres_stats* st, double* residual_trace) {
+    hdgb_ctx* c = k->ctx;
+    const int64_t n = k->n_dof();
+    const int m = cfg.restart;
+    if (m < 1) throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: GMRES restart length must be >= 1");
+    if (2 * static_cast<size_t>(m + 1) + 2 > c->pinned_doubles) throw Failure(HDGB_ERR_UNSUPPORTED, "GMRES restart length too large");
+    GmresWork& W = gmres_work(k, m);
+    std::memset(st, 0, sizeof(*st));
+    double* kv = W.kv.p;
+    double* r = W.r.p;
+    double* V = W.basis.p;
+
+    auto norm_of = [&](const double* v) {
+        launch_sumsq(c, v, n, W.coef.p, W.partial.p);
+        double s;
+        HDGB_CUDA(cudaMemcpyAsync(&s, W.coef.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        HDGB_CUDA(cudaStreamSynchronize(c->stream));
+        return std::sqrt(s);
+    };
+    // r = P^-1 (rhs - K x)   (gmres.cpp:73-81)
+    auto residual = [&](double* out) {
+        PhaseTimer tm(c, &st->t_mv);
+        matvec_device(k, x, kv);
+        launch_lincomb(c, 1.0, rhs, -1.0, kv, kv, n);
+        tm.stop();
+        PhaseTimer tp(c, &st->t_prec);
+        apply_precond_device(p, k, kv, out);
+        tp.stop();
+    };
+
+    residual(r);
+    const double beta0 = norm_of(r);
+    if (!std::isfinite(beta0)) throw Failure(HDGB_ERR_NAN_DETECTED, "NaN detected in gmres initial residual");
+    if (beta0 == 0.0) {
+        st->converged = 1;
+        return;
+    }
+    const double target = cfg.tol * beta0;
+    std::vector<std::vector<double>> rcols;
+    std::vector<double> cs(m), sn(m), g(m + 1), h(m + 2);
+    int n_trace = 0;
+
+    bool first_cycle = true;
+    while (true) {
+        if (!first_cycle) residual(r);
+        first_cycle = false;
+        const double beta = norm_of(r);
+        if (beta <= target) {
+            st->converged = 1;
+            break;
+        }
+        if (st->iters >= cfg.max_iters) break;
+
+        rcols.clear();
+        launch_axpby(c, 1.0 / beta, r, 0.0, V, n);  // v0 = r / beta
+        std::fill(g.begin(), g.end(), 0.0);
+        g[0] = beta;
+        int nbasis = 1;
+        int jused = 0;
+        bool cycle_converged = false;
+        for (int j = 0; j < m && st->iters < cfg.max_iters; ++j) {
+            double* w = V + static_cast<size_t>(j + 1) * n;  // the candidate lands in its basis slot
+            {
+                PhaseTimer tm(c, &st->t_mv);
+                matvec_device(k, V + static_cast<size_t>(j) * n, kv);
+                tm.stop();
+                PhaseTimer tp(c, &st->t_prec);
+                apply_precond_device(p, k, kv, w);
+                tp.stop();
+            }
+            {
+                PhaseTimer to(c, &st->t_orth);
+                orthogonalize_device(c, V, nbasis, n, w, cfg.orth, W.coef.p, W.partial.p, h.data());
+                to.stop();
+            }
+            for (int i = 0; i <= nbasis; ++i)
+                if (!std::isfinite(h[i])) throw Failure(HDGB_ERR_NAN_DETECTED, "NaN detected in gmres Hessenberg column");
+            const double hsub = h[j + 1];
+            for (int i = 0; i < j; ++i) {
+                const double t1 = cs[i] * h[i] + sn[i] * h[i + 1];
+                const double t2 = -sn[i] * h[i] + cs[i] * h[i + 1];
+                h[i] = t1;
+                h[i + 1] = t2;
+            }
+            const double den = std::hypot(h[j], h[j + 1]);
+            if (den == 0.0) break;
+            cs[j] = h[j] / den;
+            sn[j] = h[j + 1] / den;
+            h[j] = den;
+            h[j + 1] = 0.0;
+            g[j + 1] = -sn[j] * g[j];
+            g[j] = cs[j] * g[j];
+            rcols.emplace_back(h.begin(), h.begin() + j + 2);
+
+            ++st->iters;
+            jused = j + 1;
+            if (residual_trace && n_trace < cfg.max_iters) residual_trace[n_trace++] = std::abs(g[j + 1]);
+
+            double hmax = 1.0;
+            for (int i = 0; i <= j; ++i) hmax = std::max(hmax, std::abs(rcols[j][i]));
+            const bool happy = hsub <= 1e-14 * hmax;
+            if (!happy) ++nbasis;
+            if (std::abs(g[j + 1]) <= target || happy) {
+                cycle_converged = true;
+                break;
+            }
+        }
+        if (jused == 0)
+            throw Failure(HDGB_ERR_NAN_DETECTED,
+                          "NaN detected in gmres made no progress: the preconditioned operator annihilated the residual direction");
+
+        if (cfg.track_diagnostics) {
+            const int used = std::min(jused, nbasis);
+            DevBuf<double> gram(used);
+            std::vector<double> hg(used);
+            for (int a = 0; a < used; ++a) {
+                launch_multi_dot(c, V, n, used, V + static_cast<size_t>(a) * n, n, gram.p, W.partial.p);
+                HDGB_CUDA(cudaMemcpyAsync(hg.data(), gram.p, used * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+                HDGB_CUDA(cudaStreamSynchronize(c->stream));
+                for (int b = a; b < used; ++b)
+                    st->max_orth_error = std::max(st->max_orth_error, std::abs(hg[b] - (a == b ? 1.0 : 0.0)));
+            }
+        }
+
+        // back-substitution (gmres.cpp:188-193) and x += V y (:194-197)
+        std::vector<double> y(jused);
+        for (int i = jused - 1; i >= 0; --i) {
+            double v = g[i];
+            for (int cc = i + 1; cc < jused; ++cc) v -= rcols[cc][i] * y[cc];
+            y[i] = v / rcols[i][i];
+        }
+        HDGB_CUDA(cudaMemcpyAsync(W.ycoef.p, y.data(), jused * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        launch_multi_axpy(c, V, n, jused, W.ycoef.p, 1.0, x, n, nullptr, W.partial.p);
+        HDGB_CUDA(cudaStreamSynchronize(c->stream));  // y is a stack temporary
+
+        if (cfg.track_diagnostics) {
+            residual(r);
+            const double tracked = std::abs(g[jused]);
+            const double explicit_norm = norm_of(r);
+            const double gap = std::abs(tracked - explicit_norm) / std::max(explicit_norm, 1e-300);
+            st->max_residual_gap = std::max(st->max_residual_gap, gap);
+        }
+        if (cycle_converged) {
+            residual(r);
+            const double rn = norm_of(r);
+            if (rn <= target) {
+                st->converged = 1;
+                st->final_rel_residual = rn / beta0;
+                return;
+            }
+            first_cycle = true;
+            ++st->restarts;
+            continue;
+        }
+        if (st->iters >= cfg.max_iters) break;
+        ++st->restarts;
+    }
+    residual(r);
+    st->final_rel_residual = norm_of(r) / beta0;
+    st->converged = st->final_rel_residual <= cfg.tol ? 1 : 0;
+}
+
+}  // namespace hdgb
+
+extern "C" {
+
+void hdgb_gmres_config_default(hdgb_gmres_config* cfg) {
+    cfg->restart = 50;
+    cfg->tol = 1e-6;
+    cfg->max_iters = 1000;
+    cfg->orth = 0;
+    cfg->track_diagnostics = 0;
+}
+
+void hdgb_newton_config_default(hdgb_newton_config* cfg) {
+    cfg->tol = 1e-8;
+    cfg->max_newton = 50;
+    cfg->min_alpha = 1.0 / 1024.0;
+}
+
+hdgb_status hdgb_gmres_solve(hdgb_matrix* k, hdgb_precond* p, const double* rhs, const double* x0,
+                             const hdgb_gmres_config* cfg, double* x, hdgb_gmres_stats* stats, double* residual_trace) {
+    hdgb_ctx* c = k->ctx;
+    return guarded(c, [&] {
+        hdgb_gmres_config cf;
+        hdgb_gmres_config_default(&cf);
+        if (cfg) cf = *cfg;
+        const size_t n = k->n_dof();
+        if (p && static_cast<size_t>(p->mpf) * p->nf != n)
+            throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: preconditioner / operator size");
+        InArg B(c, rhs, n);
+        OutArg X(c, x, n);
+        if (x0 && x0 != x) HDGB_CUDA(cudaMemcpyAsync(X.dev, x0, n * sizeof(double), cudaMemcpyDefault, c->stream));
+        else if (!x0) HDGB_CUDA(cudaMemsetAsync(X.dev, 0, n * sizeof(double), c->stream));
+        else if (X.host) HDGB_CUDA(cudaMemcpyAsync(X.dev, x0, n * sizeof(double), cudaMemcpyDefault, c->stream));
+        hdgb_gmres_stats local;
+        gmres_device(k, p, B.dev, X.dev, cf, stats ? stats : &local, residual_trace);
+        X.commit();
+        HDGB_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+hdgb_status hdgb_orthogonalize(hdgb_ctx* c, const double* basis, int nvec, int64_t n, double* w, int orth, double* h) {
+    return guarded(c, [&] {
+        if (2 * static_cast<size_t>(nvec) + 2 > c->pinned_doubles) throw Failure(HDGB_ERR_UNSUPPORTED, "too many basis vectors");
+        DevBuf<double> coef(2 * static_cast<size_t>(nvec) + 2), partial(multi_dot_workspace_doubles(n, std::max(nvec, 1)));
+        orthogonalize_device(c, basis, nvec, n, w, orth, coef.p, partial.p, h);
+    });
+}
+
+hdgb_status hdgb_newton_solve(hdgb_disc* d, const hdgb_model* m, hdgb_state* s, const hdgb_newton_config* ncfg_in,
+                              const hdgb_gmres_config* gcfg_in, const hdgb_precond_spec* pspec_in,
+                              const hdgb_time* t, hdgb_solve_report* rep) {
+    hdgb_ctx* c = d->ctx;
+    hdgb_solve_report local;
+    if (!rep) rep = &local;
+    std::memset(rep, 0, sizeof(*rep));
+    return guarded(c, [&] {
+        using Clock = std::chrono::steady_clock;
+        const auto since = [](Clock::time_point t0) { return std::chrono::duration<double>(Clock::now() - t0).count(); };
+        const auto t_start = Clock::now();
+        hdgb_newton_config ncfg;
+        hdgb_newton_config_default(&ncfg);
+        if (ncfg_in) ncfg = *ncfg_in;
+        hdgb_gmres_config gcfg;
+        hdgb_gmres_config_default(&gcfg);
+        if (gcfg_in) gcfg = *gcfg_in;
+        hdgb_precond_spec pspec;
+        hdgb_precond_spec_default(&pspec);
+        if (pspec_in) pspec = *pspec_in;
+
+        const DiscView& v = d->view;
+        const size_t n_int = static_cast<size_t>(v.npe) * v.ne, n_tr = static_cast<size_t>(v.mpf) * v.nf;
+        const bool transient = t && t->dt > 0.0;
+        if (transient && !t->u_prev)
+            throw Failure(HDGB_ERR_INCONSISTENT_DIMENSIONS, "inconsistent dimensions: transient assembly requires the previous solution");
+        InArg uprev(c, transient ? t->u_prev : nullptr, n_int);
+        const double dt = transient ? t->dt : 0.0;
+
+        DevBuf<double> res_tr(n_tr), res_in(n_int), duhat(n_tr), du(n_int), tmp(n_int), u0(n_int), uh0(n_tr);
+        double rnorm = assemble_residual_device(d, m, s, uprev.dev, dt, res_tr.p, res_in.p);
+        rep->residual_history[rep->n_history++] = rnorm;
+
+        for (int iter = 0;; ++iter) {
+            if (rnorm <= ncfg.tol) { rep->converged = 1; break; }
+            if (iter >= ncfg.max_newton) { rep->converged = 0; break; }
+
+            auto t0 = Clock::now();
+            std::unique_ptr<hdgb_ops> ops(assemble_element_operators_device(d, m, s, uprev.dev, dt, false));
+            std::unique_ptr<hdgb_matrix> k(assemble_global_device(d, ops.get()));
+            std::unique_ptr<hdgb_precond> prec(build_preconditioner_spec(k.get(), ops.get(), d, pspec));
+            HDGB_CUDA(cudaStreamSynchronize(c->stream));
+            rep->t_ass += since(t0);
+
+            duhat.zero(c->stream);  // GMRES always starts from 0 (newton.cpp:88)
+            hdgb_gmres_stats gs;
+            std::memset(&gs, 0, sizeof(gs));
+            if (!pspec.ritz_per_restart || pspec.poly_degree == 0) {
+                gmres_device(k.get(), prec.get(), k->rhs.p, duhat.p, gcfg, &gs, nullptr);
+                rep->n_inner_prec_ops += prec->inner_ops;
+            } else {
+                // one restart cycle at a time with fresh Ritz values in between (newton.cpp:92-115)
+                hdgb_gmres_config one = gcfg;
+                while (true) {
+                    one.max_iters = std::min(gcfg.restart, gcfg.max_iters - gs.iters);
+                    if (one.max_iters <= 0) break;
+                    hdgb_gmres_stats sc;
+                    gmres_device(k.get(), prec.get(), k->rhs.p, duhat.p, one, &sc, nullptr);
+                    rep->n_inner_prec_ops += prec->inner_ops;
+                    gs.iters += sc.iters;
+                    gs.restarts += sc.restarts + 1;
+                    gs.t_mv += sc.t_mv; gs.t_prec += sc.t_prec; gs.t_orth += sc.t_orth;
+                    gs.final_rel_residual = sc.final_rel_residual;
+                    if (sc.converged) { gs.converged = 1; break; }
+                    auto tr = Clock::now();
+                    prec.reset(build_preconditioner_spec(k.get(), ops.get(), d, pspec));
+                    HDGB_CUDA(cudaStreamSynchronize(c->stream));
+                    rep->t_ass += since(tr);
+                }
+            }
+            rep->n_gmres_total += gs.iters;
+            if (rep->n_newton < HDGB_MAX_NEWTON_HISTORY) rep->gmres_per_newton[rep->n_newton] = gs.iters;
+            rep->t_mv += gs.t_mv; rep->t_prec += gs.t_prec; rep->t_orth += gs.t_orth;
+
+            recover_local_device(d, ops.get(), duhat.p, du.p, tmp.p);
+
+            // halving line search on the full nonlinear residual (newton.cpp:127-141); only u and
+            // uhat move, q is re-derived by the residual assembly
+            HDGB_CUDA(cudaMemcpyAsync(u0.p, s->u.p, n_int * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+            HDGB_CUDA(cudaMemcpyAsync(uh0.p, s->uhat.p, n_tr * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+            bool accepted = false;
+            for (double alpha = 1.0; alpha >= ncfg.min_alpha; alpha *= 0.5) {
+                launch_lincomb(c, 1.0, u0.p, alpha, du.p, s->u.p, static_cast<int64_t>(n_int));
+                launch_lincomb(c, 1.0, uh0.p, alpha, duhat.p, s->uhat.p, static_cast<int64_t>(n_tr));
+                double tnorm;
+                try {
+                    tnorm = assemble_residual_device(d, m, s, uprev.dev, dt, res_tr.p, res_in.p);
+                } catch (...) {
+                    HDGB_CUDA(cudaMemcpyAsync(s->u.p, u0.p, n_int * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+                    HDGB_CUDA(cudaMemcpyAsync(s->uhat.p, uh0.p, n_tr * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+                    throw;
+                }
+                if (tnorm < rnorm) {
+                    rnorm = tnorm;
+                    accepted = true;
+                    if (rep->n_newton < HDGB_MAX_NEWTON_HISTORY) rep->alpha_history[rep->n_newton] = alpha;
+                    break;
+                }
+            }
+            ++rep->n_newton;
+            if (!accepted) {
+                HDGB_CUDA(cudaMemcpyAsync(s->u.p, u0.p, n_int * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+                HDGB_CUDA(cudaMemcpyAsync(s->uhat.p, uh0.p, n_tr * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+                compute_q_device(d, s);
+                HDGB_CUDA(cudaStreamSynchronize(c->stream));
+                rep->t_total = since(t_start);
+                rep->final_residual = rnorm;
+                char buf[128];
+                std::snprintf(buf, sizeof(buf), "line search failed at Newton iteration %d (alpha reached %g)", iter, ncfg.min_alpha);
+                throw Failure(HDGB_ERR_LINE_SEARCH_FAILED, buf, iter);
+            }
+            if (rep->n_history <= HDGB_MAX_NEWTON_HISTORY) rep->residual_history[rep->n_history++] = rnorm;
+        }
+        rep->final_residual = rnorm;
+        HDGB_CUDA(cudaStreamSynchronize(c->stream));
+        rep->t_total = since(t_start);
+    });
+}
+
+hdgb_status hdgb_time_march(hdgb_disc* d, const hdgb_model* m, hdgb_state* s, double dt, int n_steps,
+                            const hdgb_newton_config* ncfg, const hdgb_gmres_config* gcfg,
+                            const hdgb_precond_spec* pspec, hdgb_solve_report* reports) {
+    hdgb_ctx* c = d->ctx;
+    if (!(dt > 0.0)) {
+        c->err = "time_march requires a positive dt";
+        return HDGB_ERR_GENERIC;
+    }
+    hdgb_status st = HDGB_OK;
+    try {
+        DevBuf<double> u_prev(s->u.n);
+        for (int step = 0; step < n_steps; ++step) {
+            HDGB_CUDA(cudaMemcpyAsync(u_prev.p, s->u.p, s->u.n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+            hdgb_time t{dt, u_prev.p};
+            hdgb_solve_report local;
+            st = hdgb_newton_solve(d, m, s, ncfg, gcfg, pspec, &t, reports ? &reports[step] : &local);
+            if (st != HDGB_OK) {
+                c->err = "time step " + std::to_string(step) + ": " + c->err;
+                return st;
+            }
+        }
+    } catch (const Failure& f) {
+        c->err = f.what();
+        return f.code;
+    }
+    return st;
+}
+
+}  // extern "C"

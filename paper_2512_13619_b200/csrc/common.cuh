@@ -1,0 +1,182 @@
+// Internal plumbing shared by all translation units of libhdgb200.so: the context object,
+// RAII device buffers, host<->device staging, launch accounting and error propagation.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/hdgb200.h"
+
+namespace hdgb {
+
+// Exception carrying an hdgb_status; converted back to a status code at the C boundary.
+struct Failure : std::runtime_error {
+    hdgb_status code;
+    int64_t index;
+    Failure(hdgb_status c, const std::string& msg, int64_t idx = -1)
+        : std::runtime_error(msg), code(c), index(idx) {}
+};
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+    if (e != cudaSuccess) {
+        throw Failure(HDGB_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e) + " (" + file +
+                                         ":" + std::to_string(line) + ")");
+    }
+}
+#define HDGB_CUDA(x) ::hdgb::cuda_check((x), #x, __FILE__, __LINE__)
+
+}  // namespace hdgb
+
+// The opaque context of the C ABI.
+struct hdgb_ctx {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t stream = nullptr;
+    bool owns_stream = false;
+    std::string err;
+    int64_t err_index = -1;
+    int64_t launches = 0;
+    bool phase_timing = false;
+    // pinned staging area for small host<->device traffic (Hessenberg columns, norms, flags)
+    double* pinned = nullptr;
+    size_t pinned_doubles = 0;
+    // device error words: [0] = lowest singular batch index (INT_MAX = none), [1] = non-finite flag
+    int* d_flags = nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+
+namespace hdgb {
+
+inline void count_launch(hdgb_ctx* c, int n = 1) { c->launches += n; }
+
+// Launch-site check: surfaces configuration errors immediately (asynchronous faults are caught
+// at the next synchronising call).
+#define HDGB_LAUNCH_CHECK(ctx)                                   \
+    do {                                                         \
+        ::hdgb::count_launch(ctx);                               \
+        HDGB_CUDA(cudaGetLastError());                           \
+    } while (0)
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t count) { alloc(count); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void alloc(size_t count) {
+        release();
+        n = count;
+        if (count) HDGB_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T)));
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void zero(cudaStream_t s) { if (n) HDGB_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s)); }
+    void upload(const T* host, size_t count, cudaStream_t s) {
+        if (count > n) throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "DevBuf::upload overflow");
+        if (count) HDGB_CUDA(cudaMemcpyAsync(p, host, count * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+    void from_host(const std::vector<T>& h, cudaStream_t s) {
+        alloc(h.size());
+        upload(h.data(), h.size(), s);
+        HDGB_CUDA(cudaStreamSynchronize(s));  // h may be a temporary
+    }
+    std::vector<T> to_host(cudaStream_t s) const {
+        std::vector<T> h(n);
+        if (n) {
+            HDGB_CUDA(cudaMemcpyAsync(h.data(), p, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+            HDGB_CUDA(cudaStreamSynchronize(s));
+        }
+        return h;
+    }
+};
+
+inline bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a{};
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// A read-only view of caller data on the device: passes device pointers through, stages host
+// pointers into a temporary device buffer (asynchronously on the context's stream).
+struct InArg {
+    const double* dev = nullptr;
+    DevBuf<double> tmp;
+    InArg(hdgb_ctx* c, const double* src, size_t n) {
+        if (!src || n == 0) return;
+        if (is_device_ptr(src)) {
+            dev = src;
+        } else {
+            tmp.alloc(n);
+            HDGB_CUDA(cudaMemcpyAsync(tmp.p, src, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+            dev = tmp.p;
+        }
+    }
+};
+
+// A writable view: device pointers pass through; host destinations get a device temporary that
+// commit() copies back (synchronising the stream).
+struct OutArg {
+    double* dev = nullptr;
+    double* host = nullptr;
+    size_t n = 0;
+    DevBuf<double> tmp;
+    hdgb_ctx* ctx;
+    OutArg(hdgb_ctx* c, double* dst, size_t count, bool preload = false) : n(count), ctx(c) {
+        if (!dst || count == 0) return;
+        if (is_device_ptr(dst)) {
+            dev = dst;
+        } else {
+            host = dst;
+            tmp.alloc(count);
+            dev = tmp.p;
+            if (preload)
+                HDGB_CUDA(cudaMemcpyAsync(tmp.p, dst, count * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        }
+    }
+    void commit() {
+        if (host) {
+            HDGB_CUDA(cudaMemcpyAsync(host, tmp.p, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+            HDGB_CUDA(cudaStreamSynchronize(ctx->stream));
+        }
+    }
+};
+
+// Runs fn, mapping Failure / std::exception to a status + message on the context.
+template <class F>
+hdgb_status guarded(hdgb_ctx* ctx, F&& fn) {
+    try {
+        fn();
+        return HDGB_OK;
+    } catch (const Failure& f) {
+        if (ctx) { ctx->err = f.what(); ctx->err_index = f.index; }
+        return f.code;
+    } catch (const std::exception& e) {
+        if (ctx) { ctx->err = e.what(); ctx->err_index = -1; }
+        return HDGB_ERR_GENERIC;
+    }
+}
+
+inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+}  // namespace hdgb

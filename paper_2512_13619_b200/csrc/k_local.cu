@@ -1,0 +1,465 @@
+// Element-local kernels: quadrature assembly of the weak residual and of the
+// Jacobian blocks D_d, E, F, G_d, H, J (local_ops.cpp:33-228) and the state-independent factors
+// M, B_d, C_d (local_ops.cpp:252-337).
+//
+// local_assemble: one CTA per element, two phases.
+//   (1) point evaluation: threads sweep the qe volume and n_lfe*qf face quadrature points,
+//       interpolate (u, q, uhat), evaluate the model functor and leave one coefficient record per
+//       point in shared memory (the reference calls 8 std::function objects per point instead);
+//   (2) contraction: threads own output entries and accumulate them over the points in the
+//       reference's order (volume points ascending, then faces lf ascending, gc ascending), so
+//       every entry sees the same sequence of terms as the reference (differences: FMA only).
+// Roofline: FP64 pipe; per-element traffic is one write of the raw blocks.
+#include "kernels_local.cuh"
+#include "models.cuh"
+
+namespace hdgb {
+
+namespace {
+
+// ---- setup kernels ---------------------------------------------------------------------------------
+// mass(i,j) = sum_g (phi_i phi_j)(g) * (w_g detJ_g)        (local_ops.cpp:266-281)
+// bmat_d(i,j) = sum_g (w detJ phi_j)(g) * grad_d phi_i(g)   (local_ops.cpp:288-307)
+__global__ void mass_bmat_kernel(DiscView dv, double* __restrict__ mass, double* __restrict__ b0,
+                                 double* __restrict__ b1, double* __restrict__ b2) {
+    const int e = blockIdx.x;
+    const int pe = dv.pe, qe = dv.qe, D = dv.D;
+    for (int t = threadIdx.x; t < pe * pe; t += blockDim.x) {
+        const int j = t / pe, i = t - j * pe;
+        double am = 0.0, ab[3] = {0.0, 0.0, 0.0};
+        for (int g = 0; g < qe; ++g) {
+            const size_t gi = static_cast<size_t>(e) * qe + g;
+            const double w = dv.wq[g] * dv.elem_detjac[gi];
+            const double pi = dv.phi[i + pe * g], pj = dv.phi[j + pe * g];
+            am += (pi * pj) * w;
+            const double wpj = w * pj;
+            const double* ij = dv.elem_invjac + gi * D * D;
+            for (int d = 0; d < D; ++d) {
+                double gd = 0.0;
+                for (int r = 0; r < D; ++r) gd += dv.dphi[r][i + pe * g] * ij[r * D + d];
+                ab[d] += wpj * gd;
+            }
+        }
+        const size_t o = static_cast<size_t>(e) * pe * pe + t;
+        mass[o] = am;
+        b0[o] = ab[0];
+        b1[o] = ab[1];
+        if (D == 3) b2[o] = ab[2];
+    }
+}
+
+// cmat_d(i, (lf,b)) = - sum_gc (w psi_b)(gc) * phis_i(gc) * n_d   (local_ops.cpp:310-336)
+__global__ void cmat_kernel(DiscView dv, double* __restrict__ c0, double* __restrict__ c1, double* __restrict__ c2) {
+    const int e = blockIdx.x;
+    const int pe = dv.pe, pf = dv.pf, qf = dv.qf, D = dv.D, nfs = dv.nfs;
+    for (int t = threadIdx.x; t < pe * nfs; t += blockDim.x) {
+        const int l = t / pe, i = t - l * pe;
+        const int lf = l / pf, b = l - lf * pf;
+        const int f = dv.elem_faces[e * dv.n_lfe + lf];
+        const int side = dv.elem_side[e * dv.n_lfe + lf];
+        const int o = dv.face_orient[2 * f + side];
+        const double* tp = dv.tphi + (static_cast<size_t>(lf) * dv.n_orient + o) * qf * pe;
+        double acc[3] = {0.0, 0.0, 0.0};
+        for (int gc = 0; gc < qf; ++gc) {
+            const size_t fi = static_cast<size_t>(f) * qf + gc;
+            const double w = dv.wf[gc] * dv.face_detjac[fi];
+            const double* n = dv.face_normal + ((static_cast<size_t>(f) * 2 + side) * qf + gc) * D;
+            const double pb = w * dv.psi[b + pf * gc];
+            const double ph = tp[static_cast<size_t>(gc) * pe + i];
+            for (int d = 0; d < D; ++d) acc[d] -= pb * ph * n[d];
+        }
+        const size_t off = static_cast<size_t>(e) * pe * nfs + t;
+        c0[off] = acc[0];
+        c1[off] = acc[1];
+        if (D == 3) c2[off] = acc[2];
+    }
+}
+
+// ---- the assembly kernel -------------------------------------------------------------------------------
+template <int M, int D>
+struct VolRec {
+    double w;
+    double invj[D * D];
+    double F[M * D];
+    double S[M];
+    double tm[M];  // dt_inv * (u - u_prev)
+    double dFu[M * D * M];
+    double dSu[M * M];
+    double dFq[M * D * M * D];
+    double dSq[M * M * D];
+};
+
+template <int M, int D>
+struct FaceRec {
+    double w;
+    double fhat[M];
+    double val[M];
+    double tau;
+    double dfh_q[M * M * D];
+    double dfh_uh[M * M];
+    double dv_u[M * M];
+    double dv_q[M * M * D];
+    double dv_uh[M * M];
+};
+
+template <class Model>
+__global__ void __launch_bounds__(256) local_assemble_kernel(DiscView dv, ModelView mv, LocalIn in, LocalOut out,
+                                                            int want_jac) {
+    constexpr int M = Model::M, D = Model::D;
+    using VR = VolRec<M, D>;
+    using FR = FaceRec<M, D>;
+    extern __shared__ double sm[];
+    const int e = blockIdx.x;
+    const int pe = dv.pe, pf = dv.pf, qe = dv.qe, qf = dv.qf, n_lfe = dv.n_lfe;
+    const int npe = M * pe, mpf = M * pf, nfl = n_lfe * mpf;
+    const int nfp = n_lfe * qf;
+    const int tid = threadIdx.x, nt = blockDim.x;
+
+    double* us = sm;                  // npe
+    double* qs = us + npe;            // D*npe  (direction-major)
+    double* uhs = qs + D * npe;       // nfl
+    double* ups = uhs + nfl;          // npe
+    VR* vrec = reinterpret_cast<VR*>(ups + npe);
+    FR* frec = reinterpret_cast<FR*>(vrec + qe);
+    __shared__ int s_face[8], s_side[8], s_orient[8], s_tag[8];
+
+    const Model model(mv);
+    const bool transient = in.dt_inv > 0.0;
+
+    for (int t = tid; t < npe; t += nt) {
+        us[t] = in.u[static_cast<size_t>(e) * npe + t];
+        for (int d = 0; d < D; ++d) qs[d * npe + t] = in.q[d][static_cast<size_t>(e) * npe + t];
+        ups[t] = transient ? in.u_prev[static_cast<size_t>(e) * npe + t] : 0.0;
+    }
+    if (tid < n_lfe) {
+        const int f = dv.elem_faces[e * n_lfe + tid];
+        const int side = dv.elem_side[e * n_lfe + tid];
+        s_face[tid] = f;
+        s_side[tid] = side;
+        s_orient[tid] = dv.face_orient[2 * f + side];
+        s_tag[tid] = dv.bnd_tag[f];
+    }
+    for (int t = tid; t < nfl; t += nt) {
+        const int lf = t / mpf;
+        uhs[t] = in.uhat[static_cast<size_t>(dv.elem_faces[e * n_lfe + lf]) * mpf + (t - lf * mpf)];
+    }
+    __syncthreads();
+
+    // ---- phase 1a: volume points ----
+    for (int g = tid; g < qe; g += nt) {
+        const size_t gi = static_cast<size_t>(e) * qe + g;
+        VR& r = vrec[g];
+        const double* phig = dv.phi + static_cast<size_t>(pe) * g;
+        double ug[M], qg[M * D], upg[M];
+        for (int m = 0; m < M; ++m) {
+            double a = 0.0, ap = 0.0, aq[D];
+            for (int d = 0; d < D; ++d) aq[d] = 0.0;
+            for (int i = 0; i < pe; ++i) {
+                const double p = phig[i];
+                a += us[m * pe + i] * p;
+                for (int d = 0; d < D; ++d) aq[d] += qs[d * npe + m * pe + i] * p;
+                if (transient) ap += ups[m * pe + i] * p;
+            }
+            ug[m] = a;
+            upg[m] = ap;
+            for (int d = 0; d < D; ++d) qg[m * D + d] = aq[d];
+        }
+        r.w = dv.wq[g] * dv.elem_detjac[gi];
+        for (int k = 0; k < D * D; ++k) r.invj[k] = dv.elem_invjac[gi * D * D + k];
+        const double* x = dv.elem_coords + gi * D;
+        const double* f = mv.forcing_q ? mv.forcing_q + gi * M : nullptr;
+        model.flux(ug, qg, x, r.F);
+        model.source(ug, qg, x, f, r.S);
+        for (int m = 0; m < M; ++m) r.tm[m] = transient ? in.dt_inv * (ug[m] - upg[m]) : 0.0;
+        if (want_jac) {
+            model.dflux_du(ug, qg, x, r.dFu);
+            model.dflux_dq(ug, qg, x, r.dFq);
+            model.dsource_du(ug, qg, x, r.dSu);
+            model.dsource_dq(ug, qg, x, r.dSq);
+        }
+    }
+    // ---- phase 1b: face points ----
+    for (int p = tid; p < nfp; p += nt) {
+        const int lf = p / qf, gc = p - lf * qf;
+        const int f = s_face[lf], side = s_side[lf], tag = s_tag[lf];
+        FR& r = frec[p];
+        const size_t fi = static_cast<size_t>(f) * qf + gc;
+        const double* phis = dv.tphi + ((static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf + gc) * pe;
+        const double* psic = dv.psi + static_cast<size_t>(pf) * gc;
+        const double* n = dv.face_normal + ((static_cast<size_t>(f) * 2 + side) * qf + gc) * D;
+        const double* x = dv.face_coords + fi * D;
+        double ug[M], qg[M * D], uh[M];
+        for (int m = 0; m < M; ++m) {
+            double a = 0.0, aq[D];
+            for (int d = 0; d < D; ++d) aq[d] = 0.0;
+            for (int i = 0; i < pe; ++i) {
+                const double ph = phis[i];
+                a += us[m * pe + i] * ph;
+                for (int d = 0; d < D; ++d) aq[d] += qs[d * npe + m * pe + i] * ph;
+            }
+            ug[m] = a;
+            for (int d = 0; d < D; ++d) qg[m * D + d] = aq[d];
+            double h = 0.0;
+            for (int b = 0; b < pf; ++b) h += uhs[lf * mpf + m * pf + b] * psic[b];
+            uh[m] = h;
+        }
+        r.w = dv.wf[gc] * dv.face_detjac[fi];
+        const double tau = model.tau_fn(ug, uh, n);
+        r.tau = tau;
+        double Fl[M * D];
+        model.flux(uh, qg, x, Fl);
+        for (int m = 0; m < M; ++m) {
+            double fn = 0.0;
+            for (int d = 0; d < D; ++d) fn += Fl[m * D + d] * n[d];
+            r.fhat[m] = fn + tau * (ug[m] - uh[m]);
+        }
+        double dFu[M * D * M], dFq[M * D * M * D];
+        if (want_jac || tag != 0) {
+            model.dflux_du(uh, qg, x, dFu);
+            model.dflux_dq(uh, qg, x, dFq);
+        } else {
+            for (int k = 0; k < M * D * M; ++k) dFu[k] = 0.0;
+            for (int k = 0; k < M * D * M * D; ++k) dFq[k] = 0.0;
+        }
+        // derivatives of the numerical flux (local_ops.cpp:186-189)
+        for (int m = 0; m < M; ++m)
+            for (int mp = 0; mp < M; ++mp) {
+                double su = 0.0;
+                for (int d = 0; d < D; ++d) su += dFu[(m * D + d) * M + mp] * n[d];
+                r.dfh_uh[m * M + mp] = su - ((m == mp) ? tau : 0.0);
+                for (int dp = 0; dp < D; ++dp) {
+                    double sq = 0.0;
+                    for (int d = 0; d < D; ++d) sq += dFq[((m * D + d) * M + mp) * D + dp] * n[d];
+                    r.dfh_q[(m * M + mp) * D + dp] = sq;
+                }
+            }
+        if (tag == 0) {
+            for (int m = 0; m < M; ++m) r.val[m] = r.fhat[m];
+            for (int k = 0; k < M * M; ++k) {
+                r.dv_u[k] = ((k / M) == (k % M)) ? tau : 0.0;
+                r.dv_uh[k] = r.dfh_uh[k];
+            }
+            for (int k = 0; k < M * M * D; ++k) r.dv_q[k] = r.dfh_q[k];
+        } else {
+            BFlux<M, D> b;
+            const double* gD = mv.dirichlet_q ? mv.dirichlet_q + fi * M : nullptr;
+            model.boundary(tag, ug, qg, uh, n, x, gD, b);
+            for (int m = 0; m < M; ++m) r.val[m] = b.val[m];
+            for (int k = 0; k < M * M; ++k) { r.dv_u[k] = b.d_u[k]; r.dv_uh[k] = b.d_uh[k]; }
+            for (int k = 0; k < M * M * D; ++k) r.dv_q[k] = b.d_q[k];
+        }
+    }
+    __syncthreads();
+
+    // ---- phase 2a: residuals (negated weak residuals, local_ops.cpp:223-226) ----
+    for (int i = tid; i < pe; i += nt) {
+        double acc[M];
+        for (int m = 0; m < M; ++m) acc[m] = 0.0;
+        for (int g = 0; g < qe; ++g) {
+            const VR& r = vrec[g];
+            const double ph = dv.phi[i + pe * g];
+            double grad[D];
+            for (int d = 0; d < D; ++d) {
+                double s = 0.0;
+                for (int k = 0; k < D; ++k) s += dv.dphi[k][i + pe * g] * r.invj[k * D + d];
+                grad[d] = s;
+            }
+            for (int m = 0; m < M; ++m) {
+                double fg = 0.0;
+                for (int d = 0; d < D; ++d) fg += r.F[m * D + d] * grad[d];
+                double v = -fg - r.S[m] * ph;
+                if (transient) v += r.tm[m] * ph;
+                acc[m] += r.w * v;
+            }
+        }
+        for (int p = 0; p < nfp; ++p) {
+            const int lf = p / qf, gc = p - lf * qf;
+            const FR& r = frec[p];
+            const double ph = dv.tphi[((static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf + gc) * pe + i];
+            for (int m = 0; m < M; ++m) acc[m] += r.w * r.fhat[m] * ph;
+        }
+        for (int m = 0; m < M; ++m) out.ru[static_cast<size_t>(e) * npe + m * pe + i] = -acc[m];
+    }
+    for (int t = tid; t < n_lfe * pf; t += nt) {
+        const int lf = t / pf, b = t - lf * pf;
+        double acc[M];
+        for (int m = 0; m < M; ++m) acc[m] = 0.0;
+        for (int gc = 0; gc < qf; ++gc) {
+            const FR& r = frec[lf * qf + gc];
+            const double ps = dv.psi[b + pf * gc];
+            for (int m = 0; m < M; ++m) acc[m] += r.w * r.val[m] * ps;
+        }
+        for (int m = 0; m < M; ++m) out.ruhat_e[static_cast<size_t>(e) * nfl + lf * mpf + m * pf + b] = -acc[m];
+    }
+    if (!want_jac) return;
+
+    // ---- phase 2b: E and D_d, one (i, j) scalar-basis pair per thread, all component pairs ----
+    for (int t = tid; t < pe * pe; t += nt) {
+        const int j = t / pe, i = t - j * pe;
+        double aE[M * M], aD[D * M * M];
+        for (int k = 0; k < M * M; ++k) aE[k] = 0.0;
+        for (int k = 0; k < D * M * M; ++k) aD[k] = 0.0;
+        for (int g = 0; g < qe; ++g) {
+            const VR& r = vrec[g];
+            const double phi_i = dv.phi[i + pe * g];
+            const double pj = r.w * dv.phi[j + pe * g];
+            double grad[D];
+            for (int d = 0; d < D; ++d) {
+                double s = 0.0;
+                for (int k = 0; k < D; ++k) s += dv.dphi[k][i + pe * g] * r.invj[k * D + d];
+                grad[d] = s;
+            }
+            for (int m = 0; m < M; ++m)
+                for (int mp = 0; mp < M; ++mp) {
+                    double fe = 0.0;
+                    for (int d = 0; d < D; ++d) fe += r.dFu[(m * D + d) * M + mp] * grad[d];
+                    double eij = -fe - r.dSu[m * M + mp] * phi_i;
+                    if (transient && m == mp) eij += in.dt_inv * phi_i;
+                    aE[m * M + mp] += pj * eij;
+                    for (int dp = 0; dp < D; ++dp) {
+                        double fd = 0.0;
+                        for (int d = 0; d < D; ++d) fd += r.dFq[((m * D + d) * M + mp) * D + dp] * grad[d];
+                        aD[(dp * M + m) * M + mp] += pj * (-fd - r.dSq[(m * M + mp) * D + dp] * phi_i);
+                    }
+                }
+        }
+        for (int p = 0; p < nfp; ++p) {
+            const int lf = p / qf, gc = p - lf * qf;
+            const FR& r = frec[p];
+            const double* phis = dv.tphi + ((static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf + gc) * pe;
+            const double pj = r.w * phis[j];
+            const double ph = phis[i];
+            for (int m = 0; m < M; ++m) {
+                aE[m * M + m] += pj * r.tau * ph;
+                for (int mp = 0; mp < M; ++mp)
+                    for (int dp = 0; dp < D; ++dp) aD[(dp * M + m) * M + mp] += pj * r.dfh_q[(m * M + mp) * D + dp] * ph;
+            }
+        }
+        for (int m = 0; m < M; ++m)
+            for (int mp = 0; mp < M; ++mp) {
+                const size_t o = static_cast<size_t>(e) * npe * npe + static_cast<size_t>(mp * pe + j) * npe + (m * pe + i);
+                out.E[o] = aE[m * M + mp];
+                for (int dp = 0; dp < D; ++dp) out.Dm[dp][o] = aD[(dp * M + m) * M + mp];
+            }
+    }
+    // ---- H and G_d: rows (lf, m, b), columns (mp, j) ----
+    for (int t = tid; t < n_lfe * pf * pe; t += nt) {
+        const int j = t / (n_lfe * pf);
+        const int lb = t - j * (n_lfe * pf);
+        const int lf = lb / pf, b = lb - lf * pf;
+        double aH[M * M], aG[D * M * M];
+        for (int k = 0; k < M * M; ++k) aH[k] = 0.0;
+        for (int k = 0; k < D * M * M; ++k) aG[k] = 0.0;
+        for (int gc = 0; gc < qf; ++gc) {
+            const FR& r = frec[lf * qf + gc];
+            const double pj = r.w * dv.tphi[((static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf + gc) * pe + j];
+            const double ps = dv.psi[b + pf * gc];
+            for (int k = 0; k < M * M; ++k) {
+                aH[k] += pj * r.dv_u[k] * ps;
+                for (int dp = 0; dp < D; ++dp) aG[dp * M * M + k] += pj * r.dv_q[k * D + dp] * ps;
+            }
+        }
+        for (int m = 0; m < M; ++m)
+            for (int mp = 0; mp < M; ++mp) {
+                const size_t o = static_cast<size_t>(e) * nfl * npe + static_cast<size_t>(mp * pe + j) * nfl + (lf * mpf + m * pf + b);
+                out.H[o] = aH[m * M + mp];
+                for (int dp = 0; dp < D; ++dp) out.G[dp][o] = aG[dp * M * M + m * M + mp];
+            }
+    }
+    // ---- F: rows (m, i), columns (lf, mp, bp) ----
+    for (int t = tid; t < pe * n_lfe * pf; t += nt) {
+        const int lb = t / pe, i = t - lb * pe;
+        const int lf = lb / pf, bp = lb - lf * pf;
+        double aF[M * M];
+        for (int k = 0; k < M * M; ++k) aF[k] = 0.0;
+        for (int gc = 0; gc < qf; ++gc) {
+            const FR& r = frec[lf * qf + gc];
+            const double pj = r.w * dv.psi[bp + pf * gc];
+            const double ph = dv.tphi[((static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf + gc) * pe + i];
+            for (int k = 0; k < M * M; ++k) aF[k] += pj * r.dfh_uh[k] * ph;
+        }
+        for (int m = 0; m < M; ++m)
+            for (int mp = 0; mp < M; ++mp)
+                out.F[static_cast<size_t>(e) * npe * nfl + static_cast<size_t>(lf * mpf + mp * pf + bp) * npe + (m * pe + i)] =
+                    aF[m * M + mp];
+    }
+    // ---- J: block diagonal over local faces; rows (lf, m, b), columns (lf, mp, bp); the other
+    // entries of the nfl x nfl block are zero ----
+    for (int t = tid; t < nfl * nfl; t += nt) out.J[static_cast<size_t>(e) * nfl * nfl + t] = 0.0;
+    __syncthreads();
+    for (int t = tid; t < n_lfe * pf * pf; t += nt) {
+        const int lf = t / (pf * pf);
+        const int r2 = t - lf * pf * pf;
+        const int bp = r2 / pf, b = r2 - bp * pf;
+        double aJ[M * M];
+        for (int k = 0; k < M * M; ++k) aJ[k] = 0.0;
+        for (int gc = 0; gc < qf; ++gc) {
+            const FR& r = frec[lf * qf + gc];
+            const double pj = r.w * dv.psi[bp + pf * gc];
+            const double ps = dv.psi[b + pf * gc];
+            for (int k = 0; k < M * M; ++k) aJ[k] += pj * r.dv_uh[k] * ps;
+        }
+        for (int m = 0; m < M; ++m)
+            for (int mp = 0; mp < M; ++mp)
+                out.J[static_cast<size_t>(e) * nfl * nfl + static_cast<size_t>(lf * mpf + mp * pf + bp) * nfl + (lf * mpf + m * pf + b)] =
+                    aJ[m * M + mp];
+    }
+}
+
+template <class Model>
+void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, const LocalIn& in,
+                       const LocalOut& out, bool want_jac) {
+    constexpr int M = Model::M, D = Model::D;
+    const int npe = M * dv.pe, nfl = dv.n_lfe * M * dv.pf;
+    const size_t smem = (static_cast<size_t>(npe) * (2 + D) + nfl) * sizeof(double) +
+                        static_cast<size_t>(dv.qe) * sizeof(VolRec<M, D>) +
+                        static_cast<size_t>(dv.n_lfe) * dv.qf * sizeof(FaceRec<M, D>);
+    if (smem > 220 * 1024)
+        throw Failure(HDGB_ERR_UNSUPPORTED, "local assembly: per-element point records exceed shared memory ("
+                                                + std::to_string(smem) + " B); reduce quad_points");
+    if (smem > 48 * 1024)
+        HDGB_CUDA(cudaFuncSetAttribute(local_assemble_kernel<Model>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    local_assemble_kernel<Model><<<dv.ne, 256, smem, ctx->stream>>>(dv, mv, in, out, want_jac ? 1 : 0);
+    HDGB_LAUNCH_CHECK(ctx);
+}
+
+}  // namespace
+
+void launch_local_factors(hdgb_ctx* ctx, const DiscView& dv, double* mass, double* const bmat[3], double* const cmat[3]) {
+    mass_bmat_kernel<<<dv.ne, 128, 0, ctx->stream>>>(dv, mass, bmat[0], bmat[1], bmat[2]);
+    HDGB_LAUNCH_CHECK(ctx);
+    cmat_kernel<<<dv.ne, 128, 0, ctx->stream>>>(dv, cmat[0], cmat[1], cmat[2]);
+    HDGB_LAUNCH_CHECK(ctx);
+}
+
+void launch_local_assemble(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, const LocalIn& in,
+                           const LocalOut& out, bool want_jac) {
+    if (dv.n_lfe > 8) throw Failure(HDGB_ERR_UNSUPPORTED, "local assembly: more than 8 local faces");
+    const int D = dv.D;
+    switch (mv.kind) {
+        case HDGB_MODEL_POISSON:
+            if (D == 2) launch_assemble_t<PoissonModel<2>>(ctx, dv, mv, in, out, want_jac);
+            else launch_assemble_t<PoissonModel<3>>(ctx, dv, mv, in, out, want_jac);
+            break;
+        case HDGB_MODEL_REACTION:
+            if (D == 2) launch_assemble_t<ReactionModel<2>>(ctx, dv, mv, in, out, want_jac);
+            else launch_assemble_t<ReactionModel<3>>(ctx, dv, mv, in, out, want_jac);
+            break;
+        case HDGB_MODEL_BURGERS:
+            if (D == 2) launch_assemble_t<BurgersModel<2>>(ctx, dv, mv, in, out, want_jac);
+            else launch_assemble_t<BurgersModel<3>>(ctx, dv, mv, in, out, want_jac);
+            break;
+        case HDGB_MODEL_CONVDIFF:
+            if (D == 2) launch_assemble_t<ConvDiffModel<2>>(ctx, dv, mv, in, out, want_jac);
+            else launch_assemble_t<ConvDiffModel<3>>(ctx, dv, mv, in, out, want_jac);
+            break;
+        case HDGB_MODEL_ELASTICITY:
+            if (D == 2) launch_assemble_t<ElasticityModel<2>>(ctx, dv, mv, in, out, want_jac);
+            else launch_assemble_t<ElasticityModel<3>>(ctx, dv, mv, in, out, want_jac);
+            break;
+        default:
+            throw Failure(HDGB_ERR_UNSUPPORTED, "unknown model kind " + std::to_string(mv.kind));
+    }
+}
+
+}  // namespace hdgb

@@ -1,0 +1,83 @@
+// Launcher declarations for the hand-written sm_100a kernels.  Each launcher enqueues on
+// ctx->stream and never synchronises.
+#pragma once
+#include "common.cuh"
+
+namespace hdgb {
+
+// ---- team GEMV (k_gemv.cu) ---------------------------------------------------------------------
+// y_b = alpha * A_{b / a_div} * xg_b + beta * z_b   for b in [0, batch)
+//   A blocks: rows x cols column-major, stride rows*cols.
+//   xg_b: either the contiguous slice x[b*cols .. +cols] (idx == nullptr) or a gather of
+//   nslots = cols / width slices of `width` doubles:
+//       slot s -> x[ idx[(b / comp) * nslots + s] * (comp*width) + (b % comp) * width ]   (idx < 0: zeros)
+//   z (may be nullptr) and y have rows doubles per b.  y may alias z.
+struct GemvArgs {
+    const double* a = nullptr;
+    const double* x = nullptr;
+    double* y = nullptr;
+    const double* z = nullptr;
+    const int* idx = nullptr;
+    int rows = 0, cols = 0;
+    int64_t batch = 0;
+    int width = 0;  // gather slot width (only with idx)
+    int comp = 1;   // component interleave of the gather
+    int a_div = 1;  // consecutive b sharing one matrix block
+    double alpha = 1.0, beta = 0.0;
+};
+void launch_team_gemv(hdgb_ctx* ctx, const GemvArgs& g);
+
+// z_f[i] = ze[e0][l0][i] + ze[e1][l1][i]   (apply_asm scatter as an atomics-free face gather)
+// sides = 1 keeps only the owner's (side-0) term: the restricted (RAS) prolongation.
+void launch_face_sum(hdgb_ctx* ctx, const double* ze, const int* face_elems, const int* face_lidx,
+                     int nf, int mpf, int n_lfe, double* z, int sides = 2);
+// out[e][l][i] = v[elem_faces[e][l]][i]  (gather_element_trace)
+void launch_gather_element_trace(hdgb_ctx* ctx, const double* v, const int* elem_faces, int ne,
+                                 int n_lfe, int mpf, double* out);
+// out[f][s][i] = x[nbr[f][s]][i] or 0 (gather_extended)
+void launch_gather_extended(hdgb_ctx* ctx, const double* x, const int* nbr, int nf, int nb, int mpf,
+                            double* out);
+
+// ---- vector kernels (k_vec.cu) -----------------------------------------------------------------
+// out[j] = sum_i V[j*ldv + i] * w[i], j < nvec.  Deterministic two-stage reduction.
+// If sqrt_last is set the last entry is replaced by its square root (norms).
+void launch_multi_dot(hdgb_ctx* ctx, const double* V, int64_t ldv, int nvec, const double* w, int64_t n,
+                      double* out /*device nvec*/, double* partial /*device workspace*/, bool sqrt_last = false);
+size_t multi_dot_workspace_doubles(int64_t n, int nvec);
+// w[i] += sign * sum_j c[j] * V[j*ldv + i]  (ascending j).  If norm2_out != nullptr, also reduces
+// sum_i w_new[i]^2 into *norm2_out (device) using `partial`.
+void launch_multi_axpy(hdgb_ctx* ctx, const double* V, int64_t ldv, int nvec, const double* c /*device*/,
+                       double sign, double* w, int64_t n, double* norm2_out, double* partial);
+// out[i] = w[i] * s where s = (*dev_scalar is used as: mode 0: 1/sqrt(v), mode 1: 1/v, mode 2: v)
+void launch_scale_dev(hdgb_ctx* ctx, const double* w, const double* dev_scalar, int mode, double* out, int64_t n);
+// y = a*x + b*y
+void launch_axpby(hdgb_ctx* ctx, double a, const double* x, double b, double* y, int64_t n);
+// out = a*x + b*y (out may alias)
+void launch_lincomb(hdgb_ctx* ctx, double a, const double* x, double b, const double* y, double* out, int64_t n);
+// polynomial-preconditioner fused updates (preconditioner.cpp:264-278)
+//   real:  w += inv*q ;  (after op)  q -= inv*t
+//   pair:  s = 2a*q - t ; w += inv*s
+void launch_poly_pair_mid(hdgb_ctx* ctx, double two_a, double inv, const double* q, const double* t,
+                          double* s, double* w, int64_t n);
+// flags[1] |= 1 if any entry is non-finite
+void launch_check_finite(hdgb_ctx* ctx, const double* v, int64_t n, int* flags);
+void launch_fill(hdgb_ctx* ctx, double* v, double value, int64_t n);
+// sum of squares (device scalar out[0]); deterministic
+void launch_sumsq(hdgb_ctx* ctx, const double* v, int64_t n, double* out, double* partial);
+
+// ---- dense batch kernels (k_dense.cu) ----------------------------------------------------------
+// Explicit inverses; flags[0] = min(flags[0], first singular b).  a and inv may alias.
+void launch_lu_invert_batch(hdgb_ctx* ctx, int n, int64_t batch, const double* a, double* inv, int* flags);
+// C_b = alpha * op(A_b) * B_b + beta * C_b ; a_batch / b_batch == 1 broadcast.
+void launch_gemm_batch(hdgb_ctx* ctx, int m, int n, int k, const double* a, int64_t a_stride, bool trans_a,
+                       const double* b, int64_t b_stride, double* c, int64_t c_stride, int64_t batch,
+                       double alpha, double beta);
+
+// ---- shared host helpers (api_core.cu) ------------------------------------------------------------
+void reset_flags(hdgb_ctx* c);
+void read_flags(hdgb_ctx* c, int* singular_index, int* nonfinite);
+// lu_invert_batch on device pointers; throws Failure(code) carrying the lowest singular batch index.
+void device_lu_invert(hdgb_ctx* c, int n, int64_t batch, const double* a, double* inv, const char* context,
+                      hdgb_status code);
+
+}  // namespace hdgb
