@@ -107,7 +107,10 @@ typedef struct hdgb_dims {
  * / triangle / tetrahedron analogues, followed by gauss_rule(quad_points or k+2)
  * (study.cpp:69-70), tabulate_basis (basis.cpp:144-201), compute_geometry (mesh.cpp:109-182) and
  * precompute_local_factors (local_ops.cpp:252-349, device kernels).  jitter > 0 displaces interior
- * vertices by at most jitter*h with the given seed (synthetic unstructured-like meshes). */
+ * vertices by at most jitter*h with the given seed (synthetic unstructured-like meshes).
+ * ctx == NULL builds a HOST-ONLY discretisation (mesh, master element, geometry tables readable
+ * through hdgb_disc_get_*; no device state, no local factors): setup-time code needs no GPU, every
+ * operator below does. */
 hdgb_status hdgb_disc_create_structured(hdgb_ctx* ctx, int shape, int n, int degree, int n_comp,
                                         int quad_points, const double* lo, const double* hi,
                                         double jitter, uint64_t seed, hdgb_disc** out);

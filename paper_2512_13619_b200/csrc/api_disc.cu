@@ -25,6 +25,11 @@ void finish_disc(hdgb_ctx* c, hdgb_disc* d, int n_comp) {
     dm.pe = me.pe; dm.pf = me.pf; dm.qe = me.qe; dm.qf = me.qf; dm.nv = m.nv;
 
     d->geom = compute_geometry(m, me);
+    DiscView& v = d->view;
+    v.D = m.dim; v.M = n_comp; v.ne = m.ne; v.nf = m.nf; v.n_lfe = m.n_lfe; v.n_orient = me.n_orient;
+    v.pe = me.pe; v.pf = me.pf; v.qe = me.qe; v.qf = me.qf;
+    v.npe = n_comp * me.pe; v.mpf = n_comp * me.pf; v.nfl = m.n_lfe * v.mpf; v.nfs = m.n_lfe * me.pf;
+    if (!c) return;  // host-only discretisation: tables for inspection, no device state
     upload(c, d->elem_faces, m.elem_faces);
     upload(c, d->elem_side, m.elem_side);
     upload(c, d->face_elems, m.face_elems);
@@ -44,10 +49,6 @@ void finish_disc(hdgb_ctx* c, hdgb_disc* d, int n_comp) {
     upload(c, d->face_coords, d->geom.face_coords);
     upload(c, d->face_normal, d->geom.face_normal);
 
-    DiscView& v = d->view;
-    v.D = m.dim; v.M = n_comp; v.ne = m.ne; v.nf = m.nf; v.n_lfe = m.n_lfe; v.n_orient = me.n_orient;
-    v.pe = me.pe; v.pf = me.pf; v.qe = me.qe; v.qf = me.qf;
-    v.npe = n_comp * me.pe; v.mpf = n_comp * me.pf; v.nfl = m.n_lfe * v.mpf; v.nfs = m.n_lfe * me.pf;
     v.elem_faces = d->elem_faces.p; v.elem_side = d->elem_side.p; v.face_elems = d->face_elems.p;
     v.face_lidx = d->face_lidx.p; v.face_orient = d->face_orient.p; v.bnd_tag = d->bnd_tag.p;
     v.phi = d->phi.p;
@@ -87,7 +88,7 @@ hdgb_status get_vec(const hdgb_disc* d, const std::vector<T>& v, T* out, int64_t
     if (n) *n = static_cast<int64_t>(v.size());
     if (out) {
         if (cap < static_cast<int64_t>(v.size())) {
-            d->ctx->err = "destination too small";
+            if (d->ctx) d->ctx->err = "destination too small";
             return HDGB_ERR_DIMENSION_MISMATCH;
         }
         std::memcpy(out, v.data(), v.size() * sizeof(T));
@@ -96,6 +97,7 @@ hdgb_status get_vec(const hdgb_disc* d, const std::vector<T>& v, T* out, int64_t
 }
 
 hdgb_status get_dev(const hdgb_disc* d, const DevBuf<double>& b, double* out, int64_t cap, int64_t* n) {
+    if (!d->ctx) return HDGB_ERR_CUDA;  // device tables do not exist on a host-only discretisation
     if (n) *n = static_cast<int64_t>(b.n);
     if (out) {
         if (cap < static_cast<int64_t>(b.n)) {
@@ -175,7 +177,7 @@ hdgb_status hdgb_disc_get_i32(const hdgb_disc* d, const char* name, int32_t* out
     if (s == "boundary_tag") return get_vec(d, m.bnd_tag, out, cap, n);
     if (s == "elem_side") return get_vec(d, m.elem_side, out, cap, n);
     if (s == "qperm") return get_vec(d, d->me.qperm, out, cap, n);
-    d->ctx->err = "unknown int table '" + s + "'";
+    if (d->ctx) d->ctx->err = "unknown int table '" + s + "'";
     return HDGB_ERR_GENERIC;
 }
 
@@ -213,7 +215,7 @@ hdgb_status hdgb_disc_get_f64(const hdgb_disc* d, const char* name, double* out,
         if (s == "minv_b" + ks) return get_dev(d, d->minv_b[k], out, cap, n);
         if (s == "minv_c" + ks) return get_dev(d, d->minv_c[k], out, cap, n);
     }
-    d->ctx->err = "unknown table '" + s + "'";
+    if (d->ctx) d->ctx->err = "unknown table '" + s + "'";
     return HDGB_ERR_GENERIC;
 }
 

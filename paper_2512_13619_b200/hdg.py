@@ -379,8 +379,9 @@ class Discretization:
     def __init__(self, ctx: Context, handle):
         self.ctx = ctx
         self._h = handle
+        self._L = load_library()
         d = _Dims()
-        ctx._L.hdgb_disc_dims(handle, C.byref(d))
+        self._L.hdgb_disc_dims(handle, C.byref(d))
         for n, _ in _Dims._fields_:
             setattr(self, n, getattr(d, n))
         self.npe = self.n_comp * self.pe
@@ -397,6 +398,13 @@ class Discretization:
         h = _vp()
         lo_a = None if lo is None else (C.c_double * 3)(*(list(lo) + [0.0] * 3)[:3])
         hi_a = None if hi is None else (C.c_double * 3)(*(list(hi) + [1.0] * 3)[:3])
+        if ctx is None:
+            # host-only tables (mesh / master element / geometry); operators need a Context
+            st = load_library().hdgb_disc_create_structured(None, SHAPES[shape], n, degree, n_comp, quad_points, lo_a,
+                                                            hi_a, jitter, seed, C.byref(h))
+            if st != 0:
+                raise _STATUS.get(st, HdgError)(f"host-only discretisation failed (status {st})")
+            return cls(None, h)
         ctx.check(ctx._L.hdgb_disc_create_structured(ctx._h, SHAPES[shape], n, degree, n_comp, quad_points, lo_a, hi_a,
                                                      jitter, seed, C.byref(h)))
         return cls(ctx, h)
@@ -412,7 +420,7 @@ class Discretization:
 
     def close(self):
         if getattr(self, "_h", None):
-            self.ctx._L.hdgb_disc_destroy(self._h)
+            self._L.hdgb_disc_destroy(self._h)
             self._h = None
 
     def __del__(self):
@@ -423,17 +431,19 @@ class Discretization:
 
     def table(self, name: str) -> np.ndarray:
         n = C.c_int64()
-        L = self.ctx._L
+        L = self._L
         st = L.hdgb_disc_get_f64(self._h, name.encode(), None, 0, C.byref(n))
         if st == 0:
             out = np.empty(n.value)
-            self.ctx.check(L.hdgb_disc_get_f64(self._h, name.encode(), _ptr(out), n.value, C.byref(n)))
+            if L.hdgb_disc_get_f64(self._h, name.encode(), _ptr(out), n.value, C.byref(n)) != 0:
+                raise HdgError(f"table {name}")
             return out
         st = L.hdgb_disc_get_i32(self._h, name.encode(), None, 0, C.byref(n))
         if st != 0:
             raise KeyError(name)
         out = np.empty(n.value, dtype=np.int32)
-        self.ctx.check(L.hdgb_disc_get_i32(self._h, name.encode(), _ptr(out), n.value, C.byref(n)))
+        if L.hdgb_disc_get_i32(self._h, name.encode(), _ptr(out), n.value, C.byref(n)) != 0:
+            raise HdgError(f"table {name}")
         return out
 
     def set_boundary_tags(self, tags):
@@ -522,6 +532,7 @@ class Model:
                  initial=None, name=None):
         self.disc, self.kind, self.params = disc, kind, list(params)
         self.exact_solution, self.initial_state, self.name = exact, initial, name or kind
+        self._forcing, self._dirichlet = forcing, dirichlet
         ctx = disc.ctx
         xq, xf = None, None
         fq = dq = None
