@@ -68,6 +68,11 @@ hdgb_status hdgb_ctx_synchronize(hdgb_ctx* ctx);
 int64_t hdgb_ctx_launch_count(const hdgb_ctx* ctx);
 void hdgb_ctx_reset_launch_count(hdgb_ctx* ctx);
 const char* hdgb_version(void);
+/* Process-wide kernel-selection knobs for A/B measurements and tests: "use_stream" (0|1: route
+ * large GEMVs through the TMA stream kernel), "stream_min_elems" (matrix entries below which the
+ * team kernel is used).  Returns non-zero for an unknown key.  Results do not depend on them
+ * beyond rounding. */
+int hdgb_set_tuning(const char* key, int64_t value);
 
 /* ---- A0-A2: batched dense kernels (dense_batch.hpp:36-51) ---------------------------------- */
 /* lu_invert_batch (dense_batch.cpp:77-99): explicit inverses by partial-pivot LU; a pivot not

@@ -9,6 +9,13 @@ extern "C" {
 
 const char* hdgb_version(void) { return "hdgb200 0.1 (sm_100a)"; }
 
+int hdgb_set_tuning(const char* key, int64_t value) {
+    const std::string k = key ? key : "";
+    if (k == "use_stream") { hdgb::tuning().use_stream = static_cast<int>(value); return 0; }
+    if (k == "stream_min_elems") { hdgb::tuning().stream_min_elems = value; return 0; }
+    return 1;
+}
+
 hdgb_status hdgb_ctx_create(int device, hdgb_ctx** out) {
     if (!out) return HDGB_ERR_GENERIC;
     *out = nullptr;
@@ -93,6 +100,11 @@ hdgb_status hdgb_copy(hdgb_ctx* c, double* dst, const double* src, int64_t n) {
 }  // extern "C"
 
 namespace hdgb {
+
+Tuning& tuning() {
+    static Tuning t;
+    return t;
+}
 
 // Resets the device error words, returns after `fn` the lowest singular batch index (or -1).
 void reset_flags(hdgb_ctx* c) {

@@ -112,6 +112,7 @@ int env_int(const char* name, int dflt) {
 
 void launch_team_gemv(hdgb_ctx* ctx, const GemvArgs& g) {
     if (g.batch <= 0 || g.rows <= 0 || g.cols <= 0) return;
+    if (tuning().use_stream && launch_stream_gemv(ctx, g)) return;
     if (g.idx && (g.width <= 0 || g.cols % g.width != 0))
         throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "team_gemv: cols not a multiple of the gather width");
     const bool vec2 = (g.rows % 2 == 0) && (reinterpret_cast<uintptr_t>(g.a) % 16 == 0);

@@ -1,0 +1,353 @@
+// Stream GEMV: the bandwidth kernel behind block_matvec (face_matrix.cpp:83-107, gather fused),
+// apply_bj (preconditioner.cpp:48-52), the element solves of apply_asm (:86-91) and recover_local
+// (local_ops.cpp:452-460) at sizes where HBM streaming is what matters.
+//
+// The batched block rows of a DenseBatch are ONE contiguous array (dense_batch.hpp:12-34), so the
+// kernel treats the matrix data as a byte stream: a persistent CTA per SM owns a contiguous range
+// of items and pulls it through a ring of shared-memory stages with 1D bulk TMA copies
+// (cp.async.bulk ... mbarrier::complete_tx) issued by one producer thread; mbarrier full/empty
+// pairs hand stages to the consumer warps.  Each stage ("chunk") holds either a whole number of
+// small items or a column range of one large item, and is consumed by exactly one warp, which
+//   * gathers the item's input slice (neighbour slices through the index table, zeros for
+//     kNoFace) into its private shared-memory x buffer while the TMA copy is in flight,
+//   * multiplies out of shared memory (lanes own 1-2 consecutive rows x a column group; 128-bit
+//     LDS when the row count is even) keeping partial sums in registers across the chunks of an item,
+//   * combines the column groups with a fixed-order shuffle tree (deterministic) and writes y.
+// HBM sees every matrix byte exactly once, as large sequential bulk reads; x / y traffic is served
+// from L2.  Roofline: HBM.  Algorithmic bytes per item: 8*(rows*cols + cols + rows) + 4*nslots.
+#include "kernels.cuh"
+
+namespace hdgb {
+
+namespace {
+
+constexpr int kConsumerWarps = 8;
+constexpr int kThreads = (kConsumerWarps + 1) * 32;
+constexpr int kMaxStages = 8;
+constexpr int kChunkElems = 3072;  // 24 KB per stage
+
+struct StreamPlan {
+    int rows, cols;
+    int split;            // 0: chunk = ipc whole items; 1: chunk = cpc columns of one item
+    int ipc;              // items per chunk (grouped)
+    int cpc;              // columns per chunk (split)
+    int cpi;              // chunks per item (split)
+    int stages;
+    int xs_elems;         // per-warp x buffer (doubles)
+    int stage_elems;      // doubles per stage
+    int64_t batch;
+    int64_t n_units;      // grouped: chunks; split: items
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra DONE;\n"
+        "bra LAB_WAIT;\n"
+        "DONE:\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 1D bulk TMA copy global -> shared, completion counted in bytes on the mbarrier.
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+template <int V>
+__device__ __forceinline__ void lds_rows(const double* p, double (&v)[V]);
+template <>
+__device__ __forceinline__ void lds_rows<1>(const double* p, double (&v)[1]) { v[0] = *p; }
+template <>
+__device__ __forceinline__ void lds_rows<2>(const double* p, double (&v)[2]) {
+    const double2 t = *reinterpret_cast<const double2*>(p);
+    v[0] = t.x;
+    v[1] = t.y;
+}
+
+// acc += A[:, 0..ncols) * xs[0..ncols) for this lane's rows; A column-major with leading dim rows.
+template <int V, int RT>
+__device__ __forceinline__ void accumulate(const double* __restrict__ A, const double* __restrict__ xs, int rows, int ncols,
+                                           int rl, int cg, int CG, double (&acc)[RT][V]) {
+    if (cg >= CG) return;
+#pragma unroll 4
+    for (int c = cg; c < ncols; c += CG) {
+        const double xv = xs[c];
+        const double* col = A + static_cast<size_t>(c) * rows;
+#pragma unroll
+        for (int t = 0; t < RT; ++t) {
+            const int r = (rl + 32 * t) * V;
+            if (RT == 1 || r < rows) {
+                double a[V];
+                lds_rows<V>(col + r, a);
+#pragma unroll
+                for (int v = 0; v < V; ++v) acc[t][v] = fma(a[v], xv, acc[t][v]);
+            }
+        }
+    }
+}
+
+template <int V, int RT>
+__global__ void __launch_bounds__(kThreads, 1) stream_gemv_kernel(GemvArgs g, StreamPlan p) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* stage_base = reinterpret_cast<double*>(smem_raw);
+    double* xs_base = stage_base + static_cast<size_t>(p.stages) * p.stage_elems;
+    uint64_t* full = reinterpret_cast<uint64_t*>(xs_base + static_cast<size_t>(kConsumerWarps) * p.xs_elems);
+    uint64_t* empty = full + kMaxStages;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rows = p.rows, cols = p.cols;
+    const int64_t item_elems = static_cast<int64_t>(rows) * cols;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < p.stages; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    // this CTA's contiguous range of units (grouped: chunks, split: items)
+    const int64_t u0 = p.n_units * blockIdx.x / gridDim.x;
+    const int64_t u1 = p.n_units * (blockIdx.x + 1) / gridDim.x;
+    const int64_t n_chunks = p.split ? (u1 - u0) * p.cpi : (u1 - u0);
+
+    if (warp == kConsumerWarps) {
+        // ---- producer: one thread streams the CTA's byte range through the stage ring ----
+        if (lane == 0) {
+            for (int64_t k = 0; k < n_chunks; ++k) {
+                const int s = static_cast<int>(k % p.stages);
+                const int64_t use = k / p.stages;
+                if (use > 0) mbar_wait(empty + s, static_cast<uint32_t>((use - 1) & 1));
+                const double* src;
+                int64_t elems;
+                if (p.split) {
+                    const int64_t item = u0 + k / p.cpi;
+                    const int ci = static_cast<int>(k % p.cpi);
+                    const int c0 = ci * p.cpc;
+                    const int nc = min(p.cpc, cols - c0);
+                    src = g.a + item * item_elems + static_cast<int64_t>(c0) * rows;
+                    elems = static_cast<int64_t>(nc) * rows;
+                } else {
+                    const int64_t i0 = (u0 + k) * p.ipc;
+                    int64_t cnt = g.batch - i0 < p.ipc ? g.batch - i0 : p.ipc;
+                    if ((item_elems & 1) && (cnt & 1)) --cnt;  // keep the copy a multiple of 16 bytes; the odd tail item is read directly
+                    src = g.a + i0 * item_elems;
+                    elems = cnt * item_elems;
+                }
+                const uint32_t bytes = static_cast<uint32_t>(elems * sizeof(double));
+                mbar_expect_tx(full + s, bytes);
+                if (bytes) tma_bulk_g2s(stage_base + static_cast<size_t>(s) * p.stage_elems, src, bytes, full + s);
+            }
+        }
+        return;
+    }
+
+    // ---- consumers ----
+    double* xs = xs_base + static_cast<size_t>(warp) * p.xs_elems;
+    const int RL = (rows + V - 1) / V;
+    const int CG = RL >= 32 ? 1 : 32 / RL;
+    const int cg = RL >= 32 ? 0 : lane / RL;
+    const int rl = RL >= 32 ? lane : lane - cg * RL;
+    const int nslots = g.idx ? cols / g.width : 0;
+
+    auto gather_x = [&](int64_t item, int c0, int nc, double* dst) {
+        if (g.idx == nullptr) {
+            const double* xb = g.x + item * cols + c0;
+            for (int j = lane; j < nc; j += 32) dst[j] = xb[j];
+        } else {
+            const int* ib = g.idx + item * nslots;
+            for (int j = lane; j < nc; j += 32) {
+                const int c = c0 + j;
+                const int sl = c / g.width;
+                const int o = c - sl * g.width;
+                const int src = ib[sl];
+                dst[j] = src < 0 ? 0.0 : g.x[static_cast<int64_t>(src) * g.width + o];
+            }
+        }
+    };
+    auto reduce_store = [&](double (&acc)[RT][V], int64_t item) {
+        // fixed-order tree over the column groups (lane = cg*RL + rl)
+        if (CG > 1) {
+            int top = 1;
+            while (top < CG) top <<= 1;
+            for (int off = top >> 1; off > 0; off >>= 1) {
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    const double o = __shfl_down_sync(0xffffffffu, acc[0][v], off * RL);
+                    if (cg + off < CG) acc[0][v] += o;
+                }
+            }
+        }
+        if (cg == 0) {
+#pragma unroll
+            for (int t = 0; t < RT; ++t) {
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    const int r = (rl + 32 * t) * V + v;
+                    if (r < rows && (RL >= 32 || rl < RL)) {
+                        const int64_t o = item * rows + r;
+                        double out = g.alpha * acc[t][v];
+                        if (g.z != nullptr) out += g.beta * g.z[o];
+                        g.y[o] = out;
+                    }
+                }
+            }
+        }
+    };
+
+    if (p.split) {
+        // items are dealt to warps round-robin; a warp keeps its item's partial sums in registers
+        for (int64_t li = warp; li < u1 - u0; li += kConsumerWarps) {
+            const int64_t item = u0 + li;
+            gather_x(item, 0, cols, xs);
+            __syncwarp();
+            double acc[RT][V];
+#pragma unroll
+            for (int t = 0; t < RT; ++t)
+#pragma unroll
+                for (int v = 0; v < V; ++v) acc[t][v] = 0.0;
+            for (int ci = 0; ci < p.cpi; ++ci) {
+                const int64_t k = li * p.cpi + ci;
+                const int s = static_cast<int>(k % p.stages);
+                const int c0 = ci * p.cpc;
+                const int nc = min(p.cpc, cols - c0);
+                mbar_wait(full + s, static_cast<uint32_t>((k / p.stages) & 1));
+                accumulate<V, RT>(stage_base + static_cast<size_t>(s) * p.stage_elems, xs + c0, rows, nc, rl, cg, CG, acc);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty + s);
+            }
+            reduce_store(acc, item);
+            __syncwarp();
+        }
+    } else {
+        for (int64_t k = warp; k < n_chunks; k += kConsumerWarps) {
+            const int s = static_cast<int>(k % p.stages);
+            const int64_t i0 = (u0 + k) * p.ipc;
+            const int cnt = static_cast<int>(g.batch - i0 < p.ipc ? g.batch - i0 : p.ipc);
+            const int cnt_tma = ((item_elems & 1) && (cnt & 1)) ? cnt - 1 : cnt;
+            for (int it = 0; it < cnt; ++it) gather_x(i0 + it, 0, cols, xs + static_cast<size_t>(it) * cols);
+            __syncwarp();
+            mbar_wait(full + s, static_cast<uint32_t>((k / p.stages) & 1));
+            const double* st = stage_base + static_cast<size_t>(s) * p.stage_elems;
+            for (int it = 0; it < cnt; ++it) {
+                double acc[RT][V];
+#pragma unroll
+                for (int t = 0; t < RT; ++t)
+#pragma unroll
+                    for (int v = 0; v < V; ++v) acc[t][v] = 0.0;
+                if (it < cnt_tma) {
+                    accumulate<V, RT>(st + static_cast<size_t>(it) * item_elems, xs + static_cast<size_t>(it) * cols, rows, cols, rl, cg, CG, acc);
+                } else if (V == 1) {
+                    // odd tail item that the 16-byte granular copy left out: read it from global memory
+                    accumulate<V, RT>(g.a + (i0 + it) * item_elems, xs + static_cast<size_t>(it) * cols, rows, cols, rl, cg, CG, acc);
+                }
+                reduce_store(acc, i0 + it);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + s);
+        }
+    }
+}
+
+template <int V, int RT>
+void launch_t(hdgb_ctx* ctx, const GemvArgs& g, const StreamPlan& p, int grid, size_t smem) {
+    auto kern = stream_gemv_kernel<V, RT>;
+    HDGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    kern<<<grid, kThreads, smem, ctx->stream>>>(g, p);
+    HDGB_LAUNCH_CHECK(ctx);
+}
+
+}  // namespace
+
+// Returns false when the shape is outside what the streaming kernel handles (caller falls back to
+// the team kernel): component-interleaved gathers, broadcast matrices, misaligned or huge rows.
+bool launch_stream_gemv(hdgb_ctx* ctx, const GemvArgs& g) {
+    if (g.batch <= 0 || g.rows <= 0 || g.cols <= 0) return true;
+    if (g.a_div != 1 || g.comp != 1) return false;
+    if (g.idx && (g.width <= 0 || g.cols % g.width != 0)) return false;
+    if (reinterpret_cast<uintptr_t>(g.a) % 16 != 0) return false;
+    const int rows = g.rows, cols = g.cols;
+    const int64_t item_elems = static_cast<int64_t>(rows) * cols;
+    const int V = (rows % 2 == 0) ? 2 : 1;
+    const int RL = (rows + V - 1) / V;
+    const int RT = RL <= 32 ? 1 : (RL + 31) / 32;
+    if (RT > 4) return false;
+    // small problems are launch-latency bound; the persistent pipeline only pays off on real streams
+    if (item_elems * g.batch < tuning().stream_min_elems) return false;
+
+    StreamPlan p{};
+    p.rows = rows;
+    p.cols = cols;
+    p.batch = g.batch;
+    if (item_elems <= kChunkElems) {
+        p.split = 0;
+        p.ipc = static_cast<int>(kChunkElems / item_elems);
+        if ((item_elems & 1) && (p.ipc & 1)) {
+            if (p.ipc == 1) return false;
+            --p.ipc;
+        }
+        p.cpc = cols;
+        p.cpi = 1;
+        p.stage_elems = static_cast<int>(p.ipc * item_elems);
+        p.xs_elems = p.ipc * cols;
+        p.n_units = (g.batch + p.ipc - 1) / p.ipc;
+    } else {
+        if ((rows & 1) && (cols & 1)) return false;  // items would start on 8-byte boundaries
+        p.split = 1;
+        p.ipc = 1;
+        p.cpc = kChunkElems / rows;
+        if (rows & 1) p.cpc &= ~1;
+        if (p.cpc < 1) return false;
+        p.cpi = (cols + p.cpc - 1) / p.cpc;
+        p.stage_elems = p.cpc * rows;
+        p.xs_elems = cols;
+        p.n_units = g.batch;
+    }
+    p.stage_elems = (p.stage_elems + 15) & ~15;  // keep every stage 128-byte aligned
+    p.xs_elems = (p.xs_elems + 1) & ~1;
+    const size_t fixed = static_cast<size_t>(kConsumerWarps) * p.xs_elems * sizeof(double) + 2 * kMaxStages * sizeof(uint64_t);
+    const size_t budget = 220 * 1024;
+    if (fixed + 2 * p.stage_elems * sizeof(double) > budget) return false;
+    p.stages = static_cast<int>((budget - fixed) / (p.stage_elems * sizeof(double)));
+    if (p.stages > kMaxStages) p.stages = kMaxStages;
+    const size_t smem = static_cast<size_t>(p.stages) * p.stage_elems * sizeof(double) + fixed;
+    int grid = ctx->sm_count;
+    if (p.n_units < grid) grid = static_cast<int>(p.n_units);
+
+    if (V == 2) {
+        switch (RT) {
+            case 1: launch_t<2, 1>(ctx, g, p, grid, smem); break;
+            case 2: launch_t<2, 2>(ctx, g, p, grid, smem); break;
+            case 3: launch_t<2, 3>(ctx, g, p, grid, smem); break;
+            default: launch_t<2, 4>(ctx, g, p, grid, smem); break;
+        }
+    } else {
+        switch (RT) {
+            case 1: launch_t<1, 1>(ctx, g, p, grid, smem); break;
+            case 2: launch_t<1, 2>(ctx, g, p, grid, smem); break;
+            case 3: launch_t<1, 3>(ctx, g, p, grid, smem); break;
+            default: launch_t<1, 4>(ctx, g, p, grid, smem); break;
+        }
+    }
+    return true;
+}
+
+}  // namespace hdgb

@@ -26,6 +26,15 @@ struct GemvArgs {
     double alpha = 1.0, beta = 0.0;
 };
 void launch_team_gemv(hdgb_ctx* ctx, const GemvArgs& g);
+// Persistent TMA-pipelined variant for large streams (k_stream_gemv.cu); false = shape not handled.
+bool launch_stream_gemv(hdgb_ctx* ctx, const GemvArgs& g);
+
+// Process-wide tuning knobs (hdgb_set_tuning): A/B switches for benchmarks and tests.
+struct Tuning {
+    int use_stream = 1;                  // route large GEMVs through the TMA stream kernel
+    int64_t stream_min_elems = 1 << 18;  // below this many matrix entries the team kernel is used
+};
+Tuning& tuning();
 
 // z_f[i] = ze[e0][l0][i] + ze[e1][l1][i]   (apply_asm scatter as an atomics-free face gather)
 // sides = 1 keeps only the owner's (side-0) term: the restricted (RAS) prolongation.

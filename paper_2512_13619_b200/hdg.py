@@ -33,7 +33,7 @@ __all__ = [
     "assemble_residual", "gather_element_trace", "recover_local", "assemble_global", "block_matvec",
     "gather_extended", "write_matrix", "read_matrix", "build_preconditioner", "leja_order",
     "harmonic_ritz_from_hessenberg", "gmres_solve", "orthogonalize", "newton_solve", "time_march",
-    "make_case_model", "make_initial_state", "library_path", "load_library", "random_vector",
+    "make_case_model", "make_initial_state", "library_path", "load_library", "random_vector", "set_tuning",
     "SHAPES", "MODELS", "PRECONDS",
 ]
 
@@ -176,6 +176,7 @@ def load_library():
         "hdgb_last_error_index": (i64, [_vp]), "hdgb_ctx_set_stream": (i, [_vp, _vp]), "hdgb_ctx_stream": (_vp, [_vp]),
         "hdgb_ctx_synchronize": (i, [_vp]), "hdgb_ctx_launch_count": (i64, [_vp]),
         "hdgb_ctx_reset_launch_count": (None, [_vp]), "hdgb_version": (cp, []),
+        "hdgb_set_tuning": (i, [cp, i64]),
         "hdgb_lu_invert_batch": (i, [_vp, i, i, _vp, _vp]),
         "hdgb_gemm_batch": (i, [_vp, i, i, i, _vp, i, i, i, _vp, i, _vp]),
         "hdgb_gemv_strided_batch": (i, [_vp, i, i, i, _vp, _vp, _vp, i]),
@@ -228,6 +229,12 @@ def load_library():
     L._signatures = sig
     _lib = L
     return L
+
+
+def set_tuning(key: str, value: int):
+    """Kernel-selection knobs (hdgb_set_tuning): 'use_stream', 'stream_min_elems'."""
+    if load_library().hdgb_set_tuning(key.encode(), int(value)) != 0:
+        raise KeyError(key)
 
 
 def exported_symbols():
