@@ -4,14 +4,15 @@
 //
 // The batched block rows of a DenseBatch are ONE contiguous array (dense_batch.hpp:12-34), so the
 // kernel treats the matrix data as a byte stream: a persistent CTA per SM owns a contiguous range
-// of items and pulls it through a ring of shared-memory stages with 1D bulk TMA copies
-// (cp.async.bulk ... mbarrier::complete_tx) issued by one producer thread; mbarrier full/empty
-// pairs hand stages to the consumer warps.  Each stage ("chunk") holds either a whole number of
-// small items or a column range of one large item, and is consumed by exactly one warp, which
+// of items and pulls it through shared memory with 1D bulk TMA copies (cp.async.bulk ...
+// mbarrier::complete_tx).  Each warp runs its own ring of stages: lane 0 issues the copy of the
+// warp's next chunk, the warp waits on the stage's mbarrier, multiplies out of shared memory and
+// re-arms the stage -- no CTA-wide barrier anywhere, 8 x 24 KB in flight per SM.  A stage
+// ("chunk") holds either a whole number of small items or a column range of one large item; the warp
 //   * gathers the item's input slice (neighbour slices through the index table, zeros for
 //     kNoFace) into its private shared-memory x buffer while the TMA copy is in flight,
-//   * multiplies out of shared memory (lanes own 1-2 consecutive rows x a column group; 128-bit
-//     LDS when the row count is even) keeping partial sums in registers across the chunks of an item,
+//   * multiplies (lanes own 1-2 consecutive rows x a column group; 128-bit LDS when the row count
+//     is even) keeping partial sums in registers across the chunks of an item,
 //   * combines the column groups with a fixed-order shuffle tree (deterministic) and writes y.
 // HBM sees every matrix byte exactly once, as large sequential bulk reads; x / y traffic is served
 // from L2.  Roofline: HBM.  Algorithmic bytes per item: 8*(rows*cols + cols + rows) + 4*nslots.
@@ -21,10 +22,11 @@ namespace hdgb {
 
 namespace {
 
-constexpr int kConsumerWarps = 8;
-constexpr int kThreads = (kConsumerWarps + 1) * 32;
-constexpr int kMaxStages = 8;
-constexpr int kChunkElems = 3072;  // 24 KB per stage
+constexpr int kWarps = 8;           // each warp runs its own TMA ring: issue -> wait -> multiply -> re-issue
+constexpr int kThreads = kWarps * 32;
+constexpr int kMaxStages = 16;      // kWarps rings of stages / kWarps stages each
+constexpr size_t kSmemBudget = 216 * 1024;
+constexpr size_t kWarpBudget = kSmemBudget / kWarps;  // stage(s) + x buffer + index buffer of one warp
 
 struct StreamPlan {
     int rows, cols;
@@ -34,6 +36,7 @@ struct StreamPlan {
     int cpi;              // chunks per item (split)
     int stages;
     int xs_elems;         // per-warp x buffer (doubles)
+    int is_elems;         // per-warp index buffer (ints, multiple of 2)
     int stage_elems;      // doubles per stage
     int64_t batch;
     int64_t n_units;      // grouped: chunks; split: items
@@ -108,80 +111,118 @@ __global__ void __launch_bounds__(kThreads, 1) stream_gemv_kernel(GemvArgs g, St
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* stage_base = reinterpret_cast<double*>(smem_raw);
     double* xs_base = stage_base + static_cast<size_t>(p.stages) * p.stage_elems;
-    uint64_t* full = reinterpret_cast<uint64_t*>(xs_base + static_cast<size_t>(kConsumerWarps) * p.xs_elems);
-    uint64_t* empty = full + kMaxStages;
+    int* is_base = reinterpret_cast<int*>(xs_base + static_cast<size_t>(kWarps) * 2 * p.xs_elems);
+    uint64_t* full = reinterpret_cast<uint64_t*>(is_base + static_cast<size_t>(kWarps) * 3 * p.is_elems);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int rows = p.rows, cols = p.cols;
     const int64_t item_elems = static_cast<int64_t>(rows) * cols;
+    const int SW = p.stages / kWarps;  // stages of this warp's private ring
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < p.stages; ++s) {
-            mbar_init(full + s, 1);
-            mbar_init(empty + s, 1);
-        }
+        for (int s = 0; s < p.stages; ++s) mbar_init(full + s, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
-    // this CTA's contiguous range of units (grouped: chunks, split: items)
+    // this CTA's contiguous range of units (grouped: chunks, split: items); units are dealt to the
+    // warps round-robin and every warp streams ITS chunks through ITS ring, so a waiter is never
+    // more than one mbarrier phase ahead of the copy it waits for.
     const int64_t u0 = p.n_units * blockIdx.x / gridDim.x;
     const int64_t u1 = p.n_units * (blockIdx.x + 1) / gridDim.x;
-    const int64_t n_chunks = p.split ? (u1 - u0) * p.cpi : (u1 - u0);
+    const int64_t my_units = (u1 - u0 > warp) ? (u1 - u0 - warp + kWarps - 1) / kWarps : 0;
+    const int64_t my_chunks = p.split ? my_units * p.cpi : my_units;
+    double* my_stage = stage_base + static_cast<size_t>(warp) * SW * p.stage_elems;
+    uint64_t* my_full = full + warp * SW;
 
-    if (warp == kConsumerWarps) {
-        // ---- producer: one thread streams the CTA's byte range through the stage ring ----
-        if (lane == 0) {
-            for (int64_t k = 0; k < n_chunks; ++k) {
-                const int s = static_cast<int>(k % p.stages);
-                const int64_t use = k / p.stages;
-                if (use > 0) mbar_wait(empty + s, static_cast<uint32_t>((use - 1) & 1));
-                const double* src;
-                int64_t elems;
-                if (p.split) {
-                    const int64_t item = u0 + k / p.cpi;
-                    const int ci = static_cast<int>(k % p.cpi);
-                    const int c0 = ci * p.cpc;
-                    const int nc = min(p.cpc, cols - c0);
-                    src = g.a + item * item_elems + static_cast<int64_t>(c0) * rows;
-                    elems = static_cast<int64_t>(nc) * rows;
-                } else {
-                    const int64_t i0 = (u0 + k) * p.ipc;
-                    int64_t cnt = g.batch - i0 < p.ipc ? g.batch - i0 : p.ipc;
-                    if ((item_elems & 1) && (cnt & 1)) --cnt;  // keep the copy a multiple of 16 bytes; the odd tail item is read directly
-                    src = g.a + i0 * item_elems;
-                    elems = cnt * item_elems;
-                }
-                const uint32_t bytes = static_cast<uint32_t>(elems * sizeof(double));
-                mbar_expect_tx(full + s, bytes);
-                if (bytes) tma_bulk_g2s(stage_base + static_cast<size_t>(s) * p.stage_elems, src, bytes, full + s);
-            }
+    // chunk n of this warp -> global source + size
+    auto issue = [&](int64_t n) {
+        const double* src;
+        int64_t elems;
+        if (p.split) {
+            const int64_t item = u0 + warp + (n / p.cpi) * kWarps;
+            const int ci = static_cast<int>(n % p.cpi);
+            const int c0 = ci * p.cpc;
+            const int nc = min(p.cpc, cols - c0);
+            src = g.a + item * item_elems + static_cast<int64_t>(c0) * rows;
+            elems = static_cast<int64_t>(nc) * rows;
+        } else {
+            const int64_t i0 = (u0 + warp + n * kWarps) * p.ipc;
+            int64_t cnt = g.batch - i0 < p.ipc ? g.batch - i0 : p.ipc;
+            if ((item_elems & 1) && (cnt & 1)) --cnt;  // keep the copy a multiple of 16 bytes; the odd tail item is read directly
+            src = g.a + i0 * item_elems;
+            elems = cnt * item_elems;
         }
-        return;
-    }
+        const int s = static_cast<int>(n % SW);
+        const uint32_t bytes = static_cast<uint32_t>(elems * sizeof(double));
+        // order the warp's earlier generic-proxy reads of this stage before the async-proxy write
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(my_full + s, bytes);
+        if (bytes) tma_bulk_g2s(my_stage + static_cast<size_t>(s) * p.stage_elems, src, bytes, my_full + s);
+    };
+    if (lane == 0)
+        for (int64_t n = 0; n < SW && n < my_chunks; ++n) issue(n);
 
-    // ---- consumers ----
-    double* xs = xs_base + static_cast<size_t>(warp) * p.xs_elems;
+    // per-warp x (double-buffered) and index (triple-buffered) staging, filled with cp.async so the
+    // gather of the NEXT unit runs behind the multiply of the current one
+    double* xs_w = xs_base + static_cast<size_t>(warp) * 2 * p.xs_elems;
+    int* is_w = is_base + static_cast<size_t>(warp) * 3 * p.is_elems;
     const int RL = (rows + V - 1) / V;
     const int CG = RL >= 32 ? 1 : 32 / RL;
     const int cg = RL >= 32 ? 0 : lane / RL;
     const int rl = RL >= 32 ? lane : lane - cg * RL;
     const int nslots = g.idx ? cols / g.width : 0;
 
-    auto gather_x = [&](int64_t item, int c0, int nc, double* dst) {
-        if (g.idx == nullptr) {
-            const double* xb = g.x + item * cols + c0;
-            for (int j = lane; j < nc; j += 32) dst[j] = xb[j];
+    // unit t of this warp -> first item and item count
+    auto unit_items = [&](int64_t t, int64_t& item0, int& cnt) {
+        if (p.split) {
+            item0 = u0 + warp + t * kWarps;
+            cnt = 1;
         } else {
-            const int* ib = g.idx + item * nslots;
-            for (int j = lane; j < nc; j += 32) {
-                const int c = c0 + j;
-                const int sl = c / g.width;
-                const int o = c - sl * g.width;
-                const int src = ib[sl];
-                dst[j] = src < 0 ? 0.0 : g.x[static_cast<int64_t>(src) * g.width + o];
+            item0 = (u0 + warp + t * kWarps) * p.ipc;
+            cnt = static_cast<int>(g.batch - item0 < p.ipc ? g.batch - item0 : p.ipc);
+        }
+    };
+    // pipeline stage 0: index rows of unit t -> is_w[t % 3]   (one cp.async group, possibly empty)
+    auto stage_idx = [&](int64_t t) {
+        if (t < my_units && g.idx != nullptr) {
+            int64_t item0;
+            int cnt;
+            unit_items(t, item0, cnt);
+            const int* ib = g.idx + item0 * nslots;
+            int* dst = is_w + (t % 3) * p.is_elems;
+            const int ts = cnt * nslots;
+            for (int j = lane; j < ts; j += 32)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst + j)), "l"(ib + j) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    // pipeline stage 1: x entries of unit t -> xs_w[t % 2]; needs the unit's index rows in shared memory
+    auto stage_x = [&](int64_t t) {
+        if (t < my_units) {
+            int64_t item0;
+            int cnt;
+            unit_items(t, item0, cnt);
+            double* dst = xs_w + (t % 2) * p.xs_elems;
+            const int total = cnt * cols;
+            if (g.idx == nullptr) {
+                const double* xb = g.x + item0 * cols;
+                for (int j = lane; j < total; j += 32)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst + j)), "l"(xb + j) : "memory");
+            } else {
+                const int* is = is_w + (t % 3) * p.is_elems;
+                for (int j = lane; j < total; j += 32) {
+                    const int it = j / cols, c = j - it * cols;
+                    const int sl = c / g.width;
+                    const int o = c - sl * g.width;
+                    const int src = is[it * nslots + sl];
+                    const double* sp = src < 0 ? g.x : g.x + static_cast<int64_t>(src) * g.width + o;
+                    const int nbytes = src < 0 ? 0 : 8;  // src-size 0 zero-fills: absent neighbour (kNoFace)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst + j)), "l"(sp), "r"(nbytes) : "memory");
+                }
             }
         }
+        asm volatile("cp.async.commit_group;" ::: "memory");
     };
     auto reduce_store = [&](double (&acc)[RT][V], int64_t item) {
         // fixed-order tree over the column groups (lane = cg*RL + rl)
@@ -202,7 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_gemv_kernel(GemvArgs g, St
 #pragma unroll
                 for (int v = 0; v < V; ++v) {
                     const int r = (rl + 32 * t) * V + v;
-                    if (r < rows && (RL >= 32 || rl < RL)) {
+                    if (r < rows) {
                         const int64_t o = item * rows + r;
                         double out = g.alpha * acc[t][v];
                         if (g.z != nullptr) out += g.beta * g.z[o];
@@ -213,64 +254,73 @@ __global__ void __launch_bounds__(kThreads, 1) stream_gemv_kernel(GemvArgs g, St
         }
     };
 
-    if (p.split) {
-        // items are dealt to warps round-robin; a warp keeps its item's partial sums in registers
-        for (int64_t li = warp; li < u1 - u0; li += kConsumerWarps) {
-            const int64_t item = u0 + li;
-            gather_x(item, 0, cols, xs);
-            __syncwarp();
+    stage_idx(0);
+    stage_idx(1);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncwarp();
+    stage_x(0);
+    int64_t n = 0;  // this warp's running chunk counter (TMA ring position)
+    for (int64_t t = 0; t < my_units; ++t) {
+        stage_idx(t + 2);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");  // index rows of t+1 and x of t have landed
+        __syncwarp();
+        stage_x(t + 1);
+        int64_t item0;
+        int cnt;
+        unit_items(t, item0, cnt);
+        const double* xs = xs_w + (t % 2) * p.xs_elems;
+        if (p.split) {
             double acc[RT][V];
 #pragma unroll
-            for (int t = 0; t < RT; ++t)
+            for (int tt = 0; tt < RT; ++tt)
 #pragma unroll
-                for (int v = 0; v < V; ++v) acc[t][v] = 0.0;
-            for (int ci = 0; ci < p.cpi; ++ci) {
-                const int64_t k = li * p.cpi + ci;
-                const int s = static_cast<int>(k % p.stages);
+                for (int v = 0; v < V; ++v) acc[tt][v] = 0.0;
+            for (int ci = 0; ci < p.cpi; ++ci, ++n) {
+                const int s = static_cast<int>(n % SW);
                 const int c0 = ci * p.cpc;
                 const int nc = min(p.cpc, cols - c0);
-                mbar_wait(full + s, static_cast<uint32_t>((k / p.stages) & 1));
-                accumulate<V, RT>(stage_base + static_cast<size_t>(s) * p.stage_elems, xs + c0, rows, nc, rl, cg, CG, acc);
+                mbar_wait(my_full + s, static_cast<uint32_t>((n / SW) & 1));
+                accumulate<V, RT>(my_stage + static_cast<size_t>(s) * p.stage_elems, xs + c0, rows, nc, rl, cg, CG, acc);
                 __syncwarp();
-                if (lane == 0) mbar_arrive(empty + s);
+                if (lane == 0 && n + SW < my_chunks) issue(n + SW);
             }
-            reduce_store(acc, item);
-            __syncwarp();
-        }
-    } else {
-        for (int64_t k = warp; k < n_chunks; k += kConsumerWarps) {
-            const int s = static_cast<int>(k % p.stages);
-            const int64_t i0 = (u0 + k) * p.ipc;
-            const int cnt = static_cast<int>(g.batch - i0 < p.ipc ? g.batch - i0 : p.ipc);
+            reduce_store(acc, item0);
+        } else {
+            const int s = static_cast<int>(n % SW);
             const int cnt_tma = ((item_elems & 1) && (cnt & 1)) ? cnt - 1 : cnt;
-            for (int it = 0; it < cnt; ++it) gather_x(i0 + it, 0, cols, xs + static_cast<size_t>(it) * cols);
-            __syncwarp();
-            mbar_wait(full + s, static_cast<uint32_t>((k / p.stages) & 1));
-            const double* st = stage_base + static_cast<size_t>(s) * p.stage_elems;
+            mbar_wait(my_full + s, static_cast<uint32_t>((n / SW) & 1));
+            const double* st = my_stage + static_cast<size_t>(s) * p.stage_elems;
             for (int it = 0; it < cnt; ++it) {
                 double acc[RT][V];
 #pragma unroll
-                for (int t = 0; t < RT; ++t)
+                for (int tt = 0; tt < RT; ++tt)
 #pragma unroll
-                    for (int v = 0; v < V; ++v) acc[t][v] = 0.0;
+                    for (int v = 0; v < V; ++v) acc[tt][v] = 0.0;
                 if (it < cnt_tma) {
                     accumulate<V, RT>(st + static_cast<size_t>(it) * item_elems, xs + static_cast<size_t>(it) * cols, rows, cols, rl, cg, CG, acc);
                 } else if (V == 1) {
                     // odd tail item that the 16-byte granular copy left out: read it from global memory
-                    accumulate<V, RT>(g.a + (i0 + it) * item_elems, xs + static_cast<size_t>(it) * cols, rows, cols, rl, cg, CG, acc);
+                    accumulate<V, RT>(g.a + (item0 + it) * item_elems, xs + static_cast<size_t>(it) * cols, rows, cols, rl, cg, CG, acc);
                 }
-                reduce_store(acc, i0 + it);
+                reduce_store(acc, item0 + it);
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(empty + s);
+            if (lane == 0 && n + SW < my_chunks) issue(n + SW);
+            ++n;
         }
+        __syncwarp();
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 template <int V, int RT>
 void launch_t(hdgb_ctx* ctx, const GemvArgs& g, const StreamPlan& p, int grid, size_t smem) {
     auto kern = stream_gemv_kernel<V, RT>;
-    HDGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    static size_t configured = 0;  // per instantiation
+    if (smem > configured) {
+        HDGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        configured = smem;
+    }
     kern<<<grid, kThreads, smem, ctx->stream>>>(g, p);
     HDGB_LAUNCH_CHECK(ctx);
 }
@@ -297,9 +347,13 @@ bool launch_stream_gemv(hdgb_ctx* ctx, const GemvArgs& g) {
     p.rows = rows;
     p.cols = cols;
     p.batch = g.batch;
-    if (item_elems <= kChunkElems) {
+    const int nslots = g.idx ? cols / g.width : 0;
+    // per-warp shared memory: one or more stages + the x slice(s) + the index row(s)
+    const size_t per_item = static_cast<size_t>(item_elems + 2 * cols) * sizeof(double) + 3 * static_cast<size_t>(nslots) * sizeof(int) + 8;
+    if (per_item + 128 <= kWarpBudget) {
         p.split = 0;
-        p.ipc = static_cast<int>(kChunkElems / item_elems);
+        p.ipc = static_cast<int>((kWarpBudget - 128) / per_item);
+        if (p.ipc > 64) p.ipc = 64;
         if ((item_elems & 1) && (p.ipc & 1)) {
             if (p.ipc == 1) return false;
             --p.ipc;
@@ -308,26 +362,37 @@ bool launch_stream_gemv(hdgb_ctx* ctx, const GemvArgs& g) {
         p.cpi = 1;
         p.stage_elems = static_cast<int>(p.ipc * item_elems);
         p.xs_elems = p.ipc * cols;
+        p.is_elems = p.ipc * nslots;
         p.n_units = (g.batch + p.ipc - 1) / p.ipc;
     } else {
         if ((rows & 1) && (cols & 1)) return false;  // items would start on 8-byte boundaries
         p.split = 1;
         p.ipc = 1;
-        p.cpc = kChunkElems / rows;
+        p.xs_elems = cols;
+        p.is_elems = nslots;
+        const size_t side = 2 * static_cast<size_t>(cols) * sizeof(double) + 3 * static_cast<size_t>(nslots) * sizeof(int) + 32;
+        if (side + 4096 > kWarpBudget) return false;
+        const size_t left = kWarpBudget - 128 - side;
+        p.cpc = static_cast<int>(left / (static_cast<size_t>(rows) * sizeof(double)));
+        if (p.cpc > cols) p.cpc = cols;
         if (rows & 1) p.cpc &= ~1;
         if (p.cpc < 1) return false;
         p.cpi = (cols + p.cpc - 1) / p.cpc;
+        int bal = (cols + p.cpi - 1) / p.cpi;  // balance the chunks of an item
+        if ((rows & 1) && (bal & 1)) ++bal;
+        if (bal <= p.cpc) p.cpc = bal;
+        p.cpi = (cols + p.cpc - 1) / p.cpc;
         p.stage_elems = p.cpc * rows;
-        p.xs_elems = cols;
         p.n_units = g.batch;
     }
     p.stage_elems = (p.stage_elems + 15) & ~15;  // keep every stage 128-byte aligned
     p.xs_elems = (p.xs_elems + 1) & ~1;
-    const size_t fixed = static_cast<size_t>(kConsumerWarps) * p.xs_elems * sizeof(double) + 2 * kMaxStages * sizeof(uint64_t);
-    const size_t budget = 220 * 1024;
-    if (fixed + 2 * p.stage_elems * sizeof(double) > budget) return false;
-    p.stages = static_cast<int>((budget - fixed) / (p.stage_elems * sizeof(double)));
+    p.is_elems = (p.is_elems + 1) & ~1;
+    const size_t fixed = static_cast<size_t>(kWarps) * (2 * p.xs_elems * sizeof(double) + 3 * p.is_elems * sizeof(int)) + kMaxStages * sizeof(uint64_t);
+    if (fixed + kWarps * p.stage_elems * sizeof(double) > kSmemBudget + 4096) return false;
+    p.stages = static_cast<int>((kSmemBudget + 4096 - fixed) / (p.stage_elems * sizeof(double)));
     if (p.stages > kMaxStages) p.stages = kMaxStages;
+    p.stages -= p.stages % kWarps;
     const size_t smem = static_cast<size_t>(p.stages) * p.stage_elems * sizeof(double) + fixed;
     int grid = ctx->sm_count;
     if (p.n_units < grid) grid = static_cast<int>(p.n_units);

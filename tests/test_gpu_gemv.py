@@ -9,7 +9,9 @@ import paper_2512_13619_b200 as hdg
 pytestmark = pytest.mark.gpu
 
 SHAPES = [(3, 21, 1001), (5, 25, 333), (16, 176, 97), (18, 126, 41), (80, 880, 5), (12, 12, 515), (15, 15, 77),
-          (96, 96, 9), (72, 72, 13), (16, 16, 1000), (27, 27, 30), (9, 63, 201), (64, 64, 7), (130, 40, 6), (7, 7, 1)]
+          (96, 96, 9), (72, 72, 13), (16, 16, 1000), (27, 27, 30), (9, 63, 201), (64, 64, 7), (130, 40, 6), (7, 7, 1),
+          # long streams: every warp's TMA ring wraps many times
+          (16, 176, 6000), (96, 96, 3000), (3, 21, 150001), (64, 96, 4001), (5, 25, 40003), (18, 126, 5000)]
 
 
 @pytest.fixture(params=["team", "stream"])
@@ -38,7 +40,8 @@ def test_gemv_strided_batch(ctx, kernel, rows, cols, batch):
     assert np.max(np.abs(got.reshape(batch, rows) - (want + y0))) <= bound + 1e-15
 
 
-@pytest.mark.parametrize("mpf,n_lfe,nf", [(3, 4, 501), (5, 3, 333), (16, 6, 131), (18, 4, 57), (80, 6, 9), (1, 4, 50)])
+@pytest.mark.parametrize("mpf,n_lfe,nf", [(3, 4, 501), (5, 3, 333), (16, 6, 131), (18, 4, 57), (80, 6, 9), (1, 4, 50),
+                                          (16, 6, 7000), (3, 4, 120001), (80, 6, 300)])
 def test_block_matvec_gather(ctx, kernel, mpf, n_lfe, nf):
     rng = np.random.default_rng(mpf * 100 + nf)
     nb = 2 * n_lfe - 1
