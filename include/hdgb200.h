@@ -326,6 +326,50 @@ hdgb_status hdgb_time_march(hdgb_disc* d, const hdgb_model* m, hdgb_state* s, do
                             const hdgb_newton_config* ncfg, const hdgb_gmres_config* gcfg,
                             const hdgb_precond_spec* pspec, hdgb_solve_report* reports);
 
+/* ---- multi-GPU: domain decomposition (north_star item 5; the reference has no distributed path,
+ * PAPER.md:1122 lists it as future work) -------------------------------------------------------
+ * One rank per GPU.  A rank's discretisation holds its owned elements first, then one layer of
+ * ghost elements (condensed redundantly); its faces are numbered owned first (a face belongs to
+ * the rank owning its side-0 element, the reference's own accumulation order, mesh.cpp:63-71),
+ * then halo faces grouped by owner.  Vectors span all local faces; rows, dot products and norms
+ * cover owned faces only.  Per operator application one halo exchange of interface trace slices,
+ * per Gram-Schmidt pass one small all-reduce. */
+/* Discretisation from explicit connectivity tables (a sub-domain cut out of a global mesh keeps the
+ * global orientation flags / side assignment).  face_to_elements entries: >= 0 local element, -1
+ * domain boundary, -2 element on another rank.  The first ne_owned elements / nf_owned faces are
+ * owned.  face_gid (nf, may be NULL = identity) / nf_global give the global face numbering used
+ * for the seeded Ritz start vector.  ctx == NULL: host-only tables. */
+hdgb_status hdgb_disc_create_from_tables(hdgb_ctx* ctx, int shape, int degree, int n_comp, int quad_points,
+                                         int ne, int nf, int nv, const int32_t* elem_verts,
+                                         const double* vertex_coords, const int32_t* element_to_face,
+                                         const int32_t* face_to_elements, const int32_t* face_local_index,
+                                         const int32_t* face_orient, const int32_t* face_vertices,
+                                         const int32_t* boundary_tag, int ne_owned, int nf_owned,
+                                         const int64_t* face_gid, int64_t nf_global, hdgb_disc** out);
+/* Connectivity of a conforming mesh given by element vertex lists (host only, no geometry, no
+ * GPU): the tables a partitioner slices.  Read them with hdgb_disc_get_i32. */
+hdgb_status hdgb_mesh_connectivity(int shape, int ne, int nv, const int32_t* elem_verts,
+                                   const double* vertex_coords, hdgb_disc** out);
+/* NCCL communicator over the ranks of one job; unique_id (128 bytes) comes from
+ * hdgb_comm_nccl_unique_id on rank 0 and is broadcast by the caller (torch.distributed / MPI). */
+hdgb_status hdgb_comm_nccl_unique_id(void* out128);
+hdgb_status hdgb_comm_create_nccl(hdgb_ctx* ctx, const void* unique_id_128, int rank, int size);
+/* Halo plan of this rank: for neighbour k, send the listed local (owned) faces and receive
+ * recv_counts[k] faces into local face positions recv_offsets[k].. (contiguous per owner). */
+hdgb_status hdgb_comm_set_halo_plan(hdgb_ctx* ctx, int n_nbr, const int32_t* nbr_ranks, const int32_t* send_counts,
+                                    const int32_t* send_ids /*concatenated*/, const int32_t* recv_offsets,
+                                    const int32_t* recv_counts);
+/* Callback communicator (tests: several virtual ranks in one process on one GPU). */
+typedef int (*hdgb_halo_fn)(void* user, double* dev_vec, int width);
+typedef int (*hdgb_allreduce_fn)(void* user, double* dev_buf, int n);
+hdgb_status hdgb_comm_set_callbacks(hdgb_ctx* ctx, int rank, int size, hdgb_halo_fn halo, hdgb_allreduce_fn allreduce,
+                                    void* user);
+void hdgb_comm_destroy(hdgb_ctx* ctx);
+hdgb_status hdgb_halo_exchange(hdgb_ctx* ctx, double* dev_vec, int width);
+hdgb_status hdgb_allreduce_sum(hdgb_ctx* ctx, double* dev_buf, int n);
+int hdgb_comm_rank(const hdgb_ctx* ctx);
+int hdgb_comm_size(const hdgb_ctx* ctx);
+
 /* ---- device vector helpers used by callers that keep data resident --------------------------- */
 hdgb_status hdgb_device_alloc(hdgb_ctx* ctx, int64_t n_doubles, double** out);
 void hdgb_device_free(hdgb_ctx* ctx, double* p);

@@ -29,6 +29,11 @@ void finish_disc(hdgb_ctx* c, hdgb_disc* d, int n_comp) {
     v.D = m.dim; v.M = n_comp; v.ne = m.ne; v.nf = m.nf; v.n_lfe = m.n_lfe; v.n_orient = me.n_orient;
     v.pe = me.pe; v.pf = me.pf; v.qe = me.qe; v.qf = me.qf;
     v.npe = n_comp * me.pe; v.mpf = n_comp * me.pf; v.nfl = m.n_lfe * v.mpf; v.nfs = m.n_lfe * me.pf;
+    if (d->ne_owned < 0) d->ne_owned = m.ne;
+    if (d->nf_owned < 0) d->nf_owned = m.nf;
+    v.ne_owned = d->ne_owned;
+    v.nf_owned = d->nf_owned;
+    if (d->nf_global < 0) d->nf_global = m.nf;
     if (!c) return;  // host-only discretisation: tables for inspection, no device state
     upload(c, d->elem_faces, m.elem_faces);
     upload(c, d->elem_side, m.elem_side);
@@ -142,6 +147,46 @@ hdgb_status hdgb_disc_create_from_mesh(hdgb_ctx* c, int shape, int degree, int n
         d->me = make_master_element(shape, degree, quad_points);
         d->mesh = build_mesh_from_elements(shape, ne, nv, elem_verts, vertex_coords);
         finish_disc(c, d, n_comp);
+    });
+    if (st != HDGB_OK) { delete d; return st; }
+    *out = d;
+    return HDGB_OK;
+}
+
+hdgb_status hdgb_disc_create_from_tables(hdgb_ctx* c, int shape, int degree, int n_comp, int quad_points, int ne, int nf,
+                                         int nv, const int32_t* elem_verts, const double* vertex_coords,
+                                         const int32_t* element_to_face, const int32_t* face_to_elements,
+                                         const int32_t* face_local_index, const int32_t* face_orient,
+                                         const int32_t* face_vertices, const int32_t* boundary_tag, int ne_owned,
+                                         int nf_owned, const int64_t* face_gid, int64_t nf_global, hdgb_disc** out) {
+    *out = nullptr;
+    hdgb_disc* d = new hdgb_disc();
+    hdgb_status st = guarded(c, [&] {
+        if (ne_owned < 0 || ne_owned > ne || nf_owned < 0 || nf_owned > nf)
+            throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: owned element / face counts");
+        d->me = make_master_element(shape, degree, quad_points);
+        d->mesh = mesh_from_tables(shape, ne, nf, nv, elem_verts, vertex_coords, element_to_face, face_to_elements,
+                                   face_local_index, face_orient, face_vertices, boundary_tag);
+        d->ne_owned = ne_owned;
+        d->nf_owned = nf_owned;
+        if (face_gid) d->face_gid.assign(face_gid, face_gid + nf);
+        d->nf_global = face_gid ? nf_global : nf;
+        finish_disc(c, d, n_comp);
+    });
+    if (st != HDGB_OK) { delete d; return st; }
+    *out = d;
+    return HDGB_OK;
+}
+
+hdgb_status hdgb_mesh_connectivity(int shape, int ne, int nv, const int32_t* elem_verts, const double* vertex_coords,
+                                   hdgb_disc** out) {
+    *out = nullptr;
+    hdgb_disc* d = new hdgb_disc();
+    hdgb_status st = guarded(nullptr, [&] {
+        d->mesh = build_mesh_from_elements(shape, ne, nv, elem_verts, vertex_coords);
+        hdgb_dims& dm = d->dims;
+        dm.dim = d->mesh.dim; dm.shape = shape; dm.ne = d->mesh.ne; dm.nf = d->mesh.nf; dm.n_lfe = d->mesh.n_lfe; dm.nv = nv;
+        dm.n_comp = 1;
     });
     if (st != HDGB_OK) { delete d; return st; }
     *out = d;
@@ -392,11 +437,13 @@ double assemble_residual_device(hdgb_disc* d, const hdgb_model* m, hdgb_state* s
     lo.ru = interior;
     lo.ruhat_e = d->res_ruhat_e.p;
     run_assemble(d, m, s, u_prev_dev, transient ? 1.0 / dt : 0.0, 0, v.ne, lo, false);
-    // face assembly of the trace residual (local_ops.cpp:439-447), side 0 then side 1
-    launch_face_sum(c, d->res_ruhat_e.p, v.face_elems, v.face_lidx, v.nf, v.mpf, v.n_lfe, trace);
-    // residual_norm (local_ops.cpp:245-250)
-    launch_sumsq(c, trace, static_cast<int64_t>(n_tr), d->res_sums.p, d->res_partial.p);
-    launch_sumsq(c, interior, static_cast<int64_t>(n_int), d->res_sums.p + 1, d->res_partial.p);
+    // face assembly of the trace residual (local_ops.cpp:439-447), side 0 then side 1; owned faces
+    // have both sides local (the ghost layer is assembled redundantly)
+    launch_face_sum(c, d->res_ruhat_e.p, v.face_elems, v.face_lidx, v.nf_owned, v.mpf, v.n_lfe, trace);
+    // residual_norm (local_ops.cpp:245-250) over owned faces / elements (+ all-reduce across ranks)
+    launch_sumsq(c, trace, static_cast<int64_t>(v.mpf) * v.nf_owned, d->res_sums.p, d->res_partial.p);
+    launch_sumsq(c, interior, static_cast<int64_t>(v.npe) * v.ne_owned, d->res_sums.p + 1, d->res_partial.p);
+    if (c->comm) c->comm->allreduce(c, d->res_sums.p, 2);
     double h[2];
     HDGB_CUDA(cudaMemcpyAsync(h, d->res_sums.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
     HDGB_CUDA(cudaStreamSynchronize(c->stream));

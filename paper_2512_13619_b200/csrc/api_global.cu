@@ -16,6 +16,8 @@ namespace hdgb {
 void matvec_device(hdgb_matrix* k, const double* x, double* y) {
     // block_matvec (face_matrix.cpp:83-107) with gather_extended (:63-81) fused into the GEMV:
     // the nb neighbour slices are staged in shared memory, the block row is streamed once.
+    // Domain decomposition: the halo part of x is refreshed from its owners first.
+    if (k->ctx->comm) k->ctx->comm->halo(k->ctx, const_cast<double*>(x), k->mpf());
     GemvArgs g;
     g.a = k->blocks.p;
     g.x = x;
@@ -48,12 +50,15 @@ void apply_base_device(hdgb_precond* p, const double* y, double* z) {
             // apply_asm (preconditioner.cpp:86-105): gather_element_trace fused into the element
             // solve, then the scatter-add written as an atomics-free face gather (side 0 first).
             const DiscView& v = p->disc->view;
+            // domain decomposition: ghost elements are solved redundantly, so y is needed on every
+            // local face; a shared face then finds both sides' corrections locally
+            if (c->comm) c->comm->halo(c, const_cast<double*>(y), v.mpf);
             GemvArgs g;
             g.a = p->asm_inv.p; g.x = y; g.y = p->ze.p;
             g.rows = v.nfl; g.cols = v.nfl; g.batch = v.ne;
             g.idx = v.elem_faces; g.width = v.mpf; g.comp = 1;
             launch_team_gemv(c, g);
-            launch_face_sum(c, p->ze.p, v.face_elems, v.face_lidx, v.nf, v.mpf, v.n_lfe, z,
+            launch_face_sum(c, p->ze.p, v.face_elems, v.face_lidx, v.nf_owned, v.mpf, v.n_lfe, z,
                             p->kind == HDGB_PC_RAS ? 1 : 2);
             break;
         }
@@ -111,19 +116,32 @@ static std::vector<std::complex<double>> harmonic_ritz_device(hdgb_precond* p, h
     hdgb_ctx* c = p->ctx;
     const int64_t n = k->n_dof();
     if (degree < 1) throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: polynomial degree must be >= 1");
-    if (degree > n) throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: polynomial degree exceeds the operator dimension");
+    // Seeded start vector over the GLOBAL unknowns (preconditioner.cpp:128-132); a rank keeps the
+    // entries of its local faces, so the sequence does not depend on the partition.
+    const int mpf = k->mpf();
+    const int64_t ld = k->n_local();
+    const int64_t n_global = p->disc && !p->disc->face_gid.empty() ? p->disc->nf_global * mpf : n;
+    if (degree > n_global) throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: polynomial degree exceeds the operator dimension");
     std::mt19937_64 rng(seed);
-    std::vector<double> v0(n);
-    for (double& x : v0) x = 2.0 * (static_cast<double>(rng() >> 11) * 0x1p-53) - 1.0;
+    std::vector<double> vg(n_global);
+    for (double& x : vg) x = 2.0 * (static_cast<double>(rng() >> 11) * 0x1p-53) - 1.0;
     double acc = 0.0;
-    for (double x : v0) acc += x * x;  // same ascending order as the reference's dot
+    for (double x : vg) acc += x * x;  // same ascending order as the reference's dot
     const double nv = std::sqrt(acc);
-    for (double& x : v0) x /= nv;
+    std::vector<double> v0(ld, 0.0);
+    if (n_global == n && ld == n) {
+        for (int64_t i = 0; i < n; ++i) v0[i] = vg[i] / nv;
+    } else {
+        for (int f = 0; f < k->nf_local; ++f) {
+            const int64_t gf = p->disc->face_gid[f];
+            for (int r = 0; r < mpf; ++r) v0[static_cast<int64_t>(f) * mpf + r] = vg[gf * mpf + r] / nv;
+        }
+    }
 
     const int pmax = degree;
-    DevBuf<double> basis(static_cast<size_t>(pmax) * n), w(n), kv(n), sc(4);
+    DevBuf<double> basis(static_cast<size_t>(pmax) * ld), w(ld), kv(ld), sc(pmax + 4);
     DevBuf<double> partial(multi_dot_workspace_doubles(n, 1));
-    HDGB_CUDA(cudaMemcpyAsync(basis.p, v0.data(), n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    HDGB_CUDA(cudaMemcpyAsync(basis.p, v0.data(), ld * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     std::vector<double> hess(static_cast<size_t>(pmax + 1) * pmax, 0.0);
     auto h = [&](int i, int j) -> double& { return hess[static_cast<size_t>(j) * (pmax + 1) + i]; };
     auto fetch = [&](const double* dev) {
@@ -132,28 +150,35 @@ static std::vector<std::complex<double>> harmonic_ritz_device(hdgb_precond* p, h
         HDGB_CUDA(cudaStreamSynchronize(c->stream));
         return v;
     };
+    auto reduce = [&](double* dev, int cnt) { if (c->comm) c->comm->allreduce(c, dev, cnt); };
     int p_eff = 0;
     double scale = 1.0;
+    std::vector<double> col(pmax + 2);
     for (int j = 0; j < pmax; ++j) {
-        matvec_device(k, basis.p + static_cast<size_t>(j) * n, kv.p);
+        matvec_device(k, basis.p + static_cast<size_t>(j) * ld, kv.p);
         apply_base_device(p, kv.p, w.p);
         if (j == 0) {
             launch_sumsq(c, w.p, n, sc.p, partial.p);
+            reduce(sc.p, 1);
             scale = std::max(1.0, std::sqrt(fetch(sc.p)));
         }
         for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt (preconditioner.cpp:146-150)
-            const double* vi = basis.p + static_cast<size_t>(i) * n;
-            launch_multi_dot(c, vi, n, 1, w.p, n, sc.p, partial.p);
-            launch_multi_axpy(c, vi, n, 1, sc.p, -1.0, w.p, n, nullptr, partial.p);
-            h(i, j) = fetch(sc.p);
+            const double* vi = basis.p + static_cast<size_t>(i) * ld;
+            launch_multi_dot(c, vi, ld, 1, w.p, n, sc.p + i, partial.p);
+            reduce(sc.p + i, 1);
+            launch_multi_axpy(c, vi, ld, 1, sc.p + i, -1.0, w.p, n, nullptr, partial.p);
         }
-        launch_sumsq(c, w.p, n, sc.p + 1, partial.p);
-        const double hn = std::sqrt(fetch(sc.p + 1));
+        launch_sumsq(c, w.p, n, sc.p + j + 1, partial.p);
+        reduce(sc.p + j + 1, 1);
+        HDGB_CUDA(cudaMemcpyAsync(col.data(), sc.p, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        HDGB_CUDA(cudaStreamSynchronize(c->stream));
+        for (int i = 0; i <= j; ++i) h(i, j) = col[i];
+        const double hn = std::sqrt(col[j + 1]);
         h(j + 1, j) = hn;
         p_eff = j + 1;
         if (!std::isfinite(hn)) throw Failure(HDGB_ERR_NAN_DETECTED, "NaN detected in harmonic Ritz Arnoldi");
         if (hn < 1e-14 * scale) break;
-        if (j + 1 < pmax) launch_scale_dev(c, w.p, sc.p + 1, 0, basis.p + static_cast<size_t>(j + 1) * n, n);
+        if (j + 1 < pmax) launch_scale_dev(c, w.p, sc.p + j + 1, 0, basis.p + static_cast<size_t>(j + 1) * ld, n);
     }
     HDGB_CUDA(cudaStreamSynchronize(c->stream));
     if (breakdown_out) *breakdown_out = p_eff < pmax;
@@ -185,7 +210,9 @@ hdgb_precond* build_preconditioner_spec(hdgb_matrix* k, const hdgb_ops* o, hdgb_
     p->kind = spec.kind;
     p->mpf = k->mpf();
     p->nf = k->nf;
+    p->nf_local = k->nf_local;
     p->n_lfe = k->n_lfe;
+    p->disc = d;
     const int64_t n = k->n_dof();
     switch (spec.kind) {
         case HDGB_PC_IDENTITY: break;
@@ -202,12 +229,17 @@ hdgb_precond* build_preconditioner_spec(hdgb_matrix* k, const hdgb_ops* o, hdgb_
             // build_asm (preconditioner.cpp:54-84)
             if (!o || !d) throw Failure(HDGB_ERR_GENERIC, "build_asm needs the element operators and the discretisation");
             const DiscView& v = d->view;
-            if (v.mpf != p->mpf || v.nf != p->nf)
+            if (v.mpf != p->mpf || v.nf_owned != p->nf)
                 throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: build_asm matrix / mesh");
-            p->disc = d;
             p->ne = v.ne;
             p->asm_inv.alloc(static_cast<size_t>(v.nfl) * v.nfl * v.ne);
-            launch_asm_enrich(c, v, o->kbar.p, p->asm_inv.p);
+            // The enriched diagonal sub-block of a face (both sides' K-bar_ll summed, side 0 first,
+            // preconditioner.cpp:59-75) IS the face's self block K_ff of the assembled operator; halo
+            // faces receive theirs from the owner, so ghost elements are enriched without a 2nd layer.
+            DevBuf<double> diag(static_cast<size_t>(p->mpf) * p->mpf * v.nf);
+            launch_extract_diag(c, k->blocks.p, k->nf, p->mpf, k->nb(), diag.p);
+            if (c->comm) c->comm->halo(c, diag.p, p->mpf * p->mpf);
+            launch_asm_enrich(c, v, o->kbar.p, diag.p, p->asm_inv.p);
             device_lu_invert(c, v.nfl, v.ne, p->asm_inv.p, p->asm_inv.p, "build_asm (element block)", HDGB_ERR_SINGULAR_BLOCK);
             p->ze.alloc(static_cast<size_t>(v.nfl) * v.ne);
             break;
@@ -216,7 +248,8 @@ hdgb_precond* build_preconditioner_spec(hdgb_matrix* k, const hdgb_ops* o, hdgb_
     }
     if (spec.poly_degree > 0) {
         const int degree = static_cast<int>(std::min<int64_t>(spec.poly_degree, n));  // newton.cpp:41
-        p->wq.alloc(n); p->wt.alloc(n); p->ws.alloc(n); p->wkv.alloc(n);
+        const int64_t ld = k->n_local();
+        p->wq.alloc(ld); p->wt.alloc(ld); p->ws.alloc(ld); p->wkv.alloc(ld);
         bool breakdown = false;
         std::vector<std::complex<double>> th = harmonic_ritz_device(p.get(), k, degree, spec.ritz_seed, &breakdown);
         p->poly_kind = spec.poly_kind;
@@ -236,13 +269,17 @@ hdgb_matrix* assemble_global_device(hdgb_disc* d, const hdgb_ops* o) {
     k->m = v.M;  // the reference leaves m = 1 (face_matrix.hpp:27); identical for its scalar models
     k->pf = v.pf;
     k->n_lfe = v.n_lfe;
-    k->nf = v.nf;
+    k->nf = v.nf_owned;   // rows: owned faces (both adjacent elements are local)
+    k->nf_local = v.nf;   // vectors: all local faces
     const size_t row = static_cast<size_t>(v.mpf) * v.mpf * k->nb();
-    k->blocks.alloc(row * v.nf);
+    k->blocks.alloc(row * k->nf);
     k->rhs.alloc(static_cast<size_t>(v.mpf) * v.nf);
-    k->nbr32.alloc(static_cast<size_t>(v.nf) * k->nb());
-    launch_fill_neighbors(c, v, k->nbr32.p);
-    launch_assemble_global(c, v, o->kbar.p, o->rbar.p, k->blocks.p, k->rhs.p);
+    k->rhs.zero(c->stream);
+    k->nbr32.alloc(static_cast<size_t>(k->nf) * k->nb());
+    DiscView rows = v;
+    rows.nf = k->nf;
+    launch_fill_neighbors(c, rows, k->nbr32.p);
+    launch_assemble_global(c, rows, o->kbar.p, o->rbar.p, k->blocks.p, k->rhs.p);
     return k.release();
 }
 
@@ -286,7 +323,7 @@ hdgb_status hdgb_matrix_create(hdgb_ctx* c, int m, int pf, int n_lfe, int nf, co
         if (m < 1 || pf < 1 || n_lfe < 1 || nf < 0)
             throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: invalid face-block matrix dimensions");
         std::unique_ptr<hdgb_matrix> k(new hdgb_matrix());
-        k->ctx = c; k->m = m; k->pf = pf; k->n_lfe = n_lfe; k->nf = nf;
+        k->ctx = c; k->m = m; k->pf = pf; k->n_lfe = n_lfe; k->nf = nf; k->nf_local = nf;
         const size_t nn = static_cast<size_t>(nf) * k->nb();
         k->neighbor.assign(neighbor, neighbor + nn);
         std::vector<int> h32(nn);
@@ -333,7 +370,7 @@ double* hdgb_matrix_rhs(hdgb_matrix* k) { return k->rhs.p; }
 hdgb_status hdgb_block_matvec(hdgb_matrix* k, const double* x, double* y) {
     hdgb_ctx* c = k->ctx;
     return guarded(c, [&] {
-        const size_t n = k->n_dof();
+        const size_t n = k->n_local();
         InArg X(c, x, n);
         OutArg Y(c, y, n);
         matvec_device(k, X.dev, Y.dev);
@@ -457,7 +494,7 @@ hdgb_status hdgb_precond_set_ritz(hdgb_precond* p, const double* reim, int count
     return guarded(p->ctx, [&] {
         p->ritz.assign(reim, reim + 2 * static_cast<size_t>(count));
         p->poly_degree = count;
-        const size_t n = static_cast<size_t>(p->mpf) * p->nf;
+        const size_t n = static_cast<size_t>(p->mpf) * std::max(p->nf, p->nf_local);
         if (count > 0 && p->wq.n != n) { p->wq.alloc(n); p->wt.alloc(n); p->ws.alloc(n); p->wkv.alloc(n); }
     });
 }
@@ -465,7 +502,7 @@ hdgb_status hdgb_precond_set_ritz(hdgb_precond* p, const double* reim, int count
 hdgb_status hdgb_precond_apply_base(hdgb_precond* p, const double* y, double* z) {
     hdgb_ctx* c = p->ctx;
     return guarded(c, [&] {
-        const size_t n = static_cast<size_t>(p->mpf) * p->nf;
+        const size_t n = static_cast<size_t>(p->mpf) * std::max(p->nf, p->nf_local);
         InArg Y(c, y, n);
         OutArg Z(c, z, n);
         apply_base_device(p, Y.dev, Z.dev);
@@ -478,7 +515,7 @@ hdgb_status hdgb_precond_apply_base(hdgb_precond* p, const double* y, double* z)
 hdgb_status hdgb_precond_apply(hdgb_precond* p, hdgb_matrix* k, const double* y, double* z) {
     hdgb_ctx* c = p->ctx;
     return guarded(c, [&] {
-        const size_t n = static_cast<size_t>(p->mpf) * p->nf;
+        const size_t n = static_cast<size_t>(p->mpf) * std::max(p->nf, p->nf_local);
         InArg Y(c, y, n);
         OutArg Z(c, z, n);
         apply_precond_device(p, k, Y.dev, Z.dev);

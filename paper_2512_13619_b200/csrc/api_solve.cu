@@ -19,14 +19,15 @@ namespace {
 
 GmresWork& gmres_work(hdgb_matrix* k, int restart) {
     const int64_t n = k->n_dof();
+    const int64_t ld = k->n_local();
     if (!k->work || k->work->restart < restart || k->work->n != n) {
         k->work.reset(new GmresWork());
         GmresWork& w = *k->work;
         w.restart = restart;
         w.n = n;
-        w.basis.alloc(static_cast<size_t>(restart + 1) * n);
-        w.kv.alloc(n);
-        w.r.alloc(n);
+        w.basis.alloc(static_cast<size_t>(restart + 1) * ld);
+        w.kv.alloc(ld);
+        w.r.alloc(ld);
         w.coef.alloc(2 * static_cast<size_t>(restart + 1) + 2);
         w.partial.alloc(multi_dot_workspace_doubles(n, restart + 1));
         w.ycoef.alloc(restart + 1);
@@ -38,24 +39,32 @@ GmresWork& gmres_work(hdgb_matrix* k, int restart) {
 // CGS mode: both projection passes are batched (c = V^T w; w -= V c; d = V^T w; w -= V d) with the
 // norm fused into the second update; the reference's second pass interleaves dot and update, which
 // differs at O(eps^2) relative.  MGS mode follows the reference sequence exactly.
-void orthogonalize_device(hdgb_ctx* c, const double* V, int nvec, int64_t n, double* w, int orth, double* coef,
-                          double* partial, double* h) {
+// n = owned unknowns (what the sums run over), ldv = distance between basis vectors; with a
+// communicator every projection pass is completed by one small all-reduce.
+void orthogonalize_device(hdgb_ctx* c, const double* V, int64_t ldv, int nvec, int64_t n, double* w, int orth,
+                          double* coef, double* partial, double* h) {
     double* dc = coef;
     double* dd = coef + nvec;
     double* dn = coef + 2 * nvec;
+    auto reduce = [&](double* dev, int cnt) { if (c->comm) c->comm->allreduce(c, dev, cnt); };
     if (orth == 1) {
         for (int i = 0; i < nvec; ++i) {
-            const double* vi = V + static_cast<size_t>(i) * n;
-            launch_multi_dot(c, vi, n, 1, w, n, dc + i, partial);
-            launch_multi_axpy(c, vi, n, 1, dc + i, -1.0, w, n, nullptr, partial);
+            const double* vi = V + static_cast<size_t>(i) * ldv;
+            launch_multi_dot(c, vi, ldv, 1, w, n, dc + i, partial);
+            reduce(dc + i, 1);
+            launch_multi_axpy(c, vi, ldv, 1, dc + i, -1.0, w, n, nullptr, partial);
         }
         launch_sumsq(c, w, n, dn, partial);
+        reduce(dn, 1);
         HDGB_CUDA(cudaMemsetAsync(dd, 0, nvec * sizeof(double), c->stream));
     } else {
-        launch_multi_dot(c, V, n, nvec, w, n, dc, partial);
-        launch_multi_axpy(c, V, n, nvec, dc, -1.0, w, n, nullptr, partial);
-        launch_multi_dot(c, V, n, nvec, w, n, dd, partial);
-        launch_multi_axpy(c, V, n, nvec, dd, -1.0, w, n, dn, partial);
+        launch_multi_dot(c, V, ldv, nvec, w, n, dc, partial);
+        reduce(dc, nvec);
+        launch_multi_axpy(c, V, ldv, nvec, dc, -1.0, w, n, nullptr, partial);
+        launch_multi_dot(c, V, ldv, nvec, w, n, dd, partial);
+        reduce(dd, nvec);
+        launch_multi_axpy(c, V, ldv, nvec, dd, -1.0, w, n, dn, partial);
+        reduce(dn, 1);
     }
     // normalise on the device (no-op when the norm is zero, gmres.cpp:54-57) while the column
     // travels to the host
@@ -72,7 +81,8 @@ void orthogonalize_device(hdgb_ctx* c, const double* V, int nvec, int64_t n, dou
 void gmres_device(hdgb_matrix* k, hdgb_precond* p, const double* rhs, double* x, const hdgb_gmres_config& cfg,
                   hdgb_gmres_stats* st, double* residual_trace) {
     hdgb_ctx* c = k->ctx;
-    const int64_t n = k->n_dof();
+    const int64_t n = k->n_dof();    // owned unknowns: rows, sums
+    const int64_t ld = k->n_local(); // vector length incl. the halo part
     const int m = cfg.restart;
     if (m < 1) throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: GMRES restart length must be >= 1");
     if (2 * static_cast<size_t>(m + 1) + 2 > c->pinned_doubles) throw Failure(HDGB_ERR_UNSUPPORTED, "GMRES restart length too large");
@@ -84,6 +94,7 @@ void gmres_device(hdgb_matrix* k, hdgb_precond* p, const double* rhs, double* x,
 
     auto norm_of = [&](const double* v) {
         launch_sumsq(c, v, n, W.coef.p, W.partial.p);
+        if (c->comm) c->comm->allreduce(c, W.coef.p, 1);
         double s;
         HDGB_CUDA(cudaMemcpyAsync(&s, W.coef.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         HDGB_CUDA(cudaStreamSynchronize(c->stream));
@@ -131,10 +142,10 @@ void gmres_device(hdgb_matrix* k, hdgb_precond* p, const double* rhs, double* x,
         int jused = 0;
         bool cycle_converged = false;
         for (int j = 0; j < m && st->iters < cfg.max_iters; ++j) {
-            double* w = V + static_cast<size_t>(j + 1) * n;  // the candidate lands in its basis slot
+            double* w = V + static_cast<size_t>(j + 1) * ld;  // the candidate lands in its basis slot
             {
                 PhaseTimer tm(c, &st->t_mv);
-                matvec_device(k, V + static_cast<size_t>(j) * n, kv);
+                matvec_device(k, V + static_cast<size_t>(j) * ld, kv);
                 tm.stop();
                 PhaseTimer tp(c, &st->t_prec);
                 apply_precond_device(p, k, kv, w);
@@ -142,7 +153,7 @@ void gmres_device(hdgb_matrix* k, hdgb_precond* p, const double* rhs, double* x,
             }
             {
                 PhaseTimer to(c, &st->t_orth);
-                orthogonalize_device(c, V, nbasis, n, w, cfg.orth, W.coef.p, W.partial.p, h.data());
+                orthogonalize_device(c, V, ld, nbasis, n, w, cfg.orth, W.coef.p, W.partial.p, h.data());
                 to.stop();
             }
             for (int i = 0; i <= nbasis; ++i)
@@ -186,7 +197,8 @@ void gmres_device(hdgb_matrix* k, hdgb_precond* p, const double* rhs, double* x,
             DevBuf<double> gram(used);
             std::vector<double> hg(used);
             for (int a = 0; a < used; ++a) {
-                launch_multi_dot(c, V, n, used, V + static_cast<size_t>(a) * n, n, gram.p, W.partial.p);
+                launch_multi_dot(c, V, ld, used, V + static_cast<size_t>(a) * ld, n, gram.p, W.partial.p);
+                if (c->comm) c->comm->allreduce(c, gram.p, used);
                 HDGB_CUDA(cudaMemcpyAsync(hg.data(), gram.p, used * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
                 HDGB_CUDA(cudaStreamSynchronize(c->stream));
                 for (int b = a; b < used; ++b)
@@ -202,7 +214,7 @@ void gmres_device(hdgb_matrix* k, hdgb_precond* p, const double* rhs, double* x,
             y[i] = v / rcols[i][i];
         }
         HDGB_CUDA(cudaMemcpyAsync(W.ycoef.p, y.data(), jused * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-        launch_multi_axpy(c, V, n, jused, W.ycoef.p, 1.0, x, n, nullptr, W.partial.p);
+        launch_multi_axpy(c, V, ld, jused, W.ycoef.p, 1.0, x, n, nullptr, W.partial.p);
         HDGB_CUDA(cudaStreamSynchronize(c->stream));  // y is a stack temporary
 
         if (cfg.track_diagnostics) {
@@ -257,9 +269,9 @@ hdgb_status hdgb_gmres_solve(hdgb_matrix* k, hdgb_precond* p, const double* rhs,
         hdgb_gmres_config cf;
         hdgb_gmres_config_default(&cf);
         if (cfg) cf = *cfg;
-        const size_t n = k->n_dof();
-        if (p && static_cast<size_t>(p->mpf) * p->nf != n)
+        if (p && static_cast<int64_t>(p->mpf) * p->nf != k->n_dof())
             throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: preconditioner / operator size");
+        const size_t n = k->n_local();
         InArg B(c, rhs, n);
         OutArg X(c, x, n);
         if (x0 && x0 != x) HDGB_CUDA(cudaMemcpyAsync(X.dev, x0, n * sizeof(double), cudaMemcpyDefault, c->stream));
@@ -276,7 +288,7 @@ hdgb_status hdgb_orthogonalize(hdgb_ctx* c, const double* basis, int nvec, int64
     return guarded(c, [&] {
         if (2 * static_cast<size_t>(nvec) + 2 > c->pinned_doubles) throw Failure(HDGB_ERR_UNSUPPORTED, "too many basis vectors");
         DevBuf<double> coef(2 * static_cast<size_t>(nvec) + 2), partial(multi_dot_workspace_doubles(n, std::max(nvec, 1)));
-        orthogonalize_device(c, basis, nvec, n, w, orth, coef.p, partial.p, h);
+        orthogonalize_device(c, basis, n, nvec, n, w, orth, coef.p, partial.p, h);
     });
 }
 
@@ -354,6 +366,8 @@ hdgb_status hdgb_newton_solve(hdgb_disc* d, const hdgb_model* m, hdgb_state* s, 
             if (rep->n_newton < HDGB_MAX_NEWTON_HISTORY) rep->gmres_per_newton[rep->n_newton] = gs.iters;
             rep->t_mv += gs.t_mv; rep->t_prec += gs.t_prec; rep->t_orth += gs.t_orth;
 
+            // ghost elements are recovered redundantly: they need the update on their (halo) faces
+            if (c->comm) c->comm->halo(c, duhat.p, v.mpf);
             recover_local_device(d, ops.get(), duhat.p, du.p, tmp.p);
 
             // halving line search on the full nonlinear residual (newton.cpp:127-141); only u and

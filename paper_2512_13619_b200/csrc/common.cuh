@@ -32,8 +32,22 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 
 }  // namespace hdgb
 
+struct hdgb_ctx;
+namespace hdgb {
+// Communicator of a domain-decomposed run (one rank per GPU).  halo(): fills the halo entries of
+// a face-major device vector (width doubles per face) from their owners; allreduce(): in-place sum
+// of n device doubles over all ranks.  Both enqueue on / order with ctx->stream.
+struct Comm {
+    int rank = 0, size = 1;
+    virtual ~Comm() = default;
+    virtual void halo(hdgb_ctx* c, double* vec, int width) = 0;
+    virtual void allreduce(hdgb_ctx* c, double* buf, int n) = 0;
+};
+}  // namespace hdgb
+
 // The opaque context of the C ABI.
 struct hdgb_ctx {
+    hdgb::Comm* comm = nullptr;  // nullptr: single GPU
     int device = 0;
     int sm_count = 148;
     cudaStream_t stream = nullptr;

@@ -16,6 +16,7 @@ struct DiscView {
     int mpf;  // M*pf
     int nfl;  // n_lfe*mpf   trace dofs per element
     int nfs;  // n_lfe*pf    scalar trace dofs per element
+    int ne_owned, nf_owned;  // domain decomposition: owned elements / faces come first (== ne / nf on one GPU)
     const int* elem_faces;   // ne x n_lfe
     const int* elem_side;    // ne x n_lfe
     const int* face_elems;   // nf x 2
@@ -51,6 +52,9 @@ struct hdgb_disc {
     hdgb_ctx* ctx = nullptr;
     hdgb_dims dims{};
     hdgb::HostMesh mesh;
+    int ne_owned = -1, nf_owned = -1;     // domain decomposition: owned entities come first
+    std::vector<int64_t> face_gid;        // local -> global face id (empty: identity)
+    int64_t nf_global = -1;
     hdgb::MasterElement me;
     hdgb::HostGeom geom;
     // device tables
@@ -102,9 +106,11 @@ struct hdgb_matrix {
     std::unique_ptr<hdgb::GmresWork> work;
     bool neighbor_valid = false;
     int m = 1, pf = 0, n_lfe = 4, nf = 0;
+    int nf_local = 0;  // faces a vector spans (owned first, then halo); == nf on one GPU
     int mpf() const { return m * pf; }
     int nb() const { return 2 * n_lfe - 1; }
-    int64_t n_dof() const { return static_cast<int64_t>(mpf()) * nf; }
+    int64_t n_dof() const { return static_cast<int64_t>(mpf()) * nf; }          // owned unknowns (rows)
+    int64_t n_local() const { return static_cast<int64_t>(mpf()) * nf_local; }  // vector length
     hdgb::DevBuf<double> blocks;           // mpf x (mpf*nb) per face
     hdgb::DevBuf<int> nbr32;               // nf x nb, device (kernels gather with 32-bit ids)
     std::vector<int64_t> neighbor;         // nf x nb, host, int64 with kNoFace = -1 (face_matrix.hpp:22)
@@ -116,12 +122,12 @@ struct hdgb_precond {
     int kind = HDGB_PC_IDENTITY;
     int poly_degree = 0;
     int poly_kind = HDGB_POLY_GMRES;
-    int mpf = 0, nf = 0, n_lfe = 0, ne = 0;
+    int mpf = 0, nf = 0, nf_local = 0, n_lfe = 0, ne = 0;
     hdgb::DevBuf<double> bj_inv;   // mpf^2 per face
     hdgb::DevBuf<double> asm_inv;  // nfl^2 per element
     const hdgb_disc* disc = nullptr;  // ASM gathers through the mesh tables
     std::vector<double> ritz;      // interleaved (re, im), Leja order
     int64_t inner_ops = 0;
     // work vectors
-    hdgb::DevBuf<double> ze, wq, ww, wt, ws, wkv;
+    hdgb::DevBuf<double> ze, wq, ww, wt, ws, wkv, yh;
 };

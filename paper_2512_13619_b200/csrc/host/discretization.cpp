@@ -399,6 +399,33 @@ HostMesh build_mesh_from_elements(int shape, int ne, int nv, const int32_t* elem
     return m;
 }
 
+HostMesh mesh_from_tables(int shape, int ne, int nf, int nv, const int32_t* elem_verts, const double* coords,
+                          const int32_t* elem_faces, const int32_t* face_elems, const int32_t* face_lidx,
+                          const int32_t* face_orient, const int32_t* face_verts, const int32_t* bnd_tag) {
+    const ShapeInfo& si = shape_info(shape);
+    HostMesh m;
+    m.shape = shape; m.dim = si.dim; m.ne = ne; m.nf = nf; m.nv = nv;
+    m.n_lfe = si.n_lfe; m.vpe = si.vpe; m.vpf = si.vpf;
+    m.elem_verts.assign(elem_verts, elem_verts + static_cast<size_t>(ne) * si.vpe);
+    m.coords.assign(coords, coords + static_cast<size_t>(nv) * si.dim);
+    m.elem_faces.assign(elem_faces, elem_faces + static_cast<size_t>(ne) * si.n_lfe);
+    m.face_elems.assign(face_elems, face_elems + static_cast<size_t>(nf) * 2);
+    m.face_lidx.assign(face_lidx, face_lidx + static_cast<size_t>(nf) * 2);
+    m.face_orient.assign(face_orient, face_orient + static_cast<size_t>(nf) * 2);
+    m.face_verts.assign(face_verts, face_verts + static_cast<size_t>(nf) * si.vpf);
+    m.bnd_tag.assign(bnd_tag, bnd_tag + nf);
+    for (int e = 0; e < ne; ++e)
+        for (int lf = 0; lf < si.n_lfe; ++lf) {
+            const int f = m.elem_faces[static_cast<size_t>(e) * si.n_lfe + lf];
+            if (f < 0 || f >= nf) throw Failure(HDGB_ERR_INVALID_MESH, "element_to_face entry out of range", e);
+            const bool s0 = m.face_elems[2 * f] == e && m.face_lidx[2 * f] == lf;
+            const bool s1 = m.face_elems[2 * f + 1] == e && m.face_lidx[2 * f + 1] == lf;
+            if (!s0 && !s1) throw Failure(HDGB_ERR_INVALID_MESH, "face_to_elements does not list the element on either side", e);
+        }
+    derive_elem_side(m);
+    return m;
+}
+
 HostMesh build_structured_mesh(int shape, int n, const double* lo, const double* hi, double jitter, uint64_t seed) {
     if (n < 1) throw Failure(HDGB_ERR_INVALID_MESH, "mesh resolution must be >= 1, got " + std::to_string(n));
     const ShapeInfo& si = shape_info(shape);

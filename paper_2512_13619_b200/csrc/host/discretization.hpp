@@ -85,6 +85,13 @@ HostMesh build_structured_mesh(int shape, int n, const double* lo, const double*
 HostMesh build_mesh_from_elements(int shape, int ne, int nv, const int32_t* elem_verts,
                                   const double* coords);
 
+// Mesh whose connectivity is given explicitly (sub-domain meshes cut out of a global mesh keep the
+// global face orientations / side assignment).  face_elems entries < 0 mean "no local element on
+// that side" (-1: domain boundary, -2: element lives on another rank).
+HostMesh mesh_from_tables(int shape, int ne, int nf, int nv, const int32_t* elem_verts, const double* coords,
+                          const int32_t* elem_faces, const int32_t* face_elems, const int32_t* face_lidx,
+                          const int32_t* face_orient, const int32_t* face_verts, const int32_t* bnd_tag);
+
 // Geometric factors at quadrature points (generalised GeomFactors, mesh.hpp:47-60).
 struct HostGeom {
     std::vector<double> elem_detjac;  // [e*qe + g]

@@ -77,9 +77,11 @@ __global__ void extract_diag_kernel(const double* __restrict__ blocks, int64_t t
     diag[i] = blocks[f * bsz * nb + (i - f * bsz)];
 }
 
-// One CTA per element: copy K-bar and overwrite the diagonal sub-block of every interior face with
-// the two-sided sum (side 0 + side 1, preconditioner.cpp:67-71).
-__global__ void asm_enrich_kernel(DiscView dv, const double* __restrict__ kbar, double* __restrict__ pbar) {
+// One CTA per element: copy K-bar and overwrite the diagonal sub-block of every face with the
+// two-sided sum (side 0 + side 1, preconditioner.cpp:67-71), which the assembled operator already
+// holds as the face's self block diag[f] (face_matrix.cpp:29-39: same terms, same order).
+__global__ void asm_enrich_kernel(DiscView dv, const double* __restrict__ kbar, const double* __restrict__ diag,
+                                  double* __restrict__ pbar) {
     const int e = blockIdx.x;
     const int mpf = dv.mpf, n_lfe = dv.n_lfe, nfl = dv.nfl;
     const double* src = kbar + static_cast<size_t>(e) * nfl * nfl;
@@ -90,13 +92,8 @@ __global__ void asm_enrich_kernel(DiscView dv, const double* __restrict__ kbar, 
         double v = src[t];
         if (lc == lr) {
             const int f = dv.elem_faces[e * n_lfe + lc];
-            const int e1 = dv.face_elems[2 * f], e2 = dv.face_elems[2 * f + 1];
-            if (e2 >= 0) {
-                const int l1 = dv.face_lidx[2 * f], l2 = dv.face_lidx[2 * f + 1];
-                const int cc = c - lc * mpf, rr = r - lr * mpf;
-                v = kbar[static_cast<size_t>(e1) * nfl * nfl + static_cast<size_t>(l1 * mpf + cc) * nfl + (l1 * mpf + rr)] +
-                    kbar[static_cast<size_t>(e2) * nfl * nfl + static_cast<size_t>(l2 * mpf + cc) * nfl + (l2 * mpf + rr)];
-            }
+            const int cc = c - lc * mpf, rr = r - lr * mpf;
+            v = diag[static_cast<size_t>(f) * mpf * mpf + static_cast<size_t>(cc) * mpf + rr];
         }
         dst[t] = v;
     }
@@ -126,9 +123,9 @@ void launch_extract_diag(hdgb_ctx* ctx, const double* blocks, int nf, int mpf, i
     HDGB_LAUNCH_CHECK(ctx);
 }
 
-void launch_asm_enrich(hdgb_ctx* ctx, const DiscView& dv, const double* kbar, double* pbar) {
+void launch_asm_enrich(hdgb_ctx* ctx, const DiscView& dv, const double* kbar, const double* diag, double* pbar) {
     if (dv.ne == 0) return;
-    asm_enrich_kernel<<<dv.ne, 256, 0, ctx->stream>>>(dv, kbar, pbar);
+    asm_enrich_kernel<<<dv.ne, 256, 0, ctx->stream>>>(dv, kbar, diag, pbar);
     HDGB_LAUNCH_CHECK(ctx);
 }
 

@@ -37,7 +37,8 @@ void launch_assemble_global(hdgb_ctx* ctx, const DiscView& dv, const double* kba
 void launch_fill_neighbors(hdgb_ctx* ctx, const DiscView& dv, int* nbr32);
 // build_bj extraction (preconditioner.cpp:33-37): diag[f] = slot-0 block of face f
 void launch_extract_diag(hdgb_ctx* ctx, const double* blocks, int nf, int mpf, int nb, double* diag);
-// build_asm enrichment (preconditioner.cpp:54-75): pbar = kbar with shared-face diagonal blocks summed
-void launch_asm_enrich(hdgb_ctx* ctx, const DiscView& dv, const double* kbar, double* pbar);
+// build_asm enrichment (preconditioner.cpp:54-75): pbar = kbar with the diagonal sub-block of every
+// local face replaced by that face's two-sided sum diag[f] (= the self block of the assembled row)
+void launch_asm_enrich(hdgb_ctx* ctx, const DiscView& dv, const double* kbar, const double* diag, double* pbar);
 
 }  // namespace hdgb

@@ -219,6 +219,13 @@ def load_library():
                                   C.POINTER(PrecondSpec), C.POINTER(_Time), C.POINTER(_Report)]),
         "hdgb_time_march": (i, [_vp, _vp, _vp, d, i, C.POINTER(NewtonConfig), C.POINTER(GmresConfig),
                                 C.POINTER(PrecondSpec), C.POINTER(_Report)]),
+        "hdgb_disc_create_from_tables": (i, [_vp, i, i, i, i, i, i, i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, i, i, _vp, i64, pp]),
+        "hdgb_mesh_connectivity": (i, [i, i, i, _vp, _vp, pp]),
+        "hdgb_comm_nccl_unique_id": (i, [_vp]), "hdgb_comm_create_nccl": (i, [_vp, _vp, i, i]),
+        "hdgb_comm_set_halo_plan": (i, [_vp, i, _vp, _vp, _vp, _vp, _vp]),
+        "hdgb_comm_set_callbacks": (i, [_vp, i, i, _vp, _vp, _vp]), "hdgb_comm_destroy": (None, [_vp]),
+        "hdgb_halo_exchange": (i, [_vp, _vp, i]), "hdgb_allreduce_sum": (i, [_vp, _vp, i]),
+        "hdgb_comm_rank": (i, [_vp]), "hdgb_comm_size": (i, [_vp]),
         "hdgb_device_alloc": (i, [_vp, i64, pp]), "hdgb_device_free": (None, [_vp, _vp]),
         "hdgb_copy": (i, [_vp, _vp, _vp, i64]),
     }
@@ -764,7 +771,8 @@ class FaceBlockMatrix:
         self.m, self.pf, self.n_lfe, self.nf = list(d)
         self.nb = 2 * self.n_lfe - 1
         self.block_dim = self.m * self.pf
-        self.n_dof = self.block_dim * self.nf
+        self.n_dof = self.block_dim * self.nf      # owned unknowns (rows)
+        self.n_vec = self.n_dof                    # vector length (incl. halo faces when partitioned)
 
     @classmethod
     def from_host(cls, ctx, m, pf, n_lfe, nf, neighbor, blocks):
@@ -831,14 +839,16 @@ def assemble_global(disc, ops: ElementOperators):
     h = _vp()
     rhs = np.empty(disc.n_dof)
     disc.ctx.check(disc.ctx._L.hdgb_assemble_global(disc._h, ops._h, C.byref(h), _ptr(rhs)))
-    return FaceBlockMatrix(disc.ctx, h), rhs
+    k = FaceBlockMatrix(disc.ctx, h)
+    k.n_vec = disc.n_dof   # a partitioned discretisation spans owned + halo faces
+    return k, rhs
 
 
 def block_matvec(k: FaceBlockMatrix, x, y=None):
     x = _f64(x)
-    if isinstance(x, np.ndarray) and x.size != k.n_dof:
-        raise DimensionMismatch(f"block_matvec: vector has {x.size} entries, operator {k.n_dof}")
-    out = np.empty(k.n_dof) if y is None else y
+    if isinstance(x, np.ndarray) and x.size != k.n_vec:
+        raise DimensionMismatch(f"block_matvec: vector has {x.size} entries, operator {k.n_vec}")
+    out = np.empty(k.n_vec) if y is None else y
     k.ctx.check(k.ctx._L.hdgb_block_matvec(k._h, _ptr(x), _ptr(out)))
     return out
 
@@ -905,14 +915,14 @@ class Preconditioner:
     def apply_base(self, y, z=None):
         """make_base_apply (preconditioner.cpp:285-299)."""
         y = _f64(y)
-        out = np.empty(self.k.n_dof) if z is None else z
+        out = np.empty(self.k.n_vec) if z is None else z
         self.ctx.check(self.ctx._L.hdgb_precond_apply_base(self._h, _ptr(y), _ptr(out)))
         return out
 
     def apply(self, y, z=None):
         """make_preconditioner_apply (preconditioner.cpp:301-308)."""
         y = _f64(y)
-        out = np.empty(self.k.n_dof) if z is None else z
+        out = np.empty(self.k.n_vec) if z is None else z
         self.ctx.check(self.ctx._L.hdgb_precond_apply(self._h, self.k._h, _ptr(y), _ptr(out)))
         return out
 
@@ -961,7 +971,7 @@ def gmres_solve(k: FaceBlockMatrix, precond: Preconditioner, rhs, x0=None, cfg: 
     cfg = cfg or GmresConfig()
     rhs = _f64(rhs)
     x0 = _f64(x0)
-    out = np.empty(k.n_dof) if x is None else x
+    out = np.empty(k.n_vec) if x is None else x
     st = GmresStats()
     trace = np.zeros(cfg.max_iters) if cfg.track_diagnostics else None
     k.ctx.check(k.ctx._L.hdgb_gmres_solve(k._h, precond._h if precond else None, _ptr(rhs), _ptr(x0), C.byref(cfg),
