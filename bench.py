@@ -39,10 +39,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=28, help="hex cells per direction (28 -> 1.09 M trace DOFs)")
+    ap.add_argument("--cells", dest="n", type=int, default=28, help="hex cells per direction (28 -> 1.09 M trace DOFs)")
+    ap.add_argument("--force-dd", action="store_true", help="use the domain-decomposition path even on one rank (testing)")
     ap.add_argument("--degree", type=int, default=3)
     ap.add_argument("--precond", default="asm", choices=["bj", "asm", "ras"])
-    ap.add_argument("--cpu-n", type=int, default=12, help="hex cells per direction of the bounded CPU sample")
+    ap.add_argument("--cpu-cells", dest="cpu_n", type=int, default=12, help="hex cells per direction of the bounded CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -150,6 +151,16 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
+def ncu_traffic(a):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the matvec kernel from the committed
+    ncu --set full capture of this workload (profiles/traffic.json), or None for other sizes."""
+    try:
+        t = json.loads((ROOT / "profiles" / "traffic.json").read_text())
+        return t.get(f"block_matvec hex {a.n}^3 p={a.degree}")
+    except Exception:
+        return None
+
+
 def run_ours(a):
     import torch
     import torch.distributed as dist
@@ -166,7 +177,21 @@ def run_ours(a):
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)  # so torch.cuda.Event sees the launching stream
 
-    disc = hdg.Discretization.structured(ctx, "hex", n=a.n, degree=a.degree)
+    if world == 1 and not a.force_dd:
+        disc = hdg.Discretization.structured(ctx, "hex", n=a.n, degree=a.degree)
+        n_dof_global = disc.n_dof
+    else:
+        # weak scaling: every rank owns an n^3 slab of an n x n x (n*world) box, partitioned by domain
+        # decomposition (one ghost layer, halo exchange + all-reduce over NCCL)
+        from paper_2512_13619_b200 import partition as P
+        lo, hi = (0.0, 0.0, 0.0), (1.0, 1.0, float(world))
+        coords, ev = P.box_hex_mesh(a.n, a.n, a.n * world, lo, hi)
+        gm = P.global_mesh("hex", coords, ev, lo=lo, hi=hi)
+        lm = P.build_my_local_mesh(gm, P.slab_partition(gm.ne, world), rank, dist if world > 1 else None)
+        disc = P.make_discretization(ctx, lm, "hex", a.degree)
+        P.install_nccl_comm(ctx, lm, dist if world > 1 else None)
+        n_dof_global = gm.nf * disc.mpf
+        del gm, coords, ev
     xq, xf = disc.quad_coords()
     pi = np.pi
     sinprod = lambda x: np.prod(np.sin(pi * x), axis=-1)
@@ -241,7 +266,7 @@ def run_ours(a):
     clocks = sampler.finish()
 
     # ---- dominant-kernel roofline: the fused gather + block GEMV (team_gemv) of block_matvec --------
-    mpf, nb, nf, ne, nfl, n_dof = disc.mpf, disc.nb, disc.nf, disc.ne, disc.nfl, disc.n_dof
+    mpf, nb, nf, ne, nfl, n_dof = disc.mpf, disc.nb, getattr(disc, 'nf_owned', disc.nf), disc.ne, disc.nfl, disc.n_dof
     ops = hdg.assemble_element_operators(disc, model, state)
     K, rhs = hdg.assemble_global(disc, ops)
     P = hdg.build_preconditioner(pspec, K, ops, disc)
@@ -280,22 +305,25 @@ def run_ours(a):
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": world * n_dof * a.steps / t_res, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "metric": METRIC, "value": n_dof_global * a.steps / t_res, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": 1e3 * t_res / a.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_name(a.n, a.degree, a.precond), "trace_dofs_per_gpu": n_dof,
                        "elements_per_gpu": ne, "faces_per_gpu": nf,
-                       "parallelism": "1 GPU" if world == 1 else f"{world} independent sub-domain problems (no halo exchange yet)",
+                       "parallelism": "1 GPU" if world == 1 else
+                       f"domain decomposition over {world} GPUs: n x n x (n*{world}) box in z-slabs, one ghost layer, "
+                       f"NCCL halo exchange per operator application + all-reduce per Gram-Schmidt pass",
+                       "trace_dofs_global": n_dof_global,
                        "l2_policy": "inputs larger than L2 (K = %.2f GB, ASM blocks = %.2f GB vs 126 MB L2)" %
                                     (8e-9 * nf * mpf * mpf * nb, 8e-9 * ne * nfl * nfl)},
-            "e2e": {"value": world * n_dof * a.steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "e2e": {"value": n_dof_global * a.steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": 1e3 * t_e2e / a.steps},
             "gpu_launches": int(launches),
             "clocks": clocks,
-            "roofline": {"kernel": "team_gemv_kernel<2> as block_matvec (fused neighbour gather + block-row GEMV)",
+            "roofline": {"kernel": "stream_gemv_kernel<2,1> as block_matvec (fused neighbour gather + block-row GEMV, bulk-TMA ring)",
                          "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "peak_source": peak_src, "frac_of_8TBs": achieved / 8000.0,
-                         "algorithmic_bytes_per_launch": bytes_mv, "avg_launch_us": 1e6 * t_mv, "traffic": None,
+                         "algorithmic_bytes_per_launch": bytes_mv, "avg_launch_us": 1e6 * t_mv, "traffic": ncu_traffic(a),
                          "in_solve_avg_launch_us": 1e6 * rep_t.t_mv / max(n_mv_calls, 1)},
             "precond_apply": {"kind": a.precond, "GBps": bytes_pc / t_pc / 1e9, "frac": bytes_pc / t_pc / 1e9 / peak,
                               "avg_us": 1e6 * t_pc, "algorithmic_bytes": bytes_pc},

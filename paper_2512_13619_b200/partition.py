@@ -256,7 +256,8 @@ def install_nccl_comm(ctx, lm: LocalMesh, dist):
         if st != 0:
             raise H.HdgError("ncclGetUniqueId failed")
     box = [bytes(uid.raw)]
-    dist.broadcast_object_list(box, src=0)
+    if dist is not None and lm.n_ranks > 1:
+        dist.broadcast_object_list(box, src=0)
     ctx.check(L.hdgb_comm_create_nccl(ctx._h, box[0], lm.rank, lm.n_ranks))
     set_halo_plan(ctx, lm)
 

@@ -108,3 +108,36 @@ def test_partitioned_operator_rows_and_preconditioners(ctx):
         assert np.max(np.abs(y[: lm.nf_owned] - y1[own])) < 1e-12 * max(1.0, np.max(np.abs(y1)))
         for kind in ("bj", "asm"):
             assert np.max(np.abs(z[kind][: lm.nf_owned] - z1[kind][own])) < 1e-10 * max(1.0, np.max(np.abs(z1[kind]))), kind
+
+
+def test_nccl_backend_single_rank(ctx):
+    """The NCCL transport itself (dlopen of libnccl.so.2, ncclCommInitRank, all-reduce, empty halo
+    plan) on the one GPU this box has: a 1-rank job must reproduce the communicator-free run."""
+    import ctypes as C
+    from paper_2512_13619_b200 import hdg as H
+    gm = mesh("quad", (6, 5))
+    lm = P.build_local_meshes(gm, np.zeros(gm.ne, dtype=np.int32))[0]
+    c2 = hdg.Context(0)
+    try:
+        P.install_nccl_comm(c2, lm, None)
+        L = H.load_library()
+        assert L.hdgb_comm_size(c2._h) == 1 and L.hdgb_comm_rank(c2._h) == 0
+        buf = c2.alloc(4)
+        c2.copy(buf, np.array([1.0, 2.0, 3.0, 4.0]), 4)
+        c2.check(L.hdgb_allreduce_sum(c2._h, buf, 4))
+        back = np.empty(4)
+        c2.copy(back, buf, 4)
+        c2.free(buf)
+        assert np.array_equal(back, [1.0, 2.0, 3.0, 4.0])
+        out = []
+        for cc in (ctx, c2):
+            disc = P.make_discretization(cc, lm, "quad", 2)
+            model = hdg.make_case_model(disc, "burgers")
+            state = hdg.make_initial_state(disc, model)
+            rep = hdg.newton_solve(disc, model, state, pspec=hdg.PrecondSpec("asm", poly_degree=4))
+            out.append((rep, state.uhat))
+        assert out[0][0].gmres_per_newton == out[1][0].gmres_per_newton
+        assert np.array_equal(out[0][1], out[1][1])
+    finally:
+        H.load_library().hdgb_comm_destroy(c2._h)
+        c2.close()
