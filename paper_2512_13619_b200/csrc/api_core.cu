@@ -13,6 +13,7 @@ int hdgb_set_tuning(const char* key, int64_t value) {
     const std::string k = key ? key : "";
     if (k == "use_stream") { hdgb::tuning().use_stream = static_cast<int>(value); return 0; }
     if (k == "stream_min_elems") { hdgb::tuning().stream_min_elems = value; return 0; }
+    if (k == "use_tile_lu") { hdgb::tuning().use_tile_lu = static_cast<int>(value); return 0; }
     return 1;
 }
 

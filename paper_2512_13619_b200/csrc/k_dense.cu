@@ -211,6 +211,166 @@ __global__ void lu_invert_cta_kernel(int n, int64_t batch, const double* __restr
     }
 }
 
+// ---- register-tiled Gauss-Jordan inverse (25 <= n <= 128) --------------------------------------------
+// One CTA of 16 x 16 threads per block; thread (ti, tj) keeps the T x T entries (ti + 16a, tj + 16b)
+// in registers.  In-place Gauss-Jordan with the reference's partial-pivot rule and singularity
+// test (dense_batch.cpp:27-36): per elimination step the pivot column and the two rows involved in
+// the interchange are published through (double-buffered) shared memory -- 3 barriers per step --
+// and every thread applies the rank-1 update to its tile with T^2 FMAs.  Working on the row-
+// interchanged matrix yields (P A)^-1; the inverse is its column permutation, applied on write-out.
+// Same 2 n^3 flops as the reference's LU + n solves, results agree to rounding.
+template <int T>
+__global__ void __launch_bounds__(256) lu_invert_tile_kernel(int n, int64_t batch, const double* __restrict__ a_in,
+                                                             double* __restrict__ inv_out, int* flags) {
+    constexpr int N = 16 * T;
+    __shared__ double s_col[2][N], s_rowk[2][N], s_rowp[2][N];
+    __shared__ double s_red[8];
+    __shared__ int s_piv[N], s_cinv[N];
+    __shared__ int s_p, s_ok;
+    const int tid = threadIdx.x, ti = tid & 15, tj = tid >> 4;
+    const int lane = tid & 31, warp = tid >> 5;
+
+    for (int64_t blk = blockIdx.x; blk < batch; blk += gridDim.x) {
+        const double* A = a_in + blk * n * n;
+        double a[T][T];
+        double amax = 0.0;
+#pragma unroll
+        for (int b_ = 0; b_ < T; ++b_)
+#pragma unroll
+            for (int a_ = 0; a_ < T; ++a_) {
+                const int i = ti + 16 * a_, j = tj + 16 * b_;
+                double v = (i == j) ? 1.0 : 0.0;  // identity padding outside the n x n block
+                if (i < n && j < n) {
+                    v = A[static_cast<size_t>(j) * n + i];
+                    amax = fmax(amax, fabs(v));
+                }
+                a[a_][b_] = v;
+            }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+        if (lane == 0) s_red[warp] = amax;
+        __syncthreads();
+        amax = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) amax = fmax(amax, s_red[w]);
+        const double tol = 1e-14 * amax;
+        bool singular = false;
+
+        for (int k = 0; k < n; ++k) {
+            const int buf = k & 1;
+            const int bk = k >> 4, rk = k & 15;
+            // 1. publish column k
+            if (tj == rk) {
+#pragma unroll
+                for (int a_ = 0; a_ < T; ++a_) {
+                    double v = 0.0;
+#pragma unroll
+                    for (int b_ = 0; b_ < T; ++b_)
+                        if (b_ == bk) v = a[a_][b_];
+                    s_col[buf][ti + 16 * a_] = v;
+                }
+            }
+            __syncthreads();
+            // 2. pivot: first row of maximal modulus among rows >= k
+            if (warp == 0) {
+                double best = -1.0;
+                int bi = INT_MAX;
+                for (int i = k + lane; i < n; i += 32) {
+                    const double v = fabs(s_col[buf][i]);
+                    if (v > best) { best = v; bi = i; }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+                    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                    if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+                }
+                if (lane == 0) {
+                    const double dkk = s_col[buf][k];
+                    s_ok = (dkk == dkk) && (best > tol);
+                    s_p = bi;
+                    s_piv[k] = bi;
+                }
+            }
+            __syncthreads();
+            if (!s_ok) { singular = true; break; }
+            const int p = s_p;
+            // 3. publish rows k and p (their pre-interchange contents)
+            if (ti == rk) {
+#pragma unroll
+                for (int b_ = 0; b_ < T; ++b_) {
+                    double v = 0.0;
+#pragma unroll
+                    for (int a_ = 0; a_ < T; ++a_)
+                        if (a_ == bk) v = a[a_][b_];
+                    s_rowk[buf][tj + 16 * b_] = v;
+                }
+            }
+            if (ti == (p & 15)) {
+                const int bp = p >> 4;
+#pragma unroll
+                for (int b_ = 0; b_ < T; ++b_) {
+                    double v = 0.0;
+#pragma unroll
+                    for (int a_ = 0; a_ < T; ++a_)
+                        if (a_ == bp) v = a[a_][b_];
+                    s_rowp[buf][tj + 16 * b_] = v;
+                }
+            }
+            __syncthreads();
+            // 4. interchange + rank-1 update of this thread's tile
+            const double inv = 1.0 / s_col[buf][p];
+            double rj[T];
+#pragma unroll
+            for (int b_ = 0; b_ < T; ++b_) rj[b_] = s_rowp[buf][tj + 16 * b_];
+#pragma unroll
+            for (int a_ = 0; a_ < T; ++a_) {
+                const int i = ti + 16 * a_;
+                if (i == k) {
+#pragma unroll
+                    for (int b_ = 0; b_ < T; ++b_) a[a_][b_] = (tj + 16 * b_ == k) ? inv : rj[b_] * inv;
+                } else {
+                    const bool was_p = (i == p);
+                    const double li = (was_p ? s_col[buf][k] : s_col[buf][i]) * inv;
+#pragma unroll
+                    for (int b_ = 0; b_ < T; ++b_) {
+                        const int j = tj + 16 * b_;
+                        const double base = was_p ? s_rowk[buf][j] : a[a_][b_];
+                        a[a_][b_] = (j == k) ? -li : fma(-li, rj[b_], base);
+                    }
+                }
+            }
+        }
+        if (singular) {
+            if (tid == 0) atomicMin(flags, static_cast<int>(blk));
+        } else {
+            // column permutation: inverse[:, j] = W[:, c[j]] with c = identity after the interchanges in
+            // reverse order; every thread writes its entries to column cinv[its column]
+            if (tid == 0) {
+                for (int j = 0; j < n; ++j) s_cinv[j] = j;  // used as c[] first
+                for (int k = n - 1; k >= 0; --k) {
+                    const int p = s_piv[k];
+                    const int t = s_cinv[k];
+                    s_cinv[k] = s_cinv[p];
+                    s_cinv[p] = t;
+                }
+                // invert c in place via s_piv as scratch
+                for (int j = 0; j < n; ++j) s_piv[s_cinv[j]] = j;
+            }
+            __syncthreads();
+            double* out = inv_out + blk * n * n;
+#pragma unroll
+            for (int b_ = 0; b_ < T; ++b_)
+#pragma unroll
+                for (int a_ = 0; a_ < T; ++a_) {
+                    const int i = ti + 16 * a_, j = tj + 16 * b_;
+                    if (i < n && j < n) out[static_cast<size_t>(s_piv[j]) * n + i] = a[a_][b_];
+                }
+        }
+        __syncthreads();
+    }
+}
+
 // ---- GEMM ----------------------------------------------------------------------------------------
 // Small blocks: one thread per output entry, several batch items per CTA; operands stream through
 // L1.  Ascending-k accumulation like the reference.
@@ -315,6 +475,16 @@ void launch_lu_invert_batch(hdgb_ctx* ctx, int n, int64_t batch, const double* a
         if (smem > 48 * 1024)
             HDGB_CUDA(cudaFuncSetAttribute(lu_invert_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         lu_invert_warp_kernel<<<ceil_div(batch, wpc), wpc * 32, smem, ctx->stream>>>(n, batch, a, inv, flags, wpc);
+        HDGB_LAUNCH_CHECK(ctx);
+        return;
+    }
+    if (n <= 128 && tuning().use_tile_lu) {
+        const int64_t cap = static_cast<int64_t>(ctx->sm_count) * 8;
+        const int grid = static_cast<int>(batch < cap ? batch : cap);
+        if (n <= 32) lu_invert_tile_kernel<2><<<grid, 256, 0, ctx->stream>>>(n, batch, a, inv, flags);
+        else if (n <= 64) lu_invert_tile_kernel<4><<<grid, 256, 0, ctx->stream>>>(n, batch, a, inv, flags);
+        else if (n <= 96) lu_invert_tile_kernel<6><<<grid, 256, 0, ctx->stream>>>(n, batch, a, inv, flags);
+        else lu_invert_tile_kernel<8><<<grid, 256, 0, ctx->stream>>>(n, batch, a, inv, flags);
         HDGB_LAUNCH_CHECK(ctx);
         return;
     }

@@ -76,16 +76,18 @@ __global__ void cmat_kernel(DiscView dv, double* __restrict__ c0, double* __rest
 }
 
 // ---- the assembly kernel -------------------------------------------------------------------------------
+// Point records keep the model coefficients already contracted with the inverse Jacobian
+// (index r = reference direction), so that the basis contraction needs d(phi_i)/d(xi_r) only:
+//   sum_d C_d * grad_d(phi_i) = sum_r dphi_r,i * (sum_d invj[r][d] * C_d).
 template <int M, int D>
 struct VolRec {
     double w;
-    double invj[D * D];
-    double F[M * D];
+    double Fr[M * D];          // [m*D + r]
     double S[M];
-    double tm[M];  // dt_inv * (u - u_prev)
-    double dFu[M * D * M];
+    double tm[M];              // dt_inv * (u - u_prev)
+    double cE[M * M * D];      // [(m*M + mp)*D + r]          from dF/du
     double dSu[M * M];
-    double dFq[M * D * M * D];
+    double cD[D * M * M * D];  // [((dp*M + m)*M + mp)*D + r] from dF/dq_dp
     double dSq[M * M * D];
 };
 
@@ -165,17 +167,38 @@ __global__ void __launch_bounds__(256) local_assemble_kernel(DiscView dv, ModelV
             for (int d = 0; d < D; ++d) qg[m * D + d] = aq[d];
         }
         r.w = dv.wq[g] * dv.elem_detjac[gi];
-        for (int k = 0; k < D * D; ++k) r.invj[k] = dv.elem_invjac[gi * D * D + k];
+        const double* ij = dv.elem_invjac + gi * D * D;  // ij[r*D + d] = d xi_r / d x_d
         const double* x = dv.elem_coords + gi * D;
         const double* f = mv.forcing_q ? mv.forcing_q + gi * M : nullptr;
-        model.flux(ug, qg, x, r.F);
+        double Fl[M * D];
+        model.flux(ug, qg, x, Fl);
         model.source(ug, qg, x, f, r.S);
-        for (int m = 0; m < M; ++m) r.tm[m] = transient ? in.dt_inv * (ug[m] - upg[m]) : 0.0;
+        for (int m = 0; m < M; ++m) {
+            r.tm[m] = transient ? in.dt_inv * (ug[m] - upg[m]) : 0.0;
+            for (int rr = 0; rr < D; ++rr) {
+                double sfl = 0.0;
+                for (int d = 0; d < D; ++d) sfl += Fl[m * D + d] * ij[rr * D + d];
+                r.Fr[m * D + rr] = sfl;
+            }
+        }
         if (want_jac) {
-            model.dflux_du(ug, qg, x, r.dFu);
-            model.dflux_dq(ug, qg, x, r.dFq);
+            double dFu[M * D * M], dFq[M * D * M * D];
+            model.dflux_du(ug, qg, x, dFu);
+            model.dflux_dq(ug, qg, x, dFq);
             model.dsource_du(ug, qg, x, r.dSu);
             model.dsource_dq(ug, qg, x, r.dSq);
+            for (int m = 0; m < M; ++m)
+                for (int mp = 0; mp < M; ++mp)
+                    for (int rr = 0; rr < D; ++rr) {
+                        double se = 0.0;
+                        for (int d = 0; d < D; ++d) se += dFu[(m * D + d) * M + mp] * ij[rr * D + d];
+                        r.cE[(m * M + mp) * D + rr] = se;
+                        for (int dp = 0; dp < D; ++dp) {
+                            double sd = 0.0;
+                            for (int d = 0; d < D; ++d) sd += dFq[((m * D + d) * M + mp) * D + dp] * ij[rr * D + d];
+                            r.cD[((dp * M + m) * M + mp) * D + rr] = sd;
+                        }
+                    }
         }
     }
     // ---- phase 1b: face points ----
@@ -258,15 +281,11 @@ __global__ void __launch_bounds__(256) local_assemble_kernel(DiscView dv, ModelV
         for (int g = 0; g < qe; ++g) {
             const VR& r = vrec[g];
             const double ph = dv.phi[i + pe * g];
-            double grad[D];
-            for (int d = 0; d < D; ++d) {
-                double s = 0.0;
-                for (int k = 0; k < D; ++k) s += dv.dphi[k][i + pe * g] * r.invj[k * D + d];
-                grad[d] = s;
-            }
+            double dp_[D];
+            for (int k = 0; k < D; ++k) dp_[k] = dv.dphi[k][i + pe * g];
             for (int m = 0; m < M; ++m) {
                 double fg = 0.0;
-                for (int d = 0; d < D; ++d) fg += r.F[m * D + d] * grad[d];
+                for (int k = 0; k < D; ++k) fg += r.Fr[m * D + k] * dp_[k];
                 double v = -fg - r.S[m] * ph;
                 if (transient) v += r.tm[m] * ph;
                 acc[m] += r.w * v;
@@ -293,54 +312,96 @@ __global__ void __launch_bounds__(256) local_assemble_kernel(DiscView dv, ModelV
     }
     if (!want_jac) return;
 
-    // ---- phase 2b: E and D_d, one (i, j) scalar-basis pair per thread, all component pairs ----
-    for (int t = tid; t < pe * pe; t += nt) {
-        const int j = t / pe, i = t - j * pe;
-        double aE[M * M], aD[D * M * M];
-        for (int k = 0; k < M * M; ++k) aE[k] = 0.0;
-        for (int k = 0; k < D * M * M; ++k) aD[k] = 0.0;
-        for (int g = 0; g < qe; ++g) {
-            const VR& r = vrec[g];
-            const double phi_i = dv.phi[i + pe * g];
-            const double pj = r.w * dv.phi[j + pe * g];
-            double grad[D];
-            for (int d = 0; d < D; ++d) {
-                double s = 0.0;
-                for (int k = 0; k < D; ++k) s += dv.dphi[k][i + pe * g] * r.invj[k * D + d];
-                grad[d] = s;
-            }
-            for (int m = 0; m < M; ++m)
-                for (int mp = 0; mp < M; ++mp) {
-                    double fe = 0.0;
-                    for (int d = 0; d < D; ++d) fe += r.dFu[(m * D + d) * M + mp] * grad[d];
-                    double eij = -fe - r.dSu[m * M + mp] * phi_i;
-                    if (transient && m == mp) eij += in.dt_inv * phi_i;
-                    aE[m * M + mp] += pj * eij;
-                    for (int dp = 0; dp < D; ++dp) {
-                        double fd = 0.0;
-                        for (int d = 0; d < D; ++d) fd += r.dFq[((m * D + d) * M + mp) * D + dp] * grad[d];
-                        aD[(dp * M + m) * M + mp] += pj * (-fd - r.dSq[(m * M + mp) * D + dp] * phi_i);
+    // ---- phase 2b: E and D_d.  A thread owns a TI x TJ tile of scalar-basis pairs (i, j) and all
+    // component pairs; per point it forms the i-side values once and rank-1 updates the tile ----
+    {
+        constexpr int TI = (M == 1) ? 2 : 1, TJ = (M == 1) ? 4 : 1;
+        constexpr int Q = M * M * (1 + D);  // E then D_0..D_{D-1} per component pair
+        const int nti = (pe + TI - 1) / TI, ntj = (pe + TJ - 1) / TJ;
+        for (int t = tid; t < nti * ntj; t += nt) {
+            const int bj = t / nti, bi = t - bj * nti;
+            double acc[TI][TJ][Q];
+#pragma unroll
+            for (int a = 0; a < TI; ++a)
+#pragma unroll
+                for (int b = 0; b < TJ; ++b)
+#pragma unroll
+                    for (int q = 0; q < Q; ++q) acc[a][b][q] = 0.0;
+            for (int g = 0; g < qe; ++g) {
+                const VR& r = vrec[g];
+                double val[TI][Q];
+#pragma unroll
+                for (int a = 0; a < TI; ++a) {
+                    const int i = min(bi * TI + a, pe - 1);
+                    const double phi_i = dv.phi[i + pe * g];
+                    double dp_[D];
+#pragma unroll
+                    for (int k = 0; k < D; ++k) dp_[k] = dv.dphi[k][i + pe * g];
+#pragma unroll
+                    for (int mm = 0; mm < M * M; ++mm) {
+                        double fe = 0.0;
+#pragma unroll
+                        for (int k = 0; k < D; ++k) fe += r.cE[mm * D + k] * dp_[k];
+                        double eij = -fe - r.dSu[mm] * phi_i;
+                        if (transient && (mm / M) == (mm % M)) eij += in.dt_inv * phi_i;
+                        val[a][mm] = eij;
+#pragma unroll
+                        for (int dp = 0; dp < D; ++dp) {
+                            double fd = 0.0;
+#pragma unroll
+                            for (int k = 0; k < D; ++k) fd += r.cD[(dp * M * M + mm) * D + k] * dp_[k];
+                            val[a][M * M * (1 + dp) + mm] = -fd - r.dSq[mm * D + dp] * phi_i;
+                        }
                     }
                 }
-        }
-        for (int p = 0; p < nfp; ++p) {
-            const int lf = p / qf, gc = p - lf * qf;
-            const FR& r = frec[p];
-            const double* phis = dv.tphi + ((static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf + gc) * pe;
-            const double pj = r.w * phis[j];
-            const double ph = phis[i];
-            for (int m = 0; m < M; ++m) {
-                aE[m * M + m] += pj * r.tau * ph;
-                for (int mp = 0; mp < M; ++mp)
-                    for (int dp = 0; dp < D; ++dp) aD[(dp * M + m) * M + mp] += pj * r.dfh_q[(m * M + mp) * D + dp] * ph;
+#pragma unroll
+                for (int b = 0; b < TJ; ++b) {
+                    const int j = min(bj * TJ + b, pe - 1);
+                    const double pj = r.w * dv.phi[j + pe * g];
+#pragma unroll
+                    for (int a = 0; a < TI; ++a)
+#pragma unroll
+                        for (int q = 0; q < Q; ++q) acc[a][b][q] = fma(pj, val[a][q], acc[a][b][q]);
+                }
             }
-        }
-        for (int m = 0; m < M; ++m)
-            for (int mp = 0; mp < M; ++mp) {
-                const size_t o = static_cast<size_t>(e) * npe * npe + static_cast<size_t>(mp * pe + j) * npe + (m * pe + i);
-                out.E[o] = aE[m * M + mp];
-                for (int dp = 0; dp < D; ++dp) out.Dm[dp][o] = aD[(dp * M + m) * M + mp];
+            for (int p = 0; p < nfp; ++p) {
+                const int lf = p / qf, gc = p - lf * qf;
+                const FR& r = frec[p];
+                const double* phis = dv.tphi + ((static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf + gc) * pe;
+                double val[TI][Q];
+#pragma unroll
+                for (int a = 0; a < TI; ++a) {
+                    const double ph = phis[min(bi * TI + a, pe - 1)];
+#pragma unroll
+                    for (int mm = 0; mm < M * M; ++mm) {
+                        val[a][mm] = ((mm / M) == (mm % M)) ? r.tau * ph : 0.0;
+#pragma unroll
+                        for (int dp = 0; dp < D; ++dp) val[a][M * M * (1 + dp) + mm] = r.dfh_q[mm * D + dp] * ph;
+                    }
+                }
+#pragma unroll
+                for (int b = 0; b < TJ; ++b) {
+                    const double pj = r.w * phis[min(bj * TJ + b, pe - 1)];
+#pragma unroll
+                    for (int a = 0; a < TI; ++a)
+#pragma unroll
+                        for (int q = 0; q < Q; ++q) acc[a][b][q] = fma(pj, val[a][q], acc[a][b][q]);
+                }
             }
+#pragma unroll
+            for (int a = 0; a < TI; ++a)
+#pragma unroll
+                for (int b = 0; b < TJ; ++b) {
+                    const int i = bi * TI + a, j = bj * TJ + b;
+                    if (i >= pe || j >= pe) continue;
+                    for (int m = 0; m < M; ++m)
+                        for (int mp = 0; mp < M; ++mp) {
+                            const size_t o = static_cast<size_t>(e) * npe * npe + static_cast<size_t>(mp * pe + j) * npe + (m * pe + i);
+                            out.E[o] = acc[a][b][m * M + mp];
+                            for (int dp = 0; dp < D; ++dp) out.Dm[dp][o] = acc[a][b][M * M * (1 + dp) + m * M + mp];
+                        }
+                }
+        }
     }
     // ---- H and G_d: rows (lf, m, b), columns (mp, j) ----
     for (int t = tid; t < n_lfe * pf * pe; t += nt) {

@@ -33,6 +33,7 @@ bool launch_stream_gemv(hdgb_ctx* ctx, const GemvArgs& g);
 struct Tuning {
     int use_stream = 1;                  // route large GEMVs through the TMA stream kernel
     int64_t stream_min_elems = 1 << 18;  // below this many matrix entries the team kernel is used
+    int use_tile_lu = 1;                 // register-tiled Gauss-Jordan for 25 <= n <= 128
 };
 Tuning& tuning();
 

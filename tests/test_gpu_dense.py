@@ -1,0 +1,64 @@
+"""Batched dense kernels against numpy and the reference's own dense_batch tests
+(test_dense_batch.cpp): inverse accuracy, pivoting, lowest singular batch index, broadcast GEMM."""
+import numpy as np
+import pytest
+
+import paper_2512_13619_b200 as hdg
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(params=["tile", "smem"])
+def lu_kernel(request):
+    hdg.set_tuning("use_tile_lu", 1 if request.param == "tile" else 0)
+    yield request.param
+    hdg.set_tuning("use_tile_lu", 1)
+
+
+@pytest.mark.parametrize("n,batch", [(1, 5), (2, 9), (5, 33), (9, 100), (12, 64), (16, 40), (24, 17), (25, 21), (32, 20),
+                                     (40, 11), (64, 9), (70, 5), (96, 7), (100, 3), (128, 2), (150, 2)])
+def test_lu_invert_batch(ctx, lu_kernel, n, batch):
+    rng = np.random.default_rng(n)
+    a = rng.standard_normal((batch, n, n)) + 0.1 * n * np.eye(n)[None]
+    a[0] = np.eye(n)[rng.permutation(n)]                       # pure permutation: pivoting (test_dense_batch.cpp:88-96)
+    got = hdg.lu_invert_batch(ctx, np.transpose(a, (0, 2, 1)).ravel(), n, batch).reshape(batch, n, n).transpose(0, 2, 1)
+    for b in range(batch):
+        defect = np.max(np.abs(a[b] @ got[b] - np.eye(n)))
+        assert defect <= 1e-10, (b, defect)                    # test_dense_batch.cpp:71-86
+    assert np.array_equal(got[0], a[0].T)
+
+
+@pytest.mark.parametrize("n", [3, 20, 40, 96])
+def test_singular_block_reports_lowest_index(ctx, lu_kernel, n):
+    rng = np.random.default_rng(7)
+    a = rng.standard_normal((6, n, n)) + n * np.eye(n)[None]
+    a[4] = 0.0
+    a[2, :, 1] = a[2, :, 0]                                    # rank deficient
+    with pytest.raises(hdg.SingularBlock) as ei:
+        hdg.lu_invert_batch(ctx, np.transpose(a, (0, 2, 1)).ravel(), n, 6)
+    assert ei.value.index == 2                                 # lowest bad index (dense_batch.cpp:84-97)
+    a[2] = np.eye(n)
+    with pytest.raises(hdg.SingularBlock) as ei:
+        hdg.lu_invert_batch(ctx, np.transpose(a, (0, 2, 1)).ravel(), n, 6)
+    assert ei.value.index == 4
+    a[4] = np.nan
+    with pytest.raises(hdg.SingularBlock):
+        hdg.lu_invert_batch(ctx, np.transpose(a, (0, 2, 1)).ravel(), n, 6)
+
+
+@pytest.mark.parametrize("m,k,n,batch", [(3, 4, 5, 7), (9, 9, 12, 33), (64, 64, 96, 3), (96, 64, 96, 2), (20, 33, 17, 5)])
+def test_gemm_batch_and_broadcast(ctx, m, k, n, batch):
+    rng = np.random.default_rng(m * 7 + n)
+    a = rng.standard_normal((batch, k, m))                     # [b][col][row]: column-major m x k
+    b = rng.standard_normal((batch, n, k))
+    want = np.einsum("bkm,bnk->bnm", a, b)                     # C[b][col n][row m]
+    tol = 1e-13 * k * max(1.0, np.max(np.abs(want)))
+    got = hdg.gemm_batch(ctx, a.ravel(), m, k, batch, b.ravel(), k, n, batch).reshape(batch, n, m)
+    assert np.max(np.abs(got - want)) <= tol
+    got = hdg.gemm_batch(ctx, a[0].ravel(), m, k, 1, b.ravel(), k, n, batch).reshape(batch, n, m)   # A broadcast
+    assert np.max(np.abs(got - np.einsum("km,bnk->bnm", a[0], b))) <= tol
+    at = rng.standard_normal((batch, m, k))                    # stored k x m, used transposed
+    got = hdg.gemm_batch(ctx, at.ravel(), k, m, batch, b.ravel(), k, n, batch, transpose_a=True).reshape(batch, n, m)
+    assert np.max(np.abs(got - np.einsum("bmk,bnk->bnm", at, b))) <= tol
+    with pytest.raises(hdg.DimensionMismatch):
+        hdg.gemm_batch(ctx, a.ravel(), m, k, batch, b.ravel(), k + 1, n, batch)
