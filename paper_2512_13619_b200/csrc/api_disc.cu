@@ -238,6 +238,8 @@ hdgb_status hdgb_disc_get_f64(const hdgb_disc* d, const char* name, double* out,
     if (s == "tphi") return get_vec(d, me.tphi, out, cap, n);
     if (s == "tphi_local") return get_vec(d, me.tphi_local, out, cap, n);
     if (s == "nodes1d") return get_vec(d, me.nodes1d, out, cap, n);
+    if (s == "elem_nodes") return get_vec(d, me.elem_nodes, out, cap, n);
+    if (s == "face_nodes") return get_vec(d, me.face_nodes, out, cap, n);
     if (s == "rule1d_points") return get_vec(d, me.rule1d.pts, out, cap, n);
     if (s == "rule1d_weights") return get_vec(d, me.rule1d.wts, out, cap, n);
     if (s == "elem_points") return get_vec(d, me.elem_pts, out, cap, n);
@@ -507,7 +509,11 @@ hdgb_ops* assemble_element_operators_device(hdgb_disc* d, const hdgb_model* m, h
 
     // Raw-block workspace: bounded chunk of elements (whole mesh when the raw blocks are kept).
     const size_t per_elem = sEE * (1 + D) + sEF * (2 + D) + sFF;
-    size_t chunk = keep_raw ? ne : static_cast<size_t>(6.0e9 / (per_elem * sizeof(double)));
+    // the workspace may take up to a third of the free HBM (180 GB parts: config 2 runs in one chunk)
+    size_t free_b = 0, total_b = 0;
+    HDGB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const double budget = std::max(2.0e9, static_cast<double>(free_b) / 3.0);
+    size_t chunk = keep_raw ? ne : static_cast<size_t>(budget / (per_elem * sizeof(double)));
     if (chunk < 1) chunk = 1;
     if (chunk > static_cast<size_t>(ne)) chunk = ne;
     DevBuf<double> wE, wD[3], wG[3], wJ, wT;

@@ -126,10 +126,22 @@ const ShapeInfo& shape_info(int shape) {
     static const ShapeInfo hex = {3, 6, 8, 4, 8,
                                   {{0, 1, 2, 3}, {0, 1, 5, 4}, {1, 2, 6, 5}, {3, 2, 6, 7}, {0, 3, 7, 4}, {4, 5, 6, 7}},
                                   {-1, +1, +1, -1, -1, +1}};
+    // Triangle: CCW vertices (0,0),(1,0),(0,1); faces v0v1, v1v2, v2v0 traversed first -> second
+    // vertex; outward normal = tangent rotated -90 degrees on every face.
+    static const ShapeInfo tri = {2, 3, 3, 2, 2,
+                                  {{0, 1, -1, -1}, {1, 2, -1, -1}, {2, 0, -1, -1}, {-1, -1, -1, -1}, {-1, -1, -1, -1}, {-1, -1, -1, -1}},
+                                  {+1, +1, +1, 0, 0, 0}};
+    // Tetrahedron: positively oriented (0,0,0),(1,0,0),(0,1,0),(0,0,1); every face is listed so that
+    // (b - a) x (c - a) points outward.  6 relative orientations of a triangular face.
+    static const ShapeInfo tet = {3, 4, 4, 3, 6,
+                                  {{1, 2, 3, -1}, {0, 3, 2, -1}, {0, 1, 3, -1}, {0, 2, 1, -1}, {-1, -1, -1, -1}, {-1, -1, -1, -1}},
+                                  {+1, +1, +1, +1, 0, 0}};
     switch (shape) {
         case HDGB_QUAD: return quad;
         case HDGB_HEX: return hex;
-        default: throw Failure(HDGB_ERR_UNSUPPORTED, "element shape not supported yet (quad and hex are)");
+        case HDGB_TRI: return tri;
+        case HDGB_TET: return tet;
+        default: throw Failure(HDGB_ERR_UNSUPPORTED, "unknown element shape");
     }
 }
 
@@ -144,6 +156,23 @@ void face_point(int shape, int lf, double s, double t, double* xi) {
             case 2: xi[0] = s; xi[1] = 1.0; break;
             default: xi[0] = 0.0; xi[1] = s; break;
         }
+        return;
+    }
+    if (shape == HDGB_TRI) {
+        switch (lf) {
+            case 0: xi[0] = s; xi[1] = 0.0; break;
+            case 1: xi[0] = 1.0 - s; xi[1] = s; break;
+            default: xi[0] = 0.0; xi[1] = 1.0 - s; break;
+        }
+        return;
+    }
+    if (shape == HDGB_TET) {
+        static const double rv[4][3] = {{0, 0, 0}, {1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
+        const ShapeInfo& si = shape_info(shape);
+        const double* a = rv[si.face_verts[lf][0]];
+        const double* b = rv[si.face_verts[lf][1]];
+        const double* c = rv[si.face_verts[lf][2]];
+        for (int d = 0; d < 3; ++d) xi[d] = a[d] + s * (b[d] - a[d]) + t * (c[d] - a[d]);
         return;
     }
     switch (lf) {  // hex
@@ -169,9 +198,183 @@ int local_corner(int o, int j) {
 
 }  // namespace
 
+namespace {
+
+// ---- simplex master elements --------------------------------------------------------------------
+// Nodal basis on the principal lattice of order k: for the node with barycentric lattice indices
+// (i_0 .. i_D), sum = k,  phi(lambda) = prod_d N_{i_d}(lambda_d),  N_i(l) = prod_{m<i} (k l - m)/(i - m)
+// -- a closed form (no Vandermonde inversion); derivatives by the product rule.
+double lattice_factor(int k, int i, double l) {
+    double v = 1.0;
+    for (int m = 0; m < i; ++m) v *= (k * l - m) / static_cast<double>(i - m);
+    return v;
+}
+double lattice_factor_deriv(int k, int i, double l) {
+    double total = 0.0;
+    for (int q = 0; q < i; ++q) {
+        double term = k / static_cast<double>(i - q);
+        for (int m = 0; m < i; ++m)
+            if (m != q) term *= (k * l - m) / static_cast<double>(i - m);
+        total += term;
+    }
+    return total;
+}
+
+// lattice index tuples (i_1 .. i_dim) with i_1 fastest; i_0 = k - sum
+std::vector<std::array<int, 3>> lattice_nodes(int dim, int k) {
+    std::vector<std::array<int, 3>> out;
+    if (dim == 1) {
+        for (int a = 0; a <= k; ++a) out.push_back({a, 0, 0});
+    } else if (dim == 2) {
+        for (int b = 0; b <= k; ++b)
+            for (int a = 0; a + b <= k; ++a) out.push_back({a, b, 0});
+    } else {
+        for (int c = 0; c <= k; ++c)
+            for (int b = 0; b + c <= k; ++b)
+                for (int a = 0; a + b + c <= k; ++a) out.push_back({a, b, c});
+    }
+    return out;
+}
+
+// values (and optionally d/dxi_r) of all lattice basis functions at the reference point xi
+void simplex_basis(int dim, int k, const std::vector<std::array<int, 3>>& nodes, const double* xi, double* val,
+                   double* const* dval) {
+    double lam[4], sum = 0.0;
+    for (int d = 0; d < dim; ++d) { lam[d + 1] = xi[d]; sum += xi[d]; }
+    lam[0] = 1.0 - sum;
+    for (size_t n = 0; n < nodes.size(); ++n) {
+        int idx[4] = {k, 0, 0, 0};
+        for (int d = 0; d < dim; ++d) { idx[d + 1] = nodes[n][d]; idx[0] -= nodes[n][d]; }
+        double f[4], df[4];
+        for (int d = 0; d <= dim; ++d) {
+            f[d] = lattice_factor(k, idx[d], lam[d]);
+            df[d] = dval ? lattice_factor_deriv(k, idx[d], lam[d]) : 0.0;
+        }
+        double v = 1.0;
+        for (int d = 0; d <= dim; ++d) v *= f[d];
+        val[n] = v;
+        if (dval) {
+            double dl[4];  // d phi / d lambda_d
+            for (int d = 0; d <= dim; ++d) {
+                double t = df[d];
+                for (int e = 0; e <= dim; ++e)
+                    if (e != d) t *= f[e];
+                dl[d] = t;
+            }
+            for (int r = 0; r < dim; ++r) dval[r][n] = dl[r + 1] - dl[0];  // lambda_0 = 1 - sum xi
+        }
+    }
+}
+
+// canonical -> side-local barycentric map of a triangular face for orientation o (orientation_of):
+// o < 3: local[(o + j) % 3] = canon[j];  o >= 3: local[(o - 3 - j) mod 3] = canon[j]
+void tri_face_local_params(int o, double s, double t, double& ls, double& lt) {
+    const double lc[3] = {1.0 - s - t, s, t};
+    double ll[3];
+    for (int j = 0; j < 3; ++j) {
+        const int r = o % 3;
+        const int li = (o < 3) ? (r + j) % 3 : ((r - j) % 3 + 3) % 3;
+        ll[li] = lc[j];
+    }
+    ls = ll[1];
+    lt = ll[2];
+}
+
+MasterElement make_simplex_master(int shape, int degree, int quad_points) {
+    const ShapeInfo& si = shape_info(shape);
+    MasterElement me;
+    me.shape = shape; me.dim = si.dim; me.degree = degree; me.n_lfe = si.n_lfe; me.n_orient = si.n_orient;
+    const int D = si.dim, k = degree;
+    const int q = quad_points > 0 ? quad_points : degree + 2;
+    me.rule1d = gauss_rule(q);
+    me.nodes1d.resize(k + 1);
+    for (int a = 0; a <= k; ++a) me.nodes1d[a] = static_cast<double>(a) / k;
+    const std::vector<double>& p = me.rule1d.pts;
+    const std::vector<double>& w = me.rule1d.wts;
+    const auto enodes = lattice_nodes(D, k);
+    const auto fnodes = lattice_nodes(D - 1, k);
+    me.pe = static_cast<int>(enodes.size());
+    me.pf = static_cast<int>(fnodes.size());
+    me.elem_nodes.resize(static_cast<size_t>(me.pe) * D);
+    for (int n = 0; n < me.pe; ++n)
+        for (int d = 0; d < D; ++d) me.elem_nodes[static_cast<size_t>(n) * D + d] = static_cast<double>(enodes[n][d]) / k;
+    me.face_nodes.resize(static_cast<size_t>(me.pf) * (D - 1));
+    for (int n = 0; n < me.pf; ++n)
+        for (int d = 0; d < D - 1; ++d) me.face_nodes[static_cast<size_t>(n) * (D - 1) + d] = static_cast<double>(fnodes[n][d]) / k;
+
+    // Collapsed-coordinate (Duffy) Gauss rules: x = u, y = v (1 - u) [, z = w (1 - u)(1 - v)];
+    // q points per direction integrate total degree 2q - D exactly.
+    me.qe = (D == 2) ? q * q : q * q * q;
+    me.elem_pts.resize(static_cast<size_t>(me.qe) * D);
+    me.elem_wts.resize(me.qe);
+    for (int g = 0; g < me.qe; ++g) {
+        const int gu = g % q, gv = (g / q) % q, gw = g / (q * q);
+        const double u = p[gu], v = p[gv];
+        if (D == 2) {
+            me.elem_pts[2 * g] = u;
+            me.elem_pts[2 * g + 1] = v * (1.0 - u);
+            me.elem_wts[g] = w[gu] * w[gv] * (1.0 - u);
+        } else {
+            // nested collapse: x = u, y = v (1 - u), z = ww (1 - u)(1 - v)
+            const double ww = p[gw];
+            me.elem_pts[3 * g] = u;
+            me.elem_pts[3 * g + 1] = v * (1.0 - u);
+            me.elem_pts[3 * g + 2] = ww * (1.0 - u) * (1.0 - v);
+            me.elem_wts[g] = w[gu] * w[gv] * w[gw] * (1.0 - u) * (1.0 - u) * (1.0 - v);
+        }
+    }
+    me.qf = (D == 2) ? q : q * q;
+    me.face_pts.resize(static_cast<size_t>(me.qf) * (D - 1));
+    me.face_wts.resize(me.qf);
+    for (int g = 0; g < me.qf; ++g) {
+        if (D == 2) {
+            me.face_pts[g] = p[g];
+            me.face_wts[g] = w[g];
+        } else {
+            const double u = p[g % q], v = p[g / q];
+            me.face_pts[2 * g] = u;
+            me.face_pts[2 * g + 1] = v * (1.0 - u);
+            me.face_wts[g] = w[g % q] * w[g / q] * (1.0 - u);
+        }
+    }
+
+    me.phi.resize(static_cast<size_t>(me.pe) * me.qe);
+    for (int d = 0; d < D; ++d) me.dphi[d].resize(me.phi.size());
+    for (int g = 0; g < me.qe; ++g) {
+        const size_t o = static_cast<size_t>(me.pe) * g;
+        double* dv[3] = {&me.dphi[0][o], &me.dphi[1][o], D == 3 ? &me.dphi[2][o] : nullptr};
+        simplex_basis(D, k, enodes, &me.elem_pts[static_cast<size_t>(g) * D], &me.phi[o], dv);
+    }
+    me.psi.resize(static_cast<size_t>(me.pf) * me.qf);
+    for (int g = 0; g < me.qf; ++g)
+        simplex_basis(D - 1, k, fnodes, &me.face_pts[static_cast<size_t>(g) * (D - 1)], &me.psi[static_cast<size_t>(me.pf) * g], nullptr);
+
+    // element basis on local face lf seen with orientation o at the CANONICAL face point gc
+    me.tphi_local.resize(static_cast<size_t>(me.n_lfe) * me.qf * me.pe);
+    me.tphi.resize(static_cast<size_t>(me.n_lfe) * me.n_orient * me.qf * me.pe);
+    for (int lf = 0; lf < me.n_lfe; ++lf)
+        for (int o = 0; o < me.n_orient; ++o)
+            for (int gc = 0; gc < me.qf; ++gc) {
+                double ls, lt = 0.0, xi[3];
+                if (D == 2) {
+                    ls = (o == 0) ? me.face_pts[gc] : 1.0 - me.face_pts[gc];
+                } else {
+                    tri_face_local_params(o, me.face_pts[2 * gc], me.face_pts[2 * gc + 1], ls, lt);
+                }
+                face_point(shape, lf, ls, lt, xi);
+                double* dst = &me.tphi[((static_cast<size_t>(lf) * me.n_orient + o) * me.qf + gc) * me.pe];
+                simplex_basis(D, k, enodes, xi, dst, nullptr);
+                if (o == 0) std::copy(dst, dst + me.pe, &me.tphi_local[(static_cast<size_t>(lf) * me.qf + gc) * me.pe]);
+            }
+    return me;
+}
+
+}  // namespace
+
 MasterElement make_master_element(int shape, int degree, int quad_points) {
     if (degree < 1 || degree > 6)
         throw Failure(HDGB_ERR_UNSUPPORTED, "supported polynomial degrees are 1..6, got " + std::to_string(degree));
+    if (shape == HDGB_TRI || shape == HDGB_TET) return make_simplex_master(shape, degree, quad_points);
     const ShapeInfo& si = shape_info(shape);
     MasterElement me;
     me.shape = shape;
@@ -302,6 +505,16 @@ MasterElement make_master_element(int shape, int degree, int quad_points) {
                 double* dst = &me.tphi[((static_cast<size_t>(lf) * me.n_orient + o) * me.qf + gc) * me.pe];
                 std::copy(src, src + me.pe, dst);
             }
+    me.elem_nodes.resize(static_cast<size_t>(me.pe) * D);
+    for (int i = 0; i < me.pe; ++i) {
+        const int idx[3] = {i % n1, (i / n1) % n1, i / (n1 * n1)};
+        for (int d = 0; d < D; ++d) me.elem_nodes[static_cast<size_t>(i) * D + d] = me.nodes1d[idx[d]];
+    }
+    me.face_nodes.resize(static_cast<size_t>(me.pf) * (D - 1));
+    for (int j = 0; j < me.pf; ++j) {
+        me.face_nodes[static_cast<size_t>(j) * (D - 1)] = me.nodes1d[j % n1];
+        if (D == 3) me.face_nodes[2 * j + 1] = me.nodes1d[j / n1];
+    }
     return me;
 }
 
@@ -326,7 +539,7 @@ int orientation_of(const ShapeInfo& si, const int* local_verts, const int* canon
     for (int r = 0; r < nv; ++r) {
         if (local_verts[r] != canon[0]) continue;
         if (local_verts[(r + 1) % nv] == canon[1]) return r;
-        if (local_verts[(r + nv - 1) % nv] == canon[1]) return r + 4;
+        if (local_verts[(r + nv - 1) % nv] == canon[1]) return r + nv;
     }
     throw Failure(HDGB_ERR_INVALID_MESH, "face vertex lists of adjacent elements do not match");
 }
@@ -560,7 +773,77 @@ HostMesh build_structured_mesh(int shape, int n, const double* lo, const double*
         apply_jitter(m, n, lo, hi, jitter, seed, lattice);
         return m;
     }
-    throw Failure(HDGB_ERR_UNSUPPORTED, "structured builder: shape not supported yet");
+    if (shape == HDGB_TRI || shape == HDGB_TET) {
+        // TRI: every cell of the n x n grid is cut along its (v00, v11) diagonal into two CCW
+        // triangles.  TET: every cube is cut into the 6 Kuhn tetrahedra (one per monotone lattice
+        // path (0,0,0) -> (1,1,1)); the same pattern in every cube is conforming.
+        const int nv = (D == 2) ? nv1 * nv1 : nv1 * nv1 * nv1;
+        std::vector<double> coords(static_cast<size_t>(nv) * D);
+        std::vector<int> lattice(static_cast<size_t>(nv) * D);
+        double h[3] = {0, 0, 0};
+        for (int d = 0; d < D; ++d) h[d] = (hi[d] - lo[d]) / n;
+        auto vertex = [nv1](int i, int j, int k) { return (k * nv1 + j) * nv1 + i; };
+        for (int k = 0; k < (D == 3 ? nv1 : 1); ++k)
+            for (int j = 0; j < nv1; ++j)
+                for (int i = 0; i < nv1; ++i) {
+                    const int v = vertex(i, j, k);
+                    const int ijk[3] = {i, j, k};
+                    for (int d = 0; d < D; ++d) {
+                        coords[static_cast<size_t>(v) * D + d] = lo[d] + ijk[d] * h[d];
+                        lattice[static_cast<size_t>(v) * D + d] = ijk[d];
+                    }
+                }
+        std::vector<int32_t> ev;
+        if (D == 2) {
+            for (int j = 0; j < n; ++j)
+                for (int i = 0; i < n; ++i) {
+                    const int v00 = vertex(i, j, 0), v10 = vertex(i + 1, j, 0), v11 = vertex(i + 1, j + 1, 0), v01 = vertex(i, j + 1, 0);
+                    const int t[6] = {v00, v10, v11, v00, v11, v01};
+                    ev.insert(ev.end(), t, t + 6);
+                }
+        } else {
+            static const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+            static const int sign[6] = {+1, -1, -1, +1, +1, -1};
+            for (int k = 0; k < n; ++k)
+                for (int j = 0; j < n; ++j)
+                    for (int i = 0; i < n; ++i)
+                        for (int pp = 0; pp < 6; ++pp) {
+                            int c[3] = {i, j, k};
+                            int t[4];
+                            t[0] = vertex(c[0], c[1], c[2]);
+                            for (int s2 = 0; s2 < 3; ++s2) {
+                                c[perms[pp][s2]] += 1;
+                                t[s2 + 1] = vertex(c[0], c[1], c[2]);
+                            }
+                            if (sign[pp] < 0) std::swap(t[1], t[2]);  // keep the tetrahedron positively oriented
+                            ev.insert(ev.end(), t, t + 4);
+                        }
+        }
+        const int ne = static_cast<int>(ev.size()) / si.vpe;
+        HostMesh m = build_mesh_from_elements(shape, ne, nv, ev.data(), coords.data());
+        for (int f = 0; f < m.nf; ++f) {
+            if (m.face_elems[2 * f + 1] >= 0) continue;
+            int mn[3] = {n, n, n}, mx[3] = {0, 0, 0};
+            for (int k = 0; k < si.vpf; ++k) {
+                const int v = m.face_verts[static_cast<size_t>(f) * si.vpf + k];
+                for (int d = 0; d < D; ++d) {
+                    mn[d] = std::min(mn[d], lattice[static_cast<size_t>(v) * D + d]);
+                    mx[d] = std::max(mx[d], lattice[static_cast<size_t>(v) * D + d]);
+                }
+            }
+            int tag = 1;
+            if (mx[1] == 0) tag = 1;
+            else if (mn[0] == n) tag = 2;
+            else if (mn[1] == n) tag = 3;
+            else if (mx[0] == 0) tag = 4;
+            else if (D == 3 && mx[2] == 0) tag = 5;
+            else if (D == 3 && mn[2] == n) tag = 6;
+            m.bnd_tag[f] = tag;
+        }
+        apply_jitter(m, n, lo, hi, jitter, seed, lattice);
+        return m;
+    }
+    throw Failure(HDGB_ERR_UNSUPPORTED, "structured builder: unknown shape");
 }
 
 // ---- geometry ----------------------------------------------------------------------------------
@@ -712,7 +995,97 @@ HostGeom compute_geometry(const HostMesh& mesh, const MasterElement& me) {
         }
         return g;
     }
-    throw Failure(HDGB_ERR_UNSUPPORTED, "compute_geometry: shape not supported yet");
+    if (mesh.shape == HDGB_TRI || mesh.shape == HDGB_TET) {
+        // affine elements: constant Jacobian
+        const int vpe = si.vpe, vpf = si.vpf;
+        for (int e = 0; e < mesh.ne; ++e) {
+            double v[4][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+            for (int c = 0; c < vpe; ++c)
+                for (int d = 0; d < D; ++d) v[c][d] = mesh.coords[static_cast<size_t>(mesh.elem_verts[static_cast<size_t>(e) * vpe + c]) * D + d];
+            double J[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};  // J[c][r] = d x_c / d xi_r
+            for (int c = 0; c < D; ++c)
+                for (int r = 0; r < D; ++r) J[c][r] = v[r + 1][c] - v[0][c];
+            double det, inv[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+            if (D == 2) {
+                det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+                if (det > 0.0) {
+                    inv[0][0] = J[1][1] / det; inv[0][1] = -J[0][1] / det;
+                    inv[1][0] = -J[1][0] / det; inv[1][1] = J[0][0] / det;
+                }
+            } else {
+                const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+                const double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+                const double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+                det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+                if (det > 0.0) {
+                    const double id = 1.0 / det;
+                    inv[0][0] = c00 * id;
+                    inv[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * id;
+                    inv[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * id;
+                    inv[1][0] = c01 * id;
+                    inv[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * id;
+                    inv[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * id;
+                    inv[2][0] = c02 * id;
+                    inv[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * id;
+                    inv[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * id;
+                }
+            }
+            if (!(det > 0.0))
+                throw Failure(HDGB_ERR_INVALID_MESH, "non-positive Jacobian determinant in element " + std::to_string(e), e);
+            for (int q = 0; q < qe; ++q) {
+                const size_t idx = static_cast<size_t>(e) * qe + q;
+                g.elem_detjac[idx] = det;
+                for (int r = 0; r < D; ++r)
+                    for (int c = 0; c < D; ++c) g.elem_invjac[idx * D * D + r * D + c] = inv[r][c];  // d xi_r / d x_c
+                for (int c = 0; c < D; ++c) {
+                    double x = v[0][c];
+                    for (int r = 0; r < D; ++r) x += J[c][r] * me.elem_pts[static_cast<size_t>(q) * D + r];
+                    g.elem_coords[idx * D + c] = x;
+                }
+            }
+        }
+        for (int f = 0; f < mesh.nf; ++f) {
+            double c[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+            for (int k = 0; k < vpf; ++k)
+                for (int d = 0; d < D; ++d) c[k][d] = mesh.coords[static_cast<size_t>(mesh.face_verts[static_cast<size_t>(f) * vpf + k]) * D + d];
+            double nrm[3] = {0, 0, 0}, meas;
+            if (D == 2) {
+                const double tx = c[1][0] - c[0][0], ty = c[1][1] - c[0][1];
+                meas = std::hypot(tx, ty);
+                nrm[0] = ty / meas;   // canonical tangent rotated by -90 degrees
+                nrm[1] = -tx / meas;
+            } else {
+                double ab[3], ac[3];
+                for (int d = 0; d < 3; ++d) { ab[d] = c[1][d] - c[0][d]; ac[d] = c[2][d] - c[0][d]; }
+                const double cr[3] = {ab[1] * ac[2] - ab[2] * ac[1], ab[2] * ac[0] - ab[0] * ac[2], ab[0] * ac[1] - ab[1] * ac[0]};
+                meas = std::sqrt(cr[0] * cr[0] + cr[1] * cr[1] + cr[2] * cr[2]);
+                for (int d = 0; d < 3; ++d) nrm[d] = cr[d] / meas;
+            }
+            for (int q = 0; q < qf; ++q) {
+                const size_t idx = static_cast<size_t>(f) * qf + q;
+                g.face_detjac[idx] = meas;  // reference edge length 1 / reference triangle area 1/2 (weights sum to 1/2)
+                const double s = me.face_pts[static_cast<size_t>(q) * (D - 1)];
+                const double t = (D == 3) ? me.face_pts[2 * q + 1] : 0.0;
+                for (int d = 0; d < D; ++d)
+                    g.face_coords[idx * D + d] = c[0][d] + s * (c[1][d] - c[0][d]) + (D == 3 ? t * (c[2][d] - c[0][d]) : 0.0);
+            }
+            for (int sd = 0; sd < 2; ++sd) {
+                const int e = mesh.face_elems[2 * f + sd];
+                if (e < 0) continue;
+                const int lf = mesh.face_lidx[2 * f + sd];
+                const int o = mesh.face_orient[2 * f + sd];
+                // same winding as the canonical listing for rotations, opposite for flips
+                const double flip = (D == 2) ? (o == 0 ? 1.0 : -1.0) : (o < 3 ? 1.0 : -1.0);
+                const double sign = static_cast<double>(si.outward_sign[lf]) * flip;
+                for (int q = 0; q < qf; ++q) {
+                    const size_t ni = (static_cast<size_t>(f) * 2 + sd) * qf + q;
+                    for (int d = 0; d < D; ++d) g.face_normal[ni * D + d] = sign * nrm[d];
+                }
+            }
+        }
+        return g;
+    }
+    throw Failure(HDGB_ERR_UNSUPPORTED, "compute_geometry: unknown shape");
 }
 
 }  // namespace hdgb

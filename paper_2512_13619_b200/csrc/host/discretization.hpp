@@ -59,7 +59,11 @@ struct MasterElement {
     // un-oriented tables in the element-local face parameterisation (== reference trace_phi[lf])
     std::vector<double> tphi_local;  // [(lf*qf + g)*pe + i]
     // canonical -> side-local face quadrature index for each orientation: qperm[o*qf + gc]
+    // (tensor shapes only: their symmetric rules map onto themselves; simplex tables are evaluated
+    // directly at the mapped points)
     std::vector<int> qperm;
+    std::vector<double> elem_nodes;  // pe x dim      reference coordinates of the nodal basis points
+    std::vector<double> face_nodes;  // pf x (dim-1)  canonical face parameters of the trace nodes
 };
 MasterElement make_master_element(int shape, int degree, int quad_points);
 

@@ -467,38 +467,37 @@ class Discretization:
     # -- nodal interpolation helpers (interpolate_volume / interpolate_trace, local_ops.cpp:462-495)
     def volume_node_coords(self) -> np.ndarray:
         """(ne, pe, dim) physical coordinates of the element nodes."""
-        nodes = self.table("nodes1d")
-        n1 = len(nodes)
         D = self.dim
         vc = self.table("vertex_coords").reshape(-1, D)
         ev = self.table("element_vertices").reshape(self.ne, -1)
         v = vc[ev]  # ne, vpe, D
-        if D == 2:
-            xi, eta = np.meshgrid(nodes, nodes, indexing="xy")  # a fastest
-            xi, eta = xi.ravel(), eta.ravel()
-            N = np.stack([(1 - xi) * (1 - eta), xi * (1 - eta), xi * eta, (1 - xi) * eta], axis=1)
+        xi = self.table("elem_nodes").reshape(self.pe, D)
+        if self.shape in (SHAPES["tri"], SHAPES["tet"]):
+            N = np.concatenate([1.0 - xi.sum(axis=1, keepdims=True), xi], axis=1)      # barycentric, affine map
+        elif D == 2:
+            a, b = xi[:, 0], xi[:, 1]
+            N = np.stack([(1 - a) * (1 - b), a * (1 - b), a * b, (1 - a) * b], axis=1)
         else:
-            a = np.tile(nodes, n1 * n1)
-            b = np.tile(np.repeat(nodes, n1), n1)
-            c = np.repeat(nodes, n1 * n1)
+            a, b, c = xi[:, 0], xi[:, 1], xi[:, 2]
             cs = [(0, 0, 0), (1, 0, 0), (1, 1, 0), (0, 1, 0), (0, 0, 1), (1, 0, 1), (1, 1, 1), (0, 1, 1)]
             N = np.stack([(a if s[0] else 1 - a) * (b if s[1] else 1 - b) * (c if s[2] else 1 - c) for s in cs], axis=1)
         return np.einsum("pc,ecd->epd", N, v)
 
     def trace_node_coords(self) -> np.ndarray:
         """(nf, pf, dim) physical coordinates of the face nodes in canonical face order."""
-        nodes = self.table("nodes1d")
-        n1 = len(nodes)
         D = self.dim
         vc = self.table("vertex_coords").reshape(-1, D)
         fv = self.table("face_vertices").reshape(self.nf, -1)
         v = vc[fv]
+        fn = self.table("face_nodes").reshape(self.pf, D - 1)
         if D == 2:
-            t = nodes
+            t = fn[:, 0]
             return v[:, None, 0, :] + t[None, :, None] * (v[:, None, 1, :] - v[:, None, 0, :])
-        s = np.tile(nodes, n1)
-        t = np.repeat(nodes, n1)
-        N = np.stack([(1 - s) * (1 - t), s * (1 - t), s * t, (1 - s) * t], axis=1)
+        s, t = fn[:, 0], fn[:, 1]
+        if self.shape == SHAPES["tet"]:
+            N = np.stack([1 - s - t, s, t], axis=1)
+        else:
+            N = np.stack([(1 - s) * (1 - t), s * (1 - t), s * t, (1 - s) * t], axis=1)
         return np.einsum("pc,fcd->fpd", N, v)
 
     def interpolate_volume(self, fn) -> np.ndarray:

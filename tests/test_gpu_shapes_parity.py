@@ -68,15 +68,19 @@ def test_hex_tables_properties(ctx, jitter):
         assert np.allclose(tot, 0.0, atol=1e-13)
 
 
-@pytest.mark.parametrize("case,k,n,ncomp,jitter", [("poisson", 2, 3, 1, 0.0), ("poisson", 3, 2, 1, 0.15),
-                                                   ("burgers", 2, 2, 1, 0.1), ("elasticity", 1, 3, 3, 0.1),
-                                                   ("elasticity", 2, 2, 3, 0.0)])
-def test_hex_operators_vs_tier_b(ctx, case, k, n, ncomp, jitter):
-    disc, model, state, oc = setup(ctx, "hex", n, k, case, n_comp=ncomp, jitter=jitter)
+@pytest.mark.parametrize("shape,case,k,n,ncomp,jitter", [
+    ("hex", "poisson", 2, 3, 1, 0.0), ("hex", "poisson", 3, 2, 1, 0.15), ("hex", "burgers", 2, 2, 1, 0.1),
+    ("hex", "elasticity", 1, 3, 3, 0.1), ("hex", "elasticity", 2, 2, 3, 0.0),
+    # BASELINE configs 3 and 4 in miniature: triangles p = 4 Burgers, tetrahedra p = 2 elasticity (M = 3)
+    ("tri", "burgers", 4, 3, 1, 0.2), ("tri", "poisson", 2, 4, 1, 0.2), ("tri", "elasticity", 3, 3, 2, 0.1),
+    ("tet", "elasticity", 2, 2, 3, 0.1), ("tet", "poisson", 3, 2, 1, 0.1), ("tet", "burgers", 1, 2, 1, 0.0),
+    ("quad", "elasticity", 2, 4, 2, 0.1)])
+def test_hex_operators_vs_tier_b(ctx, shape, case, k, n, ncomp, jitter):
+    disc, model, state, oc = setup(ctx, shape, n, k, case, n_comp=ncomp, jitter=jitter)
     perturb(disc, state, oc)
     oc.assemble()
     ops = hdg.assemble_element_operators(disc, model, state, keep_raw=True)
-    for d in range(3):
+    for d in range(disc.dim):
         assert relerr(disc.table(f"minv_b{d}"), oc.get(f"minv_b{d}")) < 1e-11
         assert relerr(disc.table(f"minv_c{d}"), oc.get(f"minv_c{d}")) < 1e-11
         assert relerr(state.q(d), oc.get(f"q{d}")) < 1e-11
@@ -105,10 +109,12 @@ def test_hex_operators_vs_tier_b(ctx, case, k, n, ncomp, jitter):
     assert relerr(hdg.recover_local(disc, ops, d), oc.recover_local(d)) < 1e-9
 
 
-@pytest.mark.parametrize("case,k,n,ncomp,kind", [("poisson", 2, 4, 1, "asm"), ("poisson", 3, 3, 1, "bj"),
-                                                 ("elasticity", 2, 2, 3, "asm"), ("burgers", 2, 3, 1, "bj")])
-def test_hex_newton_vs_tier_b(ctx, case, k, n, ncomp, kind):
-    disc, model, state, oc = setup(ctx, "hex", n, k, case, n_comp=ncomp)
+@pytest.mark.parametrize("shape,case,k,n,ncomp,kind", [
+    ("hex", "poisson", 2, 4, 1, "asm"), ("hex", "poisson", 3, 3, 1, "bj"), ("hex", "elasticity", 2, 2, 3, "asm"),
+    ("hex", "burgers", 2, 3, 1, "bj"), ("tri", "burgers", 4, 4, 1, "asm"), ("tri", "poisson", 3, 5, 1, "bj"),
+    ("tet", "elasticity", 2, 2, 3, "asm"), ("tet", "poisson", 2, 3, 1, "asm")])
+def test_hex_newton_vs_tier_b(ctx, shape, case, k, n, ncomp, kind):
+    disc, model, state, oc = setup(ctx, shape, n, k, case, n_comp=ncomp, jitter=0.1 if shape in ("tri", "tet") else 0.0)
     oc.set("u", state.u)
     oc.set("uhat", state.uhat)
     ro = oc.newton(precond=kind)
@@ -120,10 +126,11 @@ def test_hex_newton_vs_tier_b(ctx, case, k, n, ncomp, kind):
     assert relerr(state.u, oc.get("u")) < 1e-6
 
 
-def test_hex_poisson_converges_at_design_order(ctx):
+@pytest.mark.parametrize("shape", ["hex", "tri", "tet"])
+def test_hex_poisson_converges_at_design_order(ctx, shape):
     errs = []
     for n in (2, 4):
-        disc = hdg.Discretization.structured(ctx, "hex", n=n, degree=2)
+        disc = hdg.Discretization.structured(ctx, shape, n=n, degree=2)
         model = hdg.make_case_model(disc, "poisson")
         state = hdg.make_initial_state(disc, model)
         rep = hdg.newton_solve(disc, model, state, gcfg=hdg.GmresConfig(tol=1e-10), pspec=hdg.PrecondSpec("asm"))
