@@ -1,5 +1,8 @@
 // C ABI: context management and the batched dense kernels (A0-A2 of SURVEY.md section 8a).
 #include <climits>
+#include <map>
+#include <mutex>
+#include <set>
 
 #include "kernels.cuh"
 
@@ -36,6 +39,8 @@ hdgb_status hdgb_ctx_create(int device, hdgb_ctx** out) {
         c->sm_count = prop.multiProcessorCount;
         HDGB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         c->owns_stream = true;
+        pool_register(c->stream, true);
+        pool_set_current(c->stream);
         c->pinned_doubles = 1 << 16;
         HDGB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&c->pinned), c->pinned_doubles * sizeof(double)));
         HDGB_CUDA(cudaMalloc(reinterpret_cast<void**>(&c->d_flags), 4 * sizeof(int)));
@@ -53,6 +58,10 @@ hdgb_status hdgb_ctx_create(int device, hdgb_ctx** out) {
 void hdgb_ctx_destroy(hdgb_ctx* c) {
     if (!c) return;
     cudaStreamSynchronize(c->stream);
+    delete c->comm;
+    c->comm = nullptr;
+    pool_register(c->stream, false);
+    pool_trim(c->stream);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     if (c->d_flags) cudaFree(c->d_flags);
@@ -67,9 +76,13 @@ int64_t hdgb_last_error_index(const hdgb_ctx* c) { return c ? c->err_index : -1;
 hdgb_status hdgb_ctx_set_stream(hdgb_ctx* c, void* s) {
     return guarded(c, [&] {
         HDGB_CUDA(cudaStreamSynchronize(c->stream));
+        pool_register(c->stream, false);
+        pool_trim(c->stream);
         if (c->owns_stream && c->stream) cudaStreamDestroy(c->stream);
         c->stream = static_cast<cudaStream_t>(s);
         c->owns_stream = false;
+        pool_register(c->stream, true);
+        pool_set_current(c->stream);
     });
 }
 void* hdgb_ctx_stream(hdgb_ctx* c) { return c->stream; }
@@ -101,6 +114,101 @@ hdgb_status hdgb_copy(hdgb_ctx* c, double* dst, const double* src, int64_t n) {
 }  // extern "C"
 
 namespace hdgb {
+
+// ---- caching allocator ---------------------------------------------------------------------------
+namespace {
+struct Pool {
+    std::mutex mu;
+    std::map<cudaStream_t, std::multimap<size_t, void*>> parked;  // per stream: size -> block
+    std::set<cudaStream_t> active;
+    size_t parked_bytes = 0;
+};
+Pool& pool() {
+    static Pool* p = new Pool();  // leaked on purpose: outlives every static destructor that frees a DevBuf
+    return *p;
+}
+thread_local cudaStream_t tl_stream = nullptr;
+thread_local bool tl_stream_set = false;
+constexpr size_t kParkedCap = static_cast<size_t>(96) << 30;
+
+void free_all_locked(Pool& P) {
+    for (auto& kv : P.parked)
+        for (auto& b : kv.second) cudaFree(b.second);
+    P.parked.clear();
+    P.parked_bytes = 0;
+}
+}  // namespace
+
+void pool_set_current(cudaStream_t s) { tl_stream = s; tl_stream_set = true; }
+
+void pool_register(cudaStream_t s, bool on) {
+    Pool& P = pool();
+    std::lock_guard<std::mutex> g(P.mu);
+    if (on) P.active.insert(s);
+    else P.active.erase(s);
+}
+
+void* pool_alloc(size_t bytes, cudaStream_t* stream_out) {
+    Pool& P = pool();
+    cudaStream_t s = tl_stream;
+    bool pooled = tl_stream_set;
+    {
+        std::lock_guard<std::mutex> g(P.mu);
+        if (pooled && !P.active.count(s)) pooled = false;
+        if (pooled) {
+            auto it = P.parked.find(s);
+            if (it != P.parked.end()) {
+                auto b = it->second.find(bytes);
+                if (b != it->second.end()) {
+                    void* p = b->second;
+                    it->second.erase(b);
+                    P.parked_bytes -= bytes;
+                    *stream_out = s;
+                    return p;
+                }
+            }
+        }
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        cudaDeviceSynchronize();
+        {
+            std::lock_guard<std::mutex> g(P.mu);
+            free_all_locked(P);
+        }
+        HDGB_CUDA(cudaMalloc(&p, bytes));
+    }
+    // blocks allocated outside any context are tagged with a stream nobody registers: never parked
+    *stream_out = pooled ? s : reinterpret_cast<cudaStream_t>(~static_cast<uintptr_t>(0));
+    return p;
+}
+
+void pool_free(void* p, size_t bytes, cudaStream_t s) {
+    Pool& P = pool();
+    {
+        std::lock_guard<std::mutex> g(P.mu);
+        if (P.active.count(s) && bytes >= (1 << 16) && P.parked_bytes + bytes <= kParkedCap) {
+            P.parked[s].emplace(bytes, p);
+            P.parked_bytes += bytes;
+            return;
+        }
+    }
+    cudaFree(p);
+}
+
+void pool_trim(cudaStream_t s) {
+    Pool& P = pool();
+    std::lock_guard<std::mutex> g(P.mu);
+    auto it = P.parked.find(s);
+    if (it == P.parked.end()) return;
+    for (auto& b : it->second) {
+        cudaFree(b.second);
+        P.parked_bytes -= b.first;
+    }
+    P.parked.erase(it);
+}
 
 Tuning& tuning() {
     static Tuning t;

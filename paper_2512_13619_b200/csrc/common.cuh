@@ -76,27 +76,38 @@ inline void count_launch(hdgb_ctx* c, int n = 1) { c->launches += n; }
         HDGB_CUDA(cudaGetLastError());                           \
     } while (0)
 
+// Stream-keyed caching allocator behind DevBuf (api_core.cu).  A Newton solve allocates and frees the
+// same multi-GB blocks every iteration; cudaMalloc / cudaFree of such blocks costs tens of
+// milliseconds, so freed blocks are parked and handed back to the next request of the same size ON
+// THE SAME STREAM (stream order makes the reuse safe without synchronising).
+void* pool_alloc(size_t bytes, cudaStream_t* stream_out);
+void pool_free(void* p, size_t bytes, cudaStream_t stream);
+void pool_trim(cudaStream_t stream);        // frees the parked blocks of a stream (ctx destroy / OOM)
+void pool_register(cudaStream_t stream, bool active);
+void pool_set_current(cudaStream_t stream); // the stream subsequent DevBuf allocations belong to (thread local)
+
 template <class T>
 struct DevBuf {
     T* p = nullptr;
     size_t n = 0;
+    cudaStream_t owner = nullptr;
     DevBuf() = default;
     explicit DevBuf(size_t count) { alloc(count); }
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
-    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), owner(o.owner) { o.p = nullptr; o.n = 0; }
     DevBuf& operator=(DevBuf&& o) noexcept {
-        if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        if (this != &o) { release(); p = o.p; n = o.n; owner = o.owner; o.p = nullptr; o.n = 0; }
         return *this;
     }
     ~DevBuf() { release(); }
     void alloc(size_t count) {
         release();
         n = count;
-        if (count) HDGB_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T)));
+        if (count) p = static_cast<T*>(pool_alloc(count * sizeof(T), &owner));
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) pool_free(p, n * sizeof(T), owner);
         p = nullptr;
         n = 0;
     }
@@ -179,6 +190,7 @@ struct OutArg {
 // Runs fn, mapping Failure / std::exception to a status + message on the context.
 template <class F>
 hdgb_status guarded(hdgb_ctx* ctx, F&& fn) {
+    if (ctx) pool_set_current(ctx->stream);
     try {
         fn();
         return HDGB_OK;

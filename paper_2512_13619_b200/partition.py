@@ -249,6 +249,11 @@ def make_discretization(ctx, lm: LocalMesh, shape: str, degree: int, n_comp=1, q
 def install_nccl_comm(ctx, lm: LocalMesh, dist):
     """NCCL communicator + halo plan on this rank's context; the unique id travels over
     torch.distributed (whatever backend the job initialised)."""
+    import os
+    # one box: keep NCCL's bootstrap on the loopback interface (the container hostname may not resolve,
+    # and probing absent NICs can stall communicator creation for minutes)
+    os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")
+    os.environ.setdefault("NCCL_IB_DISABLE", "1")
     L = H.load_library()
     uid = (C.c_char * 128)()
     if lm.rank == 0:
