@@ -141,7 +141,8 @@ typedef enum hdgb_model_kind {
     HDGB_MODEL_BURGERS = 1,   /* burgers_model  (models.cpp:32-61)  params: nu, tau             */
     HDGB_MODEL_CONVDIFF = 2,  /* convdiff_model (models.cpp:63-93)  params: c[3], kappa, tau|-1 */
     HDGB_MODEL_ELASTICITY = 3,/* linear elasticity, M = D (PAPER.md 5.3) params: lambda, mu, tau */
-    HDGB_MODEL_REACTION = 4   /* Poisson + cubic reaction u^3 (test_newton.cpp:80-99 analogue)  */
+    HDGB_MODEL_REACTION = 4,  /* Poisson + cubic reaction u^3 (test_newton.cpp:80-99 analogue)  */
+    HDGB_MODEL_NAVIER_STOKES = 5 /* compressible NS, M = D + 2 (PAPER.md 5.5-5.7) params: gamma, mu, Pr, tau */
 } hdgb_model_kind;
 
 /* The reference's PdeModel is a bundle of host std::function callbacks evaluated at every

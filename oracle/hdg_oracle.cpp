@@ -141,6 +141,53 @@ double dot(const Vec& a, const Vec& b) {
 }
 double norm2(const Vec& a) { return std::sqrt(dot(a, a)); }
 
+// ---- compressible Navier-Stokes flux (PAPER.md 5.5-5.7; no reference implementation) --------------
+// u = (rho, rho v, rho E), q = grad u.  Written for a generic scalar so that the same routine run on
+// first-order dual numbers yields the exact Jacobians.
+struct Dn {
+    double v, d;
+};
+inline Dn operator+(Dn a, Dn b) { return {a.v + b.v, a.d + b.d}; }
+inline Dn operator-(Dn a, Dn b) { return {a.v - b.v, a.d - b.d}; }
+inline Dn operator*(Dn a, Dn b) { return {a.v * b.v, a.d * b.v + a.v * b.d}; }
+inline Dn operator/(Dn a, Dn b) { const double iv = 1.0 / b.v; return {a.v * iv, (a.d - a.v * iv * b.d) * iv}; }
+inline Dn operator*(double a, Dn b) { return {a * b.v, a * b.d}; }
+inline double lift(double, double v) { return v; }
+inline Dn lift(Dn, double v) { return {v, 0.0}; }
+
+template <class T>
+void navier_stokes_flux(int D, const T* u, const T* q, T* F, double gamma, double mu, double pr) {
+    const int M = D + 2;
+    const T rinv = lift(T{}, 1.0) / u[0];
+    T vel[MAXD], gradv[MAXD][MAXD];
+    T kinetic = lift(T{}, 0.0);
+    for (int i = 0; i < D; ++i) {
+        vel[i] = u[1 + i] * rinv;
+        kinetic = kinetic + 0.5 * (vel[i] * vel[i]);
+    }
+    const T etot = u[M - 1] * rinv;
+    const T pres = (gamma - 1.0) * (u[M - 1] - u[0] * kinetic);
+    T divv = lift(T{}, 0.0);
+    for (int i = 0; i < D; ++i)
+        for (int d = 0; d < D; ++d) gradv[i][d] = (q[(1 + i) * D + d] - vel[i] * q[d]) * rinv;
+    for (int i = 0; i < D; ++i) divv = divv + gradv[i][i];
+    for (int d = 0; d < D; ++d) {
+        T grad_e = (q[(M - 1) * D + d] - etot * q[d]) * rinv;
+        for (int i = 0; i < D; ++i) grad_e = grad_e - vel[i] * gradv[i][d];
+        F[d] = u[1 + d];
+        T work = lift(T{}, 0.0);
+        for (int i = 0; i < D; ++i) {
+            T stress = mu * (gradv[i][d] + gradv[d][i]);
+            if (i == d) stress = stress - (2.0 / 3.0 * mu) * divv;
+            T mom = u[1 + i] * vel[d] - stress;
+            if (i == d) mom = mom + pres;
+            F[(1 + i) * D + d] = mom;
+            work = work + vel[i] * stress;
+        }
+        F[(M - 1) * D + d] = (u[M - 1] + pres) * vel[d] - work - (mu * gamma / pr) * grad_e;
+    }
+}
+
 // ---- PDE models (models.cpp, generalised) --------------------------------------------------------
 struct BFlux {
     double val[MAXM], d_u[MAXM * MAXM], d_q[MAXM * MAXM * MAXD], d_uh[MAXM * MAXM];
@@ -170,16 +217,38 @@ struct Model {
                         F[m * D + d] = -(p[1] * (q[m * D + d] + q[d * D + m]) + ((m == d) ? p[0] * tr : 0.0));
                 break;
             }
+            case 5: navier_stokes_flux<double>(D, u, q, F, p[0], p[1], p[2]); break;
         }
     }
+    void ns_jacobians(const double* u, const double* q, double* dFu, double* dFq) const {
+        Dn ud[MAXM], qd[MAXM * MAXD], Fd[MAXM * MAXD];
+        for (int i = 0; i < M; ++i) ud[i] = {u[i], 0.0};
+        for (int i = 0; i < M * D; ++i) qd[i] = {q[i], 0.0};
+        if (dFu)
+            for (int mp = 0; mp < M; ++mp) {
+                ud[mp].d = 1.0;
+                navier_stokes_flux<Dn>(D, ud, qd, Fd, p[0], p[1], p[2]);
+                ud[mp].d = 0.0;
+                for (int k = 0; k < M * D; ++k) dFu[k * M + mp] = Fd[k].d;
+            }
+        if (dFq)
+            for (int s = 0; s < M * D; ++s) {
+                qd[s].d = 1.0;
+                navier_stokes_flux<Dn>(D, ud, qd, Fd, p[0], p[1], p[2]);
+                qd[s].d = 0.0;
+                for (int k = 0; k < M * D; ++k) dFq[k * M * D + s] = Fd[k].d;
+            }
+    }
     // dFu[(m*D+d)*M+mp]
-    void dflux_du(const double* u, double* dFu) const {
+    void dflux_du(const double* u, const double* q, double* dFu) const {
+        if (kind == 5) { ns_jacobians(u, q, dFu, nullptr); return; }
         for (int i = 0; i < M * D * M; ++i) dFu[i] = 0.0;
         if (kind == 1) { dFu[0] = u[0]; dFu[1] = 1.0; }
         if (kind == 2) for (int d = 0; d < D; ++d) dFu[d] = p[d];
     }
     // dFq[((m*D+d)*M+mp)*D+dp]
-    void dflux_dq(double* dFq) const {
+    void dflux_dq(const double* u, const double* q, double* dFq) const {
+        if (kind == 5) { ns_jacobians(u, q, nullptr, dFq); return; }
         for (int i = 0; i < M * D * M * D; ++i) dFq[i] = 0.0;
         if (kind == 3) {
             for (int m = 0; m < M; ++m)
@@ -215,6 +284,7 @@ struct Model {
                 for (int d = 0; d < D; ++d) cn += p[d] * n[d];
                 return p[3] + std::abs(cn);
             }
+            case 5: return p[3];
             default: return p[2];
         }
     }
@@ -244,7 +314,7 @@ struct Model {
             if (!clamp) {
                 double F[MAXM * MAXD], dFq[MAXM * MAXD * MAXM * MAXD];
                 flux(uh, q, F);
-                dflux_dq(dFq);
+                dflux_dq(uh, q, dFq);
                 for (int m = 0; m < M; ++m) {
                     double fn = 0.0;
                     for (int d = 0; d < D; ++d) fn += F[m * D + d] * n[d];
@@ -475,8 +545,8 @@ struct Case {
                         }
                     if (want_jac) {
                         double dFu[MAXM * MAXD * MAXM], dFq[MAXM * MAXD * MAXM * MAXD], dSu[MAXM * MAXM];
-                        mdl.dflux_du(ug, dFu);
-                        mdl.dflux_dq(dFq);
+                        mdl.dflux_du(ug, qg, dFu);
+                        mdl.dflux_dq(ug, qg, dFq);
                         mdl.dsource_du(ug, dSu);
                         for (int j = 0; j < pe; ++j) {
                             const double pj = w * phig[j];
@@ -535,7 +605,7 @@ struct Case {
                             for (int i = 0; i < pe; ++i) Ru[m * pe + i] += w * fhat[m] * phis[i];
                         }
                         double dFu[MAXM * MAXD * MAXM], dFq[MAXM * MAXD * MAXM * MAXD];
-                        if (want_jac || tag != 0) { mdl.dflux_du(uh, dFu); mdl.dflux_dq(dFq); }
+                        if (want_jac || tag != 0) { mdl.dflux_du(uh, qg, dFu); mdl.dflux_dq(uh, qg, dFq); }
                         else {
                             for (int k = 0; k < M * D * M; ++k) dFu[k] = 0.0;
                             for (int k = 0; k < M * D * M * D; ++k) dFq[k] = 0.0;

@@ -18,7 +18,7 @@ _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int)
 _lib = None
 
-MODELS = {"poisson": 0, "burgers": 1, "convdiff": 2, "elasticity": 3, "reaction": 4}
+MODELS = {"poisson": 0, "burgers": 1, "convdiff": 2, "elasticity": 3, "reaction": 4, "navier_stokes": 5}
 PRECOND = {"none": 0, "identity": 0, "bj": 1, "asm": 2, "ras": 3}
 
 

@@ -17,6 +17,7 @@ int hdgb_set_tuning(const char* key, int64_t value) {
     if (k == "use_stream") { hdgb::tuning().use_stream = static_cast<int>(value); return 0; }
     if (k == "stream_min_elems") { hdgb::tuning().stream_min_elems = value; return 0; }
     if (k == "use_tile_lu") { hdgb::tuning().use_tile_lu = static_cast<int>(value); return 0; }
+    if (k == "assemble_budget_kb") { hdgb::tuning().assemble_budget_kb = static_cast<int>(value); return 0; }
     return 1;
 }
 

@@ -276,11 +276,11 @@ hdgb_status hdgb_model_create(hdgb_ctx* c, const hdgb_disc* d, int kind, const d
         m->view.kind = kind;
         for (int i = 0; i < 16; ++i) m->view.p[i] = (params && i < n_params) ? params[i] : 0.0;
         const int M = d->dims.n_comp;
-        const int need = (kind == HDGB_MODEL_ELASTICITY) ? d->dims.dim : 1;
+        const int need = (kind == HDGB_MODEL_ELASTICITY) ? d->dims.dim : (kind == HDGB_MODEL_NAVIER_STOKES ? d->dims.dim + 2 : 1);
         if (M != need)
             throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "model needs " + std::to_string(need) +
                                                            " components, discretisation has " + std::to_string(M));
-        if (kind < 0 || kind > HDGB_MODEL_REACTION) throw Failure(HDGB_ERR_UNSUPPORTED, "unknown model kind");
+        if (kind < 0 || kind > HDGB_MODEL_NAVIER_STOKES) throw Failure(HDGB_ERR_UNSUPPORTED, "unknown model kind");
         m->n_comp = M;
         if (forcing_q) {
             m->forcing_q.alloc(static_cast<size_t>(d->dims.ne) * d->dims.qe * M);

@@ -106,7 +106,11 @@ struct FaceRec {
 
 template <class Model>
 __global__ void __launch_bounds__(256) local_assemble_kernel(DiscView dv, ModelView mv, LocalIn in, LocalOut out,
-                                                            int want_jac) {
+                                                            int want_jac, int gv0, int gv1, int fp0, int fp1, int first) {
+    // Point records of the volume points [gv0, gv1) and face points [fp0, fp1) live in shared memory.
+    // When all points of an element fit (scalar models) there is ONE launch (first = 1) and every
+    // output entry is written once.  Wide systems (M = 5) are swept in several launches over point
+    // chunks that accumulate into the outputs -- still volume points ascending, then faces.
     constexpr int M = Model::M, D = Model::D;
     using VR = VolRec<M, D>;
     using FR = FaceRec<M, D>;
@@ -122,7 +126,7 @@ __global__ void __launch_bounds__(256) local_assemble_kernel(DiscView dv, ModelV
     double* uhs = qs + D * npe;       // nfl
     double* ups = uhs + nfl;          // npe
     VR* vrec = reinterpret_cast<VR*>(ups + npe);
-    FR* frec = reinterpret_cast<FR*>(vrec + qe);
+    FR* frec = reinterpret_cast<FR*>(vrec + (gv1 - gv0));
     __shared__ int s_face[8], s_side[8], s_orient[8], s_tag[8];
 
     const Model model(mv);
@@ -148,9 +152,9 @@ __global__ void __launch_bounds__(256) local_assemble_kernel(DiscView dv, ModelV
     __syncthreads();
 
     // ---- phase 1a: volume points ----
-    for (int g = tid; g < qe; g += nt) {
+    for (int g = gv0 + tid; g < gv1; g += nt) {
         const size_t gi = static_cast<size_t>(e) * qe + g;
-        VR& r = vrec[g];
+        VR& r = vrec[g - gv0];
         const double* phig = dv.phi + static_cast<size_t>(pe) * g;
         double ug[M], qg[M * D], upg[M];
         for (int m = 0; m < M; ++m) {
@@ -202,10 +206,10 @@ __global__ void __launch_bounds__(256) local_assemble_kernel(DiscView dv, ModelV
         }
     }
     // ---- phase 1b: face points ----
-    for (int p = tid; p < nfp; p += nt) {
+    for (int p = fp0 + tid; p < fp1; p += nt) {
         const int lf = p / qf, gc = p - lf * qf;
         const int f = s_face[lf], side = s_side[lf], tag = s_tag[lf];
-        FR& r = frec[p];
+        FR& r = frec[p - fp0];
         const size_t fi = static_cast<size_t>(f) * qf + gc;
         const double* phis = dv.tphi + ((static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf + gc) * pe;
         const double* psic = dv.psi + static_cast<size_t>(pf) * gc;
@@ -278,8 +282,8 @@ __global__ void __launch_bounds__(256) local_assemble_kernel(DiscView dv, ModelV
     for (int i = tid; i < pe; i += nt) {
         double acc[M];
         for (int m = 0; m < M; ++m) acc[m] = 0.0;
-        for (int g = 0; g < qe; ++g) {
-            const VR& r = vrec[g];
+        for (int g = gv0; g < gv1; ++g) {
+            const VR& r = vrec[g - gv0];
             const double ph = dv.phi[i + pe * g];
             double dp_[D];
             for (int k = 0; k < D; ++k) dp_[k] = dv.dphi[k][i + pe * g];
@@ -291,116 +295,131 @@ __global__ void __launch_bounds__(256) local_assemble_kernel(DiscView dv, ModelV
                 acc[m] += r.w * v;
             }
         }
-        for (int p = 0; p < nfp; ++p) {
+        for (int p = fp0; p < fp1; ++p) {
             const int lf = p / qf, gc = p - lf * qf;
-            const FR& r = frec[p];
+            const FR& r = frec[p - fp0];
             const double ph = dv.tphi[((static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf + gc) * pe + i];
             for (int m = 0; m < M; ++m) acc[m] += r.w * r.fhat[m] * ph;
         }
-        for (int m = 0; m < M; ++m) out.ru[static_cast<size_t>(e) * npe + m * pe + i] = -acc[m];
+        for (int m = 0; m < M; ++m) {
+            double* o = out.ru + static_cast<size_t>(e) * npe + m * pe + i;
+            *o = first ? -acc[m] : *o - acc[m];
+        }
     }
     for (int t = tid; t < n_lfe * pf; t += nt) {
         const int lf = t / pf, b = t - lf * pf;
         double acc[M];
         for (int m = 0; m < M; ++m) acc[m] = 0.0;
-        for (int gc = 0; gc < qf; ++gc) {
-            const FR& r = frec[lf * qf + gc];
+        const int g0 = max(0, fp0 - lf * qf), g1 = min(qf, fp1 - lf * qf);
+        for (int gc = g0; gc < g1; ++gc) {
+            const FR& r = frec[lf * qf + gc - fp0];
             const double ps = dv.psi[b + pf * gc];
             for (int m = 0; m < M; ++m) acc[m] += r.w * r.val[m] * ps;
         }
-        for (int m = 0; m < M; ++m) out.ruhat_e[static_cast<size_t>(e) * nfl + lf * mpf + m * pf + b] = -acc[m];
+        for (int m = 0; m < M; ++m) {
+            double* o = out.ruhat_e + static_cast<size_t>(e) * nfl + lf * mpf + m * pf + b;
+            *o = first ? -acc[m] : *o - acc[m];
+        }
     }
     if (!want_jac) return;
 
-    // ---- phase 2b: E and D_d.  A thread owns a TI x TJ tile of scalar-basis pairs (i, j) and all
-    // component pairs; per point it forms the i-side values once and rank-1 updates the tile ----
+    // ---- phase 2b: E and D_d.  A thread owns a TI x TJ tile of scalar-basis pairs (i, j); per point it
+    // forms the i-side values once and rank-1 updates the tile.  Component columns mp are swept one
+    // at a time so that the accumulators (M (1 + D) per pair) stay in registers for wide systems ----
     {
         constexpr int TI = (M == 1) ? 2 : 1, TJ = (M == 1) ? 4 : 1;
-        constexpr int Q = M * M * (1 + D);  // E then D_0..D_{D-1} per component pair
+        constexpr int Q = M * (1 + D);  // per row component m: E then D_0..D_{D-1}
         const int nti = (pe + TI - 1) / TI, ntj = (pe + TJ - 1) / TJ;
         for (int t = tid; t < nti * ntj; t += nt) {
             const int bj = t / nti, bi = t - bj * nti;
-            double acc[TI][TJ][Q];
+            for (int mp = 0; mp < M; ++mp) {
+                double acc[TI][TJ][Q];
 #pragma unroll
-            for (int a = 0; a < TI; ++a)
+                for (int a = 0; a < TI; ++a)
 #pragma unroll
-                for (int b = 0; b < TJ; ++b)
+                    for (int b = 0; b < TJ; ++b)
 #pragma unroll
-                    for (int q = 0; q < Q; ++q) acc[a][b][q] = 0.0;
-            for (int g = 0; g < qe; ++g) {
-                const VR& r = vrec[g];
-                double val[TI][Q];
+                        for (int q = 0; q < Q; ++q) acc[a][b][q] = 0.0;
+                for (int g = gv0; g < gv1; ++g) {
+                    const VR& r = vrec[g - gv0];
+                    double val[TI][Q];
 #pragma unroll
-                for (int a = 0; a < TI; ++a) {
-                    const int i = min(bi * TI + a, pe - 1);
-                    const double phi_i = dv.phi[i + pe * g];
-                    double dp_[D];
+                    for (int a = 0; a < TI; ++a) {
+                        const int i = min(bi * TI + a, pe - 1);
+                        const double phi_i = dv.phi[i + pe * g];
+                        double dp_[D];
 #pragma unroll
-                    for (int k = 0; k < D; ++k) dp_[k] = dv.dphi[k][i + pe * g];
+                        for (int k = 0; k < D; ++k) dp_[k] = dv.dphi[k][i + pe * g];
 #pragma unroll
-                    for (int mm = 0; mm < M * M; ++mm) {
-                        double fe = 0.0;
+                        for (int m = 0; m < M; ++m) {
+                            const int mm = m * M + mp;
+                            double fe = 0.0;
 #pragma unroll
-                        for (int k = 0; k < D; ++k) fe += r.cE[mm * D + k] * dp_[k];
-                        double eij = -fe - r.dSu[mm] * phi_i;
-                        if (transient && (mm / M) == (mm % M)) eij += in.dt_inv * phi_i;
-                        val[a][mm] = eij;
+                            for (int k = 0; k < D; ++k) fe += r.cE[mm * D + k] * dp_[k];
+                            double eij = -fe - r.dSu[mm] * phi_i;
+                            if (transient && m == mp) eij += in.dt_inv * phi_i;
+                            val[a][m] = eij;
 #pragma unroll
-                        for (int dp = 0; dp < D; ++dp) {
-                            double fd = 0.0;
+                            for (int dp = 0; dp < D; ++dp) {
+                                double fd = 0.0;
 #pragma unroll
-                            for (int k = 0; k < D; ++k) fd += r.cD[(dp * M * M + mm) * D + k] * dp_[k];
-                            val[a][M * M * (1 + dp) + mm] = -fd - r.dSq[mm * D + dp] * phi_i;
+                                for (int k = 0; k < D; ++k) fd += r.cD[(dp * M * M + mm) * D + k] * dp_[k];
+                                val[a][M * (1 + dp) + m] = -fd - r.dSq[mm * D + dp] * phi_i;
+                            }
                         }
                     }
+#pragma unroll
+                    for (int b = 0; b < TJ; ++b) {
+                        const int j = min(bj * TJ + b, pe - 1);
+                        const double pj = r.w * dv.phi[j + pe * g];
+#pragma unroll
+                        for (int a = 0; a < TI; ++a)
+#pragma unroll
+                            for (int q = 0; q < Q; ++q) acc[a][b][q] = fma(pj, val[a][q], acc[a][b][q]);
+                    }
                 }
+                for (int p = fp0; p < fp1; ++p) {
+                    const int lf = p / qf, gc = p - lf * qf;
+                    const FR& r = frec[p - fp0];
+                    const double* phis = dv.tphi + ((static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf + gc) * pe;
+                    double val[TI][Q];
 #pragma unroll
-                for (int b = 0; b < TJ; ++b) {
-                    const int j = min(bj * TJ + b, pe - 1);
-                    const double pj = r.w * dv.phi[j + pe * g];
+                    for (int a = 0; a < TI; ++a) {
+                        const double ph = phis[min(bi * TI + a, pe - 1)];
 #pragma unroll
-                    for (int a = 0; a < TI; ++a)
+                        for (int m = 0; m < M; ++m) {
+                            val[a][m] = (m == mp) ? r.tau * ph : 0.0;
 #pragma unroll
-                        for (int q = 0; q < Q; ++q) acc[a][b][q] = fma(pj, val[a][q], acc[a][b][q]);
-                }
-            }
-            for (int p = 0; p < nfp; ++p) {
-                const int lf = p / qf, gc = p - lf * qf;
-                const FR& r = frec[p];
-                const double* phis = dv.tphi + ((static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf + gc) * pe;
-                double val[TI][Q];
+                            for (int dp = 0; dp < D; ++dp) val[a][M * (1 + dp) + m] = r.dfh_q[(m * M + mp) * D + dp] * ph;
+                        }
+                    }
 #pragma unroll
-                for (int a = 0; a < TI; ++a) {
-                    const double ph = phis[min(bi * TI + a, pe - 1)];
+                    for (int b = 0; b < TJ; ++b) {
+                        const double pj = r.w * phis[min(bj * TJ + b, pe - 1)];
 #pragma unroll
-                    for (int mm = 0; mm < M * M; ++mm) {
-                        val[a][mm] = ((mm / M) == (mm % M)) ? r.tau * ph : 0.0;
+                        for (int a = 0; a < TI; ++a)
 #pragma unroll
-                        for (int dp = 0; dp < D; ++dp) val[a][M * M * (1 + dp) + mm] = r.dfh_q[mm * D + dp] * ph;
+                            for (int q = 0; q < Q; ++q) acc[a][b][q] = fma(pj, val[a][q], acc[a][b][q]);
                     }
                 }
 #pragma unroll
-                for (int b = 0; b < TJ; ++b) {
-                    const double pj = r.w * phis[min(bj * TJ + b, pe - 1)];
+                for (int a = 0; a < TI; ++a)
 #pragma unroll
-                    for (int a = 0; a < TI; ++a)
-#pragma unroll
-                        for (int q = 0; q < Q; ++q) acc[a][b][q] = fma(pj, val[a][q], acc[a][b][q]);
-                }
-            }
-#pragma unroll
-            for (int a = 0; a < TI; ++a)
-#pragma unroll
-                for (int b = 0; b < TJ; ++b) {
-                    const int i = bi * TI + a, j = bj * TJ + b;
-                    if (i >= pe || j >= pe) continue;
-                    for (int m = 0; m < M; ++m)
-                        for (int mp = 0; mp < M; ++mp) {
+                    for (int b = 0; b < TJ; ++b) {
+                        const int i = bi * TI + a, j = bj * TJ + b;
+                        if (i >= pe || j >= pe) continue;
+                        for (int m = 0; m < M; ++m) {
                             const size_t o = static_cast<size_t>(e) * npe * npe + static_cast<size_t>(mp * pe + j) * npe + (m * pe + i);
-                            out.E[o] = acc[a][b][m * M + mp];
-                            for (int dp = 0; dp < D; ++dp) out.Dm[dp][o] = acc[a][b][M * M * (1 + dp) + m * M + mp];
+                            if (first) {
+                                out.E[o] = acc[a][b][m];
+                                for (int dp = 0; dp < D; ++dp) out.Dm[dp][o] = acc[a][b][M * (1 + dp) + m];
+                            } else {
+                                out.E[o] += acc[a][b][m];
+                                for (int dp = 0; dp < D; ++dp) out.Dm[dp][o] += acc[a][b][M * (1 + dp) + m];
+                            }
                         }
-                }
+                    }
+            }
         }
     }
     // ---- H and G_d: rows (lf, m, b), columns (mp, j) ----
@@ -411,8 +430,10 @@ __global__ void __launch_bounds__(256) local_assemble_kernel(DiscView dv, ModelV
         double aH[M * M], aG[D * M * M];
         for (int k = 0; k < M * M; ++k) aH[k] = 0.0;
         for (int k = 0; k < D * M * M; ++k) aG[k] = 0.0;
-        for (int gc = 0; gc < qf; ++gc) {
-            const FR& r = frec[lf * qf + gc];
+        const int g0 = max(0, fp0 - lf * qf), g1 = min(qf, fp1 - lf * qf);
+        if (!first && g0 >= g1) continue;
+        for (int gc = g0; gc < g1; ++gc) {
+            const FR& r = frec[lf * qf + gc - fp0];
             const double pj = r.w * dv.tphi[((static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf + gc) * pe + j];
             const double ps = dv.psi[b + pf * gc];
             for (int k = 0; k < M * M; ++k) {
@@ -423,8 +444,13 @@ __global__ void __launch_bounds__(256) local_assemble_kernel(DiscView dv, ModelV
         for (int m = 0; m < M; ++m)
             for (int mp = 0; mp < M; ++mp) {
                 const size_t o = static_cast<size_t>(e) * nfl * npe + static_cast<size_t>(mp * pe + j) * nfl + (lf * mpf + m * pf + b);
-                out.H[o] = aH[m * M + mp];
-                for (int dp = 0; dp < D; ++dp) out.G[dp][o] = aG[dp * M * M + m * M + mp];
+                if (first) {
+                    out.H[o] = aH[m * M + mp];
+                    for (int dp = 0; dp < D; ++dp) out.G[dp][o] = aG[dp * M * M + m * M + mp];
+                } else {
+                    out.H[o] += aH[m * M + mp];
+                    for (int dp = 0; dp < D; ++dp) out.G[dp][o] += aG[dp * M * M + m * M + mp];
+                }
             }
     }
     // ---- F: rows (m, i), columns (lf, mp, bp) ----
@@ -433,20 +459,24 @@ __global__ void __launch_bounds__(256) local_assemble_kernel(DiscView dv, ModelV
         const int lf = lb / pf, bp = lb - lf * pf;
         double aF[M * M];
         for (int k = 0; k < M * M; ++k) aF[k] = 0.0;
-        for (int gc = 0; gc < qf; ++gc) {
-            const FR& r = frec[lf * qf + gc];
+        const int g0 = max(0, fp0 - lf * qf), g1 = min(qf, fp1 - lf * qf);
+        if (!first && g0 >= g1) continue;
+        for (int gc = g0; gc < g1; ++gc) {
+            const FR& r = frec[lf * qf + gc - fp0];
             const double pj = r.w * dv.psi[bp + pf * gc];
             const double ph = dv.tphi[((static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf + gc) * pe + i];
             for (int k = 0; k < M * M; ++k) aF[k] += pj * r.dfh_uh[k] * ph;
         }
         for (int m = 0; m < M; ++m)
-            for (int mp = 0; mp < M; ++mp)
-                out.F[static_cast<size_t>(e) * npe * nfl + static_cast<size_t>(lf * mpf + mp * pf + bp) * npe + (m * pe + i)] =
-                    aF[m * M + mp];
+            for (int mp = 0; mp < M; ++mp) {
+                double* o = out.F + static_cast<size_t>(e) * npe * nfl + static_cast<size_t>(lf * mpf + mp * pf + bp) * npe + (m * pe + i);
+                *o = first ? aF[m * M + mp] : *o + aF[m * M + mp];
+            }
     }
     // ---- J: block diagonal over local faces; rows (lf, m, b), columns (lf, mp, bp); the other
     // entries of the nfl x nfl block are zero ----
-    for (int t = tid; t < nfl * nfl; t += nt) out.J[static_cast<size_t>(e) * nfl * nfl + t] = 0.0;
+    if (first)
+        for (int t = tid; t < nfl * nfl; t += nt) out.J[static_cast<size_t>(e) * nfl * nfl + t] = 0.0;
     __syncthreads();
     for (int t = tid; t < n_lfe * pf * pf; t += nt) {
         const int lf = t / (pf * pf);
@@ -454,16 +484,19 @@ __global__ void __launch_bounds__(256) local_assemble_kernel(DiscView dv, ModelV
         const int bp = r2 / pf, b = r2 - bp * pf;
         double aJ[M * M];
         for (int k = 0; k < M * M; ++k) aJ[k] = 0.0;
-        for (int gc = 0; gc < qf; ++gc) {
-            const FR& r = frec[lf * qf + gc];
+        const int g0 = max(0, fp0 - lf * qf), g1 = min(qf, fp1 - lf * qf);
+        if (!first && g0 >= g1) continue;
+        for (int gc = g0; gc < g1; ++gc) {
+            const FR& r = frec[lf * qf + gc - fp0];
             const double pj = r.w * dv.psi[bp + pf * gc];
             const double ps = dv.psi[b + pf * gc];
             for (int k = 0; k < M * M; ++k) aJ[k] += pj * r.dv_uh[k] * ps;
         }
         for (int m = 0; m < M; ++m)
-            for (int mp = 0; mp < M; ++mp)
-                out.J[static_cast<size_t>(e) * nfl * nfl + static_cast<size_t>(lf * mpf + mp * pf + bp) * nfl + (lf * mpf + m * pf + b)] =
-                    aJ[m * M + mp];
+            for (int mp = 0; mp < M; ++mp) {
+                double* o = out.J + static_cast<size_t>(e) * nfl * nfl + static_cast<size_t>(lf * mpf + mp * pf + bp) * nfl + (lf * mpf + m * pf + b);
+                *o = first ? aJ[m * M + mp] : *o + aJ[m * M + mp];
+            }
     }
 }
 
@@ -472,16 +505,40 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
                        const LocalOut& out, bool want_jac) {
     constexpr int M = Model::M, D = Model::D;
     const int npe = M * dv.pe, nfl = dv.n_lfe * M * dv.pf;
-    const size_t smem = (static_cast<size_t>(npe) * (2 + D) + nfl) * sizeof(double) +
-                        static_cast<size_t>(dv.qe) * sizeof(VolRec<M, D>) +
-                        static_cast<size_t>(dv.n_lfe) * dv.qf * sizeof(FaceRec<M, D>);
-    if (smem > 220 * 1024)
-        throw Failure(HDGB_ERR_UNSUPPORTED, "local assembly: per-element point records exceed shared memory ("
-                                                + std::to_string(smem) + " B); reduce quad_points");
-    if (smem > 48 * 1024)
-        HDGB_CUDA(cudaFuncSetAttribute(local_assemble_kernel<Model>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    local_assemble_kernel<Model><<<dv.ne, 256, smem, ctx->stream>>>(dv, mv, in, out, want_jac ? 1 : 0);
-    HDGB_LAUNCH_CHECK(ctx);
+    const int nfp = dv.n_lfe * dv.qf;
+    const size_t fixed = (static_cast<size_t>(npe) * (2 + D) + nfl) * sizeof(double);
+    const size_t cap = 216 * 1024;
+    const size_t budget = std::min<size_t>(cap, static_cast<size_t>(tuning().assemble_budget_kb) * 1024);
+    const size_t svr = sizeof(VolRec<M, D>), sfr = sizeof(FaceRec<M, D>);
+    if (fixed + std::max(svr, sfr) > budget)
+        throw Failure(HDGB_ERR_UNSUPPORTED, "local assembly: element state exceeds shared memory");
+    auto kern = local_assemble_kernel<Model>;
+    static bool configured = false;
+    if (!configured) {
+        HDGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cap)));
+        configured = true;
+    }
+    const size_t all = fixed + dv.qe * svr + nfp * sfr;
+    if (all <= budget) {
+        kern<<<dv.ne, 256, all, ctx->stream>>>(dv, mv, in, out, want_jac ? 1 : 0, 0, dv.qe, 0, nfp, 1);
+        HDGB_LAUNCH_CHECK(ctx);
+        return;
+    }
+    // point-chunked sweep: volume chunks first, then face chunks (the reference's accumulation order)
+    const int vc = static_cast<int>((budget - fixed) / svr), fc = static_cast<int>((budget - fixed) / sfr);
+    int first = 1;
+    for (int g0 = 0; g0 < dv.qe; g0 += vc) {
+        const int g1 = std::min(dv.qe, g0 + vc);
+        kern<<<dv.ne, 256, fixed + (g1 - g0) * svr, ctx->stream>>>(dv, mv, in, out, want_jac ? 1 : 0, g0, g1, 0, 0, first);
+        HDGB_LAUNCH_CHECK(ctx);
+        first = 0;
+    }
+    for (int p0 = 0; p0 < nfp; p0 += fc) {
+        const int p1 = std::min(nfp, p0 + fc);
+        kern<<<dv.ne, 256, fixed + (p1 - p0) * sfr, ctx->stream>>>(dv, mv, in, out, want_jac ? 1 : 0, 0, 0, p0, p1, first);
+        HDGB_LAUNCH_CHECK(ctx);
+        first = 0;
+    }
 }
 
 }  // namespace
@@ -517,6 +574,10 @@ void launch_local_assemble(hdgb_ctx* ctx, const DiscView& dv, const ModelView& m
         case HDGB_MODEL_ELASTICITY:
             if (D == 2) launch_assemble_t<ElasticityModel<2>>(ctx, dv, mv, in, out, want_jac);
             else launch_assemble_t<ElasticityModel<3>>(ctx, dv, mv, in, out, want_jac);
+            break;
+        case HDGB_MODEL_NAVIER_STOKES:
+            if (D == 2) launch_assemble_t<NavierStokesModel<2>>(ctx, dv, mv, in, out, want_jac);
+            else launch_assemble_t<NavierStokesModel<3>>(ctx, dv, mv, in, out, want_jac);
             break;
         default:
             throw Failure(HDGB_ERR_UNSUPPORTED, "unknown model kind " + std::to_string(mv.kind));

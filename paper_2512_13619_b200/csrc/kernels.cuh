@@ -34,6 +34,7 @@ struct Tuning {
     int use_stream = 1;                  // route large GEMVs through the TMA stream kernel
     int64_t stream_min_elems = 1 << 18;  // below this many matrix entries the team kernel is used
     int use_tile_lu = 1;                 // register-tiled Gauss-Jordan for 25 <= n <= 128
+    int assemble_budget_kb = 216;        // shared memory for the assembly kernel's point records (smaller: chunked sweeps)
 };
 Tuning& tuning();
 

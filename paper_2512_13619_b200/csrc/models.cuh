@@ -223,4 +223,102 @@ struct ElasticityModel : ModelBase<D_, D_> {
     }
 };
 
+// ---- compressible Navier-Stokes (section 5.5-5.7; not in the reference code) ------------
+// Conservative variables u = (rho, rho v_1..rho v_D, rho E), M = D + 2, q = grad u; ideal gas,
+// constant viscosity mu, Prandtl number Pr:
+//   F = F_inv(u) - F_visc(u, q),  p = (gamma - 1)(rho E - rho |v|^2 / 2),
+//   tau = mu (grad v + grad v^T - (2/3) div v I),  heat flux = (mu gamma / Pr) grad e.
+// The Jacobians dF/du and dF/dq are exact forward-mode derivatives (dual numbers) of ONE templated
+// flux routine -- no hand-derived 5 x 3 x 5 x 3 tables.
+struct Dual {
+    double v, d;
+};
+__host__ __device__ inline Dual operator+(Dual a, Dual b) { return {a.v + b.v, a.d + b.d}; }
+__host__ __device__ inline Dual operator-(Dual a, Dual b) { return {a.v - b.v, a.d - b.d}; }
+__host__ __device__ inline Dual operator*(Dual a, Dual b) { return {a.v * b.v, a.d * b.v + a.v * b.d}; }
+__host__ __device__ inline Dual operator/(Dual a, Dual b) {
+    const double iv = 1.0 / b.v;
+    return {a.v * iv, (a.d - a.v * iv * b.d) * iv};
+}
+__host__ __device__ inline Dual operator*(double a, Dual b) { return {a * b.v, a * b.d}; }
+__host__ __device__ inline Dual operator-(Dual a) { return {-a.v, -a.d}; }
+__host__ __device__ inline double make_scalar(double, double v) { return v; }
+__host__ __device__ inline Dual make_scalar(Dual, double v) { return {v, 0.0}; }
+
+template <int D, class T>
+__host__ __device__ void ns_flux(const T* u, const T* q, T* F, double gamma, double mu, double pr) {
+    constexpr int M = D + 2;
+    const T one = make_scalar(T{}, 1.0);
+    const T rinv = one / u[0];
+    T v[D];
+    T ke = make_scalar(T{}, 0.0);
+    for (int i = 0; i < D; ++i) {
+        v[i] = u[1 + i] * rinv;
+        ke = ke + 0.5 * (v[i] * v[i]);
+    }
+    const T E = u[M - 1] * rinv;
+    const T p = (gamma - 1.0) * (u[M - 1] - u[0] * ke);
+    T dv[D][D];
+    T div = make_scalar(T{}, 0.0);
+    for (int i = 0; i < D; ++i)
+        for (int d = 0; d < D; ++d) dv[i][d] = (q[(1 + i) * D + d] - v[i] * q[d]) * rinv;
+    for (int i = 0; i < D; ++i) div = div + dv[i][i];
+    for (int d = 0; d < D; ++d) {
+        T de = (q[(M - 1) * D + d] - E * q[d]) * rinv;
+        for (int i = 0; i < D; ++i) de = de - v[i] * dv[i][d];
+        F[d] = u[1 + d];
+        T work = make_scalar(T{}, 0.0);
+        for (int i = 0; i < D; ++i) {
+            T tau = mu * (dv[i][d] + dv[d][i]);
+            if (i == d) tau = tau - (2.0 / 3.0 * mu) * div;
+            T f = u[1 + i] * v[d] - tau;
+            if (i == d) f = f + p;
+            F[(1 + i) * D + d] = f;
+            work = work + v[i] * tau;
+        }
+        F[(M - 1) * D + d] = (u[M - 1] + p) * v[d] - work - (mu * gamma / pr) * de;
+    }
+}
+
+template <int D_>
+struct NavierStokesModel : ModelBase<D_ + 2, D_> {
+    static constexpr int M = D_ + 2, D = D_;
+    double gamma, mu, pr, tau;
+    __device__ explicit NavierStokesModel(const ModelView& v) : gamma(v.p[0]), mu(v.p[1]), pr(v.p[2]), tau(v.p[3]) {}
+    __device__ void flux(const double* u, const double* q, const double*, double* F) const {
+        ns_flux<D, double>(u, q, F, gamma, mu, pr);
+    }
+    __device__ void dflux_du(const double* u, const double* q, const double*, double* dFu) const {
+        Dual ud[M], qd[M * D], Fd[M * D];
+        for (int i = 0; i < M; ++i) ud[i] = {u[i], 0.0};
+        for (int i = 0; i < M * D; ++i) qd[i] = {q[i], 0.0};
+        for (int mp = 0; mp < M; ++mp) {
+            ud[mp].d = 1.0;
+            ns_flux<D, Dual>(ud, qd, Fd, gamma, mu, pr);
+            ud[mp].d = 0.0;
+            for (int k = 0; k < M * D; ++k) dFu[k * M + mp] = Fd[k].d;
+        }
+    }
+    __device__ void dflux_dq(const double* u, const double* q, const double*, double* dFq) const {
+        Dual ud[M], qd[M * D], Fd[M * D];
+        for (int i = 0; i < M; ++i) ud[i] = {u[i], 0.0};
+        for (int i = 0; i < M * D; ++i) qd[i] = {q[i], 0.0};
+        for (int s = 0; s < M * D; ++s) {  // s = mp*D + dp
+            qd[s].d = 1.0;
+            ns_flux<D, Dual>(ud, qd, Fd, gamma, mu, pr);
+            qd[s].d = 0.0;
+            for (int k = 0; k < M * D; ++k) dFq[k * M * D + s] = Fd[k].d;
+        }
+    }
+    __device__ void source(const double*, const double*, const double*, const double* f, double* S) const {
+        for (int m = 0; m < M; ++m) S[m] = f ? f[m] : 0.0;
+    }
+    __device__ double tau_fn(const double*, const double*, const double*) const { return tau; }
+    // every boundary face pins the trace to the tabulated state (far field / manufactured data)
+    __device__ void boundary(int, const double*, const double*, const double* uhat, const double*, const double*,
+                             const double* g, BFlux<M, D>& b) const {
+        this->dirichlet(uhat, g, b);
+    }
+};
+
 }  // namespace hdgb

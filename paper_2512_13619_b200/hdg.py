@@ -72,7 +72,7 @@ _STATUS = {1: HdgError, 2: SingularBlock, 3: SingularMass, 4: SingularLocalSolve
            10: TooLargeForDense, 11: IoError, 12: InvalidMesh, 13: Unsupported, 14: CudaError}
 
 SHAPES = {"quad": 0, "hex": 1, "tri": 2, "tet": 3}
-MODELS = {"poisson": 0, "burgers": 1, "convdiff": 2, "elasticity": 3, "reaction": 4}
+MODELS = {"poisson": 0, "burgers": 1, "convdiff": 2, "elasticity": 3, "reaction": 4, "navier_stokes": 5}
 PRECONDS = {"none": 0, "identity": 0, "bj": 1, "asm": 2, "ras": 3}
 POLYS = {"gmres": 0, "chebyshev": 1}
 
@@ -573,6 +573,7 @@ class Model:
 
 def make_case_model(disc: Discretization, case: str, tau=None, nu=1.0 / 200.0, kappa=1.0, velocity=(0.0, 1.0),
                     lam=1.0, mu=1.0, alpha=1.0) -> Model:
+    # (mu doubles as the dynamic viscosity of the Navier-Stokes case)
     """make_case_model (study.cpp:31-65) plus the 3D / multi-component cases of BASELINE.json."""
     pi = np.pi
     D = disc.dim
@@ -634,6 +635,26 @@ def make_case_model(disc: Discretization, case: str, tau=None, nu=1.0 / 200.0, k
             return np.stack(out, axis=-1)
         return Model(disc, "elasticity", [lam, mu, 1.0 if tau is None else tau, 0.0], forcing=forcing,
                      dirichlet=exact, exact=exact, name=case)
+    if case in ("navier_stokes", "ns", "taylor_green"):
+        # compressible Navier-Stokes, conservative variables (rho, rho v, rho E); the initial / boundary
+        # state is a smooth low-Mach vortex field of Taylor-Green type on the unit box (PAPER.md 5.7)
+        gamma, pr = 1.4, 0.71
+        mach = 0.1
+        p0 = 1.0 / (gamma * mach * mach)
+
+        def state(x):
+            X = [2 * pi * x[..., d] for d in range(D)]
+            if D == 2:
+                v = [np.sin(X[0]) * np.cos(X[1]), -np.cos(X[0]) * np.sin(X[1])]
+                p = p0 + 0.25 * (np.cos(2 * X[0]) + np.cos(2 * X[1]))
+            else:
+                v = [np.sin(X[0]) * np.cos(X[1]) * np.cos(X[2]), -np.cos(X[0]) * np.sin(X[1]) * np.cos(X[2]), 0.0 * X[0]]
+                p = p0 + (np.cos(2 * X[0]) + np.cos(2 * X[1])) * (np.cos(2 * X[2]) + 2.0) / 16.0
+            rho = np.ones_like(X[0])
+            rhoE = p / (gamma - 1.0) + 0.5 * rho * sum(vi * vi for vi in v)
+            return np.stack([rho] + [rho * vi for vi in v] + [rhoE], axis=-1)
+        return Model(disc, "navier_stokes", [gamma, mu, pr, (1.0 / mach + 1.0) if tau is None else tau], dirichlet=state,
+                     initial=state, name=case)
     raise HdgError(f"unknown case '{case}'")
 
 

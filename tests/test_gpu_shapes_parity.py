@@ -137,3 +137,30 @@ def test_hex_poisson_converges_at_design_order(ctx, shape):
         assert rep.converged
         errs.append(disc.l2_error(state.u, model.exact_solution))
     assert np.log2(errs[0] / errs[1]) >= 2.5          # acceptance_main.cpp:392-395: order >= k + 0.5
+
+
+@pytest.mark.parametrize("shape,case,k,n,ncomp", [("hex", "burgers", 2, 2, 1), ("tet", "elasticity", 2, 2, 3), ("quad", "burgers", 3, 3, 1)])
+def test_point_chunked_assembly_matches_single_sweep(ctx, shape, case, k, n, ncomp):
+    """Wide systems sweep the quadrature points in chunks that accumulate into the outputs; forcing tiny
+    chunks on small systems must reproduce the one-sweep blocks (chunk partial sums are added in the
+    same point order, so only the association of the additions changes)."""
+    disc = hdg.Discretization.structured(ctx, shape, n=n, degree=k, n_comp=ncomp, jitter=0.1, seed=5)
+    model = hdg.make_case_model(disc, case)
+    state = hdg.make_initial_state(disc, model)
+    state.u = state.u + hdg.random_vector(disc.npe * disc.ne, 5, 0.1)
+    state.uhat = state.uhat + hdg.random_vector(disc.n_dof, 6, 0.1)
+    names = ["e_raw", "f_raw", "h_raw", "j_raw", "ru", "ruhat_e", "kbar", "rbar"] + [f"d_raw{d}" for d in range(disc.dim)] + \
+            [f"g_raw{d}" for d in range(disc.dim)]
+    out = {}
+    for kb in (216, 8):
+        hdg.set_tuning("assemble_budget_kb", kb)
+        try:
+            ops = hdg.assemble_element_operators(disc, model, state, keep_raw=True)
+            out[kb] = {nm: ops.get(nm) for nm in names}
+            out[kb]["res"] = hdg.assemble_residual(disc, model, state)
+        finally:
+            hdg.set_tuning("assemble_budget_kb", 216)
+    for nm in names:
+        assert relerr(out[8][nm], out[216][nm]) < (1e-11 if nm in ("kbar", "rbar") else 1e-13), nm
+    for a, b in zip(out[8]["res"][:2], out[216]["res"][:2]):
+        assert relerr(a, b) < 1e-13
