@@ -22,11 +22,13 @@ namespace hdgb {
 
 namespace {
 
-constexpr int kWarps = 8;           // each warp runs its own TMA ring: issue -> wait -> multiply -> re-issue
-constexpr int kThreads = kWarps * 32;
-constexpr int kMaxStages = 16;      // kWarps rings of stages / kWarps stages each
+// Each warp runs its own TMA ring: issue -> wait -> multiply -> re-issue.  8 warps for large items
+// (24 KB stages); 16 warps for small items (a few KB per stage), where the per-item dependency chain
+// -- not the byte stream -- is what has to be hidden.
+constexpr int kMaxWarps = 16;
+constexpr int kMaxThreads = kMaxWarps * 32;
+constexpr int kMaxStages = 32;      // warps rings of stages / warps stages each
 constexpr size_t kSmemBudget = 216 * 1024;
-constexpr size_t kWarpBudget = kSmemBudget / kWarps;  // stage(s) + x buffer + index buffer of one warp
 
 struct StreamPlan {
     int rows, cols;
@@ -40,6 +42,9 @@ struct StreamPlan {
     int stage_elems;      // doubles per stage
     int64_t batch;
     int64_t n_units;      // grouped: chunks; split: items
+    int warps;            // warps per CTA (8 or 16)
+    int ipw;              // packed mode (> 0): items a warp multiplies side by side, one (item, row group) per lane
+    float inv_cols, inv_width;  // reciprocals for the gather's index arithmetic
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -107,10 +112,11 @@ __device__ __forceinline__ void accumulate(const double* __restrict__ A, const d
 }
 
 template <int V, int RT>
-__global__ void __launch_bounds__(kThreads, 1) stream_gemv_kernel(GemvArgs g, StreamPlan p) {
+__global__ void __launch_bounds__(kMaxThreads, 1) stream_gemv_kernel(GemvArgs g, StreamPlan p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* stage_base = reinterpret_cast<double*>(smem_raw);
     double* xs_base = stage_base + static_cast<size_t>(p.stages) * p.stage_elems;
+    const int kWarps = p.warps;
     int* is_base = reinterpret_cast<int*>(xs_base + static_cast<size_t>(kWarps) * 2 * p.xs_elems);
     uint64_t* full = reinterpret_cast<uint64_t*>(is_base + static_cast<size_t>(kWarps) * 3 * p.is_elems);
 
@@ -127,33 +133,35 @@ __global__ void __launch_bounds__(kThreads, 1) stream_gemv_kernel(GemvArgs g, St
 
     // this CTA's contiguous range of units (grouped: chunks, split: items); units are dealt to the
     // warps round-robin and every warp streams ITS chunks through ITS ring, so a waiter is never
-    // more than one mbarrier phase ahead of the copy it waits for.
+    // more than one mbarrier phase ahead of the copy it waits for.  Per-warp counters are 32-bit and
+    // ring positions are carried incrementally: no 64-bit divisions on the per-item path.
     const int64_t u0 = p.n_units * blockIdx.x / gridDim.x;
     const int64_t u1 = p.n_units * (blockIdx.x + 1) / gridDim.x;
-    const int64_t my_units = (u1 - u0 > warp) ? (u1 - u0 - warp + kWarps - 1) / kWarps : 0;
-    const int64_t my_chunks = p.split ? my_units * p.cpi : my_units;
+    const int my_units = (u1 - u0 > warp) ? static_cast<int>((u1 - u0 - warp + kWarps - 1) / kWarps) : 0;
+    const int my_chunks = p.split ? my_units * p.cpi : my_units;
     double* my_stage = stage_base + static_cast<size_t>(warp) * SW * p.stage_elems;
     uint64_t* my_full = full + warp * SW;
+    const int64_t w0 = u0 + warp;  // first unit of this warp; its unit t is w0 + t * kWarps
 
-    // chunk n of this warp -> global source + size
-    auto issue = [&](int64_t n) {
+    // chunk n of this warp into ring stage s
+    auto issue = [&](int n, int s) {
         const double* src;
         int64_t elems;
         if (p.split) {
-            const int64_t item = u0 + warp + (n / p.cpi) * kWarps;
-            const int ci = static_cast<int>(n % p.cpi);
+            const int ui = n / p.cpi;
+            const int ci = n - ui * p.cpi;
+            const int64_t item = w0 + static_cast<int64_t>(ui) * kWarps;
             const int c0 = ci * p.cpc;
             const int nc = min(p.cpc, cols - c0);
             src = g.a + item * item_elems + static_cast<int64_t>(c0) * rows;
             elems = static_cast<int64_t>(nc) * rows;
         } else {
-            const int64_t i0 = (u0 + warp + n * kWarps) * p.ipc;
+            const int64_t i0 = (w0 + static_cast<int64_t>(n) * kWarps) * p.ipc;
             int64_t cnt = g.batch - i0 < p.ipc ? g.batch - i0 : p.ipc;
             if ((item_elems & 1) && (cnt & 1)) --cnt;  // keep the copy a multiple of 16 bytes; the odd tail item is read directly
             src = g.a + i0 * item_elems;
             elems = cnt * item_elems;
         }
-        const int s = static_cast<int>(n % SW);
         const uint32_t bytes = static_cast<uint32_t>(elems * sizeof(double));
         // order the warp's earlier generic-proxy reads of this stage before the async-proxy write
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -161,7 +169,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_gemv_kernel(GemvArgs g, St
         if (bytes) tma_bulk_g2s(my_stage + static_cast<size_t>(s) * p.stage_elems, src, bytes, my_full + s);
     };
     if (lane == 0)
-        for (int64_t n = 0; n < SW && n < my_chunks; ++n) issue(n);
+        for (int n = 0; n < SW && n < my_chunks; ++n) issue(n, n);
 
     // per-warp x (double-buffered) and index (triple-buffered) staging, filled with cp.async so the
     // gather of the NEXT unit runs behind the multiply of the current one
@@ -172,53 +180,69 @@ __global__ void __launch_bounds__(kThreads, 1) stream_gemv_kernel(GemvArgs g, St
     const int cg = RL >= 32 ? 0 : lane / RL;
     const int rl = RL >= 32 ? lane : lane - cg * RL;
     const int nslots = g.idx ? cols / g.width : 0;
+    const int width = g.width;
 
     // unit t of this warp -> first item and item count
-    auto unit_items = [&](int64_t t, int64_t& item0, int& cnt) {
+    auto unit_items = [&](int t, int64_t& item0, int& cnt) {
         if (p.split) {
-            item0 = u0 + warp + t * kWarps;
+            item0 = w0 + static_cast<int64_t>(t) * kWarps;
             cnt = 1;
         } else {
-            item0 = (u0 + warp + t * kWarps) * p.ipc;
+            item0 = (w0 + static_cast<int64_t>(t) * kWarps) * p.ipc;
             cnt = static_cast<int>(g.batch - item0 < p.ipc ? g.batch - item0 : p.ipc);
         }
     };
-    // pipeline stage 0: index rows of unit t -> is_w[t % 3]   (one cp.async group, possibly empty)
-    auto stage_idx = [&](int64_t t) {
+    // pipeline stage 0: index rows of unit t -> index buffer ib   (one cp.async group, possibly empty)
+    auto stage_idx = [&](int t, int ib) {
         if (t < my_units && g.idx != nullptr) {
             int64_t item0;
             int cnt;
             unit_items(t, item0, cnt);
-            const int* ib = g.idx + item0 * nslots;
-            int* dst = is_w + (t % 3) * p.is_elems;
+            const int* src = g.idx + item0 * nslots;
+            const uint32_t dst = smem_u32(is_w + ib * p.is_elems);
             const int ts = cnt * nslots;
             for (int j = lane; j < ts; j += 32)
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst + j)), "l"(ib + j) : "memory");
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst + 4u * j), "l"(src + j) : "memory");
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    // pipeline stage 1: x entries of unit t -> xs_w[t % 2]; needs the unit's index rows in shared memory
-    auto stage_x = [&](int64_t t) {
+    // pipeline stage 1: x entries of unit t -> x buffer xb; needs the unit's index rows (buffer ib) in shared memory
+    auto stage_x = [&](int t, int xb, int ib) {
         if (t < my_units) {
             int64_t item0;
             int cnt;
             unit_items(t, item0, cnt);
-            double* dst = xs_w + (t % 2) * p.xs_elems;
+            const uint32_t dst = smem_u32(xs_w + xb * p.xs_elems);
             const int total = cnt * cols;
             if (g.idx == nullptr) {
-                const double* xb = g.x + item0 * cols;
+                const double* xg = g.x + item0 * cols;
                 for (int j = lane; j < total; j += 32)
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst + j)), "l"(xb + j) : "memory");
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 8u * j), "l"(xg + j) : "memory");
             } else {
-                const int* is = is_w + (t % 3) * p.is_elems;
-                for (int j = lane; j < total; j += 32) {
-                    const int it = j / cols, c = j - it * cols;
-                    const int sl = c / g.width;
-                    const int o = c - sl * g.width;
-                    const int src = is[it * nslots + sl];
-                    const double* sp = src < 0 ? g.x : g.x + static_cast<int64_t>(src) * g.width + o;
-                    const int nbytes = src < 0 ? 0 : 8;  // src-size 0 zero-fills: absent neighbour (kNoFace)
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst + j)), "l"(sp), "r"(nbytes) : "memory");
+                const int* is = is_w + ib * p.is_elems;
+                if (p.ipw > 0) {
+                    // narrow slices: one lane per (item, slot) copies the whole slice -- no per-entry index arithmetic
+                    const int ts = cnt * nslots;
+                    for (int j = lane; j < ts; j += 32) {
+                        const int src = is[j];
+                        const double* sp = g.x + static_cast<int64_t>(src < 0 ? 0 : src) * width;
+                        const int nbytes = src < 0 ? 0 : 8;  // src-size 0 zero-fills: absent neighbour (kNoFace)
+                        uint32_t d = dst + 8u * static_cast<uint32_t>(j * width);
+#pragma unroll 5
+                        for (int o = 0; o < width; ++o, d += 8u, ++sp)
+                            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(sp), "r"(nbytes) : "memory");
+                    }
+                } else {
+                    for (int j = lane; j < total; j += 32) {
+                        // exact for j < 2^21: (j + 0.5) / cols is at least 0.5 / cols away from an integer
+                        const int it = static_cast<int>((j + 0.5f) * p.inv_cols), c = j - it * cols;
+                        const int sl = static_cast<int>((c + 0.5f) * p.inv_width);
+                        const int o = c - sl * width;
+                        const int src = is[it * nslots + sl];
+                        const double* sp = src < 0 ? g.x : g.x + static_cast<int64_t>(src) * width + o;
+                        const int nbytes = src < 0 ? 0 : 8;
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst + 8u * j), "l"(sp), "r"(nbytes) : "memory");
+                    }
                 }
             }
         }
@@ -254,21 +278,27 @@ __global__ void __launch_bounds__(kThreads, 1) stream_gemv_kernel(GemvArgs g, St
         }
     };
 
-    stage_idx(0);
-    stage_idx(1);
+    stage_idx(0, 0);
+    stage_idx(1, 1);
     asm volatile("cp.async.wait_group 1;" ::: "memory");
     __syncwarp();
-    stage_x(0);
-    int64_t n = 0;  // this warp's running chunk counter (TMA ring position)
-    for (int64_t t = 0; t < my_units; ++t) {
-        stage_idx(t + 2);
+    stage_x(0, 0, 0);
+    int n = 0;             // this warp's running chunk counter
+    int rs = 0;            // ring stage of chunk n
+    uint32_t rph = 0;      // mbarrier phase parity of chunk n
+    int i3 = 0, i2 = 0;    // t % 3, t % 2
+    const int si = lane / RL, prl = lane - si * RL;  // packed mode: item slot and row group of this lane
+    for (int t = 0; t < my_units; ++t) {
+        const int i3n = (i3 == 2) ? 0 : i3 + 1;        // (t + 1) % 3
+        const int i3nn = (i3n == 2) ? 0 : i3n + 1;     // (t + 2) % 3
+        stage_idx(t + 2, i3nn);
         asm volatile("cp.async.wait_group 1;" ::: "memory");  // index rows of t+1 and x of t have landed
         __syncwarp();
-        stage_x(t + 1);
+        stage_x(t + 1, i2 ^ 1, i3n);
         int64_t item0;
         int cnt;
         unit_items(t, item0, cnt);
-        const double* xs = xs_w + (t % 2) * p.xs_elems;
+        const double* xs = xs_w + i2 * p.xs_elems;
         if (p.split) {
             double acc[RT][V];
 #pragma unroll
@@ -276,39 +306,86 @@ __global__ void __launch_bounds__(kThreads, 1) stream_gemv_kernel(GemvArgs g, St
 #pragma unroll
                 for (int v = 0; v < V; ++v) acc[tt][v] = 0.0;
             for (int ci = 0; ci < p.cpi; ++ci, ++n) {
-                const int s = static_cast<int>(n % SW);
                 const int c0 = ci * p.cpc;
                 const int nc = min(p.cpc, cols - c0);
-                mbar_wait(my_full + s, static_cast<uint32_t>((n / SW) & 1));
-                accumulate<V, RT>(my_stage + static_cast<size_t>(s) * p.stage_elems, xs + c0, rows, nc, rl, cg, CG, acc);
+                mbar_wait(my_full + rs, rph);
+                accumulate<V, RT>(my_stage + static_cast<size_t>(rs) * p.stage_elems, xs + c0, rows, nc, rl, cg, CG, acc);
                 __syncwarp();
-                if (lane == 0 && n + SW < my_chunks) issue(n + SW);
+                if (lane == 0 && n + SW < my_chunks) issue(n + SW, rs);
+                if (++rs == SW) { rs = 0; rph ^= 1u; }
             }
             reduce_store(acc, item0);
         } else {
-            const int s = static_cast<int>(n % SW);
             const int cnt_tma = ((item_elems & 1) && (cnt & 1)) ? cnt - 1 : cnt;
-            mbar_wait(my_full + s, static_cast<uint32_t>((n / SW) & 1));
-            const double* st = my_stage + static_cast<size_t>(s) * p.stage_elems;
-            for (int it = 0; it < cnt; ++it) {
-                double acc[RT][V];
+            mbar_wait(my_full + rs, rph);
+            const double* st = my_stage + static_cast<size_t>(rs) * p.stage_elems;
+            if (p.ipw > 0) {
+                // packed: lane = (item slot si, row group prl); every lane sweeps all columns of its
+                // item with two independent accumulators -- no cross-lane reduction
+                const int ie = static_cast<int>(item_elems);
+                for (int it0 = 0; it0 < cnt; it0 += p.ipw) {
+                    const int it = it0 + si;
+                    if (si < p.ipw && it < cnt) {
+                        const double* ap = ((it < cnt_tma) ? st + it * ie : g.a + (item0 + it) * item_elems) + prl * V;
+                        const double* xp = xs + it * cols;
+                        double a0[V], a1[V];
 #pragma unroll
-                for (int tt = 0; tt < RT; ++tt)
+                        for (int v = 0; v < V; ++v) a0[v] = a1[v] = 0.0;
+                        int c = cols;
+#pragma unroll 4
+                        for (; c >= 2; c -= 2, ap += 2 * rows, xp += 2) {
+                            double r0[V], r1[V];
+                            lds_rows<V>(ap, r0);
+                            lds_rows<V>(ap + rows, r1);
+                            const double x0 = xp[0], x1 = xp[1];
 #pragma unroll
-                    for (int v = 0; v < V; ++v) acc[tt][v] = 0.0;
-                if (it < cnt_tma) {
-                    accumulate<V, RT>(st + static_cast<size_t>(it) * item_elems, xs + static_cast<size_t>(it) * cols, rows, cols, rl, cg, CG, acc);
-                } else if (V == 1) {
-                    // odd tail item that the 16-byte granular copy left out: read it from global memory
-                    accumulate<V, RT>(g.a + (item0 + it) * item_elems, xs + static_cast<size_t>(it) * cols, rows, cols, rl, cg, CG, acc);
+                            for (int v = 0; v < V; ++v) {
+                                a0[v] = fma(r0[v], x0, a0[v]);
+                                a1[v] = fma(r1[v], x1, a1[v]);
+                            }
+                        }
+                        if (c > 0) {
+                            double r0[V];
+                            lds_rows<V>(ap, r0);
+                            const double x0 = xp[0];
+#pragma unroll
+                            for (int v = 0; v < V; ++v) a0[v] = fma(r0[v], x0, a0[v]);
+                        }
+                        const int64_t o = (item0 + it) * rows + prl * V;
+#pragma unroll
+                        for (int v = 0; v < V; ++v) {
+                            if (prl * V + v < rows) {
+                                double out = g.alpha * (a0[v] + a1[v]);
+                                if (g.z != nullptr) out += g.beta * g.z[o + v];
+                                g.y[o + v] = out;
+                            }
+                        }
+                    }
                 }
-                reduce_store(acc, item0 + it);
+            } else {
+                for (int it = 0; it < cnt; ++it) {
+                    double acc[RT][V];
+#pragma unroll
+                    for (int tt = 0; tt < RT; ++tt)
+#pragma unroll
+                        for (int v = 0; v < V; ++v) acc[tt][v] = 0.0;
+                    if (it < cnt_tma) {
+                        accumulate<V, RT>(st + static_cast<size_t>(it) * item_elems, xs + static_cast<size_t>(it) * cols, rows, cols, rl, cg, CG, acc);
+                    } else if (V == 1) {
+                        // odd tail item that the 16-byte granular copy left out: read it from global memory
+                        accumulate<V, RT>(g.a + (item0 + it) * item_elems, xs + static_cast<size_t>(it) * cols, rows, cols, rl, cg, CG, acc);
+                    }
+                    reduce_store(acc, item0 + it);
+                }
             }
             __syncwarp();
-            if (lane == 0 && n + SW < my_chunks) issue(n + SW);
+            if (lane == 0 && n + SW < my_chunks) issue(n + SW, rs);
+            if (++rs == SW) { rs = 0; rph ^= 1u; }
             ++n;
         }
         __syncwarp();
+        i3 = i3n;
+        i2 ^= 1;
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
@@ -321,7 +398,7 @@ void launch_t(hdgb_ctx* ctx, const GemvArgs& g, const StreamPlan& p, int grid, s
         HDGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         configured = smem;
     }
-    kern<<<grid, kThreads, smem, ctx->stream>>>(g, p);
+    kern<<<grid, p.warps * 32, smem, ctx->stream>>>(g, p);
     HDGB_LAUNCH_CHECK(ctx);
 }
 
@@ -348,12 +425,30 @@ bool launch_stream_gemv(hdgb_ctx* ctx, const GemvArgs& g) {
     p.cols = cols;
     p.batch = g.batch;
     const int nslots = g.idx ? cols / g.width : 0;
+    p.inv_cols = 1.0f / static_cast<float>(cols);
+    p.inv_width = g.idx ? 1.0f / static_cast<float>(g.width) : 1.0f;
+    // small items (short column sweeps): 16 warps, several items side by side in a warp
+    const bool packed = tuning().stream_packed && RT == 1 && RL <= 16 && cols <= tuning().stream_packed_max_cols;
+    const int kWarps = packed ? 16 : 8;
+    p.warps = kWarps;
+    p.ipw = packed ? 32 / RL : 0;
+    const size_t kWarpBudget = kSmemBudget / kWarps;  // stage(s) + x buffer + index buffer of one warp
     // per-warp shared memory: one or more stages + the x slice(s) + the index row(s)
     const size_t per_item = static_cast<size_t>(item_elems + 2 * cols) * sizeof(double) + 3 * static_cast<size_t>(nslots) * sizeof(int) + 8;
     if (per_item + 128 <= kWarpBudget) {
         p.split = 0;
         p.ipc = static_cast<int>((kWarpBudget - 128) / per_item);
         if (p.ipc > 64) p.ipc = 64;
+        if (packed) {
+            // two stages of a few KB per warp: whole passes of ipw items
+            const int want = static_cast<int>(tuning().stream_packed_stage_bytes / (item_elems * sizeof(double)));
+            int ipc = (want / p.ipw) * p.ipw;
+            if (ipc < p.ipw) ipc = p.ipw;
+            const int half = static_cast<int>((kWarpBudget - 128) / (2 * per_item));
+            if (ipc > half) ipc = half;
+            if (ipc < 1) ipc = 1;
+            if (ipc < p.ipc) p.ipc = ipc;
+        }
         if ((item_elems & 1) && (p.ipc & 1)) {
             if (p.ipc == 1) return false;
             --p.ipc;

@@ -33,6 +33,9 @@ bool launch_stream_gemv(hdgb_ctx* ctx, const GemvArgs& g);
 struct Tuning {
     int use_stream = 1;                  // route large GEMVs through the TMA stream kernel
     int64_t stream_min_elems = 1 << 18;  // below this many matrix entries the team kernel is used
+    int stream_packed = 1;               // small items: 16 warps, several items side by side per warp, no shuffle tree
+    int stream_packed_max_cols = 32;     // ... for items with at most this many columns
+    int64_t stream_packed_stage_bytes = 6144;  // ... bytes per TMA stage of a warp in packed mode
     int use_tile_lu = 1;                 // register-tiled Gauss-Jordan for 25 <= n <= 128
     int assemble_budget_kb = 216;        // shared memory for the assembly kernel's point records (smaller: chunked sweeps)
 };

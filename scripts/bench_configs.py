@@ -47,6 +47,10 @@ def run(cfg_id, a):
     if a.n.get(cfg_id):
         cfg["n"] = a.n[cfg_id]
     ctx = hdg.Context(0)
+    for kv in a.tune.split(","):
+        if kv:
+            k, v = kv.split("=")
+            hdg.set_tuning(k, int(v))
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
 
@@ -98,6 +102,12 @@ def run(cfg_id, a):
     peak = peak_gbs()
     del P, K, rhs, ops
 
+    if a.no_solve:
+        ctx.close()
+        return {"config": cfg_id, "name": cfg["name"], "tuning": a.tune,
+                "matvec_GBps": bytes_mv / t_mv / 1e9, "matvec_frac": bytes_mv / t_mv / 1e9 / peak, "matvec_us": 1e6 * t_mv,
+                "precond_GBps": bytes_pc / t_pc / 1e9, "precond_frac": bytes_pc / t_pc / 1e9 / peak, "precond_us": 1e6 * t_pc,
+                "assemble_element_operators_s": t_ass, "assemble_global_s": t_glob, "precond_build_s": t_pb}
     # one complete solve from the initial state (second run timed: warm allocator, as in bench.py)
     gcfg, ncfg = hdg.GmresConfig(), hdg.NewtonConfig()
 
@@ -140,6 +150,8 @@ def main():
     ap.add_argument("--configs", default="1,2,3,4,5")
     ap.add_argument("--out", default="gpurun_out/configs.json")
     ap.add_argument("--n", default="", help="override mesh sizes, e.g. 5=24,3=256")
+    ap.add_argument("--no-solve", action="store_true", help="kernel and phase timings only")
+    ap.add_argument("--tune", default="", help="tuning knobs, e.g. stream_packed=0,stream_packed_stage_bytes=4096")
     a = ap.parse_args()
     a.n = {int(k): int(v) for k, v in (kv.split("=") for kv in a.n.split(",") if kv)}
     lines = []
