@@ -44,7 +44,8 @@ struct StreamPlan {
     int64_t n_units;      // grouped: chunks; split: items
     int warps;            // warps per CTA (8 or 16)
     int ipw;              // packed mode (> 0): items a warp multiplies side by side, one (item, row group) per lane
-    float inv_cols, inv_width;  // reciprocals for the gather's index arithmetic
+    int xstride;          // doubles between the x slices of consecutive items of a chunk (cols, or cols + 1 in packed mode with odd cols)
+    float inv_cols, inv_width, inv_nslots;  // reciprocals for the gather's index arithmetic
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -163,8 +164,9 @@ __global__ void __launch_bounds__(kMaxThreads, 1) stream_gemv_kernel(GemvArgs g,
             elems = cnt * item_elems;
         }
         const uint32_t bytes = static_cast<uint32_t>(elems * sizeof(double));
-        // order the warp's earlier generic-proxy reads of this stage before the async-proxy write
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        // The stage is re-armed by lane 0 after __syncwarp(): every lane's reads of it have returned
+        // (their values fed FMAs).  Write-after-read across proxies needs no proxy fence -- the same
+        // ordering TMA producer/consumer pipelines rely on when a consumer releases a stage.
         mbar_expect_tx(my_full + s, bytes);
         if (bytes) tma_bulk_g2s(my_stage + static_cast<size_t>(s) * p.stage_elems, src, bytes, my_full + s);
     };
@@ -216,8 +218,15 @@ __global__ void __launch_bounds__(kMaxThreads, 1) stream_gemv_kernel(GemvArgs g,
             const int total = cnt * cols;
             if (g.idx == nullptr) {
                 const double* xg = g.x + item0 * cols;
-                for (int j = lane; j < total; j += 32)
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 8u * j), "l"(xg + j) : "memory");
+                if (p.xstride == cols) {
+                    for (int j = lane; j < total; j += 32)
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 8u * j), "l"(xg + j) : "memory");
+                } else {
+                    for (int j = lane; j < total; j += 32) {
+                        const int it = static_cast<int>((j + 0.5f) * p.inv_cols);
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 8u * (j + it)), "l"(xg + j) : "memory");
+                    }
+                }
             } else {
                 const int* is = is_w + ib * p.is_elems;
                 if (p.ipw > 0) {
@@ -227,7 +236,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1) stream_gemv_kernel(GemvArgs g,
                         const int src = is[j];
                         const double* sp = g.x + static_cast<int64_t>(src < 0 ? 0 : src) * width;
                         const int nbytes = src < 0 ? 0 : 8;  // src-size 0 zero-fills: absent neighbour (kNoFace)
-                        uint32_t d = dst + 8u * static_cast<uint32_t>(j * width);
+                        const int it = static_cast<int>((j + 0.5f) * p.inv_nslots);
+                        uint32_t d = dst + 8u * static_cast<uint32_t>(j * width + it * (p.xstride - cols));
 #pragma unroll 5
                         for (int o = 0; o < width; ++o, d += 8u, ++sp)
                             asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(sp), "r"(nbytes) : "memory");
@@ -326,30 +336,39 @@ __global__ void __launch_bounds__(kMaxThreads, 1) stream_gemv_kernel(GemvArgs g,
                 for (int it0 = 0; it0 < cnt; it0 += p.ipw) {
                     const int it = it0 + si;
                     if (si < p.ipw && it < cnt) {
-                        const double* ap = ((it < cnt_tma) ? st + it * ie : g.a + (item0 + it) * item_elems) + prl * V;
-                        const double* xp = xs + it * cols;
+                        const double* xp = xs + it * p.xstride;
                         double a0[V], a1[V];
 #pragma unroll
                         for (int v = 0; v < V; ++v) a0[v] = a1[v] = 0.0;
                         int c = cols;
+                        if (it < cnt_tma) {
+                            const double* ap = st + it * ie + prl * V;  // shared memory
 #pragma unroll 4
-                        for (; c >= 2; c -= 2, ap += 2 * rows, xp += 2) {
-                            double r0[V], r1[V];
-                            lds_rows<V>(ap, r0);
-                            lds_rows<V>(ap + rows, r1);
-                            const double x0 = xp[0], x1 = xp[1];
+                            for (; c >= 2; c -= 2, ap += 2 * rows, xp += 2) {
+                                double r0[V], r1[V];
+                                lds_rows<V>(ap, r0);
+                                lds_rows<V>(ap + rows, r1);
+                                const double2 xx = *reinterpret_cast<const double2*>(xp);
 #pragma unroll
-                            for (int v = 0; v < V; ++v) {
-                                a0[v] = fma(r0[v], x0, a0[v]);
-                                a1[v] = fma(r1[v], x1, a1[v]);
+                                for (int v = 0; v < V; ++v) {
+                                    a0[v] = fma(r0[v], xx.x, a0[v]);
+                                    a1[v] = fma(r1[v], xx.y, a1[v]);
+                                }
                             }
-                        }
-                        if (c > 0) {
-                            double r0[V];
-                            lds_rows<V>(ap, r0);
-                            const double x0 = xp[0];
+                            if (c > 0) {
+                                double r0[V];
+                                lds_rows<V>(ap, r0);
+                                const double x0 = xp[0];
 #pragma unroll
-                            for (int v = 0; v < V; ++v) a0[v] = fma(r0[v], x0, a0[v]);
+                                for (int v = 0; v < V; ++v) a0[v] = fma(r0[v], x0, a0[v]);
+                            }
+                        } else {
+                            // odd tail item that the 16-byte granular copy left out: read it from global memory
+                            const double* ap = g.a + (item0 + it) * item_elems + prl * V;
+                            for (; c > 0; --c, ap += rows, ++xp) {
+#pragma unroll
+                                for (int v = 0; v < V; ++v) a0[v] = fma(__ldg(ap + v), xp[0], a0[v]);
+                            }
                         }
                         const int64_t o = (item0 + it) * rows + prl * V;
 #pragma unroll
@@ -427,6 +446,7 @@ bool launch_stream_gemv(hdgb_ctx* ctx, const GemvArgs& g) {
     const int nslots = g.idx ? cols / g.width : 0;
     p.inv_cols = 1.0f / static_cast<float>(cols);
     p.inv_width = g.idx ? 1.0f / static_cast<float>(g.width) : 1.0f;
+    p.inv_nslots = nslots > 0 ? 1.0f / static_cast<float>(nslots) : 1.0f;
     // small items (short column sweeps): 16 warps, several items side by side in a warp
     const bool packed = tuning().stream_packed && RT == 1 && RL <= 16 && cols <= tuning().stream_packed_max_cols;
     const int kWarps = packed ? 16 : 8;
@@ -434,7 +454,7 @@ bool launch_stream_gemv(hdgb_ctx* ctx, const GemvArgs& g) {
     p.ipw = packed ? 32 / RL : 0;
     const size_t kWarpBudget = kSmemBudget / kWarps;  // stage(s) + x buffer + index buffer of one warp
     // per-warp shared memory: one or more stages + the x slice(s) + the index row(s)
-    const size_t per_item = static_cast<size_t>(item_elems + 2 * cols) * sizeof(double) + 3 * static_cast<size_t>(nslots) * sizeof(int) + 8;
+    const size_t per_item = static_cast<size_t>(item_elems + 2 * (cols + 1)) * sizeof(double) + 3 * static_cast<size_t>(nslots) * sizeof(int) + 8;
     if (per_item + 128 <= kWarpBudget) {
         p.split = 0;
         p.ipc = static_cast<int>((kWarpBudget - 128) / per_item);
@@ -456,13 +476,15 @@ bool launch_stream_gemv(hdgb_ctx* ctx, const GemvArgs& g) {
         p.cpc = cols;
         p.cpi = 1;
         p.stage_elems = static_cast<int>(p.ipc * item_elems);
-        p.xs_elems = p.ipc * cols;
+        p.xstride = packed ? ((cols + 1) & ~1) : cols;
+        p.xs_elems = p.ipc * p.xstride;
         p.is_elems = p.ipc * nslots;
         p.n_units = (g.batch + p.ipc - 1) / p.ipc;
     } else {
         if ((rows & 1) && (cols & 1)) return false;  // items would start on 8-byte boundaries
         p.split = 1;
         p.ipc = 1;
+        p.xstride = cols;
         p.xs_elems = cols;
         p.is_elems = nslots;
         const size_t side = 2 * static_cast<size_t>(cols) * sizeof(double) + 3 * static_cast<size_t>(nslots) * sizeof(int) + 32;
