@@ -572,6 +572,13 @@ hdgb_ops* assemble_element_operators_device(hdgb_disc* d, const hdgb_model* m, h
                 if (M == 1) {
                     launch_gemm_batch(c, npe, nfl, pe, lo.Dm[k], sEE, false, mc, sc, lo.F, sEF, cnt, -1.0, 1.0);
                     launch_gemm_batch(c, nfl, nfl, pe, lo.G[k], sEF, false, mc, sc, lo.J, sFF, cnt, -1.0, 1.0);
+                } else if (tuning().use_dmma) {
+                    // all local faces in one product: B = M^-1 C_d (pe x n_lfe pf); output column (lf, b)
+                    // lands in column lf*mpf + mp*pf + b of F-bar / J-bar
+                    launch_gemm_dmma(c, npe, v.nfs, pe, lo.Dm[k] + colblk * npe, sEE, mc, sc,
+                                     lo.F + static_cast<size_t>(mp) * pf * npe, sEF, cnt, -1.0, 1.0, pf, mpf);
+                    launch_gemm_dmma(c, nfl, v.nfs, pe, lo.G[k] + colblk * nfl, sEF, mc, sc,
+                                     lo.J + static_cast<size_t>(mp) * pf * nfl, sFF, cnt, -1.0, 1.0, pf, mpf);
                 } else {
                     for (int lf = 0; lf < v.n_lfe; ++lf) {
                         const size_t tcol = static_cast<size_t>(lf) * mpf + static_cast<size_t>(mp) * pf;

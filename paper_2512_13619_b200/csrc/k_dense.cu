@@ -478,6 +478,10 @@ void launch_lu_invert_batch(hdgb_ctx* ctx, int n, int64_t batch, const double* a
         HDGB_LAUNCH_CHECK(ctx);
         return;
     }
+    if (tuning().use_blocked_gj) {
+        launch_gj_invert_batch(ctx, n, batch, a, inv, flags);
+        return;
+    }
     if (n <= 128 && tuning().use_tile_lu) {
         const int64_t cap = static_cast<int64_t>(ctx->sm_count) * 8;
         const int grid = static_cast<int>(batch < cap ? batch : cap);
@@ -521,6 +525,10 @@ void launch_gemm_batch(hdgb_ctx* ctx, int m, int n, int k, const double* a, int6
         gemm_small_kernel<<<ceil_div(batch, items), threads, 0, ctx->stream>>>(
             m, n, k, a, a_stride, trans_a, b, b_stride, c, c_stride, batch, alpha, beta, items);
         HDGB_LAUNCH_CHECK(ctx);
+        return;
+    }
+    if (!trans_a && tuning().use_dmma) {
+        launch_gemm_dmma(ctx, m, n, k, a, a_stride, b, b_stride, c, c_stride, batch, alpha, beta);
         return;
     }
     int64_t done = 0;

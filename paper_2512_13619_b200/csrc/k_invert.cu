@@ -1,0 +1,446 @@
+// Blocked in-place Gauss-Jordan inverse for batches of n x n blocks, any n (lu_invert_batch,
+// dense_batch.cpp:19-99: explicit inverses with partial pivoting, singularity test pivot <= 1e-14 max|A|,
+// lowest failing batch index).  Used for E-bar^-1 (local_ops.cpp:400-404), the block-Jacobi and the
+// additive-Schwarz inverses (preconditioner.cpp:30-46, 54-84).
+//
+// Algorithm (panel width NB = 16).  Gauss-Jordan with row interchanges, in place, leaves (P A)^-1; the
+// inverse is its column permutation.  One elimination step k maps the matrix to G_k S_k M where S_k
+// swaps rows k and p_k and G_k differs from the identity in column k only.  For a panel of NB pivots
+//     G_{k+NB-1} S_{k+NB-1} ... G_k S_k  =  G' (S_{k+NB-1} ... S_k),
+// and the NB non-trivial columns of G' are exactly what the in-place algorithm leaves in the panel
+// columns.  So per panel:
+//   (1) gj_panel_kernel  -- one warp per block factors the n x NB panel in shared memory (pivot search =
+//       first row of maximal modulus among rows >= k, the reference's rule), records the pivots and the
+//       row gather map of the panel's interchanges, and writes the panel into the NEW buffer;
+//   (2) gj_update_kernel -- every other column c:  new[:, c] = rowperm(old[:, c]) + (G' - I) old[piv rows, c],
+//       a rank-NB update on the FP64 tensor-core path (DMMA m8n8k4), the row interchanges folded into the
+//       gather of the operands.  Reads the old buffer, writes the new one (ping-pong), so each panel costs
+//       one read + one write of the batch: the kernel is HBM bound, 2 n^3 flops per block like the reference.
+// After ceil(n / NB) panels gj_colperm_kernel applies the column permutation into the destination.
+// Results agree with the reference's LU + solves to rounding (different but equally stable operation order).
+#include <climits>
+
+#include "kernels.cuh"
+
+namespace hdgb {
+
+namespace {
+
+constexpr int NB = 16;
+constexpr int LDB = NB + 4;  // = 4 (mod 16): conflict-free DMMA fragment loads
+
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+// ---- prepass: copy a -> x0 and amax[b] = max |A_b| ------------------------------------------------------
+__global__ void gj_prepare_kernel(int n, const double* __restrict__ a, double* __restrict__ x0, double* __restrict__ amax) {
+    const int64_t b = blockIdx.x;
+    const int64_t nn = static_cast<int64_t>(n) * n;
+    const double* A = a + b * nn;
+    double* X = x0 + b * nn;
+    double m = 0.0;
+    for (int64_t t = threadIdx.x; t < nn; t += blockDim.x) {
+        const double v = A[t];
+        m = fmax(m, fabs(v));  // fmax drops NaNs like the reference's std::max scan
+        if (X != A) X[t] = v;
+    }
+    __shared__ double red[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (blockDim.x >> 5); ++w) m = fmax(m, red[w]);
+        amax[b] = m;
+    }
+}
+
+// ---- panel factorisation: one warp per block ---------------------------------------------------------------
+// src[b][r] = row of the OLD buffer that ends up in row r after this panel's interchanges.
+__global__ void gj_panel_kernel(int n, int j0, int64_t batch, const double* __restrict__ old, double* __restrict__ nw,
+                                const double* __restrict__ amax, int* __restrict__ piv, int* __restrict__ src,
+                                int* flags, int ldp, int64_t b_base) {
+    extern __shared__ double sm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t b = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + warp;
+    if (b >= batch) return;
+    double* P = sm + static_cast<size_t>(warp) * NB * ldp;
+    const int64_t nn = static_cast<int64_t>(n) * n;
+    const int nbk = min(NB, n - j0);
+    const double* O = old + b * nn + static_cast<int64_t>(j0) * n;
+    for (int c = 0; c < nbk; ++c)
+        for (int r = lane; r < n; r += 32) P[c * ldp + r] = O[static_cast<int64_t>(c) * n + r];
+    int* S = src + b * n;
+    for (int r = lane; r < n; r += 32) S[r] = r;
+    __syncwarp();
+    const double tol = 1e-14 * amax[b];
+    bool bad = false;
+    for (int c = 0; c < nbk; ++c) {
+        const int k = j0 + c;
+        const double* col = P + c * ldp;
+        // first row of maximal modulus among rows >= k (dense_batch.cpp:27-33)
+        double best = -1.0;
+        int bi = INT_MAX;
+        for (int r = k + lane; r < n; r += 32) {
+            const double v = fabs(col[r]);
+            if (v > best) { best = v; bi = r; }
+        }
+        // |v| compares like its bit pattern: three integer warp reductions instead of a shuffle tree
+        const unsigned long long bits = best < 0.0 ? 0ull : static_cast<unsigned long long>(__double_as_longlong(best));
+        const unsigned hi = static_cast<unsigned>(bits >> 32), lo = static_cast<unsigned>(bits);
+        const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+        const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+        const bool win = (bi != INT_MAX) && hi == mhi && lo == mlo;
+        const int p = static_cast<int>(__reduce_min_sync(0xffffffffu, win ? static_cast<unsigned>(bi) : 0xffffffffu));
+        const double dkk = col[k];
+        const double bestv = __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(mhi) << 32) | mlo));
+        const bool ok = (dkk == dkk) && (bestv > tol) && p < n;
+        const int pp = ok ? p : k;
+        if (!ok) bad = true;
+        if (lane == 0) {
+            piv[b * n + k] = pp;
+            const int t = S[k];
+            S[k] = S[pp];
+            S[pp] = t;
+        }
+        // interchange rows k and pp inside the panel
+        if (lane < nbk && pp != k) {
+            double* q = P + lane * ldp;
+            const double t = q[k];
+            q[k] = q[pp];
+            q[pp] = t;
+        }
+        __syncwarp();
+        double rowk[NB];
+#pragma unroll
+        for (int c2 = 0; c2 < NB; ++c2) rowk[c2] = c2 < nbk ? P[c2 * ldp + k] : 0.0;
+        const double pvt = ok ? P[c * ldp + k] : 1.0;
+        const double inv = 1.0 / pvt;
+        __syncwarp();
+        for (int r = lane; r < n; r += 32) {
+            if (r == k) {
+#pragma unroll
+                for (int c2 = 0; c2 < NB; ++c2)
+                    if (c2 < nbk) P[c2 * ldp + r] = (c2 == c) ? inv : rowk[c2] * inv;
+            } else {
+                const double li = P[c * ldp + r] * inv;
+#pragma unroll
+                for (int c2 = 0; c2 < NB; ++c2)
+                    if (c2 < nbk) P[c2 * ldp + r] = (c2 == c) ? -li : fma(-li, rowk[c2], P[c2 * ldp + r]);
+            }
+        }
+        __syncwarp();
+    }
+    if (bad && lane == 0) atomicMin(flags, static_cast<int>(b_base + b));
+    double* W = nw + b * nn + static_cast<int64_t>(j0) * n;
+    for (int c = 0; c < nbk; ++c)
+        for (int r = lane; r < n; r += 32) W[static_cast<int64_t>(c) * n + r] = P[c * ldp + r];
+}
+
+// Register variant for n <= 128: lane owns rows lane + 32 t (t < RT), the whole panel lives in registers and
+// only the two interchanged rows travel through a shared-memory scratch line per pivot.
+template <int RT>
+__global__ void __launch_bounds__(128) gj_panel_reg_kernel(int n, int j0, int64_t batch, const double* __restrict__ old,
+                                                           double* __restrict__ nw, const double* __restrict__ amax,
+                                                           int* __restrict__ piv, int* __restrict__ src, int* flags,
+                                                           int64_t b_base) {
+    __shared__ double s_scr[4][2][NB];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t b = static_cast<int64_t>(blockIdx.x) * 4 + warp;
+    if (b >= batch) return;
+    const int64_t nn = static_cast<int64_t>(n) * n;
+    const int nbk = min(NB, n - j0);
+    const double* O = old + b * nn + static_cast<int64_t>(j0) * n;
+    double a[RT][NB];
+#pragma unroll
+    for (int c = 0; c < NB; ++c)
+#pragma unroll
+        for (int t = 0; t < RT; ++t) {
+            const int r = lane + 32 * t;
+            a[t][c] = (c < nbk && r < n) ? O[static_cast<int64_t>(c) * n + r] : 0.0;
+        }
+    int* S = src + b * n;
+    for (int r = lane; r < n; r += 32) S[r] = r;
+    __syncwarp();
+    const double tol = 1e-14 * amax[b];
+    bool bad = false;
+    double* scr0 = s_scr[warp][0];
+    double* scr1 = s_scr[warp][1];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) {
+        if (c < nbk) {
+            const int k = j0 + c;
+            double best = -1.0, dkk = 0.0;
+            int bi = INT_MAX;
+#pragma unroll
+            for (int t = 0; t < RT; ++t) {
+                const int r = lane + 32 * t;
+                const double v = fabs(a[t][c]);
+                if (r >= k && r < n && v > best) { best = v; bi = r; }
+                if (r == k) dkk = a[t][c];
+            }
+            const unsigned long long bits = best < 0.0 ? 0ull : static_cast<unsigned long long>(__double_as_longlong(best));
+            const unsigned hi = static_cast<unsigned>(bits >> 32), lo = static_cast<unsigned>(bits);
+            const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+            const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+            const bool win = (bi != INT_MAX) && hi == mhi && lo == mlo;
+            const int p = static_cast<int>(__reduce_min_sync(0xffffffffu, win ? static_cast<unsigned>(bi) : 0xffffffffu));
+            const bool nan_diag = __any_sync(0xffffffffu, dkk != dkk);
+            const double bestv = __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(mhi) << 32) | mlo));
+            const bool ok = !nan_diag && (bestv > tol) && p < n;
+            const int pp = ok ? p : k;
+            if (!ok) bad = true;
+            if (lane == 0) {
+                piv[b * n + k] = pp;
+                const int t = S[k];
+                S[k] = S[pp];
+                S[pp] = t;
+            }
+#pragma unroll
+            for (int t = 0; t < RT; ++t) {
+                const int r = lane + 32 * t;
+                if (r == pp) {
+#pragma unroll
+                    for (int c2 = 0; c2 < NB; ++c2) scr0[c2] = a[t][c2];
+                }
+                if (r == k) {
+#pragma unroll
+                    for (int c2 = 0; c2 < NB; ++c2) scr1[c2] = a[t][c2];
+                }
+            }
+            __syncwarp();
+            double rowk[NB];
+#pragma unroll
+            for (int c2 = 0; c2 < NB; ++c2) rowk[c2] = scr0[c2];
+            const double inv = 1.0 / (ok ? rowk[c] : 1.0);
+#pragma unroll
+            for (int t = 0; t < RT; ++t) {
+                const int r = lane + 32 * t;
+                if (r == pp && pp != k) {
+#pragma unroll
+                    for (int c2 = 0; c2 < NB; ++c2) a[t][c2] = scr1[c2];
+                }
+                if (r == k) {
+#pragma unroll
+                    for (int c2 = 0; c2 < NB; ++c2) a[t][c2] = (c2 == c) ? inv : rowk[c2] * inv;
+                } else {
+                    const double li = a[t][c] * inv;
+#pragma unroll
+                    for (int c2 = 0; c2 < NB; ++c2) a[t][c2] = (c2 == c) ? -li : fma(-li, rowk[c2], a[t][c2]);
+                }
+            }
+            __syncwarp();
+        }
+    }
+    if (bad && lane == 0) atomicMin(flags, static_cast<int>(b_base + b));
+    double* W = nw + b * nn + static_cast<int64_t>(j0) * n;
+#pragma unroll
+    for (int c = 0; c < NB; ++c)
+#pragma unroll
+        for (int t = 0; t < RT; ++t) {
+            const int r = lane + 32 * t;
+            if (c < nbk && r < n) W[static_cast<int64_t>(c) * n + r] = a[t][c];
+        }
+}
+
+// ---- rank-NB update of the non-panel columns ---------------------------------------------------------------
+// CTA = WM warps stacked along the rows, one 32 x 32 DMMA warp tile each, 32 columns per CTA: small CTAs so
+// that several are resident per SM and their load -> multiply -> store phases overlap.
+template <int WM>
+__global__ void __launch_bounds__(WM * 32, (WM <= 2) ? 6 : 4) gj_update_kernel(int n, int j0, const double* __restrict__ old,
+                                                                               double* __restrict__ nw, const int* __restrict__ src) {
+    constexpr int BM = 32 * WM, BN = 32, NT = WM * 32;
+    constexpr int LDA = BM + 4;
+    __shared__ __align__(16) double As[NB * LDA];  // panel rows of this tile: As[kk][row]
+    __shared__ __align__(16) double Bs[BN * LDB];  // gathered pivot rows: Bs[col][kk]
+    const int tid = threadIdx.x, lane = tid & 31, wm = tid >> 5;
+    const int grp = lane >> 2, tig = lane & 3;
+    const int64_t b = blockIdx.z;
+    const int64_t nn = static_cast<int64_t>(n) * n;
+    const double* O = old + b * nn;
+    double* W = nw + b * nn;
+    const int* S = src + b * n;
+    const int nbk = min(NB, n - j0);
+    const int ncol = n - nbk;  // non-panel columns, index c' -> column c' (< j0) or c' + nbk
+    const int row0 = blockIdx.x * BM, cp0 = blockIdx.y * BN;
+
+    // accumulators start from the row-permuted old entries (zero for the pivot rows: those are replaced);
+    // these loads are issued first, the operand staging below runs behind them
+    int srow[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int r = row0 + wm * 32 + i * 8 + grp;
+        srow[i] = (r < n && (r < j0 || r >= j0 + nbk)) ? S[r] : -1;
+    }
+    double acc[4][4][2];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int cp = cp0 + j * 8 + 2 * tig + h;
+            const int c = cp < j0 ? cp : cp + nbk;
+            const double* oc = O + static_cast<int64_t>(c) * n;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[i][j][h] = (cp < ncol && srow[i] >= 0) ? oc[srow[i]] : 0.0;
+        }
+    // panel tile (already in the new buffer; these columns are not written by this kernel): thread = row,
+    // all NB loads issued before the first shared-memory store
+    {
+        const int r = row0 + tid;  // NT == BM
+        double v[NB];
+#pragma unroll
+        for (int kk = 0; kk < NB; ++kk)
+            v[kk] = (kk < nbk && r < n) ? __ldg(W + static_cast<int64_t>(j0 + kk) * n + r) : 0.0;
+#pragma unroll
+        for (int kk = 0; kk < NB; ++kk) As[kk * LDA + tid] = v[kk];
+    }
+    // gathered pivot rows: thread = (kk = tid % NB, columns tid / NB + it * NT / NB)
+    {
+        constexpr int IT = (BN * NB + NT - 1) / NT;
+        const int kk = tid & (NB - 1), jb = tid / NB;
+        const int ps = (kk < nbk) ? S[j0 + kk] : -1;
+        double v[IT];
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+            const int cp = cp0 + jb + it * (NT / NB);
+            const int c = cp < j0 ? cp : cp + nbk;
+            v[it] = (cp < ncol && ps >= 0 && jb + it * (NT / NB) < BN) ? O[static_cast<int64_t>(c) * n + ps] : 0.0;
+        }
+#pragma unroll
+        for (int it = 0; it < IT; ++it)
+            if (jb + it * (NT / NB) < BN) Bs[(jb + it * (NT / NB)) * LDB + kk] = v[it];
+    }
+    __syncthreads();
+    const double* as = As + wm * 32 + grp;
+    const double* bs = Bs + grp * LDB;
+#pragma unroll
+    for (int kk = 0; kk < NB; kk += 4) {
+        double af[4], bf[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) af[i] = as[(kk + tig) * LDA + i * 8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bf[j] = bs[j * 8 * LDB + kk + tig];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int cp = cp0 + j * 8 + 2 * tig + h;
+            if (cp >= ncol) continue;
+            const int c = cp < j0 ? cp : cp + nbk;
+            double* wc = W + static_cast<int64_t>(c) * n;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int r = row0 + wm * 32 + i * 8 + grp;
+                if (r < n) wc[r] = acc[i][j][h];
+            }
+        }
+}
+
+// ---- final column permutation: inverse[:, j] = W[:, c[j]] ---------------------------------------------------
+__global__ void gj_colperm_kernel(int n, const double* __restrict__ w, double* __restrict__ out, const int* __restrict__ piv) {
+    extern __shared__ int s_map[];  // [2][n]
+    int* cmap = s_map;
+    int* dst = s_map + n;
+    const int64_t b = blockIdx.x;
+    const int64_t nn = static_cast<int64_t>(n) * n;
+    if (threadIdx.x == 0) {
+        const int* pv = piv + b * n;
+        for (int j = 0; j < n; ++j) cmap[j] = j;
+        for (int k = n - 1; k >= 0; --k) {  // c = identity after the interchanges in reverse order
+            const int p = pv[k];
+            const int t = cmap[k];
+            cmap[k] = cmap[p];
+            cmap[p] = t;
+        }
+        for (int j = 0; j < n; ++j) dst[cmap[j]] = j;  // column j of W goes to column dst[j]
+    }
+    __syncthreads();
+    const double* Wb = w + b * nn;
+    double* Ob = out + b * nn;
+    for (int64_t t = threadIdx.x; t < nn; t += blockDim.x) {
+        const int j = static_cast<int>(t / n), i = static_cast<int>(t - static_cast<int64_t>(j) * n);
+        Ob[static_cast<int64_t>(dst[j]) * n + i] = Wb[t];
+    }
+}
+
+}  // namespace
+
+// inv may alias a.  Work buffers come from the context's caching allocator.
+void launch_gj_invert_batch(hdgb_ctx* ctx, int n, int64_t batch, const double* a, double* inv, int* flags) {
+    if (batch <= 0) return;
+    const int64_t nn = static_cast<int64_t>(n) * n;
+    const int steps = (n + NB - 1) / NB;
+    DevBuf<double> tmp(static_cast<size_t>(nn) * batch);
+    DevBuf<double> amax(static_cast<size_t>(batch));
+    DevBuf<int> piv(static_cast<size_t>(batch) * n), src(static_cast<size_t>(batch) * n);
+    // ping-pong so that the last panel leaves the result in tmp and the column permutation writes inv
+    double* x[2];
+    x[0] = (steps % 2 == 0) ? tmp.p : inv;
+    x[1] = (steps % 2 == 0) ? inv : tmp.p;
+    int64_t done = 0;
+    while (done < batch) {  // gridDim.x / z limits
+        const int64_t nbt = (batch - done) < 65535 ? (batch - done) : 65535;
+        const int64_t off = done * nn;
+        gj_prepare_kernel<<<static_cast<unsigned>(nbt), 256, 0, ctx->stream>>>(n, a + off, x[0] + off, amax.p + done);
+        HDGB_LAUNCH_CHECK(ctx);
+        const int ldp = n | 1;
+        const size_t per_warp = static_cast<size_t>(NB) * ldp * sizeof(double);
+        int wpc = static_cast<int>((200 * 1024) / per_warp);
+        if (wpc < 1) throw Failure(HDGB_ERR_UNSUPPORTED, "lu_invert_batch: block too large for the panel kernel");
+        if (wpc > 8) wpc = 8;
+        const size_t psm = per_warp * wpc;
+        static size_t configured = 0;
+        if (psm > 48 * 1024 && psm > configured) {
+            HDGB_CUDA(cudaFuncSetAttribute(gj_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(psm)));
+            configured = psm;
+        }
+        for (int s = 0; s < steps; ++s) {
+            const int j0 = s * NB;
+            const double* old = x[s & 1] + off;
+            double* nw = x[(s + 1) & 1] + off;
+            if (n <= 128) {
+                const int rt = ceil_div(n, 32);
+                const unsigned pg = static_cast<unsigned>(ceil_div(nbt, 4));
+                int* pp = piv.p + done * n;
+                int* sp = src.p + done * n;
+                switch (rt) {
+                    case 1: gj_panel_reg_kernel<1><<<pg, 128, 0, ctx->stream>>>(n, j0, nbt, old, nw, amax.p + done, pp, sp, flags, done); break;
+                    case 2: gj_panel_reg_kernel<2><<<pg, 128, 0, ctx->stream>>>(n, j0, nbt, old, nw, amax.p + done, pp, sp, flags, done); break;
+                    case 3: gj_panel_reg_kernel<3><<<pg, 128, 0, ctx->stream>>>(n, j0, nbt, old, nw, amax.p + done, pp, sp, flags, done); break;
+                    default: gj_panel_reg_kernel<4><<<pg, 128, 0, ctx->stream>>>(n, j0, nbt, old, nw, amax.p + done, pp, sp, flags, done); break;
+                }
+            } else
+            gj_panel_kernel<<<ceil_div(nbt, wpc), wpc * 32, psm, ctx->stream>>>(n, j0, nbt, old, nw, amax.p + done,
+                                                                                 piv.p + done * n, src.p + done * n, flags, ldp, done);
+            HDGB_LAUNCH_CHECK(ctx);
+            const int nbk = n - j0 < NB ? n - j0 : NB;
+            const int ncol = n - nbk;
+            if (ncol > 0) {
+                int wm = ceil_div(n, 32);
+                if (wm > 4) wm = 4;
+                dim3 grid(ceil_div(n, 32 * wm), ceil_div(ncol, 32), static_cast<unsigned>(nbt));
+                const int* sp = src.p + done * n;
+                switch (wm) {
+                    case 1: gj_update_kernel<1><<<grid, 32, 0, ctx->stream>>>(n, j0, old, nw, sp); break;
+                    case 2: gj_update_kernel<2><<<grid, 64, 0, ctx->stream>>>(n, j0, old, nw, sp); break;
+                    case 3: gj_update_kernel<3><<<grid, 96, 0, ctx->stream>>>(n, j0, old, nw, sp); break;
+                    default: gj_update_kernel<4><<<grid, 128, 0, ctx->stream>>>(n, j0, old, nw, sp); break;
+                }
+                HDGB_LAUNCH_CHECK(ctx);
+            }
+        }
+        gj_colperm_kernel<<<static_cast<unsigned>(nbt), 256, 2 * n * sizeof(int), ctx->stream>>>(n, tmp.p + off, inv + off, piv.p + done * n);
+        HDGB_LAUNCH_CHECK(ctx);
+        done += nbt;
+    }
+}
+
+}  // namespace hdgb

@@ -36,6 +36,8 @@ struct Tuning {
     int stream_packed = 1;               // small items: 16 warps, several items side by side per warp, no shuffle tree
     int stream_packed_max_cols = 32;     // ... for items with at most this many columns
     int64_t stream_packed_stage_bytes = 6144;  // ... bytes per TMA stage of a warp in packed mode
+    int use_dmma = 1;                    // batched GEMMs on the FP64 tensor-core path (k_gemm_dmma.cu)
+    int use_blocked_gj = 1;              // n > 24: blocked Gauss-Jordan inverse, panel kernel + DMMA updates (k_invert.cu)
     int use_tile_lu = 1;                 // register-tiled Gauss-Jordan for 25 <= n <= 128
     int assemble_budget_kb = 216;        // shared memory for the assembly kernel's point records (smaller: chunked sweeps)
 };
@@ -82,10 +84,18 @@ void launch_sumsq(hdgb_ctx* ctx, const double* v, int64_t n, double* out, double
 // ---- dense batch kernels (k_dense.cu) ----------------------------------------------------------
 // Explicit inverses; flags[0] = min(flags[0], first singular b).  a and inv may alias.
 void launch_lu_invert_batch(hdgb_ctx* ctx, int n, int64_t batch, const double* a, double* inv, int* flags);
+// Blocked Gauss-Jordan with DMMA rank-16 updates (k_invert.cu), any n; same contract.
+void launch_gj_invert_batch(hdgb_ctx* ctx, int n, int64_t batch, const double* a, double* inv, int* flags);
 // C_b = alpha * op(A_b) * B_b + beta * C_b ; a_batch / b_batch == 1 broadcast.
 void launch_gemm_batch(hdgb_ctx* ctx, int m, int n, int k, const double* a, int64_t a_stride, bool trans_a,
                        const double* b, int64_t b_stride, double* c, int64_t c_stride, int64_t batch,
                        double alpha, double beta);
+
+// DMMA (FP64 tensor core) batched GEMM, k_gemm_dmma.cu; output column j -> (j / c_colw) * c_colstride + j % c_colw
+// (c_colw <= 0: identity).
+void launch_gemm_dmma(hdgb_ctx* ctx, int m, int n, int k, const double* a, int64_t a_stride, const double* b,
+                      int64_t b_stride, double* c, int64_t c_stride, int64_t batch, double alpha, double beta,
+                      int c_colw = 0, int c_colstride = 0);
 
 // ---- shared host helpers (api_core.cu) ------------------------------------------------------------
 void reset_flags(hdgb_ctx* c);

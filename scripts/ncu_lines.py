@@ -12,7 +12,8 @@ import os
 def main():
     rep, kid, obj, sub = sys.argv[1:5]
     top = int(sys.argv[5]) if len(sys.argv) > 5 else 40
-    src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-id", kid], capture_output=True, text=True).stdout
+    cmd = ["ncu", "-i", rep, "--page", "source", "--csv"] + ([] if kid == "all" else ["--kernel-id", kid])
+    src = subprocess.run(cmd, capture_output=True, text=True).stdout
     rows = list(csv.reader(src.splitlines()))
     h = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
     hdr = rows[h]
