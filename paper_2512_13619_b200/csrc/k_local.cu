@@ -104,9 +104,318 @@ struct FaceRec {
     double dv_uh[M * M];
 };
 
-template <class Model>
-__global__ void __launch_bounds__(256) local_assemble_kernel(DiscView dv, ModelView mv, LocalIn in, LocalOut out,
-                                                            int want_jac, int gv0, int gv1, int fp0, int fp1, int first) {
+// ---- E and D_d on the FP64 tensor-core path -----------------------------------------------------------
+// For one component pair (m, mp) the 1 + D blocks E[(m,.),(mp,.)], D_dp[(m,.),(mp,.)] are
+//     X_w[i, j] = sum_pts V_w[i, pt] * (w_pt phi_j(pt)),   w = 0 (E), 1 + dp (D_dp),
+// with the volume points followed by the face points as the contraction index: a batch of
+// (pe x npts) x (npts x pe) products sharing their right operand.  The points are swept in chunks of
+// 16; per chunk the CTA builds V_w (point coefficients x basis tables, a few FMAs per entry) and the
+// weighted basis in shared memory and every warp multiplies its 16 x 32 output tiles with DMMA
+// m8n8k4.  Several component pairs are processed per pass when pe is small.  Summation order: points
+// in groups of 4 inside the tensor core (reference: strictly ascending), equal to rounding.
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+constexpr int kResParts = 8;   // thread groups sharing one basis function's point sweep in the residual phase
+constexpr int kEdKc = 16;      // points per chunk
+constexpr int kEdLdb = 20;     // leading dimension of the right operand chunk (= 4 mod 16)
+constexpr int kEdSlots = 2;    // 16 x 32 output tiles per warp
+constexpr int kEdGroups = 32;  // ... of 16 warps
+
+struct EdPlan {
+    int rg, cg;   // 16-row / 32-column tile groups covering pe
+    int pp;       // component pairs per pass
+    int lda;      // leading dimension of a V_w chunk (= 4 mod 16)
+    __host__ __device__ int qp(int D) const { return pp * (1 + D); }
+    __host__ __device__ size_t doubles(int D) const {
+        return static_cast<size_t>(qp(D)) * kEdKc * lda + static_cast<size_t>(cg) * 32 * kEdLdb;
+    }
+};
+inline __host__ __device__ EdPlan ed_plan(int pe, int M, int D) {
+    EdPlan p;
+    p.rg = (pe + 15) / 16;
+    p.cg = (pe + 31) / 32;
+    p.lda = p.rg * 16 + 4;
+    const int per_pair = (1 + D) * p.rg * p.cg;
+    int pp = kEdGroups / per_pair;
+    if (pp < 1) pp = 1;
+    if (pp > M * M) pp = M * M;
+    p.pp = pp;
+    return p;
+}
+// usable when one pass's tiles fit the warps' accumulator slots
+inline bool ed_dmma_ok(int pe, int M, int D) { return pe <= 64; }
+
+template <int M, int D>
+__device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& out, int e, const VolRec<M, D>* vrec,
+                        const FaceRec<M, D>* frec, const int* s_orient, double* opbuf) {
+    const int pe = dv.pe, qe = dv.qe, qf = dv.qf, npe = M * pe;
+    const int nfp = dv.n_lfe * qf;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
+    const int grp = lane >> 2, tig = lane & 3;
+    const EdPlan pl = ed_plan(pe, M, D);
+    const int QP = pl.qp(D), lda = pl.lda;
+    const int bufd = static_cast<int>(pl.doubles(D));  // one operand buffer: [QP][kc][lda] then [cg*32][kEdLdb]; two of them
+    const int boff0 = QP * kEdKc * lda;
+    const bool transient = in.dt_inv > 0.0;
+    const int cols_pad = pl.cg * 32;
+    const int gpp = (1 + D) * pl.rg * pl.cg;  // tile groups per component pair
+    const int nchunk_v = (qe + kEdKc - 1) / kEdKc, nchunk_f = (nfp + kEdKc - 1) / kEdKc;
+    const int nchunk = nchunk_v + nchunk_f;
+
+    // the (point-in-chunk, basis function) pairs this thread builds are the same for every chunk
+    constexpr int kMaxBuild = 4;  // 16 * pe / nt with pe <= 64, nt >= 256
+    int bkk[kMaxBuild], bi[kMaxBuild];
+#pragma unroll
+    for (int it = 0; it < kMaxBuild; ++it) {
+        const int t = tid + it * nt;
+        bkk[it] = (t < kEdKc * pe) ? t / pe : -1;
+        bi[it] = t - (t / pe) * pe;
+    }
+    for (int pair0 = 0; pair0 < M * M; pair0 += pl.pp) {
+        const int npair = min(pl.pp, M * M - pair0);
+        const int ngroups = npair * gpp;
+        // chunk builder: V_w and the weighted basis of points [p0, p0 + 16) into operand buffer `buf`
+        auto build = [&](int ch, int buf) {
+            double* Ab = opbuf + buf * bufd;
+            double* Bb = Ab + boff0;
+            const bool vol = ch < nchunk_v;
+            const int p0 = vol ? ch * kEdKc : (ch - nchunk_v) * kEdKc;
+            const int np = min(kEdKc, (vol ? qe : nfp) - p0);
+#pragma unroll
+            for (int it = 0; it < kMaxBuild; ++it) {
+                const int kk = bkk[it], i = bi[it];
+                if (kk < 0) break;
+                double bval = 0.0;
+                if (kk < np) {
+                    if (vol) {
+                        const int g = p0 + kk;
+                        const VolRec<M, D>& r = vrec[g];
+                        const double ph = dv.phi[i + pe * g];
+                        double dp_[D];
+#pragma unroll
+                        for (int k = 0; k < D; ++k) dp_[k] = dv.dphi[k][i + pe * g];
+                        bval = r.w * ph;
+                        for (int pi = 0; pi < npair; ++pi) {
+                            const int pr = pair0 + pi, mp = pr / M, m = pr - mp * M, mm = m * M + mp;
+                            double fe = 0.0;
+#pragma unroll
+                            for (int k = 0; k < D; ++k) fe += r.cE[mm * D + k] * dp_[k];
+                            double eij = -fe - r.dSu[mm] * ph;
+                            if (transient && m == mp) eij += in.dt_inv * ph;
+                            Ab[((pi * (1 + D)) * kEdKc + kk) * lda + i] = eij;
+#pragma unroll
+                            for (int dq = 0; dq < D; ++dq) {
+                                double fd = 0.0;
+#pragma unroll
+                                for (int k = 0; k < D; ++k) fd += r.cD[(dq * M * M + mm) * D + k] * dp_[k];
+                                Ab[((pi * (1 + D) + 1 + dq) * kEdKc + kk) * lda + i] = -fd - r.dSq[mm * D + dq] * ph;
+                            }
+                        }
+                    } else {
+                        const int p = p0 + kk;
+                        const int lf = p / qf, gc = p - lf * qf;
+                        const FaceRec<M, D>& r = frec[p];
+                        const double ph = dv.tphi[((static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf + gc) * pe + i];
+                        bval = r.w * ph;
+                        for (int pi = 0; pi < npair; ++pi) {
+                            const int pr = pair0 + pi, mp = pr / M, m = pr - mp * M, mm = m * M + mp;
+                            Ab[((pi * (1 + D)) * kEdKc + kk) * lda + i] = (m == mp) ? r.tau * ph : 0.0;
+#pragma unroll
+                            for (int dq = 0; dq < D; ++dq)
+                                Ab[((pi * (1 + D) + 1 + dq) * kEdKc + kk) * lda + i] = r.dfh_q[mm * D + dq] * ph;
+                        }
+                    }
+                } else {
+                    for (int w = 0; w < npair * (1 + D); ++w) Ab[(w * kEdKc + kk) * lda + i] = 0.0;
+                }
+                Bb[i * kEdLdb + kk] = bval;
+            }
+        };
+        for (int g0 = 0; g0 < ngroups; g0 += nwarps * kEdSlots) {  // sub-passes when the CTA has fewer warps than tiles
+            double acc[kEdSlots][2][4][2];
+#pragma unroll
+            for (int s = 0; s < kEdSlots; ++s)
+#pragma unroll
+                for (int a = 0; a < 2; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) acc[s][a][b][0] = acc[s][a][b][1] = 0.0;
+            // zero the padding rows / columns of both buffers once per pass (the builders never write them)
+            __syncthreads();
+            for (int t = tid; t < 2 * bufd; t += nt) opbuf[t] = 0.0;
+            // tile coordinates of this warp's accumulator slots (fixed over the point sweep)
+            int aoff[kEdSlots], boff[kEdSlots];
+#pragma unroll
+            for (int s = 0; s < kEdSlots; ++s) {
+                const int gid = g0 + warp + nwarps * s;
+                const int w = gid / (pl.rg * pl.cg), rem = gid - w * (pl.rg * pl.cg);
+                const int rgi = rem / pl.cg, cgi = rem - rgi * pl.cg;
+                aoff[s] = gid < ngroups ? w * kEdKc * lda + rgi * 16 + grp + tig * lda : -1;
+                boff[s] = boff0 + (cgi * 32 + grp) * kEdLdb + tig;
+            }
+            __syncthreads();
+            build(0, 0);
+            __syncthreads();
+            for (int ch = 0; ch < nchunk; ++ch) {
+                const int buf = ch & 1;
+                // the next chunk's operands are built in the same barrier interval as this chunk's products:
+                // warps drift apart, so table loads and DMMA issue overlap across the CTA
+                if (ch + 1 < nchunk) build(ch + 1, buf ^ 1);
+                const double* Ob = opbuf + buf * bufd;
+#pragma unroll
+                for (int s = 0; s < kEdSlots; ++s) {
+                    if (aoff[s] >= 0) {
+                        const double* as = Ob + aoff[s];
+                        const double* bs = Ob + boff[s];
+#pragma unroll
+                        for (int kk = 0; kk < kEdKc; kk += 4) {
+                            double af[2], bf[4];
+#pragma unroll
+                            for (int a = 0; a < 2; ++a) af[a] = as[kk * lda + a * 8];
+#pragma unroll
+                            for (int b = 0; b < 4; ++b) bf[b] = bs[b * 8 * kEdLdb + kk];
+#pragma unroll
+                            for (int a = 0; a < 2; ++a)
+#pragma unroll
+                                for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[s][a][b][0], acc[s][a][b][1], af[a], bf[b]);
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+            // ---- write this pass's blocks ----
+#pragma unroll
+            for (int s = 0; s < kEdSlots; ++s) {
+                const int gid = g0 + warp + nwarps * s;
+                if (gid >= ngroups) continue;
+                const int w = gid / (pl.rg * pl.cg), rem = gid - w * (pl.rg * pl.cg);
+                const int rgi = rem / pl.cg, cgi = rem - rgi * pl.cg;
+                const int pi = w / (1 + D), which = w - pi * (1 + D);
+                const int pr = pair0 + pi, mp = pr / M, m = pr - mp * M;
+                double* dst = (which == 0 ? out.E : out.Dm[which - 1]) + static_cast<size_t>(e) * npe * npe;
+#pragma unroll
+                for (int b = 0; b < 4; ++b)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int j = cgi * 32 + b * 8 + 2 * tig + h;
+                        if (j >= pe) continue;
+#pragma unroll
+                        for (int a = 0; a < 2; ++a) {
+                            const int i = rgi * 16 + a * 8 + grp;
+                            if (i < pe) dst[static_cast<size_t>(mp * pe + j) * npe + (m * pe + i)] = acc[s][a][b][h];
+                        }
+                    }
+            }
+        }
+    }
+}
+
+// ---- H, G_d and F of scalar systems (M = 1) on the tensor-core path ------------------------------------------
+// Per local face lf (K = the qf face points):
+//   [H | G_0 .. G_{D-1}](lf b, j) = sum_gc psi_b(gc) * (c_w(gc) w_gc phis_j(gc)),  c_0 = dv_u, c_{1+dp} = dv_q[dp]
+//   F(i, lf bp)                   = sum_gc phis_i(gc) * (w_gc dfh_uh(gc) psi_bp(gc))
+// (local_ops.cpp:186-219).  psi^T and phis are the left operands, the coefficient-scaled tables the right ones.
+struct HgfPlan {
+    int pfp, qfp, ldp, lda, ldk, pep;
+    __host__ __device__ size_t doubles(int D) const {
+        return static_cast<size_t>(qfp) * ldp + static_cast<size_t>(qfp) * lda + static_cast<size_t>(1 + D) * pep * ldk +
+               static_cast<size_t>(pfp) * ldk;
+    }
+};
+inline __host__ __device__ HgfPlan hgf_plan(int pe, int pf, int qf) {
+    HgfPlan p;
+    p.pfp = (pf + 7) / 8 * 8;
+    p.pep = (pe + 7) / 8 * 8;
+    p.qfp = (qf + 3) / 4 * 4;
+    p.ldp = (p.pfp + 15) / 16 * 16 + 4;
+    p.lda = (p.pep + 15) / 16 * 16 + 4;
+    p.ldk = (p.qfp + 15) / 16 * 16 + 4;
+    return p;
+}
+
+template <int D>
+__device__ void hgf_dmma(const DiscView& dv, const LocalOut& out, int e, const FaceRec<1, D>* frec, const int* s_orient,
+                         double* buf) {
+    const int pe = dv.pe, pf = dv.pf, qf = dv.qf, n_lfe = dv.n_lfe;
+    const int nfl = n_lfe * pf, npe = pe;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
+    const int grp = lane >> 2, tig = lane & 3;
+    const HgfPlan pl = hgf_plan(pe, pf, qf);
+    double* Ps = buf;                                        // psi^T: [gc][b]
+    double* Fs = Ps + pl.qfp * pl.ldp;  // phis:  [gc][i]
+    double* Bh = Fs + pl.qfp * pl.lda;  // [w][j][gc]
+    double* Bf = Bh + (1 + D) * pl.pep * pl.ldk;  // [bp][gc]
+    __syncthreads();
+    for (int t = tid; t < static_cast<int>(pl.doubles(D)); t += nt) buf[t] = 0.0;
+    __syncthreads();
+    for (int t = tid; t < qf * pf; t += nt) {
+        const int gc = t / pf, b = t - gc * pf;
+        Ps[gc * pl.ldp + b] = dv.psi[b + pf * gc];
+    }
+    const int rt_h = pl.pfp / 8, ct_h = pl.pep / 8;  // H/G tiles per block: rows b, columns j
+    const int ntile_h = (1 + D) * rt_h * ct_h;
+    const int ntile_f = ct_h * rt_h;                 // F tiles: rows i, columns bp
+    const int ksteps = pl.qfp / 4;
+    for (int lf = 0; lf < n_lfe; ++lf) {
+        const double* tp = dv.tphi + (static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf * pe;
+        const FaceRec<1, D>* fr = frec + lf * qf;
+        for (int t = tid; t < qf * pe; t += nt) {
+            const int gc = t / pe, j = t - gc * pe;
+            const double ph = tp[t];
+            const FaceRec<1, D>& r = fr[gc];
+            const double wp = r.w * ph;
+            Fs[gc * pl.lda + j] = ph;
+            Bh[j * pl.ldk + gc] = wp * r.dv_u[0];
+#pragma unroll
+            for (int dp = 0; dp < D; ++dp) Bh[((1 + dp) * pl.pep + j) * pl.ldk + gc] = wp * r.dv_q[dp];
+        }
+        for (int t = tid; t < qf * pf; t += nt) {
+            const int gc = t / pf, bp = t - gc * pf;
+            const FaceRec<1, D>& r = fr[gc];
+            Bf[bp * pl.ldk + gc] = r.w * r.dfh_uh[0] * dv.psi[bp + pf * gc];
+        }
+        __syncthreads();
+        for (int tile = warp; tile < ntile_h + ntile_f; tile += nwarps) {
+            double c0 = 0.0, c1 = 0.0;
+            if (tile < ntile_h) {
+                const int w = tile / (rt_h * ct_h), rem = tile - w * (rt_h * ct_h);
+                const int rt = rem / ct_h, ct = rem - rt * ct_h;
+                const double* as = Ps + rt * 8 + grp;
+                const double* bs = Bh + (w * pl.pep + ct * 8 + grp) * pl.ldk;
+                for (int ks = 0; ks < ksteps; ++ks) dmma_8x8x4(c0, c1, as[(4 * ks + tig) * pl.ldp], bs[4 * ks + tig]);
+                const int b = rt * 8 + grp;
+                double* dst = (w == 0 ? out.H : out.G[w - 1]) + static_cast<size_t>(e) * nfl * npe;
+                if (b < pf) {
+                    const int j = ct * 8 + 2 * tig;
+                    if (j < pe) dst[static_cast<size_t>(j) * nfl + lf * pf + b] = c0;
+                    if (j + 1 < pe) dst[static_cast<size_t>(j + 1) * nfl + lf * pf + b] = c1;
+                }
+            } else {
+                const int tf = tile - ntile_h;
+                const int rt = tf / rt_h, ct = tf - rt * rt_h;  // rt over i (pep / 8), ct over bp (pfp / 8)
+                const double* as = Fs + rt * 8 + grp;
+                const double* bs = Bf + (ct * 8 + grp) * pl.ldk;
+                for (int ks = 0; ks < ksteps; ++ks) dmma_8x8x4(c0, c1, as[(4 * ks + tig) * pl.lda], bs[4 * ks + tig]);
+                const int i = rt * 8 + grp;
+                double* dst = out.F + static_cast<size_t>(e) * npe * nfl;
+                if (i < pe) {
+                    const int bp = ct * 8 + 2 * tig;
+                    if (bp < pf) dst[static_cast<size_t>(lf * pf + bp) * npe + i] = c0;
+                    if (bp + 1 < pf) dst[static_cast<size_t>(lf * pf + bp + 1) * npe + i] = c1;
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+template <class Model, int NT, bool ED>
+__global__ void __launch_bounds__(NT) local_assemble_kernel(DiscView dv, ModelView mv, LocalIn in, LocalOut out,
+                                                            int want_jac, int gv0, int gv1, int fp0, int fp1, int first,
+                                                            int ed_dmma_on) {
     // Point records of the volume points [gv0, gv1) and face points [fp0, fp1) live in shared memory.
     // When all points of an element fit (scalar models) there is ONE launch (first = 1) and every
     // output entry is written once.  Wide systems (M = 5) are swept in several launches over point
@@ -125,7 +434,8 @@ __global__ void __launch_bounds__(256) local_assemble_kernel(DiscView dv, ModelV
     double* qs = us + npe;            // D*npe  (direction-major)
     double* uhs = qs + D * npe;       // nfl
     double* ups = uhs + nfl;          // npe
-    VR* vrec = reinterpret_cast<VR*>(ups + npe);
+    double* red = ups + npe;          // kResParts * npe: partial residual sums
+    VR* vrec = reinterpret_cast<VR*>(red + kResParts * npe);
     FR* frec = reinterpret_cast<FR*>(vrec + (gv1 - gv0));
     __shared__ int s_face[8], s_side[8], s_orient[8], s_tag[8];
 
@@ -278,32 +588,48 @@ __global__ void __launch_bounds__(256) local_assemble_kernel(DiscView dv, ModelV
     }
     __syncthreads();
 
-    // ---- phase 2a: residuals (negated weak residuals, local_ops.cpp:223-226) ----
-    for (int i = tid; i < pe; i += nt) {
-        double acc[M];
-        for (int m = 0; m < M; ++m) acc[m] = 0.0;
-        for (int g = gv0; g < gv1; ++g) {
-            const VR& r = vrec[g - gv0];
-            const double ph = dv.phi[i + pe * g];
-            double dp_[D];
-            for (int k = 0; k < D; ++k) dp_[k] = dv.dphi[k][i + pe * g];
-            for (int m = 0; m < M; ++m) {
-                double fg = 0.0;
-                for (int k = 0; k < D; ++k) fg += r.Fr[m * D + k] * dp_[k];
-                double v = -fg - r.S[m] * ph;
-                if (transient) v += r.tm[m] * ph;
-                acc[m] += r.w * v;
+    // ---- phase 2a: residuals (negated weak residuals, local_ops.cpp:223-226).  The point sweep of basis
+    // function i is split over NP thread groups (contiguous point ranges, volume points first); the partial
+    // sums are combined in ascending range order, so the result does not depend on timing ----
+    {
+        const int NP = min(kResParts, max(1, nt / pe));
+        const int nvp = gv1 - gv0, ntot = nvp + (fp1 - fp0);
+        for (int t = tid; t < NP * pe; t += nt) {  // one trip unless pe > nt (then NP = 1)
+            const int part = t / pe, i = t - part * pe;
+            const int q0 = static_cast<int>(static_cast<long long>(ntot) * part / NP);
+            const int q1 = static_cast<int>(static_cast<long long>(ntot) * (part + 1) / NP);
+            double acc[M];
+            for (int m = 0; m < M; ++m) acc[m] = 0.0;
+            for (int q = q0; q < min(q1, nvp); ++q) {
+                const int g = gv0 + q;
+                const VR& r = vrec[q];
+                const double ph = dv.phi[i + pe * g];
+                double dp_[D];
+                for (int k = 0; k < D; ++k) dp_[k] = dv.dphi[k][i + pe * g];
+                for (int m = 0; m < M; ++m) {
+                    double fg = 0.0;
+                    for (int k = 0; k < D; ++k) fg += r.Fr[m * D + k] * dp_[k];
+                    double v = -fg - r.S[m] * ph;
+                    if (transient) v += r.tm[m] * ph;
+                    acc[m] += r.w * v;
+                }
             }
+            for (int q = max(q0, nvp); q < q1; ++q) {
+                const int p = fp0 + q - nvp;
+                const int lf = p / qf, gc = p - lf * qf;
+                const FR& r = frec[p - fp0];
+                const double ph = dv.tphi[((static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf + gc) * pe + i];
+                for (int m = 0; m < M; ++m) acc[m] += r.w * r.fhat[m] * ph;
+            }
+            for (int m = 0; m < M; ++m) red[(part * M + m) * pe + i] = acc[m];
         }
-        for (int p = fp0; p < fp1; ++p) {
-            const int lf = p / qf, gc = p - lf * qf;
-            const FR& r = frec[p - fp0];
-            const double ph = dv.tphi[((static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf + gc) * pe + i];
-            for (int m = 0; m < M; ++m) acc[m] += r.w * r.fhat[m] * ph;
-        }
-        for (int m = 0; m < M; ++m) {
-            double* o = out.ru + static_cast<size_t>(e) * npe + m * pe + i;
-            *o = first ? -acc[m] : *o - acc[m];
+        __syncthreads();
+        for (int t = tid; t < npe; t += nt) {
+            const int m = t / pe, i = t - m * pe;
+            double a = 0.0;
+            for (int part = 0; part < NP; ++part) a += red[(part * M + m) * pe + i];
+            double* o = out.ru + static_cast<size_t>(e) * npe + t;
+            *o = first ? -a : *o - a;
         }
     }
     for (int t = tid; t < n_lfe * pf; t += nt) {
@@ -326,7 +652,11 @@ __global__ void __launch_bounds__(256) local_assemble_kernel(DiscView dv, ModelV
     // ---- phase 2b: E and D_d.  A thread owns a TI x TJ tile of scalar-basis pairs (i, j); per point it
     // forms the i-side values once and rank-1 updates the tile.  Component columns mp are swept one
     // at a time so that the accumulators (M (1 + D) per pair) stay in registers for wide systems ----
-    {
+    if (ED && ed_dmma_on) {
+        // operand chunks live behind the point records (16-byte aligned)
+        double* opbuf = sm + ((reinterpret_cast<const char*>(frec + (fp1 - fp0)) - reinterpret_cast<const char*>(sm) + 15) / 16) * 2;
+        ed_dmma<M, D>(dv, in, out, e, vrec, frec, s_orient, opbuf);
+    } else {
         constexpr int TI = (M == 1) ? 2 : 1, TJ = (M == 1) ? 4 : 1;
         constexpr int Q = M * (1 + D);  // per row component m: E then D_0..D_{D-1}
         const int nti = (pe + TI - 1) / TI, ntj = (pe + TJ - 1) / TJ;
@@ -422,8 +752,16 @@ __global__ void __launch_bounds__(256) local_assemble_kernel(DiscView dv, ModelV
             }
         }
     }
+    bool hgf_done = false;
+    if constexpr (ED && M == 1) {
+        if (ed_dmma_on) {
+            double* opbuf = sm + ((reinterpret_cast<const char*>(frec + (fp1 - fp0)) - reinterpret_cast<const char*>(sm) + 15) / 16) * 2;
+            hgf_dmma<D>(dv, out, e, reinterpret_cast<const FaceRec<1, D>*>(frec), s_orient, opbuf);
+            hgf_done = true;
+        }
+    }
     // ---- H and G_d: rows (lf, m, b), columns (mp, j) ----
-    for (int t = tid; t < n_lfe * pf * pe; t += nt) {
+    for (int t = tid; t < (hgf_done ? 0 : n_lfe * pf * pe); t += nt) {
         const int j = t / (n_lfe * pf);
         const int lb = t - j * (n_lfe * pf);
         const int lf = lb / pf, b = lb - lf * pf;
@@ -454,7 +792,7 @@ __global__ void __launch_bounds__(256) local_assemble_kernel(DiscView dv, ModelV
             }
     }
     // ---- F: rows (m, i), columns (lf, mp, bp) ----
-    for (int t = tid; t < pe * n_lfe * pf; t += nt) {
+    for (int t = tid; t < (hgf_done ? 0 : pe * n_lfe * pf); t += nt) {
         const int lb = t / pe, i = t - lb * pe;
         const int lf = lb / pf, bp = lb - lf * pf;
         double aF[M * M];
@@ -506,21 +844,29 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
     constexpr int M = Model::M, D = Model::D;
     const int npe = M * dv.pe, nfl = dv.n_lfe * M * dv.pf;
     const int nfp = dv.n_lfe * dv.qf;
-    const size_t fixed = (static_cast<size_t>(npe) * (2 + D) + nfl) * sizeof(double);
+    const size_t fixed = (static_cast<size_t>(npe) * (2 + D + kResParts) + nfl) * sizeof(double);
     const size_t cap = 216 * 1024;
     const size_t budget = std::min<size_t>(cap, static_cast<size_t>(tuning().assemble_budget_kb) * 1024);
     const size_t svr = sizeof(VolRec<M, D>), sfr = sizeof(FaceRec<M, D>);
     if (fixed + std::max(svr, sfr) > budget)
         throw Failure(HDGB_ERR_UNSUPPORTED, "local assembly: element state exceeds shared memory");
-    auto kern = local_assemble_kernel<Model>;
+    auto kern = local_assemble_kernel<Model, 256, false>;
+    constexpr int NTD = (M == 1) ? 512 : 256;  // tensor-core mode: 16 warps for scalar systems
+    auto kern_d = local_assemble_kernel<Model, NTD, true>;
     static bool configured = false;
     if (!configured) {
         HDGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cap)));
+        HDGB_CUDA(cudaFuncSetAttribute(kern_d, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cap)));
         configured = true;
     }
     const size_t all = fixed + dv.qe * svr + nfp * sfr;
     if (all <= budget) {
-        kern<<<dv.ne, 256, all, ctx->stream>>>(dv, mv, in, out, want_jac ? 1 : 0, 0, dv.qe, 0, nfp, 1);
+        // E / D_d on the tensor-core path when the operand chunks fit next to the point records
+        size_t ed_bytes = 2 * ed_plan(dv.pe, M, D).doubles(D) * sizeof(double) + 16;
+        if (M == 1) ed_bytes = std::max(ed_bytes, hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D) * sizeof(double) + 16);
+        const bool ed = want_jac && tuning().use_dmma && ed_dmma_ok(dv.pe, M, D) && all + ed_bytes <= cap;
+        if (ed) kern_d<<<dv.ne, NTD, all + ed_bytes, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 1);
+        else kern<<<dv.ne, 256, all, ctx->stream>>>(dv, mv, in, out, want_jac ? 1 : 0, 0, dv.qe, 0, nfp, 1, 0);
         HDGB_LAUNCH_CHECK(ctx);
         return;
     }
@@ -529,13 +875,13 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
     int first = 1;
     for (int g0 = 0; g0 < dv.qe; g0 += vc) {
         const int g1 = std::min(dv.qe, g0 + vc);
-        kern<<<dv.ne, 256, fixed + (g1 - g0) * svr, ctx->stream>>>(dv, mv, in, out, want_jac ? 1 : 0, g0, g1, 0, 0, first);
+        kern<<<dv.ne, 256, fixed + (g1 - g0) * svr, ctx->stream>>>(dv, mv, in, out, want_jac ? 1 : 0, g0, g1, 0, 0, first, 0);
         HDGB_LAUNCH_CHECK(ctx);
         first = 0;
     }
     for (int p0 = 0; p0 < nfp; p0 += fc) {
         const int p1 = std::min(nfp, p0 + fc);
-        kern<<<dv.ne, 256, fixed + (p1 - p0) * sfr, ctx->stream>>>(dv, mv, in, out, want_jac ? 1 : 0, 0, 0, p0, p1, first);
+        kern<<<dv.ne, 256, fixed + (p1 - p0) * sfr, ctx->stream>>>(dv, mv, in, out, want_jac ? 1 : 0, 0, 0, p0, p1, first, 0);
         HDGB_LAUNCH_CHECK(ctx);
         first = 0;
     }

@@ -519,8 +519,10 @@ class Discretization:
 
     def quad_coords(self):
         """((ne, qe, dim), (nf, qf, dim)) physical quadrature point coordinates."""
-        return (self.table("elem_coords").reshape(self.ne, self.qe, self.dim),
-                self.table("face_coords").reshape(self.nf, self.qf, self.dim))
+        if getattr(self, "_quad_coords", None) is None:  # geometry is immutable: fetch the tables once
+            self._quad_coords = (self.table("elem_coords").reshape(self.ne, self.qe, self.dim),
+                                 self.table("face_coords").reshape(self.nf, self.qf, self.dim))
+        return self._quad_coords
 
     def l2_error(self, u, exact) -> float:
         """L2 error of component-wise nodal coefficients u against exact(x) at the assembly
