@@ -8,16 +8,23 @@ import paper_2512_13619_b200 as hdg
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["tile", "smem"])
+@pytest.fixture(params=["gj", "tile", "smem"])
 def lu_kernel(request):
+    """gj: blocked Gauss-Jordan with DMMA rank-16 updates (the default for n > 24); tile: register-tiled
+    Gauss-Jordan (n <= 128); smem: one block per CTA in shared memory / the global-memory fallback."""
+    hdg.set_tuning("use_blocked_gj", 1 if request.param == "gj" else 0)
     hdg.set_tuning("use_tile_lu", 1 if request.param == "tile" else 0)
     yield request.param
+    hdg.set_tuning("use_blocked_gj", 1)
     hdg.set_tuning("use_tile_lu", 1)
 
 
 @pytest.mark.parametrize("n,batch", [(1, 5), (2, 9), (5, 33), (9, 100), (12, 64), (16, 40), (24, 17), (25, 21), (32, 20),
-                                     (40, 11), (64, 9), (70, 5), (96, 7), (100, 3), (128, 2), (150, 2)])
+                                     (40, 11), (64, 9), (70, 5), (96, 7), (100, 3), (128, 2), (150, 2), (33, 300), (200, 3),
+                                     (320, 2)])
 def test_lu_invert_batch(ctx, lu_kernel, n, batch):
+    if lu_kernel != "gj" and n > 150:
+        pytest.skip("the fallback kernels are slow at this size")
     rng = np.random.default_rng(n)
     a = rng.standard_normal((batch, n, n)) + 0.1 * n * np.eye(n)[None]
     a[0] = np.eye(n)[rng.permutation(n)]                       # pure permutation: pivoting (test_dense_batch.cpp:88-96)
@@ -28,7 +35,7 @@ def test_lu_invert_batch(ctx, lu_kernel, n, batch):
     assert np.array_equal(got[0], a[0].T)
 
 
-@pytest.mark.parametrize("n", [3, 20, 40, 96])
+@pytest.mark.parametrize("n", [3, 20, 40, 96, 150])
 def test_singular_block_reports_lowest_index(ctx, lu_kernel, n):
     rng = np.random.default_rng(7)
     a = rng.standard_normal((6, n, n)) + n * np.eye(n)[None]
@@ -46,8 +53,36 @@ def test_singular_block_reports_lowest_index(ctx, lu_kernel, n):
         hdg.lu_invert_batch(ctx, np.transpose(a, (0, 2, 1)).ravel(), n, 6)
 
 
-@pytest.mark.parametrize("m,k,n,batch", [(3, 4, 5, 7), (9, 9, 12, 33), (64, 64, 96, 3), (96, 64, 96, 2), (20, 33, 17, 5)])
-def test_gemm_batch_and_broadcast(ctx, m, k, n, batch):
+def test_blocked_gj_large_batch_and_ill_scaled_rows(ctx):
+    """More blocks than one grid chunk (65 535) and rows of wildly different scale: the pivot search has to
+    pick the large rows first (partial pivoting, dense_batch.cpp:27-36)."""
+    n, batch = 26, 66000
+    rng = np.random.default_rng(5)
+    a = rng.standard_normal((batch, n, n)) + 3.0 * np.eye(n)[None]
+    a[:, ::3, :] *= 1e6
+    a[65999] = np.eye(n)[::-1]
+    got = hdg.lu_invert_batch(ctx, np.transpose(a, (0, 2, 1)).ravel(), n, batch).reshape(batch, n, n).transpose(0, 2, 1)
+    for b in (0, 1, 40000, 65535, 65536, 65999):
+        assert np.max(np.abs(got[b] @ a[b] - np.eye(n))) <= 1e-9, b
+    a[65990] = 0.0
+    with pytest.raises(hdg.SingularBlock) as ei:
+        hdg.lu_invert_batch(ctx, np.transpose(a, (0, 2, 1)).ravel(), n, batch)
+    assert ei.value.index == 65990
+
+
+@pytest.fixture(params=["dmma", "fma"])
+def gemm_kernel(request):
+    hdg.set_tuning("use_dmma", 1 if request.param == "dmma" else 0)
+    yield request.param
+    hdg.set_tuning("use_dmma", 1)
+
+
+@pytest.mark.parametrize("m,k,n,batch", [(3, 4, 5, 7), (9, 9, 12, 33), (64, 64, 96, 3), (96, 64, 96, 2), (20, 33, 17, 5),
+                                         (30, 10, 24, 50), (72, 10, 10, 9), (15, 15, 33, 11), (320, 64, 96, 2),
+                                         (130, 70, 129, 2), (16, 16, 24, 70000)])
+def test_gemm_batch_and_broadcast(ctx, gemm_kernel, m, k, n, batch):
+    if batch > 1000 and gemm_kernel != "dmma":
+        pytest.skip("large batch: tensor-core path only")
     rng = np.random.default_rng(m * 7 + n)
     a = rng.standard_normal((batch, k, m))                     # [b][col][row]: column-major m x k
     b = rng.standard_normal((batch, n, k))

@@ -11,18 +11,25 @@ pytestmark = pytest.mark.gpu
 SHAPES = [(3, 21, 1001), (5, 25, 333), (16, 176, 97), (18, 126, 41), (80, 880, 5), (12, 12, 515), (15, 15, 77),
           (96, 96, 9), (72, 72, 13), (16, 16, 1000), (27, 27, 30), (9, 63, 201), (64, 64, 7), (130, 40, 6), (7, 7, 1),
           # long streams: every warp's TMA ring wraps many times
-          (16, 176, 6000), (96, 96, 3000), (3, 21, 150001), (64, 96, 4001), (5, 25, 40003), (18, 126, 5000)]
+          (16, 176, 6000), (96, 96, 3000), (3, 21, 150001), (64, 96, 4001), (5, 25, 40003), (18, 126, 5000),
+          # packed small-item mode: odd / even rows, odd column counts, items per pass 2 .. 32
+          (1, 1, 5000), (2, 3, 70001), (5, 5, 90001), (6, 18, 30000), (10, 30, 20001), (15, 15, 50001), (16, 16, 40000),
+          (32, 32, 9001), (4, 31, 12345)]
 
 
-@pytest.fixture(params=["team", "stream"])
+@pytest.fixture(params=["team", "stream", "stream-unpacked"])
 def kernel(request):
-    if request.param == "stream":
+    """stream: small items take the packed mode (several items per warp pass); stream-unpacked forces the
+    one-item-per-warp mapping for every shape."""
+    if request.param.startswith("stream"):
         hdg.set_tuning("use_stream", 1)
         hdg.set_tuning("stream_min_elems", 0)
+        hdg.set_tuning("stream_packed", 0 if request.param == "stream-unpacked" else 1)
     else:
         hdg.set_tuning("use_stream", 0)
     yield request.param
     hdg.set_tuning("use_stream", 1)
+    hdg.set_tuning("stream_packed", 1)
     hdg.set_tuning("stream_min_elems", 1 << 18)
 
 

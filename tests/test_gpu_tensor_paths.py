@@ -1,0 +1,51 @@
+"""The FP64 tensor-core (DMMA) paths against the scalar FMA paths they replace, on the same inputs: raw
+local blocks (E, D_d, F, G_d, H, J), condensed operators, the assembled block rows and the preconditioner
+inverses must agree to rounding for every element shape / model family (the scalar paths are the ones
+pinned bit-level against the CPU oracle in the other parity suites)."""
+import numpy as np
+import pytest
+
+import paper_2512_13619_b200 as hdg
+
+pytestmark = pytest.mark.gpu
+
+CASES = [("quad", 5, 2, 1, "poisson2d"), ("quad", 4, 3, 1, "burgers"), ("tri", 4, 4, 1, "burgers"), ("hex", 3, 3, 1, "poisson"),
+         ("hex", 3, 2, 1, "reaction"), ("tet", 2, 2, 1, "poisson"), ("tet", 2, 2, 3, "elasticity"), ("quad", 4, 2, 2, "elasticity"),
+         ("hex", 2, 2, 5, "navier_stokes"), ("quad", 3, 3, 4, "navier_stokes")]
+
+
+def rel(a, b):
+    return np.max(np.abs(a - b)) / max(1e-300, np.max(np.abs(b)))
+
+
+@pytest.mark.parametrize("shape,n,k,M,case", CASES)
+def test_dmma_paths_match_scalar_paths(ctx, shape, n, k, M, case):
+    disc = hdg.Discretization.structured(ctx, shape, n=n, degree=k, n_comp=M, jitter=0.15 if shape in ("tri", "tet") else 0.0)
+    kw = {"mu": 0.02} if case == "navier_stokes" else {}
+    model = hdg.make_case_model(disc, case, **kw)
+    state = hdg.make_initial_state(disc, model)
+    rng = np.random.default_rng(3)
+    state.u = state.u + 0.05 * rng.standard_normal(state.u.shape)       # away from the trivial state
+    state.uhat = state.uhat + 0.05 * rng.standard_normal(state.uhat.shape)
+    tkw = dict(dt=0.05, u_prev=state.u) if case == "navier_stokes" else {}
+    out = {}
+    for flag in (0, 1):
+        hdg.set_tuning("use_dmma", flag)
+        hdg.set_tuning("use_blocked_gj", flag)
+        try:
+            ops = hdg.assemble_element_operators(disc, model, state, keep_raw=True, **tkw)
+            K, rhs = hdg.assemble_global(disc, ops)
+            P = hdg.build_preconditioner("asm", K, ops, disc)
+            names = ["e_raw", "f_raw", "h_raw", "j_raw"] + [f"d_raw{d}" for d in range(disc.dim)] + \
+                    [f"g_raw{d}" for d in range(disc.dim)] + ["kbar", "ebar_inv", "fbar", "hbar", "rbar", "ru"]
+            out[flag] = {nm: ops.get(nm) for nm in names}
+            out[flag]["K"] = K.blocks
+            out[flag]["rhs"] = rhs
+            out[flag]["asm_inv"] = P.get("asm_inv")
+        finally:
+            hdg.set_tuning("use_dmma", 1)
+            hdg.set_tuning("use_blocked_gj", 1)
+    for nm in out[0]:
+        a, b = np.asarray(out[1][nm]), np.asarray(out[0][nm])
+        tol = 1e-9 if nm in ("asm_inv", "ebar_inv", "kbar", "K", "rbar", "rhs") else 1e-12
+        assert rel(a, b) <= tol, (nm, rel(a, b))
