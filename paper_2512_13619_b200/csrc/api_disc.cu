@@ -558,7 +558,40 @@ hdgb_ops* assemble_element_operators_device(hdgb_disc* d, const hdgb_model* m, h
         }
         // q-elimination (local_ops.cpp:389-398): X-bar = X - sum_d Y_d (I_M (x) M^-1 B_d | M^-1 C_d)
         const int64_t sb = static_cast<int64_t>(pe) * pe, sc = static_cast<int64_t>(pe) * v.nfs;
-        for (int k = 0; k < D; ++k) {
+        bool fused = false;
+        if (tuning().use_dmma && tuning().use_qelim_fused && (tuning().qelim_split_rows || (npe + 31) / 32 + (nfl + 31) / 32 <= 8)) {
+            // two stacked products per component column block: [E-bar; H-bar] -= sum_d [D_d; G_d] M^-1 B_d and
+            // [F-bar; J-bar] -= sum_d [D_d; G_d] M^-1 C_d, the latter scattering its columns (lf, b) to
+            // lf*mpf + mp*pf + b
+            fused = true;
+            for (int mp = 0; mp < M && fused; ++mp) {
+                const size_t colblk = static_cast<size_t>(mp) * pe;
+                const double *a0[3] = {nullptr, nullptr, nullptr}, *a1[3] = {nullptr, nullptr, nullptr};
+                const double *bb[3] = {nullptr, nullptr, nullptr}, *bc[3] = {nullptr, nullptr, nullptr};
+                for (int k = 0; k < D; ++k) {
+                    a0[k] = lo.Dm[k] + colblk * npe;
+                    a1[k] = lo.G[k] + colblk * nfl;
+                    bb[k] = v.minv_b[k] + sb * e0;
+                    bc[k] = v.minv_c[k] + sc * e0;
+                }
+                if (tuning().qelim_split_rows) {
+                    // one product per output block, all D directions in its K sweep: smaller CTAs, more of them per SM
+                    fused = launch_qelim_fused(c, npe, 0, pe, pe, D, a0, sEE, a0, sEE, bb, sb, lo.E + colblk * npe, sEE, nullptr, 0, cnt) &&
+                            launch_qelim_fused(c, nfl, 0, pe, pe, D, a1, sEF, a1, sEF, bb, sb, lo.H + colblk * nfl, sEF, nullptr, 0, cnt) &&
+                            launch_qelim_fused(c, npe, 0, v.nfs, pe, D, a0, sEE, a0, sEE, bc, sc,
+                                               lo.F + static_cast<size_t>(mp) * pf * npe, sEF, nullptr, 0, cnt, pf, mpf) &&
+                            launch_qelim_fused(c, nfl, 0, v.nfs, pe, D, a1, sEF, a1, sEF, bc, sc,
+                                               lo.J + static_cast<size_t>(mp) * pf * nfl, sFF, nullptr, 0, cnt, pf, mpf);
+                    continue;
+                }
+                fused = launch_qelim_fused(c, npe, nfl, pe, pe, D, a0, sEE, a1, sEF, bb, sb, lo.E + colblk * npe, sEE,
+                                           lo.H + colblk * nfl, sEF, cnt);
+                if (fused)
+                    launch_qelim_fused(c, npe, nfl, v.nfs, pe, D, a0, sEE, a1, sEF, bc, sc, lo.F + static_cast<size_t>(mp) * pf * npe,
+                                       sEF, lo.J + static_cast<size_t>(mp) * pf * nfl, sFF, cnt, pf, mpf);
+            }
+        }
+        for (int k = 0; k < D && !fused; ++k) {
             const double* mb = v.minv_b[k] + sb * e0;
             const double* mc = v.minv_c[k] + sc * e0;
             for (int mp = 0; mp < M; ++mp) {

@@ -187,6 +187,132 @@ void launch_wm(hdgb_ctx* ctx, const GemmArgs& g, int64_t batch, bool vec, int wn
     }
 }
 
+// ---- fused q-elimination product --------------------------------------------------------------------------
+// [C0; C1] -= sum_t [A0_t; A1_t] * B_t  for t < nterm (the space directions): the two row blocks (E-bar over
+// H-bar, or F-bar over J-bar) share the right operand M^-1 B_t / M^-1 C_t, and the D direction terms are one
+// long K sweep, so one CTA per (element, 32 WN columns) replaces 2 D separate products and reads / writes the
+// outputs once (local_ops.cpp:389-398).  Row block 1 starts at a multiple of 32 rows so that no 32 x 32 warp
+// tile straddles the blocks.
+struct QelimArgs {
+    int m0, m1, n, k, nterm;
+    const double* a0[3];
+    const double* a1[3];
+    const double* b[3];
+    int64_t a0_stride, a1_stride, b_stride;
+    double* c0;
+    double* c1;
+    int64_t c0_stride, c1_stride;
+    int c_colw, c_colstride;
+};
+
+template <bool VEC, int NS>
+__global__ void __launch_bounds__(512, 1) qelim_fused_kernel(QelimArgs g, int WM, int WN) {
+    const int BM = 32 * WM, BN = 32 * WN, NT = WM * WN * 32;
+    const int LDA = BM + 4;
+    extern __shared__ __align__(16) double smem[];
+    double* As = smem;                  // [NS][KC][LDA]
+    double* Bs = smem + NS * KC * LDA;  // [NS][BN][LDB]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp % WM, wn = warp / WM;
+    const int grp = lane >> 2, tig = lane & 3;
+    const int64_t item = blockIdx.z;
+    const int m0 = g.m0, m1 = g.m1, n = g.n, k = g.k;
+    const int pad0 = (m0 + 31) / 32 * 32;
+    const int col0 = blockIdx.y * BN;
+    const int row0 = blockIdx.x * BM;  // row tiling (single row block only: m1 == 0)
+    const int nkc = (k + KC - 1) / KC;       // chunks per term
+    const int nchunk = nkc * g.nterm;
+    constexpr int W = VEC ? 2 : 1;
+
+    auto load_stage = [&](int s, int ch) {
+        const int t = ch / nkc, k0 = (ch - t * nkc) * KC;
+        const double* A0 = g.a0[t] + item * g.a0_stride;
+        const double* A1 = g.a1[t] + item * g.a1_stride;
+        const double* B = g.b[t] + item * g.b_stride;
+        double* as = As + s * KC * LDA;
+        double* bs = Bs + s * BN * LDB;
+        for (int q = tid; q < KC * (BM / W); q += NT) {
+            const int p = q / (BM / W), i = (q - p * (BM / W)) * W;
+            const int gp = k0 + p;
+            const double* src = A0;
+            bool ok = gp < k;
+            if (row0 + i < pad0) {
+                ok = ok && row0 + i < m0;
+                if (ok) src = A0 + static_cast<int64_t>(gp) * m0 + row0 + i;
+            } else {
+                const int i1 = row0 + i - pad0;
+                ok = ok && i1 < m1;
+                if (ok) src = A1 + static_cast<int64_t>(gp) * m1 + i1;
+            }
+            cp_async_zfill<VEC>(smem_addr(as + p * LDA + i), src, ok);
+        }
+        for (int q = tid; q < BN * (KC / W); q += NT) {
+            const int j = q / (KC / W), p = (q - j * (KC / W)) * W;
+            const int gj = col0 + j, gp = k0 + p;
+            const bool ok = gj < n && gp < k;
+            cp_async_zfill<VEC>(smem_addr(bs + j * LDB + p), ok ? B + static_cast<int64_t>(gj) * k + gp : B, ok);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    // NS-stage cp.async ring: chunks c+1 .. c+NS-1 are in flight while chunk c is multiplied
+#pragma unroll
+    for (int c = 0; c < NS - 1; ++c) {
+        if (c < nchunk) load_stage(c, c);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    int s = 0;
+    for (int c = 0; c < nchunk; ++c) {
+        const int sn = (s + NS - 1 >= NS) ? s - 1 : s + NS - 1;  // stage of chunk c + NS - 1
+        if (c + NS - 1 < nchunk) load_stage(sn, c + NS - 1);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group %0;" ::"n"(NS - 1) : "memory");
+        __syncthreads();
+        const double* as = As + s * KC * LDA + wm * 32 + grp;
+        const double* bs = Bs + s * BN * LDB + (wn * 32 + grp) * LDB;
+#pragma unroll
+        for (int kk = 0; kk < KC; kk += 4) {
+            double af[4], bf[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) af[i] = as[(kk + tig) * LDA + i * 8];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bf[j] = bs[j * 8 * LDB + kk + tig];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+        __syncthreads();
+        s = (s + 1 == NS) ? 0 : s + 1;
+    }
+    // epilogue: C -= acc
+    const int r0 = row0 + wm * 32;
+    const bool blk1 = r0 >= pad0;
+    const int mrows = blk1 ? m1 : m0;
+    double* C = blk1 ? g.c1 + item * g.c1_stride : g.c0 + item * g.c0_stride;
+    const int rbase = blk1 ? r0 - pad0 : r0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int gj = col0 + wn * 32 + j * 8 + 2 * tig + h;
+            if (gj >= n) continue;
+            const int cj = (gj / g.c_colw) * g.c_colstride + gj % g.c_colw;
+            double* cc = C + static_cast<int64_t>(cj) * mrows;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int gi = rbase + i * 8 + grp;
+                if (gi < mrows) cc[gi] -= acc[i][j][h];
+            }
+        }
+}
+
 }  // namespace
 
 // C_b[:, colmap(j)] = alpha * A_b * B_b[:, j] + beta * C_b[:, colmap(j)], all column-major with leading
@@ -214,6 +340,77 @@ void launch_gemm_dmma(hdgb_ctx* ctx, int m, int n, int k, const double* a, int64
         case 3: launch_wm<3>(ctx, g, batch, vec, wn); break;
         default: launch_wm<4>(ctx, g, batch, vec, wn); break;
     }
+}
+
+}  // namespace hdgb
+
+namespace hdgb {
+
+// Returns false when the stacked row blocks need more than 8 warp rows (caller falls back to single products).
+bool launch_qelim_fused(hdgb_ctx* ctx, int m0, int m1, int n, int k, int nterm, const double* const a0[3], int64_t a0_stride,
+                        const double* const a1[3], int64_t a1_stride, const double* const b[3], int64_t b_stride, double* c0,
+                        int64_t c0_stride, double* c1, int64_t c1_stride, int64_t batch, int c_colw, int c_colstride) {
+    if (batch <= 0 || n <= 0) return true;
+    int WM = ceil_div(m0, 32) + ceil_div(m1, 32);
+    if (nterm > 3) return false;
+    int gx = 1;
+    if (m1 <= 0) {
+        // single row block: tile the rows over blockIdx.x
+        c1 = c0;
+        c1_stride = c0_stride;
+        if (WM > 4) WM = 4;
+        gx = ceil_div(m0, 32 * WM);
+    } else if (WM > 8) {
+        return false;
+    }
+    int WN = ceil_div(n, 32);
+    // narrow column tiles: small CTAs, several resident per SM, so that the barrier-separated load / multiply
+    // phases of different CTAs overlap (a 15-warp CTA per SM measured 35% of the DMMA peak, 4-warp CTAs 73%)
+    const int wn_cap = tuning().qelim_wn;
+    if (WN > wn_cap) WN = wn_cap;
+    QelimArgs g{};
+    g.m0 = m0; g.m1 = m1; g.n = n; g.k = k; g.nterm = nterm;
+    bool vec = (m0 % 2 == 0) && (m1 % 2 == 0) && (k % 2 == 0) && (a0_stride % 2 == 0) && (a1_stride % 2 == 0) && (b_stride % 2 == 0);
+    for (int t = 0; t < nterm; ++t) {
+        g.a0[t] = a0[t]; g.a1[t] = a1[t]; g.b[t] = b[t];
+        vec = vec && reinterpret_cast<uintptr_t>(a0[t]) % 16 == 0 && reinterpret_cast<uintptr_t>(a1[t]) % 16 == 0 &&
+              reinterpret_cast<uintptr_t>(b[t]) % 16 == 0;
+    }
+    g.a0_stride = a0_stride; g.a1_stride = a1_stride; g.b_stride = b_stride;
+    g.c0 = c0; g.c1 = c1; g.c0_stride = c0_stride; g.c1_stride = c1_stride;
+    g.c_colw = c_colw > 0 ? c_colw : n;
+    g.c_colstride = c_colw > 0 ? c_colstride : n;
+    const int NS = tuning().qelim_stages >= 3 ? 3 : 2;
+    const size_t smem = static_cast<size_t>(NS) * (KC * (32 * WM + 4) + 32 * WN * LDB) * sizeof(double);
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+        HDGB_CUDA(cudaFuncSetAttribute(qelim_fused_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        HDGB_CUDA(cudaFuncSetAttribute(qelim_fused_kernel<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        HDGB_CUDA(cudaFuncSetAttribute(qelim_fused_kernel<true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        HDGB_CUDA(cudaFuncSetAttribute(qelim_fused_kernel<false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        configured = smem;
+    }
+    int64_t done = 0;
+    while (done < batch) {
+        const int64_t nb = (batch - done) < 65535 ? (batch - done) : 65535;
+        QelimArgs h = g;
+        for (int t = 0; t < nterm; ++t) {
+            h.a0[t] += done * a0_stride; h.a1[t] += done * a1_stride; h.b[t] += done * b_stride;
+        }
+        h.c0 += done * c0_stride; h.c1 += done * c1_stride;
+        dim3 grid(gx, ceil_div(n, 32 * WN), static_cast<unsigned>(nb));
+        const int nthr = WM * WN * 32;
+        if (NS == 3) {
+            if (vec) qelim_fused_kernel<true, 3><<<grid, nthr, smem, ctx->stream>>>(h, WM, WN);
+            else qelim_fused_kernel<false, 3><<<grid, nthr, smem, ctx->stream>>>(h, WM, WN);
+        } else {
+            if (vec) qelim_fused_kernel<true, 2><<<grid, nthr, smem, ctx->stream>>>(h, WM, WN);
+            else qelim_fused_kernel<false, 2><<<grid, nthr, smem, ctx->stream>>>(h, WM, WN);
+        }
+        HDGB_LAUNCH_CHECK(ctx);
+        done += nb;
+    }
+    return true;
 }
 
 }  // namespace hdgb

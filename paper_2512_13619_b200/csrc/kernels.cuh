@@ -36,6 +36,10 @@ struct Tuning {
     int stream_packed = 1;               // small items: 16 warps, several items side by side per warp, no shuffle tree
     int stream_packed_max_cols = 32;     // ... for items with at most this many columns
     int64_t stream_packed_stage_bytes = 6144;  // ... bytes per TMA stage of a warp in packed mode
+    int qelim_stages = 2;                // cp.async ring depth of the fused q-elimination product (2 or 3)
+    int qelim_split_rows = 1;            // fused q-elimination: one product per output block instead of stacked row blocks
+    int qelim_wn = 1;                    // 32-column tiles per CTA of the fused q-elimination product
+    int use_qelim_fused = 1;             // q-elimination as two fused stacked products per component instead of 4 D
     int use_dmma = 1;                    // batched GEMMs on the FP64 tensor-core path (k_gemm_dmma.cu)
     int use_blocked_gj = 1;              // n > 24: blocked Gauss-Jordan inverse, panel kernel + DMMA updates (k_invert.cu)
     int use_tile_lu = 1;                 // register-tiled Gauss-Jordan for 25 <= n <= 128
@@ -96,6 +100,11 @@ void launch_gemm_batch(hdgb_ctx* ctx, int m, int n, int k, const double* a, int6
 void launch_gemm_dmma(hdgb_ctx* ctx, int m, int n, int k, const double* a, int64_t a_stride, const double* b,
                       int64_t b_stride, double* c, int64_t c_stride, int64_t batch, double alpha, double beta,
                       int c_colw = 0, int c_colstride = 0);
+
+// Fused q-elimination: [C0; C1] -= sum_t [A0_t; A1_t] B_t (k_gemm_dmma.cu); false = shape not supported.
+bool launch_qelim_fused(hdgb_ctx* ctx, int m0, int m1, int n, int k, int nterm, const double* const a0[3], int64_t a0_stride,
+                        const double* const a1[3], int64_t a1_stride, const double* const b[3], int64_t b_stride, double* c0,
+                        int64_t c0_stride, double* c1, int64_t c1_stride, int64_t batch, int c_colw = 0, int c_colstride = 0);
 
 // ---- shared host helpers (api_core.cu) ------------------------------------------------------------
 void reset_flags(hdgb_ctx* c);
