@@ -73,6 +73,9 @@ const char* hdgb_version(void);
  * team kernel is used).  Returns non-zero for an unknown key.  Results do not depend on them
  * beyond rounding. */
 int hdgb_set_tuning(const char* key, int64_t value);
+/* Caching-allocator diagnostics: device allocations / frees issued so far (no reference counterpart; the
+ * reference allocates std::vector storage per call, newton.cpp:76-88). */
+void hdgb_pool_stats(int64_t* device_allocs, int64_t* device_frees);
 
 /* ---- A0-A2: batched dense kernels (dense_batch.hpp:36-51) ---------------------------------- */
 /* lu_invert_batch (dense_batch.cpp:77-99): explicit inverses by partial-pivot LU; a pivot not

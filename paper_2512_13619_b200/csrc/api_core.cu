@@ -12,6 +12,14 @@ extern "C" {
 
 const char* hdgb_version(void) { return "hdgb200 0.1 (sm_100a)"; }
 
+namespace hdgb { int64_t g_pool_device_allocs = 0, g_pool_device_frees = 0; }
+
+// Diagnostics of the caching allocator: cudaMalloc / cudaFree calls issued so far (a steady-state solve makes none).
+void hdgb_pool_stats(int64_t* device_allocs, int64_t* device_frees) {
+    if (device_allocs) *device_allocs = hdgb::g_pool_device_allocs;
+    if (device_frees) *device_frees = hdgb::g_pool_device_frees;
+}
+
 int hdgb_set_tuning(const char* key, int64_t value) {
     const std::string k = key ? key : "";
     if (k == "use_stream") { hdgb::tuning().use_stream = static_cast<int>(value); return 0; }
@@ -180,6 +188,7 @@ void* pool_alloc(size_t bytes, cudaStream_t* stream_out) {
         }
     }
     void* p = nullptr;
+    ++g_pool_device_allocs;
     cudaError_t e = cudaMalloc(&p, bytes);
     if (e != cudaSuccess) {
         cudaGetLastError();
@@ -199,12 +208,13 @@ void pool_free(void* p, size_t bytes, cudaStream_t s) {
     Pool& P = pool();
     {
         std::lock_guard<std::mutex> g(P.mu);
-        if (P.active.count(s) && bytes >= (1 << 16) && P.parked_bytes + bytes <= kParkedCap) {
+        if (P.active.count(s) && P.parked_bytes + bytes <= kParkedCap) {  // small blocks too: cudaFree synchronises the device
             P.parked[s].emplace(bytes, p);
             P.parked_bytes += bytes;
             return;
         }
     }
+    ++g_pool_device_frees;
     cudaFree(p);
 }
 

@@ -177,6 +177,7 @@ def load_library():
         "hdgb_ctx_synchronize": (i, [_vp]), "hdgb_ctx_launch_count": (i64, [_vp]),
         "hdgb_ctx_reset_launch_count": (None, [_vp]), "hdgb_version": (cp, []),
         "hdgb_set_tuning": (i, [cp, i64]),
+        "hdgb_pool_stats": (None, [C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
         "hdgb_lu_invert_batch": (i, [_vp, i, i, _vp, _vp]),
         "hdgb_gemm_batch": (i, [_vp, i, i, i, _vp, i, i, i, _vp, i, _vp]),
         "hdgb_gemv_strided_batch": (i, [_vp, i, i, i, _vp, _vp, _vp, i]),
@@ -242,6 +243,13 @@ def set_tuning(key: str, value: int):
     """Kernel-selection knobs (hdgb_set_tuning): 'use_stream', 'stream_min_elems'."""
     if load_library().hdgb_set_tuning(key.encode(), int(value)) != 0:
         raise KeyError(key)
+
+
+def pool_stats():
+    """(cudaMalloc calls, cudaFree calls) issued by the caching allocator so far."""
+    a, f = C.c_int64(0), C.c_int64(0)
+    load_library().hdgb_pool_stats(C.byref(a), C.byref(f))
+    return a.value, f.value
 
 
 def exported_symbols():
