@@ -151,9 +151,12 @@ inline bool ed_dmma_ok(int pe, int M, int D) { return pe <= 64; }
 
 template <int M, int D>
 __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& out, int e, const VolRec<M, D>* vrec,
-                        const FaceRec<M, D>* frec, const int* s_orient, double* opbuf) {
-    const int pe = dv.pe, qe = dv.qe, qf = dv.qf, npe = M * pe;
-    const int nfp = dv.n_lfe * qf;
+                        const FaceRec<M, D>* frec, const int* s_orient, double* opbuf, int gv0, int gv1, int fp0, int fp1,
+                        int first) {
+    // vrec / frec hold the records of volume points [gv0, gv1) and face points [fp0, fp1) (one chunk of a
+    // point-chunked sweep, or all points); later chunks accumulate into the blocks (first == 0)
+    const int pe = dv.pe, qf = dv.qf, npe = M * pe;
+    const int qe = gv1 - gv0, nfp = fp1 - fp0;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
     const int grp = lane >> 2, tig = lane & 3;
     const EdPlan pl = ed_plan(pe, M, D);
@@ -192,8 +195,8 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
                 double bval = 0.0;
                 if (kk < np) {
                     if (vol) {
-                        const int g = p0 + kk;
-                        const VolRec<M, D>& r = vrec[g];
+                        const int g = gv0 + p0 + kk;
+                        const VolRec<M, D>& r = vrec[p0 + kk];
                         const double ph = dv.phi[i + pe * g];
                         double dp_[D];
 #pragma unroll
@@ -216,9 +219,9 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
                             }
                         }
                     } else {
-                        const int p = p0 + kk;
+                        const int p = fp0 + p0 + kk;
                         const int lf = p / qf, gc = p - lf * qf;
-                        const FaceRec<M, D>& r = frec[p];
+                        const FaceRec<M, D>& r = frec[p0 + kk];
                         const double ph = dv.tphi[((static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf + gc) * pe + i];
                         bval = r.w * ph;
                         for (int pi = 0; pi < npair; ++pi) {
@@ -305,7 +308,10 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
 #pragma unroll
                         for (int a = 0; a < 2; ++a) {
                             const int i = rgi * 16 + a * 8 + grp;
-                            if (i < pe) dst[static_cast<size_t>(mp * pe + j) * npe + (m * pe + i)] = acc[s][a][b][h];
+                            if (i < pe) {
+                                double* o = dst + static_cast<size_t>(mp * pe + j) * npe + (m * pe + i);
+                                *o = first ? acc[s][a][b][h] : *o + acc[s][a][b][h];
+                            }
                         }
                     }
             }
@@ -655,7 +661,7 @@ __global__ void __launch_bounds__(NT) local_assemble_kernel(DiscView dv, ModelVi
     if (ED && ed_dmma_on) {
         // operand chunks live behind the point records (16-byte aligned)
         double* opbuf = sm + ((reinterpret_cast<const char*>(frec + (fp1 - fp0)) - reinterpret_cast<const char*>(sm) + 15) / 16) * 2;
-        ed_dmma<M, D>(dv, in, out, e, vrec, frec, s_orient, opbuf);
+        ed_dmma<M, D>(dv, in, out, e, vrec, frec, s_orient, opbuf, gv0, gv1, fp0, fp1, first);
     } else {
         constexpr int TI = (M == 1) ? 2 : 1, TJ = (M == 1) ? 4 : 1;
         constexpr int Q = M * (1 + D);  // per row component m: E then D_0..D_{D-1}
@@ -754,7 +760,7 @@ __global__ void __launch_bounds__(NT) local_assemble_kernel(DiscView dv, ModelVi
     }
     bool hgf_done = false;
     if constexpr (ED && M == 1) {
-        if (ed_dmma_on) {
+        if (ed_dmma_on == 2) {  // all face points in this launch
             double* opbuf = sm + ((reinterpret_cast<const char*>(frec + (fp1 - fp0)) - reinterpret_cast<const char*>(sm) + 15) / 16) * 2;
             hgf_dmma<D>(dv, out, e, reinterpret_cast<const FaceRec<1, D>*>(frec), s_orient, opbuf);
             hgf_done = true;
@@ -865,23 +871,35 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
         size_t ed_bytes = 2 * ed_plan(dv.pe, M, D).doubles(D) * sizeof(double) + 16;
         if (M == 1) ed_bytes = std::max(ed_bytes, hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D) * sizeof(double) + 16);
         const bool ed = want_jac && tuning().use_dmma && ed_dmma_ok(dv.pe, M, D) && all + ed_bytes <= cap;
-        if (ed) kern_d<<<dv.ne, NTD, all + ed_bytes, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 1);
+        if (ed) kern_d<<<dv.ne, NTD, all + ed_bytes, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2);
         else kern<<<dv.ne, 256, all, ctx->stream>>>(dv, mv, in, out, want_jac ? 1 : 0, 0, dv.qe, 0, nfp, 1, 0);
         HDGB_LAUNCH_CHECK(ctx);
         return;
     }
-    // point-chunked sweep: volume chunks first, then face chunks (the reference's accumulation order)
-    const int vc = static_cast<int>((budget - fixed) / svr), fc = static_cast<int>((budget - fixed) / sfr);
+    // point-chunked sweep: volume chunks first, then face chunks (the reference's accumulation order).  With
+    // the Jacobian on the tensor-core path the operand tiles share the budget with the point records.
+    size_t ed_bytes = 0;
+    // (measured on config 5: the 50 operand passes per launch cost more than the scalar sweep saves -- off by default)
+    if (want_jac && tuning().use_dmma && tuning().local_dmma_chunked && ed_dmma_ok(dv.pe, M, D)) {
+        ed_bytes = 2 * ed_plan(dv.pe, M, D).doubles(D) * sizeof(double) + 16;
+        if (fixed + ed_bytes + 8 * std::max(svr, sfr) > budget) ed_bytes = 0;
+    }
+    const int edf = ed_bytes ? 1 : 0;
+    const int vc = static_cast<int>((budget - fixed - ed_bytes) / svr), fc = static_cast<int>((budget - fixed - ed_bytes) / sfr);
     int first = 1;
     for (int g0 = 0; g0 < dv.qe; g0 += vc) {
         const int g1 = std::min(dv.qe, g0 + vc);
-        kern<<<dv.ne, 256, fixed + (g1 - g0) * svr, ctx->stream>>>(dv, mv, in, out, want_jac ? 1 : 0, g0, g1, 0, 0, first, 0);
+        const size_t sm_b = fixed + (g1 - g0) * svr + ed_bytes;
+        if (edf) kern_d<<<dv.ne, NTD, sm_b, ctx->stream>>>(dv, mv, in, out, 1, g0, g1, 0, 0, first, 1);
+        else kern<<<dv.ne, 256, sm_b, ctx->stream>>>(dv, mv, in, out, want_jac ? 1 : 0, g0, g1, 0, 0, first, 0);
         HDGB_LAUNCH_CHECK(ctx);
         first = 0;
     }
     for (int p0 = 0; p0 < nfp; p0 += fc) {
         const int p1 = std::min(nfp, p0 + fc);
-        kern<<<dv.ne, 256, fixed + (p1 - p0) * sfr, ctx->stream>>>(dv, mv, in, out, want_jac ? 1 : 0, 0, 0, p0, p1, first, 0);
+        const size_t sm_b = fixed + (p1 - p0) * sfr + ed_bytes;
+        if (edf) kern_d<<<dv.ne, NTD, sm_b, ctx->stream>>>(dv, mv, in, out, 1, 0, 0, p0, p1, first, 1);
+        else kern<<<dv.ne, 256, sm_b, ctx->stream>>>(dv, mv, in, out, want_jac ? 1 : 0, 0, 0, p0, p1, first, 0);
         HDGB_LAUNCH_CHECK(ctx);
         first = 0;
     }

@@ -36,6 +36,7 @@ struct Tuning {
     int stream_packed = 1;               // small items: 16 warps, several items side by side per warp, no shuffle tree
     int stream_packed_max_cols = 32;     // ... for items with at most this many columns
     int64_t stream_packed_stage_bytes = 6144;  // ... bytes per TMA stage of a warp in packed mode
+    int local_dmma_chunked = 0;          // E / D_d on the tensor-core path also in point-chunked sweeps (wide systems)
     int qelim_stages = 2;                // cp.async ring depth of the fused q-elimination product (2 or 3)
     int qelim_split_rows = 1;            // fused q-elimination: one product per output block instead of stacked row blocks
     int qelim_wn = 1;                    // 32-column tiles per CTA of the fused q-elimination product

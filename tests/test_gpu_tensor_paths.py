@@ -49,3 +49,21 @@ def test_dmma_paths_match_scalar_paths(ctx, shape, n, k, M, case):
         a, b = np.asarray(out[1][nm]), np.asarray(out[0][nm])
         tol = 1e-9 if nm in ("asm_inv", "ebar_inv", "kbar", "K", "rbar", "rhs") else 1e-12
         assert rel(a, b) <= tol, (nm, rel(a, b))
+
+
+def test_point_chunked_sweep_with_tensor_core_blocks(ctx):
+    """Wide systems sweep the quadrature points in chunks that accumulate into the blocks; with
+    `local_dmma_chunked` the E / D_d part of every chunk runs on the tensor-core path (off by default)."""
+    disc = hdg.Discretization.structured(ctx, "hex", n=2, degree=2, n_comp=5)
+    model = hdg.make_case_model(disc, "navier_stokes", mu=0.02)
+    state = hdg.make_initial_state(disc, model)
+    out = {}
+    for flag in (0, 1):
+        hdg.set_tuning("local_dmma_chunked", flag)
+        try:
+            ops = hdg.assemble_element_operators(disc, model, state, keep_raw=True, dt=0.05, u_prev=state.u)
+            out[flag] = {nm: ops.get(nm) for nm in ["e_raw", "d_raw0", "d_raw1", "d_raw2", "f_raw", "h_raw", "j_raw", "kbar", "ru"]}
+        finally:
+            hdg.set_tuning("local_dmma_chunked", 0)
+    for nm in out[0]:
+        assert rel(out[1][nm], out[0][nm]) <= (1e-9 if nm == "kbar" else 1e-12), nm
