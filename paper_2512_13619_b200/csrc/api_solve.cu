@@ -60,8 +60,10 @@ void orthogonalize_device(hdgb_ctx* c, const double* V, int64_t ldv, int nvec, i
     } else {
         launch_multi_dot(c, V, ldv, nvec, w, n, dc, partial);
         reduce(dc, nvec);
-        launch_multi_axpy(c, V, ldv, nvec, dc, -1.0, w, n, nullptr, partial);
-        launch_multi_dot(c, V, ldv, nvec, w, n, dd, partial);
+        if (!(tuning().fused_cgs && launch_multi_axpy_dot(c, V, ldv, nvec, dc, w, n, dd, partial))) {
+            launch_multi_axpy(c, V, ldv, nvec, dc, -1.0, w, n, nullptr, partial);
+            launch_multi_dot(c, V, ldv, nvec, w, n, dd, partial);
+        }
         reduce(dd, nvec);
         launch_multi_axpy(c, V, ldv, nvec, dd, -1.0, w, n, dn, partial);
         reduce(dn, 1);

@@ -123,6 +123,79 @@ __global__ void __launch_bounds__(kAxpyThreads) multi_axpy_kernel(
     }
 }
 
+// Fused first update + second projection of CGS2 (gmres.cpp:38-50):  w -= V c ;  d = V^T w  in ONE pass over the
+// Krylov basis.  The dot products of a row need only that row's updated w, so a thread that holds the basis
+// entries V_j[row] in registers for the update reuses them for its share of d: V is read once instead of
+// twice (8 n (nvec + 2) bytes instead of 8 n (2 nvec + 3)).  Thread = (row, quarter q): it owns the vectors
+// j = q (mod 4); the four partial sums of a row meet in shared memory (one barrier per tile of 64 rows), the
+// dot-product partials stay lane-wise in registers over all tiles of the persistent CTA and are reduced once.
+constexpr int kFuseRows = 64;
+constexpr int kFuseQ = 4;
+constexpr int kFuseThreads = kFuseRows * kFuseQ;
+constexpr int kFuseSlots = 16;                      // vectors per thread
+constexpr int kFuseMaxVec = kFuseSlots * kFuseQ;    // 64
+
+__global__ void __launch_bounds__(kFuseThreads) multi_axpy_dot_kernel(const double* __restrict__ V, int64_t ldv, int nvec,
+                                                                      const double* __restrict__ c, double* __restrict__ w,
+                                                                      int64_t n, double* __restrict__ partial) {
+    __shared__ double wp[2][kFuseQ][kFuseRows];  // partial sums of V c, double-buffered over tiles
+    __shared__ double red[kFuseThreads / 32][kFuseMaxVec];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int r = tid & (kFuseRows - 1), q = tid / kFuseRows;
+    double cj[kFuseSlots], dsum[kFuseSlots];
+#pragma unroll
+    for (int s = 0; s < kFuseSlots; ++s) {
+        const int j = q + kFuseQ * s;
+        cj[s] = j < nvec ? c[j] : 0.0;
+        dsum[s] = 0.0;
+    }
+    const int64_t tiles = (n + kFuseRows - 1) / kFuseRows;
+    const int64_t t0 = tiles * blockIdx.x / gridDim.x, t1 = tiles * (blockIdx.x + 1) / gridDim.x;
+    int buf = 0;
+    for (int64_t t = t0; t < t1; ++t, buf ^= 1) {
+        const int64_t row = t * kFuseRows + r;
+        const bool ok = row < n;
+        const double* vp = V + (ok ? row : n - 1) + static_cast<int64_t>(q) * ldv;
+        double v[kFuseSlots];
+#pragma unroll
+        for (int s = 0; s < kFuseSlots; ++s)
+            v[s] = (ok && q + kFuseQ * s < nvec) ? __ldg(vp + static_cast<int64_t>(kFuseQ * s) * ldv) : 0.0;
+        const double wold = (ok && q == 0) ? w[row] : 0.0;
+        double acc = 0.0;
+#pragma unroll
+        for (int s = 0; s < kFuseSlots; ++s) acc = fma(cj[s], v[s], acc);
+        wp[buf][q][r] = acc;
+        __syncthreads();
+        // quarter 0 owns the entry: it combines the four partial sums (fixed order), updates w and publishes it
+        double wn = 0.0;
+        if (q == 0) {
+            const double sub = (wp[buf][0][r] + wp[buf][1][r]) + (wp[buf][2][r] + wp[buf][3][r]);
+            wn = ok ? wold - sub : 0.0;
+            if (ok) w[row] = wn;
+            wp[buf][0][r] = wn;
+        }
+        __syncthreads();
+        if (q != 0) wn = wp[buf][0][r];
+#pragma unroll
+        for (int s = 0; s < kFuseSlots; ++s) dsum[s] = fma(v[s], wn, dsum[s]);
+    }
+    // one reduction per CTA: rows of a quarter live in two warps (64 rows)
+#pragma unroll
+    for (int s = 0; s < kFuseSlots; ++s) {
+        const double tot = warp_sum(dsum[s]);
+        if (lane == 0) red[warp][q + kFuseQ * s] = tot;
+    }
+    __syncthreads();
+    for (int j = tid; j < nvec; j += kFuseThreads) {
+        const int qq = j % kFuseQ;
+        const int w0 = qq * (kFuseRows / 32);
+        double sacc = 0.0;
+#pragma unroll
+        for (int k = 0; k < kFuseRows / 32; ++k) sacc += red[w0 + k][j];
+        partial[static_cast<int64_t>(j) * gridDim.x + blockIdx.x] = sacc;
+    }
+}
+
 __global__ void scale_dev_kernel(const double* __restrict__ w, const double* __restrict__ scalar, int mode,
                                  double* __restrict__ out, int64_t n) {
     const double v = *scalar;
@@ -186,7 +259,9 @@ int stream_grid(hdgb_ctx* ctx, int64_t n, int threads) {
 size_t multi_dot_workspace_doubles(int64_t n, int nvec) {
     const int64_t nblocks = (n + kDotChunk - 1) / kDotChunk;
     const int64_t ablocks = (n + kAxpyThreads * kAxpyPerThread - 1) / (kAxpyThreads * kAxpyPerThread);
-    const int64_t a = nblocks * (nvec > 0 ? nvec : 1);
+    int64_t a = nblocks * (nvec > 0 ? nvec : 1);
+    const int64_t fused = 1024 * static_cast<int64_t>(nvec > 0 ? nvec : 1);  // multi_axpy_dot: at most 1024 CTAs
+    if (fused > a) a = fused;
     return static_cast<size_t>(a > ablocks ? a : ablocks) + 16;
 }
 
@@ -214,6 +289,23 @@ void launch_multi_axpy(hdgb_ctx* ctx, const double* V, int64_t ldv, int nvec, co
         reduce_partials_kernel<<<1, 128, 0, ctx->stream>>>(partial, nblocks, norm2_out, -1);
         HDGB_LAUNCH_CHECK(ctx);
     }
+}
+
+// w -= V c ; d = V^T w (both over the n owned rows).  Returns false when nvec exceeds the kernel's slots.
+bool launch_multi_axpy_dot(hdgb_ctx* ctx, const double* V, int64_t ldv, int nvec, const double* c, double* w, int64_t n,
+                           double* d_out, double* partial) {
+    if (nvec <= 0 || n <= 0) return true;
+    if (nvec > kFuseMaxVec) return false;
+    const int64_t tiles = (n + kFuseRows - 1) / kFuseRows;
+    int64_t grid = static_cast<int64_t>(ctx->sm_count) * 3;
+    if (grid > 1024) grid = 1024;
+    if (grid > tiles) grid = tiles;
+    const size_t smem = 0;
+    multi_axpy_dot_kernel<<<static_cast<unsigned>(grid), kFuseThreads, smem, ctx->stream>>>(V, ldv, nvec, c, w, n, partial);
+    HDGB_LAUNCH_CHECK(ctx);
+    reduce_partials_kernel<<<nvec, 128, 0, ctx->stream>>>(partial, static_cast<int>(grid), d_out, -1);
+    HDGB_LAUNCH_CHECK(ctx);
+    return true;
 }
 
 void launch_sumsq(hdgb_ctx* ctx, const double* v, int64_t n, double* out, double* partial) {

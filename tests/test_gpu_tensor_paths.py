@@ -67,3 +67,23 @@ def test_point_chunked_sweep_with_tensor_core_blocks(ctx):
             hdg.set_tuning("local_dmma_chunked", 0)
     for nm in out[0]:
         assert rel(out[1][nm], out[0][nm]) <= (1e-9 if nm == "kbar" else 1e-12), nm
+
+
+@pytest.mark.parametrize("nvec,n", [(1, 1000), (7, 12345), (50, 70001), (64, 5000), (65, 3000)])
+def test_fused_cgs2_pass_matches_two_kernel_pass(ctx, nvec, n):
+    """CGS2 with the first update and the second projection fused into one pass over the basis
+    (`fused_cgs`, off by default) against the two-kernel sequence (gmres.cpp:38-57): same Hessenberg
+    column and the same normalised vector to rounding; more than 64 vectors falls back transparently."""
+    rng = np.random.default_rng(nvec)
+    V, _ = np.linalg.qr(rng.standard_normal((n, nvec)))
+    w = rng.standard_normal(n)
+    out = {}
+    for flag in (0, 1):
+        hdg.set_tuning("fused_cgs", flag)
+        try:
+            out[flag] = hdg.orthogonalize(ctx, V.T.copy(), w)
+        finally:
+            hdg.set_tuning("fused_cgs", 0)
+    assert np.max(np.abs(out[1][0] - out[0][0])) <= 1e-12 * np.max(np.abs(out[0][0]))
+    assert np.max(np.abs(out[1][1] - out[0][1])) <= 1e-12
+    assert np.max(np.abs(V.T @ out[1][1])) <= 1e-12
