@@ -27,6 +27,7 @@ int hdgb_set_tuning(const char* key, int64_t value) {
     if (k == "use_blocked_gj") { hdgb::tuning().use_blocked_gj = static_cast<int>(value); return 0; }
     if (k == "qelim_split_rows") { hdgb::tuning().qelim_split_rows = static_cast<int>(value); return 0; }
     if (k == "fused_cgs") { hdgb::tuning().fused_cgs = static_cast<int>(value); return 0; }
+    if (k == "local_global_records") { hdgb::tuning().local_global_records = static_cast<int>(value); return 0; }
     if (k == "local_dmma_chunked") { hdgb::tuning().local_dmma_chunked = static_cast<int>(value); return 0; }
     if (k == "qelim_stages") { hdgb::tuning().qelim_stages = static_cast<int>(value); return 0; }
     if (k == "qelim_wn") { hdgb::tuning().qelim_wn = static_cast<int>(value); return 0; }
@@ -218,6 +219,12 @@ void pool_free(void* p, size_t bytes, cudaStream_t s) {
     }
     ++g_pool_device_frees;
     cudaFree(p);
+}
+
+size_t pool_parked_bytes() {
+    Pool& P = pool();
+    std::lock_guard<std::mutex> g(P.mu);
+    return P.parked_bytes;
 }
 
 void pool_trim(cudaStream_t s) {

@@ -512,7 +512,9 @@ hdgb_ops* assemble_element_operators_device(hdgb_disc* d, const hdgb_model* m, h
     // the workspace may take up to a third of the free HBM (180 GB parts: config 2 runs in one chunk)
     size_t free_b = 0, total_b = 0;
     HDGB_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    const double budget = std::max(2.0e9, static_cast<double>(free_b) / 3.0);
+    // parked blocks of the caching allocator count as free: the chunking must not depend on what earlier calls left
+    // cached, or buffer sizes change from call to call and every allocation misses the cache
+    const double budget = std::max(2.0e9, static_cast<double>(free_b + pool_parked_bytes()) / 3.0);
     size_t chunk = keep_raw ? ne : static_cast<size_t>(budget / (per_elem * sizeof(double)));
     if (chunk < 1) chunk = 1;
     if (chunk > static_cast<size_t>(ne)) chunk = ne;

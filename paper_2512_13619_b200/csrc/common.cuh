@@ -82,6 +82,7 @@ inline void count_launch(hdgb_ctx* c, int n = 1) { c->launches += n; }
 // THE SAME STREAM (stream order makes the reuse safe without synchronising).
 void* pool_alloc(size_t bytes, cudaStream_t* stream_out);
 void pool_free(void* p, size_t bytes, cudaStream_t stream);
+size_t pool_parked_bytes();  // bytes held by the caching allocator for reuse
 void pool_trim(cudaStream_t stream);        // frees the parked blocks of a stream (ctx destroy / OOM)
 void pool_register(cudaStream_t stream, bool active);
 void pool_set_current(cudaStream_t stream); // the stream subsequent DevBuf allocations belong to (thread local)

@@ -418,10 +418,13 @@ __device__ void hgf_dmma(const DiscView& dv, const LocalOut& out, int e, const F
     }
 }
 
-template <class Model, int NT, bool ED>
+template <class Model, int NT, bool ED, bool GREC>
 __global__ void __launch_bounds__(NT) local_assemble_kernel(DiscView dv, ModelView mv, LocalIn in, LocalOut out,
                                                             int want_jac, int gv0, int gv1, int fp0, int fp1, int first,
-                                                            int ed_dmma_on) {
+                                                            int ed_dmma_on, char* rec_scratch, size_t rec_stride) {
+    // GREC: the point records of wide systems do not fit shared memory; they are staged per element in a
+    // global scratch buffer (written and re-read by the same CTA, i.e. served from L2), which keeps the
+    // whole point sweep in ONE launch and leaves shared memory to the tensor-core operand tiles.
     // Point records of the volume points [gv0, gv1) and face points [fp0, fp1) live in shared memory.
     // When all points of an element fit (scalar models) there is ONE launch (first = 1) and every
     // output entry is written once.  Wide systems (M = 5) are swept in several launches over point
@@ -441,8 +444,19 @@ __global__ void __launch_bounds__(NT) local_assemble_kernel(DiscView dv, ModelVi
     double* uhs = qs + D * npe;       // nfl
     double* ups = uhs + nfl;          // npe
     double* red = ups + npe;          // kResParts * npe: partial residual sums
-    VR* vrec = reinterpret_cast<VR*>(red + kResParts * npe);
-    FR* frec = reinterpret_cast<FR*>(vrec + (gv1 - gv0));
+    VR* vrec;
+    FR* frec;
+    double* opbuf_base;
+    if constexpr (GREC) {
+        char* base = rec_scratch + static_cast<size_t>(blockIdx.x) * rec_stride;
+        vrec = reinterpret_cast<VR*>(base);
+        frec = reinterpret_cast<FR*>(vrec + (gv1 - gv0));
+        opbuf_base = red + ((kResParts * npe + 1) & ~1);
+    } else {
+        vrec = reinterpret_cast<VR*>(red + kResParts * npe);
+        frec = reinterpret_cast<FR*>(vrec + (gv1 - gv0));
+        opbuf_base = sm + ((reinterpret_cast<const char*>(frec + (fp1 - fp0)) - reinterpret_cast<const char*>(sm) + 15) / 16) * 2;
+    }
     __shared__ int s_face[8], s_side[8], s_orient[8], s_tag[8];
 
     const Model model(mv);
@@ -660,7 +674,7 @@ __global__ void __launch_bounds__(NT) local_assemble_kernel(DiscView dv, ModelVi
     // at a time so that the accumulators (M (1 + D) per pair) stay in registers for wide systems ----
     if (ED && ed_dmma_on) {
         // operand chunks live behind the point records (16-byte aligned)
-        double* opbuf = sm + ((reinterpret_cast<const char*>(frec + (fp1 - fp0)) - reinterpret_cast<const char*>(sm) + 15) / 16) * 2;
+        double* opbuf = opbuf_base;
         ed_dmma<M, D>(dv, in, out, e, vrec, frec, s_orient, opbuf, gv0, gv1, fp0, fp1, first);
     } else {
         constexpr int TI = (M == 1) ? 2 : 1, TJ = (M == 1) ? 4 : 1;
@@ -761,7 +775,7 @@ __global__ void __launch_bounds__(NT) local_assemble_kernel(DiscView dv, ModelVi
     bool hgf_done = false;
     if constexpr (ED && M == 1) {
         if (ed_dmma_on == 2) {  // all face points in this launch
-            double* opbuf = sm + ((reinterpret_cast<const char*>(frec + (fp1 - fp0)) - reinterpret_cast<const char*>(sm) + 15) / 16) * 2;
+            double* opbuf = opbuf_base;
             hgf_dmma<D>(dv, out, e, reinterpret_cast<const FaceRec<1, D>*>(frec), s_orient, opbuf);
             hgf_done = true;
         }
@@ -856,9 +870,9 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
     const size_t svr = sizeof(VolRec<M, D>), sfr = sizeof(FaceRec<M, D>);
     if (fixed + std::max(svr, sfr) > budget)
         throw Failure(HDGB_ERR_UNSUPPORTED, "local assembly: element state exceeds shared memory");
-    auto kern = local_assemble_kernel<Model, 256, false>;
+    auto kern = local_assemble_kernel<Model, 256, false, false>;
     constexpr int NTD = (M == 1) ? 512 : 256;  // tensor-core mode: 16 warps for scalar systems
-    auto kern_d = local_assemble_kernel<Model, NTD, true>;
+    auto kern_d = local_assemble_kernel<Model, NTD, true, false>;
     static bool configured = false;
     if (!configured) {
         HDGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cap)));
@@ -871,10 +885,29 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
         size_t ed_bytes = 2 * ed_plan(dv.pe, M, D).doubles(D) * sizeof(double) + 16;
         if (M == 1) ed_bytes = std::max(ed_bytes, hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D) * sizeof(double) + 16);
         const bool ed = want_jac && tuning().use_dmma && ed_dmma_ok(dv.pe, M, D) && all + ed_bytes <= cap;
-        if (ed) kern_d<<<dv.ne, NTD, all + ed_bytes, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2);
-        else kern<<<dv.ne, 256, all, ctx->stream>>>(dv, mv, in, out, want_jac ? 1 : 0, 0, dv.qe, 0, nfp, 1, 0);
+        if (ed) kern_d<<<dv.ne, NTD, all + ed_bytes, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2, nullptr, 0);
+        else kern<<<dv.ne, 256, all, ctx->stream>>>(dv, mv, in, out, want_jac ? 1 : 0, 0, dv.qe, 0, nfp, 1, 0, nullptr, 0);
         HDGB_LAUNCH_CHECK(ctx);
         return;
+    }
+    // wide systems with the Jacobian on the tensor-core path: records in a global (L2) scratch, one launch
+    if constexpr (M > 1) {
+        if (want_jac && tuning().use_dmma && tuning().local_global_records && ed_dmma_ok(dv.pe, M, D)) {
+            const size_t edb = 2 * ed_plan(dv.pe, M, D).doubles(D) * sizeof(double) + 32;
+            const size_t rec_stride = (dv.qe * svr + nfp * sfr + 15) & ~static_cast<size_t>(15);
+            if (fixed + edb <= cap) {
+                auto kern_g = local_assemble_kernel<Model, 256, true, true>;
+                static bool cfg_g = false;
+                if (!cfg_g) {
+                    HDGB_CUDA(cudaFuncSetAttribute(kern_g, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cap)));
+                    cfg_g = true;
+                }
+                DevBuf<char> scratch(rec_stride * static_cast<size_t>(dv.ne));
+                kern_g<<<dv.ne, 256, fixed + edb, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 1, scratch.p, rec_stride);
+                HDGB_LAUNCH_CHECK(ctx);
+                return;
+            }
+        }
     }
     // point-chunked sweep: volume chunks first, then face chunks (the reference's accumulation order).  With
     // the Jacobian on the tensor-core path the operand tiles share the budget with the point records.
@@ -890,16 +923,16 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
     for (int g0 = 0; g0 < dv.qe; g0 += vc) {
         const int g1 = std::min(dv.qe, g0 + vc);
         const size_t sm_b = fixed + (g1 - g0) * svr + ed_bytes;
-        if (edf) kern_d<<<dv.ne, NTD, sm_b, ctx->stream>>>(dv, mv, in, out, 1, g0, g1, 0, 0, first, 1);
-        else kern<<<dv.ne, 256, sm_b, ctx->stream>>>(dv, mv, in, out, want_jac ? 1 : 0, g0, g1, 0, 0, first, 0);
+        if (edf) kern_d<<<dv.ne, NTD, sm_b, ctx->stream>>>(dv, mv, in, out, 1, g0, g1, 0, 0, first, 1, nullptr, 0);
+        else kern<<<dv.ne, 256, sm_b, ctx->stream>>>(dv, mv, in, out, want_jac ? 1 : 0, g0, g1, 0, 0, first, 0, nullptr, 0);
         HDGB_LAUNCH_CHECK(ctx);
         first = 0;
     }
     for (int p0 = 0; p0 < nfp; p0 += fc) {
         const int p1 = std::min(nfp, p0 + fc);
         const size_t sm_b = fixed + (p1 - p0) * sfr + ed_bytes;
-        if (edf) kern_d<<<dv.ne, NTD, sm_b, ctx->stream>>>(dv, mv, in, out, 1, 0, 0, p0, p1, first, 1);
-        else kern<<<dv.ne, 256, sm_b, ctx->stream>>>(dv, mv, in, out, want_jac ? 1 : 0, 0, 0, p0, p1, first, 0);
+        if (edf) kern_d<<<dv.ne, NTD, sm_b, ctx->stream>>>(dv, mv, in, out, 1, 0, 0, p0, p1, first, 1, nullptr, 0);
+        else kern<<<dv.ne, 256, sm_b, ctx->stream>>>(dv, mv, in, out, want_jac ? 1 : 0, 0, 0, p0, p1, first, 0, nullptr, 0);
         HDGB_LAUNCH_CHECK(ctx);
         first = 0;
     }
