@@ -27,6 +27,7 @@ int hdgb_set_tuning(const char* key, int64_t value) {
     if (k == "use_blocked_gj") { hdgb::tuning().use_blocked_gj = static_cast<int>(value); return 0; }
     if (k == "qelim_split_rows") { hdgb::tuning().qelim_split_rows = static_cast<int>(value); return 0; }
     if (k == "fused_cgs") { hdgb::tuning().fused_cgs = static_cast<int>(value); return 0; }
+    if (k == "local_dmma_min_pe") { hdgb::tuning().local_dmma_min_pe = static_cast<int>(value); return 0; }
     if (k == "local_global_records") { hdgb::tuning().local_global_records = static_cast<int>(value); return 0; }
     if (k == "local_dmma_chunked") { hdgb::tuning().local_dmma_chunked = static_cast<int>(value); return 0; }
     if (k == "qelim_stages") { hdgb::tuning().qelim_stages = static_cast<int>(value); return 0; }

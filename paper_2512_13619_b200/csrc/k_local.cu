@@ -147,7 +147,7 @@ inline __host__ __device__ EdPlan ed_plan(int pe, int M, int D) {
     return p;
 }
 // usable when one pass's tiles fit the warps' accumulator slots
-inline bool ed_dmma_ok(int pe, int M, int D) { return pe <= 64; }
+inline bool ed_dmma_ok(int pe, int M, int D) { return pe <= 64 && pe >= tuning().local_dmma_min_pe; }
 
 template <int M, int D>
 __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& out, int e, const VolRec<M, D>* vrec,

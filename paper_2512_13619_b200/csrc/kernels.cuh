@@ -37,6 +37,7 @@ struct Tuning {
     int stream_packed_max_cols = 32;     // ... for items with at most this many columns
     int64_t stream_packed_stage_bytes = 6144;  // ... bytes per TMA stage of a warp in packed mode
     int fused_cgs = 0;                   // CGS2: first update and second projection in one pass over the basis (measured slower: 112 us vs 85 us at cfg2)
+    int local_dmma_min_pe = 20;          // local blocks on the tensor-core path from this many basis functions per element
     int local_global_records = 1;        // wide systems: point records in an L2-resident scratch, one launch, E / D_d on DMMA
     int local_dmma_chunked = 0;          // E / D_d on the tensor-core path also in point-chunked sweeps (wide systems)
     int qelim_stages = 2;                // cp.async ring depth of the fused q-elimination product (2 or 3)

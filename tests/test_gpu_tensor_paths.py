@@ -32,6 +32,7 @@ def test_dmma_paths_match_scalar_paths(ctx, shape, n, k, M, case):
     for flag in (0, 1):
         hdg.set_tuning("use_dmma", flag)
         hdg.set_tuning("use_blocked_gj", flag)
+        hdg.set_tuning("local_dmma_min_pe", 0)   # small elements too (default: tensor-core path from pe = 20)
         try:
             ops = hdg.assemble_element_operators(disc, model, state, keep_raw=True, **tkw)
             K, rhs = hdg.assemble_global(disc, ops)
@@ -45,6 +46,7 @@ def test_dmma_paths_match_scalar_paths(ctx, shape, n, k, M, case):
         finally:
             hdg.set_tuning("use_dmma", 1)
             hdg.set_tuning("use_blocked_gj", 1)
+            hdg.set_tuning("local_dmma_min_pe", 20)
     for nm in out[0]:
         a, b = np.asarray(out[1][nm]), np.asarray(out[0][nm])
         tol = 1e-9 if nm in ("asm_inv", "ebar_inv", "kbar", "K", "rbar", "rhs") else 1e-12
@@ -60,11 +62,13 @@ def test_point_chunked_sweep_with_tensor_core_blocks(ctx):
     out = {}
     for flag in (0, 1):
         hdg.set_tuning("local_dmma_chunked", flag)
+        hdg.set_tuning("local_global_records", 0)   # otherwise the single-launch L2-scratch path takes over
         try:
             ops = hdg.assemble_element_operators(disc, model, state, keep_raw=True, dt=0.05, u_prev=state.u)
             out[flag] = {nm: ops.get(nm) for nm in ["e_raw", "d_raw0", "d_raw1", "d_raw2", "f_raw", "h_raw", "j_raw", "kbar", "ru"]}
         finally:
             hdg.set_tuning("local_dmma_chunked", 0)
+            hdg.set_tuning("local_global_records", 1)
     for nm in out[0]:
         assert rel(out[1][nm], out[0][nm]) <= (1e-9 if nm == "kbar" else 1e-12), nm
 
@@ -87,3 +91,21 @@ def test_fused_cgs2_pass_matches_two_kernel_pass(ctx, nvec, n):
     assert np.max(np.abs(out[1][0] - out[0][0])) <= 1e-12 * np.max(np.abs(out[0][0]))
     assert np.max(np.abs(out[1][1] - out[0][1])) <= 1e-12
     assert np.max(np.abs(V.T @ out[1][1])) <= 1e-12
+
+
+def test_wide_system_records_in_l2_scratch(ctx):
+    """Wide systems (M = 5): point records staged in a global scratch, one launch, E / D_d on DMMA (the default)
+    against the scalar point-chunked sweep."""
+    disc = hdg.Discretization.structured(ctx, "hex", n=2, degree=2, n_comp=5)
+    model = hdg.make_case_model(disc, "navier_stokes", mu=0.02)
+    state = hdg.make_initial_state(disc, model)
+    out = {}
+    for flag in (0, 1):
+        hdg.set_tuning("local_global_records", flag)
+        try:
+            ops = hdg.assemble_element_operators(disc, model, state, keep_raw=True, dt=0.05, u_prev=state.u)
+            out[flag] = {nm: ops.get(nm) for nm in ["e_raw", "d_raw0", "d_raw1", "d_raw2", "f_raw", "h_raw", "j_raw", "kbar", "ru", "rbar"]}
+        finally:
+            hdg.set_tuning("local_global_records", 1)
+    for nm in out[0]:
+        assert rel(out[1][nm], out[0][nm]) <= (1e-9 if nm in ("kbar", "rbar") else 1e-12), nm
