@@ -21,7 +21,7 @@ namespace hdgb {
 
 namespace {
 
-constexpr int KC = 32;       // k-chunk per pipeline stage
+constexpr int KC = 16;       // k-chunk per pipeline stage
 constexpr int LDB = KC + 4;  // = 4 (mod 16)
 
 __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
