@@ -129,12 +129,13 @@ struct EdPlan {
     int rg, cg;   // 16-row / 32-column tile groups covering pe
     int pp;       // component pairs per pass
     int lda;      // leading dimension of a V_w chunk (= 4 mod 16)
+    int wsub;     // V_w matrices resident per sub-pass (the warps' accumulator slots cover that many at a time)
     __host__ __device__ int qp(int D) const { return pp * (1 + D); }
     __host__ __device__ size_t doubles(int D) const {
-        return static_cast<size_t>(qp(D)) * kEdKc * lda + static_cast<size_t>(cg) * 32 * kEdLdb;
+        return static_cast<size_t>(wsub) * kEdKc * lda + static_cast<size_t>(cg) * 32 * kEdLdb;
     }
 };
-inline __host__ __device__ EdPlan ed_plan(int pe, int M, int D) {
+inline __host__ __device__ EdPlan ed_plan(int pe, int M, int D, int nwarps) {
     EdPlan p;
     p.rg = (pe + 15) / 16;
     p.cg = (pe + 31) / 32;
@@ -144,6 +145,10 @@ inline __host__ __device__ EdPlan ed_plan(int pe, int M, int D) {
     if (pp < 1) pp = 1;
     if (pp > M * M) pp = M * M;
     p.pp = pp;
+    const int gs = nwarps * kEdSlots, rc = p.rg * p.cg, qp = pp * (1 + D);
+    int wsub = (gs + rc - 1) / rc + ((gs % rc) ? 1 : 0);
+    if (wsub > qp) wsub = qp;
+    p.wsub = wsub;
     return p;
 }
 // usable when one pass's tiles fit the warps' accumulator slots
@@ -159,10 +164,11 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
     const int qe = gv1 - gv0, nfp = fp1 - fp0;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
     const int grp = lane >> 2, tig = lane & 3;
-    const EdPlan pl = ed_plan(pe, M, D);
-    const int QP = pl.qp(D), lda = pl.lda;
-    const int bufd = static_cast<int>(pl.doubles(D));  // one operand buffer: [QP][kc][lda] then [cg*32][kEdLdb]; two of them
-    const int boff0 = QP * kEdKc * lda;
+    const EdPlan pl = ed_plan(pe, M, D, nwarps);
+    const int lda = pl.lda;
+    const int bufd = static_cast<int>(pl.doubles(D));  // one operand buffer: [wsub][kc][lda] then [cg*32][kEdLdb]; two of them
+    const int boff0 = pl.wsub * kEdKc * lda;
+    const int rc = pl.rg * pl.cg;
     const bool transient = in.dt_inv > 0.0;
     const int cols_pad = pl.cg * 32;
     const int gpp = (1 + D) * pl.rg * pl.cg;  // tile groups per component pair
@@ -181,6 +187,7 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
     for (int pair0 = 0; pair0 < M * M; pair0 += pl.pp) {
         const int npair = min(pl.pp, M * M - pair0);
         const int ngroups = npair * gpp;
+        int wlo = 0, whi = npair * (1 + D);  // V_w matrices of the current sub-pass
         // chunk builder: V_w and the weighted basis of points [p0, p0 + 16) into operand buffer `buf`
         auto build = [&](int ch, int buf) {
             double* Ab = opbuf + buf * bufd;
@@ -209,13 +216,16 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
                             for (int k = 0; k < D; ++k) fe += r.cE[mm * D + k] * dp_[k];
                             double eij = -fe - r.dSu[mm] * ph;
                             if (transient && m == mp) eij += in.dt_inv * ph;
-                            Ab[((pi * (1 + D)) * kEdKc + kk) * lda + i] = eij;
+                            const int w0 = pi * (1 + D);
+                            if (w0 >= wlo && w0 < whi) Ab[((w0 - wlo) * kEdKc + kk) * lda + i] = eij;
 #pragma unroll
                             for (int dq = 0; dq < D; ++dq) {
+                                const int w = w0 + 1 + dq;
+                                if (w < wlo || w >= whi) continue;
                                 double fd = 0.0;
 #pragma unroll
                                 for (int k = 0; k < D; ++k) fd += r.cD[(dq * M * M + mm) * D + k] * dp_[k];
-                                Ab[((pi * (1 + D) + 1 + dq) * kEdKc + kk) * lda + i] = -fd - r.dSq[mm * D + dq] * ph;
+                                Ab[((w - wlo) * kEdKc + kk) * lda + i] = -fd - r.dSq[mm * D + dq] * ph;
                             }
                         }
                     } else {
@@ -226,19 +236,24 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
                         bval = r.w * ph;
                         for (int pi = 0; pi < npair; ++pi) {
                             const int pr = pair0 + pi, mp = pr / M, m = pr - mp * M, mm = m * M + mp;
-                            Ab[((pi * (1 + D)) * kEdKc + kk) * lda + i] = (m == mp) ? r.tau * ph : 0.0;
+                            const int w0 = pi * (1 + D);
+                            if (w0 >= wlo && w0 < whi) Ab[((w0 - wlo) * kEdKc + kk) * lda + i] = (m == mp) ? r.tau * ph : 0.0;
 #pragma unroll
-                            for (int dq = 0; dq < D; ++dq)
-                                Ab[((pi * (1 + D) + 1 + dq) * kEdKc + kk) * lda + i] = r.dfh_q[mm * D + dq] * ph;
+                            for (int dq = 0; dq < D; ++dq) {
+                                const int w = w0 + 1 + dq;
+                                if (w >= wlo && w < whi) Ab[((w - wlo) * kEdKc + kk) * lda + i] = r.dfh_q[mm * D + dq] * ph;
+                            }
                         }
                     }
                 } else {
-                    for (int w = 0; w < npair * (1 + D); ++w) Ab[(w * kEdKc + kk) * lda + i] = 0.0;
+                    for (int w = wlo; w < whi; ++w) Ab[((w - wlo) * kEdKc + kk) * lda + i] = 0.0;
                 }
                 Bb[i * kEdLdb + kk] = bval;
             }
         };
         for (int g0 = 0; g0 < ngroups; g0 += nwarps * kEdSlots) {  // sub-passes when the CTA has fewer warps than tiles
+            wlo = g0 / rc;
+            whi = (min(g0 + nwarps * kEdSlots, ngroups) - 1) / rc + 1;
             double acc[kEdSlots][2][4][2];
 #pragma unroll
             for (int s = 0; s < kEdSlots; ++s)
@@ -256,7 +271,7 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
                 const int gid = g0 + warp + nwarps * s;
                 const int w = gid / (pl.rg * pl.cg), rem = gid - w * (pl.rg * pl.cg);
                 const int rgi = rem / pl.cg, cgi = rem - rgi * pl.cg;
-                aoff[s] = gid < ngroups ? w * kEdKc * lda + rgi * 16 + grp + tig * lda : -1;
+                aoff[s] = gid < ngroups ? (w - wlo) * kEdKc * lda + rgi * 16 + grp + tig * lda : -1;
                 boff[s] = boff0 + (cgi * 32 + grp) * kEdLdb + tig;
             }
             __syncthreads();
@@ -324,10 +339,11 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
 //   [H | G_0 .. G_{D-1}](lf b, j) = sum_gc psi_b(gc) * (c_w(gc) w_gc phis_j(gc)),  c_0 = dv_u, c_{1+dp} = dv_q[dp]
 //   F(i, lf bp)                   = sum_gc phis_i(gc) * (w_gc dfh_uh(gc) psi_bp(gc))
 // (local_ops.cpp:186-219).  psi^T and phis are the left operands, the coefficient-scaled tables the right ones.
+constexpr int kHgfW = 2;  // coefficient sets (H, G_d) resident at a time
 struct HgfPlan {
     int pfp, qfp, ldp, lda, ldk, pep;
     __host__ __device__ size_t doubles(int D) const {
-        return static_cast<size_t>(qfp) * ldp + static_cast<size_t>(qfp) * lda + static_cast<size_t>(1 + D) * pep * ldk +
+        return static_cast<size_t>(qfp) * ldp + static_cast<size_t>(qfp) * lda + static_cast<size_t>(kHgfW) * pep * ldk +
                static_cast<size_t>(pfp) * ldk;
     }
 };
@@ -353,7 +369,7 @@ __device__ void hgf_dmma(const DiscView& dv, const LocalOut& out, int e, const F
     double* Ps = buf;                                        // psi^T: [gc][b]
     double* Fs = Ps + pl.qfp * pl.ldp;  // phis:  [gc][i]
     double* Bh = Fs + pl.qfp * pl.lda;  // [w][j][gc]
-    double* Bf = Bh + (1 + D) * pl.pep * pl.ldk;  // [bp][gc]
+    double* Bf = Bh + kHgfW * pl.pep * pl.ldk;  // [bp][gc]
     __syncthreads();
     for (int t = tid; t < static_cast<int>(pl.doubles(D)); t += nt) buf[t] = 0.0;
     __syncthreads();
@@ -362,64 +378,70 @@ __device__ void hgf_dmma(const DiscView& dv, const LocalOut& out, int e, const F
         Ps[gc * pl.ldp + b] = dv.psi[b + pf * gc];
     }
     const int rt_h = pl.pfp / 8, ct_h = pl.pep / 8;  // H/G tiles per block: rows b, columns j
-    const int ntile_h = (1 + D) * rt_h * ct_h;
     const int ntile_f = ct_h * rt_h;                 // F tiles: rows i, columns bp
     const int ksteps = pl.qfp / 4;
     for (int lf = 0; lf < n_lfe; ++lf) {
         const double* tp = dv.tphi + (static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf * pe;
         const FaceRec<1, D>* fr = frec + lf * qf;
-        for (int t = tid; t < qf * pe; t += nt) {
-            const int gc = t / pe, j = t - gc * pe;
-            const double ph = tp[t];
-            const FaceRec<1, D>& r = fr[gc];
-            const double wp = r.w * ph;
-            Fs[gc * pl.lda + j] = ph;
-            Bh[j * pl.ldk + gc] = wp * r.dv_u[0];
-#pragma unroll
-            for (int dp = 0; dp < D; ++dp) Bh[((1 + dp) * pl.pep + j) * pl.ldk + gc] = wp * r.dv_q[dp];
-        }
-        for (int t = tid; t < qf * pf; t += nt) {
-            const int gc = t / pf, bp = t - gc * pf;
-            const FaceRec<1, D>& r = fr[gc];
-            Bf[bp * pl.ldk + gc] = r.w * r.dfh_uh[0] * dv.psi[bp + pf * gc];
-        }
-        __syncthreads();
-        for (int tile = warp; tile < ntile_h + ntile_f; tile += nwarps) {
-            double c0 = 0.0, c1 = 0.0;
-            if (tile < ntile_h) {
-                const int w = tile / (rt_h * ct_h), rem = tile - w * (rt_h * ct_h);
-                const int rt = rem / ct_h, ct = rem - rt * ct_h;
-                const double* as = Ps + rt * 8 + grp;
-                const double* bs = Bh + (w * pl.pep + ct * 8 + grp) * pl.ldk;
-                for (int ks = 0; ks < ksteps; ++ks) dmma_8x8x4(c0, c1, as[(4 * ks + tig) * pl.ldp], bs[4 * ks + tig]);
-                const int b = rt * 8 + grp;
-                double* dst = (w == 0 ? out.H : out.G[w - 1]) + static_cast<size_t>(e) * nfl * npe;
-                if (b < pf) {
-                    const int j = ct * 8 + 2 * tig;
-                    if (j < pe) dst[static_cast<size_t>(j) * nfl + lf * pf + b] = c0;
-                    if (j + 1 < pe) dst[static_cast<size_t>(j + 1) * nfl + lf * pf + b] = c1;
-                }
-            } else {
-                const int tf = tile - ntile_h;
-                const int rt = tf / rt_h, ct = tf - rt * rt_h;  // rt over i (pep / 8), ct over bp (pfp / 8)
-                const double* as = Fs + rt * 8 + grp;
-                const double* bs = Bf + (ct * 8 + grp) * pl.ldk;
-                for (int ks = 0; ks < ksteps; ++ks) dmma_8x8x4(c0, c1, as[(4 * ks + tig) * pl.lda], bs[4 * ks + tig]);
-                const int i = rt * 8 + grp;
-                double* dst = out.F + static_cast<size_t>(e) * npe * nfl;
-                if (i < pe) {
-                    const int bp = ct * 8 + 2 * tig;
-                    if (bp < pf) dst[static_cast<size_t>(lf * pf + bp) * npe + i] = c0;
-                    if (bp + 1 < pf) dst[static_cast<size_t>(lf * pf + bp + 1) * npe + i] = c1;
+        for (int w0 = 0; w0 < 1 + D; w0 += kHgfW) {  // coefficient sets [w0, w0 + nw): 0 = dv_u (H), 1 + dp = dv_q[dp] (G_dp)
+            const int nw = min(kHgfW, 1 + D - w0);
+            for (int t = tid; t < qf * pe; t += nt) {
+                const int gc = t / pe, j = t - gc * pe;
+                const double ph = tp[t];
+                const FaceRec<1, D>& r = fr[gc];
+                const double wp = r.w * ph;
+                if (w0 == 0) Fs[gc * pl.lda + j] = ph;
+                for (int ww = 0; ww < nw; ++ww) {
+                    const int w = w0 + ww;
+                    Bh[(ww * pl.pep + j) * pl.ldk + gc] = wp * (w == 0 ? r.dv_u[0] : r.dv_q[w - 1]);
                 }
             }
+            if (w0 == 0) {
+                for (int t = tid; t < qf * pf; t += nt) {
+                    const int gc = t / pf, bp = t - gc * pf;
+                    const FaceRec<1, D>& r = fr[gc];
+                    Bf[bp * pl.ldk + gc] = r.w * r.dfh_uh[0] * dv.psi[bp + pf * gc];
+                }
+            }
+            __syncthreads();
+            const int ntile_h = nw * rt_h * ct_h;
+            for (int tile = warp; tile < ntile_h + (w0 == 0 ? ntile_f : 0); tile += nwarps) {
+                double c0 = 0.0, c1 = 0.0;
+                if (tile < ntile_h) {
+                    const int ww = tile / (rt_h * ct_h), rem = tile - ww * (rt_h * ct_h);
+                    const int rt = rem / ct_h, ct = rem - rt * ct_h;
+                    const double* as = Ps + rt * 8 + grp;
+                    const double* bs = Bh + (ww * pl.pep + ct * 8 + grp) * pl.ldk;
+                    for (int ks = 0; ks < ksteps; ++ks) dmma_8x8x4(c0, c1, as[(4 * ks + tig) * pl.ldp], bs[4 * ks + tig]);
+                    const int b = rt * 8 + grp, w = w0 + ww;
+                    double* dst = (w == 0 ? out.H : out.G[w - 1]) + static_cast<size_t>(e) * nfl * npe;
+                    if (b < pf) {
+                        const int j = ct * 8 + 2 * tig;
+                        if (j < pe) dst[static_cast<size_t>(j) * nfl + lf * pf + b] = c0;
+                        if (j + 1 < pe) dst[static_cast<size_t>(j + 1) * nfl + lf * pf + b] = c1;
+                    }
+                } else {
+                    const int tf = tile - ntile_h;
+                    const int rt = tf / rt_h, ct = tf - rt * rt_h;  // rt over i (pep / 8), ct over bp (pfp / 8)
+                    const double* as = Fs + rt * 8 + grp;
+                    const double* bs = Bf + (ct * 8 + grp) * pl.ldk;
+                    for (int ks = 0; ks < ksteps; ++ks) dmma_8x8x4(c0, c1, as[(4 * ks + tig) * pl.lda], bs[4 * ks + tig]);
+                    const int i = rt * 8 + grp;
+                    double* dst = out.F + static_cast<size_t>(e) * npe * nfl;
+                    if (i < pe) {
+                        const int bp = ct * 8 + 2 * tig;
+                        if (bp < pf) dst[static_cast<size_t>(lf * pf + bp) * npe + i] = c0;
+                        if (bp + 1 < pf) dst[static_cast<size_t>(lf * pf + bp + 1) * npe + i] = c1;
+                    }
+                }
+            }
+            __syncthreads();
         }
-        __syncthreads();
     }
 }
 
 template <class Model, int NT, bool ED, bool GREC>
-__global__ void __launch_bounds__(NT) local_assemble_kernel(DiscView dv, ModelView mv, LocalIn in, LocalOut out,
+__global__ void __launch_bounds__(NT, (!GREC && Model::M == 1 && NT <= 256) ? 2 : 1) local_assemble_kernel(DiscView dv, ModelView mv, LocalIn in, LocalOut out,
                                                             int want_jac, int gv0, int gv1, int fp0, int fp1, int first,
                                                             int ed_dmma_on, char* rec_scratch, size_t rec_stride) {
     // GREC: the point records of wide systems do not fit shared memory; they are staged per element in a
@@ -871,7 +893,7 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
     if (fixed + std::max(svr, sfr) > budget)
         throw Failure(HDGB_ERR_UNSUPPORTED, "local assembly: element state exceeds shared memory");
     auto kern = local_assemble_kernel<Model, 256, false, false>;
-    constexpr int NTD = (M == 1) ? 512 : 256;  // tensor-core mode: 16 warps for scalar systems
+    constexpr int NTD = 256;  // tensor-core mode: 8 warps, two CTAs per SM for scalar systems (their phases overlap)
     auto kern_d = local_assemble_kernel<Model, NTD, true, false>;
     static bool configured = false;
     if (!configured) {
@@ -882,7 +904,7 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
     const size_t all = fixed + dv.qe * svr + nfp * sfr;
     if (all <= budget) {
         // E / D_d on the tensor-core path when the operand chunks fit next to the point records
-        size_t ed_bytes = 2 * ed_plan(dv.pe, M, D).doubles(D) * sizeof(double) + 16;
+        size_t ed_bytes = 2 * ed_plan(dv.pe, M, D, NTD / 32).doubles(D) * sizeof(double) + 16;
         if (M == 1) ed_bytes = std::max(ed_bytes, hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D) * sizeof(double) + 16);
         const bool ed = want_jac && tuning().use_dmma && ed_dmma_ok(dv.pe, M, D) && all + ed_bytes <= cap;
         if (ed) kern_d<<<dv.ne, NTD, all + ed_bytes, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2, nullptr, 0);
@@ -893,7 +915,7 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
     // wide systems with the Jacobian on the tensor-core path: records in a global (L2) scratch, one launch
     if constexpr (M > 1) {
         if (want_jac && tuning().use_dmma && tuning().local_global_records && ed_dmma_ok(dv.pe, M, D)) {
-            const size_t edb = 2 * ed_plan(dv.pe, M, D).doubles(D) * sizeof(double) + 32;
+            const size_t edb = 2 * ed_plan(dv.pe, M, D, 8).doubles(D) * sizeof(double) + 32;
             const size_t rec_stride = (dv.qe * svr + nfp * sfr + 15) & ~static_cast<size_t>(15);
             if (fixed + edb <= cap) {
                 auto kern_g = local_assemble_kernel<Model, 256, true, true>;
@@ -914,7 +936,7 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
     size_t ed_bytes = 0;
     // (measured on config 5: the 50 operand passes per launch cost more than the scalar sweep saves -- off by default)
     if (want_jac && tuning().use_dmma && tuning().local_dmma_chunked && ed_dmma_ok(dv.pe, M, D)) {
-        ed_bytes = 2 * ed_plan(dv.pe, M, D).doubles(D) * sizeof(double) + 16;
+        ed_bytes = 2 * ed_plan(dv.pe, M, D, NTD / 32).doubles(D) * sizeof(double) + 16;
         if (fixed + ed_bytes + 8 * std::max(svr, sfr) > budget) ed_bytes = 0;
     }
     const int edf = ed_bytes ? 1 : 0;
