@@ -26,6 +26,16 @@ from pathlib import Path
 
 import numpy as np
 
+# stdout carries exactly ONE JSON line: native libraries (NCCL prints its version banner there) and anything
+# else that writes to fd 1 during the run are diverted to stderr; emit() writes the line to the real stdout
+_REAL_STDOUT = os.dup(1)
+os.dup2(2, 1)
+
+
+def emit(line):
+    sys.stdout.flush()
+    os.write(_REAL_STDOUT, (json.dumps(line) + "\n").encode())
+
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
@@ -96,7 +106,7 @@ def run_reference(a):
         "note": "the unmodified reference (oracle/_ref) is 2D/quad-only; this arm is the tier-B restatement "
                 "(oracle/hdg_oracle.cpp, bit-identical to the reference on 2D quads) run on all host threads",
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ---- GPU arm ---------------------------------------------------------------------------------------
@@ -341,7 +351,7 @@ def run_ours(a):
                 "sample": f"one Newton solve of hex {a.cpu_n}^3 p={a.degree} ({nd} trace DOFs, {rc['n_gmres_total']} GMRES "
                           f"iterations), tier-B oracle port, {dt:.1f} s",
                 "gmres_ms_per_iter": 1e3 * (rc["t_mv"] + rc["t_prec"] + rc["t_orth"]) / max(rc["n_gmres_total"], 1)}
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
 
