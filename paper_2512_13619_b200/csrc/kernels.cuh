@@ -42,6 +42,7 @@ struct Tuning {
     int local_dmma_chunked = 0;          // E / D_d on the tensor-core path also in point-chunked sweeps (wide systems)
     int qelim_stages = 2;                // cp.async ring depth of the fused q-elimination product (2 or 3)
     int qelim_split_rows = 1;            // fused q-elimination: one product per output block instead of stacked row blocks
+    int gemm_wn_cap = 4;                 // 32-column tiles per CTA of the generic DMMA GEMM (1..4)
     int qelim_wn = 1;                    // 32-column tiles per CTA of the fused q-elimination product
     int use_qelim_fused = 1;             // q-elimination as two fused stacked products per component instead of 4 D
     int use_dmma = 1;                    // batched GEMMs on the FP64 tensor-core path (k_gemm_dmma.cu)
