@@ -46,8 +46,8 @@ UNIT = "DOF/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cells", dest="n", type=int, default=28, help="hex cells per direction (28 -> 1.09 M trace DOFs)")
     ap.add_argument("--force-dd", action="store_true", help="use the domain-decomposition path even on one rank (testing)")

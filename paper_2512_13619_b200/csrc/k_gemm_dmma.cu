@@ -128,24 +128,35 @@ __global__ void __launch_bounds__(WM * WN * 32) gemm_dmma_kernel(GemmArgs g) {
         __syncthreads();
     }
 
-    // epilogue: lane holds C[grp][2 tig], C[grp][2 tig + 1] of every 8 x 8 tile
+    // epilogue: lane holds C[grp][2 tig], C[grp][2 tig + 1] of every 8 x 8 tile.  For beta != 0 the old entries of a
+    // column group are loaded as one batch before the first store (a load after a store to possibly aliasing
+    // memory cannot be hoisted by the compiler: entry-by-entry read-modify-write serialises 32 round trips)
     const double alpha = g.alpha, beta = g.beta;
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < 4; ++j) {
+        double old[2][4];
+        double* cc[2];
+        bool okc[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int gj = col0 + wn * 32 + j * 8 + 2 * tig + h;
-            if (gj >= n) continue;
-            const int cj = (gj / g.c_colw) * g.c_colstride + gj % g.c_colw;
-            double* cc = C + static_cast<int64_t>(cj) * m;
+            okc[h] = gj < n;
+            const int cj = okc[h] ? (gj / g.c_colw) * g.c_colstride + gj % g.c_colw : 0;
+            cc[h] = C + static_cast<int64_t>(cj) * m;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int gi = row0 + wm * 32 + i * 8 + grp;
-                if (gi >= m) continue;
-                const double v = alpha * acc[i][j][h];
-                cc[gi] = (beta == 0.0) ? v : v + beta * cc[gi];
+                old[h][i] = (beta != 0.0 && okc[h] && gi < m) ? cc[h][gi] : 0.0;
             }
         }
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int gi = row0 + wm * 32 + i * 8 + grp;
+                if (okc[h] && gi < m) cc[h][gi] = alpha * acc[i][j][h] + beta * old[h][i];
+            }
+    }
 }
 
 template <int WM, int WN>
@@ -223,6 +234,7 @@ __global__ void __launch_bounds__(512, 1) qelim_fused_kernel(QelimArgs g, int WM
     const int nkc = (k + KC - 1) / KC;       // chunks per term
     const int nchunk = nkc * g.nterm;
     constexpr int W = VEC ? 2 : 1;
+    const int a_p0 = tid / (BM / W), a_i0 = (tid - a_p0 * (BM / W)) * W, a_pstep = NT / (BM / W);
 
     auto load_stage = [&](int s, int ch) {
         const int t = ch / nkc, k0 = (ch - t * nkc) * KC;
@@ -231,8 +243,9 @@ __global__ void __launch_bounds__(512, 1) qelim_fused_kernel(QelimArgs g, int WM
         const double* B = g.b[t] + item * g.b_stride;
         double* as = As + s * KC * LDA;
         double* bs = Bs + s * BN * LDB;
-        for (int q = tid; q < KC * (BM / W); q += NT) {
-            const int p = q / (BM / W), i = (q - p * (BM / W)) * W;
+        // thread = (k-row p0 + 2 WN it, row pair i0): NT / (BM / W) = 2 WN exactly, so the row is fixed per thread
+        for (int p = a_p0; p < KC; p += a_pstep) {
+            const int i = a_i0;
             const int gp = k0 + p;
             const double* src = A0;
             bool ok = gp < k;
@@ -291,26 +304,37 @@ __global__ void __launch_bounds__(512, 1) qelim_fused_kernel(QelimArgs g, int WM
         __syncthreads();
         s = (s + 1 == NS) ? 0 : s + 1;
     }
-    // epilogue: C -= acc
+    // epilogue: C -= acc, the old entries of a column group loaded as one batch before the first store
     const int r0 = row0 + wm * 32;
     const bool blk1 = r0 >= pad0;
     const int mrows = blk1 ? m1 : m0;
     double* C = blk1 ? g.c1 + item * g.c1_stride : g.c0 + item * g.c0_stride;
     const int rbase = blk1 ? r0 - pad0 : r0;
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < 4; ++j) {
+        double old[2][4];
+        double* cc[2];
+        bool okc[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int gj = col0 + wn * 32 + j * 8 + 2 * tig + h;
-            if (gj >= n) continue;
-            const int cj = (gj / g.c_colw) * g.c_colstride + gj % g.c_colw;
-            double* cc = C + static_cast<int64_t>(cj) * mrows;
+            okc[h] = gj < n;
+            const int cj = okc[h] ? (gj / g.c_colw) * g.c_colstride + gj % g.c_colw : 0;
+            cc[h] = C + static_cast<int64_t>(cj) * mrows;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int gi = rbase + i * 8 + grp;
-                if (gi < mrows) cc[gi] -= acc[i][j][h];
+                old[h][i] = (okc[h] && gi < mrows) ? cc[h][gi] : 0.0;
             }
         }
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int gi = rbase + i * 8 + grp;
+                if (okc[h] && gi < mrows) cc[h][gi] = old[h][i] - acc[i][j][h];
+            }
+    }
 }
 
 }  // namespace
