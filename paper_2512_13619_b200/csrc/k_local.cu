@@ -204,10 +204,10 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
                     if (vol) {
                         const int g = gv0 + p0 + kk;
                         const VolRec<M, D>& r = vrec[p0 + kk];
-                        const double ph = dv.phi[i + pe * g];
+                        const double ph = __ldg(dv.phi + i + pe * g);
                         double dp_[D];
 #pragma unroll
-                        for (int k = 0; k < D; ++k) dp_[k] = dv.dphi[k][i + pe * g];
+                        for (int k = 0; k < D; ++k) dp_[k] = __ldg(dv.dphi[k] + i + pe * g);
                         bval = r.w * ph;
                         for (int pi = 0; pi < npair; ++pi) {
                             const int pr = pair0 + pi, mp = pr / M, m = pr - mp * M, mm = m * M + mp;
@@ -232,7 +232,7 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
                         const int p = fp0 + p0 + kk;
                         const int lf = p / qf, gc = p - lf * qf;
                         const FaceRec<M, D>& r = frec[p0 + kk];
-                        const double ph = dv.tphi[((static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf + gc) * pe + i];
+                        const double ph = __ldg(dv.tphi + ((static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf + gc) * pe + i);
                         bval = r.w * ph;
                         for (int pi = 0; pi < npair; ++pi) {
                             const int pr = pair0 + pi, mp = pr / M, m = pr - mp * M, mm = m * M + mp;
@@ -375,7 +375,7 @@ __device__ void hgf_dmma(const DiscView& dv, const LocalOut& out, int e, const F
     __syncthreads();
     for (int t = tid; t < qf * pf; t += nt) {
         const int gc = t / pf, b = t - gc * pf;
-        Ps[gc * pl.ldp + b] = dv.psi[b + pf * gc];
+        Ps[gc * pl.ldp + b] = __ldg(dv.psi + b + pf * gc);
     }
     const int rt_h = pl.pfp / 8, ct_h = pl.pep / 8;  // H/G tiles per block: rows b, columns j
     const int ntile_f = ct_h * rt_h;                 // F tiles: rows i, columns bp
@@ -387,7 +387,7 @@ __device__ void hgf_dmma(const DiscView& dv, const LocalOut& out, int e, const F
             const int nw = min(kHgfW, 1 + D - w0);
             for (int t = tid; t < qf * pe; t += nt) {
                 const int gc = t / pe, j = t - gc * pe;
-                const double ph = tp[t];
+                const double ph = __ldg(tp + t);
                 const FaceRec<1, D>& r = fr[gc];
                 const double wp = r.w * ph;
                 if (w0 == 0) Fs[gc * pl.lda + j] = ph;
@@ -400,7 +400,7 @@ __device__ void hgf_dmma(const DiscView& dv, const LocalOut& out, int e, const F
                 for (int t = tid; t < qf * pf; t += nt) {
                     const int gc = t / pf, bp = t - gc * pf;
                     const FaceRec<1, D>& r = fr[gc];
-                    Bf[bp * pl.ldk + gc] = r.w * r.dfh_uh[0] * dv.psi[bp + pf * gc];
+                    Bf[bp * pl.ldk + gc] = r.w * r.dfh_uh[0] * __ldg(dv.psi + bp + pf * gc);
                 }
             }
             __syncthreads();
