@@ -111,41 +111,68 @@ def run_reference(a):
 
 # ---- GPU arm ---------------------------------------------------------------------------------------
 class ClockSampler(threading.Thread):
+    """Samples SM clock and throttle reasons DURING the timed region.  NVML in-process (a handful of light queries
+    every 200 ms); polling through an `nvidia-smi -lms` child process was measured to add sporadic 20-100 ms stalls
+    to individual solves, so it is only the fallback when the NVML binding is missing."""
+
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
     def __init__(self, device):
         super().__init__(daemon=True)
         self.device, self.rows, self.stop_flag = device, [], False
         self.proc = None
 
+    def _run_nvml(self):
+        import pynvml as nv
+        nv.nvmlInit()
+        h = nv.nvmlDeviceGetHandleByIndex(self.device)
+        cmax = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+        bits = {"hw_slowdown": nv.nvmlClocksThrottleReasonHwSlowdown,
+                "hw_thermal_slowdown": nv.nvmlClocksThrottleReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": nv.nvmlClocksThrottleReasonSwThermalSlowdown,
+                "sw_power_cap": nv.nvmlClocksThrottleReasonSwPowerCap}
+        while not self.stop_flag:
+            clk = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+            util = float(nv.nvmlDeviceGetUtilizationRates(h).gpu)
+            mask = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+            self.rows.append([clk, cmax, util] + [bool(mask & bits[nm]) for nm in self.NAMES])
+            time.sleep(0.2)
+
+    def _run_smi(self):
+        q = ("clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits", "-lms", "500"], stdout=subprocess.PIPE, text=True)
+        for ln in self.proc.stdout:
+            r = [c.strip() for c in ln.split(",")]
+            try:
+                self.rows.append([float(r[0]), float(r[1]), float(r[2])] + [v.lower().startswith("active") for v in r[3:7]])
+            except (ValueError, IndexError):
+                pass
+            if self.stop_flag:
+                break
+
     def run(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, text=True)
-            for ln in self.proc.stdout:
-                self.rows.append([c.strip() for c in ln.split(",")])
-                if self.stop_flag:
-                    break
+            self._run_nvml()
         except Exception:
-            pass
+            try:
+                self._run_smi()
+            except Exception:
+                pass
 
     def finish(self):
         self.stop_flag = True
         if self.proc:
             self.proc.terminate()
         sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for r in self.rows:
-            try:
-                clk, cmax, util = float(r[0]), float(r[1]), float(r[6])
-            except (ValueError, IndexError):
-                continue
-            mx = max(mx, cmax)
-            if util > 10:
-                sm.append(clk)
-            for nm, v in zip(names, r[2:6]):
-                if v.lower().startswith("active"):
+            mx = max(mx, r[1])
+            if r[2] > 10:
+                sm.append(r[0])
+            for nm, v in zip(self.NAMES, r[3:7]):
+                if v:
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None, "reasons": sorted(reasons),
                 "samples_under_load": len(sm)}
@@ -255,7 +282,11 @@ def run_ours(a):
             ctx.reset_launch_count()
         e0.record(stream)
         for _ in range(steps):
+            t_dbg = time.perf_counter()
             fn()
+            if os.environ.get("BENCH_DEBUG"):
+                torch.cuda.synchronize()
+                print(f"[bench debug] step {1e3 * (time.perf_counter() - t_dbg):.1f} ms pool {hdg.hdg.pool_stats()}", file=sys.stderr)
         e1.record(stream)
         barrier()
         ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
