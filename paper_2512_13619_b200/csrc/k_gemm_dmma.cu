@@ -54,6 +54,7 @@ struct GemmArgs {
     int64_t c_stride;
     double alpha, beta;
     int c_colw, c_colstride;  // output column j lives at column (j / c_colw) * c_colstride + j % c_colw of C
+    const double* c_in;       // beta term read from here (same layout and stride as c); nullptr: from c
 };
 
 template <int WM, int WN, bool VEC>
@@ -70,6 +71,7 @@ __global__ void __launch_bounds__(WM * WN * 32) gemm_dmma_kernel(GemmArgs g) {
     const double* A = g.a + item * g.a_stride;
     const double* B = g.b + item * g.b_stride;
     double* C = g.c + item * g.c_stride;
+    const double* Cin = g.c_in ? g.c_in + item * g.c_stride : C;
     const int m = g.m, n = g.n, k = g.k;
     const int row0 = blockIdx.x * BM, col0 = blockIdx.y * BN;
 
@@ -143,10 +145,11 @@ __global__ void __launch_bounds__(WM * WN * 32) gemm_dmma_kernel(GemmArgs g) {
             okc[h] = gj < n;
             const int cj = okc[h] ? (gj / g.c_colw) * g.c_colstride + gj % g.c_colw : 0;
             cc[h] = C + static_cast<int64_t>(cj) * m;
+            const double* ci = Cin + static_cast<int64_t>(cj) * m;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int gi = row0 + wm * 32 + i * 8 + grp;
-                old[h][i] = (beta != 0.0 && okc[h] && gi < m) ? cc[h][gi] : 0.0;
+                old[h][i] = (beta != 0.0 && okc[h] && gi < m) ? ci[gi] : 0.0;
             }
         }
 #pragma unroll
@@ -180,6 +183,7 @@ void launch_wmwn(hdgb_ctx* ctx, const GemmArgs& g, int64_t batch, bool vec) {
         h.a += done * g.a_stride;
         h.b += done * g.b_stride;
         h.c += done * g.c_stride;
+        if (h.c_in) h.c_in += done * g.c_stride;
         dim3 grid(ceil_div(g.m, BM), ceil_div(g.n, BN), static_cast<unsigned>(nb));
         if (vec) kv<<<grid, WM * WN * 32, smem, ctx->stream>>>(h);
         else ks<<<grid, WM * WN * 32, smem, ctx->stream>>>(h);
@@ -345,10 +349,10 @@ __global__ void __launch_bounds__(512, 1) qelim_fused_kernel(QelimArgs g, int WM
 // F-bar / J-bar for multi-component systems.
 void launch_gemm_dmma(hdgb_ctx* ctx, int m, int n, int k, const double* a, int64_t a_stride, const double* b,
                       int64_t b_stride, double* c, int64_t c_stride, int64_t batch, double alpha, double beta,
-                      int c_colw, int c_colstride) {
+                      int c_colw, int c_colstride, const double* c_in) {
     if (batch <= 0 || m <= 0 || n <= 0) return;
     GemmArgs g{m, n, k, a, a_stride, b, b_stride, c, c_stride, alpha, beta, c_colw > 0 ? c_colw : n,
-               c_colw > 0 ? c_colstride : n};
+               c_colw > 0 ? c_colstride : n, c_in};
     // 16-byte cp.async needs even leading dimensions / strides and 16-byte aligned bases
     const bool vec = (m % 2 == 0) && (k % 2 == 0) && (a_stride % 2 == 0) && (b_stride % 2 == 0) &&
                      (reinterpret_cast<uintptr_t>(a) % 16 == 0) && (reinterpret_cast<uintptr_t>(b) % 16 == 0);

@@ -107,7 +107,7 @@ void launch_gemm_batch(hdgb_ctx* ctx, int m, int n, int k, const double* a, int6
 // (c_colw <= 0: identity).
 void launch_gemm_dmma(hdgb_ctx* ctx, int m, int n, int k, const double* a, int64_t a_stride, const double* b,
                       int64_t b_stride, double* c, int64_t c_stride, int64_t batch, double alpha, double beta,
-                      int c_colw = 0, int c_colstride = 0);
+                      int c_colw = 0, int c_colstride = 0, const double* c_in = nullptr);
 
 // Fused q-elimination: [C0; C1] -= sum_t [A0_t; A1_t] B_t (k_gemm_dmma.cu); false = shape not supported.
 bool launch_qelim_fused(hdgb_ctx* ctx, int m0, int m1, int n, int k, int nterm, const double* const a0[3], int64_t a0_stride,
