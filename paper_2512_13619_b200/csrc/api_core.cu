@@ -26,6 +26,7 @@ int hdgb_set_tuning(const char* key, int64_t value) {
     if (k == "stream_min_elems") { hdgb::tuning().stream_min_elems = value; return 0; }
     if (k == "use_blocked_gj") { hdgb::tuning().use_blocked_gj = static_cast<int>(value); return 0; }
     if (k == "qelim_split_rows") { hdgb::tuning().qelim_split_rows = static_cast<int>(value); return 0; }
+    if (k == "spin_sync") { hdgb::tuning().spin_sync = static_cast<int>(value); return 0; }
     if (k == "fused_cgs") { hdgb::tuning().fused_cgs = static_cast<int>(value); return 0; }
     if (k == "local_dmma_min_pe") { hdgb::tuning().local_dmma_min_pe = static_cast<int>(value); return 0; }
     if (k == "local_global_records") { hdgb::tuning().local_global_records = static_cast<int>(value); return 0; }
@@ -87,6 +88,7 @@ void hdgb_ctx_destroy(hdgb_ctx* c) {
     pool_trim(c->stream);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
+    if (c->spin_ev) cudaEventDestroy(c->spin_ev);
     if (c->d_flags) cudaFree(c->d_flags);
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->owns_stream && c->stream) cudaStreamDestroy(c->stream);

@@ -73,7 +73,8 @@ void orthogonalize_device(hdgb_ctx* c, const double* V, int64_t ldv, int nvec, i
     double* stage = c->pinned;
     HDGB_CUDA(cudaMemcpyAsync(stage, coef, (2 * nvec + 1) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     launch_scale_dev(c, w, dn, 0, w, n);
-    HDGB_CUDA(cudaStreamSynchronize(c->stream));
+    if (tuning().spin_sync) host_wait(c);
+    else HDGB_CUDA(cudaStreamSynchronize(c->stream));
     for (int i = 0; i < nvec; ++i) h[i] = stage[i] + stage[nvec + i];
     h[nvec] = std::sqrt(stage[2 * nvec]);
 }

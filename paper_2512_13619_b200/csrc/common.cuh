@@ -62,7 +62,28 @@ struct hdgb_ctx {
     // device error words: [0] = lowest singular batch index (INT_MAX = none), [1] = non-finite flag
     int* d_flags = nullptr;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t spin_ev = nullptr;  // host_wait(): event polled by the calling thread
 };
+
+namespace hdgb {
+// Wait for everything enqueued on the context's stream by POLLING an event: the per-iteration host reads of
+// GMRES (one Hessenberg column each) must not pay a thread wake-up, whatever the device scheduling flags are.
+inline void host_wait(hdgb_ctx* c) {
+    if (!c->spin_ev) {
+        if (cudaEventCreateWithFlags(&c->spin_ev, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            c->spin_ev = nullptr;
+            HDGB_CUDA(cudaStreamSynchronize(c->stream));
+            return;
+        }
+    }
+    HDGB_CUDA(cudaEventRecord(c->spin_ev, c->stream));
+    cudaError_t e;
+    while ((e = cudaEventQuery(c->spin_ev)) == cudaErrorNotReady) {
+    }
+    if (e != cudaSuccess) HDGB_CUDA(e);
+}
+}  // namespace hdgb
 
 namespace hdgb {
 

@@ -36,6 +36,7 @@ struct Tuning {
     int stream_packed = 1;               // small items: 16 warps, several items side by side per warp, no shuffle tree
     int stream_packed_max_cols = 32;     // ... for items with at most this many columns
     int64_t stream_packed_stage_bytes = 6144;  // ... bytes per TMA stage of a warp in packed mode
+    int spin_sync = 1;                   // GMRES: poll an event for the per-iteration Hessenberg column instead of a blocking sync
     int fused_cgs = 0;                   // CGS2: first update and second projection in one pass over the basis (measured slower: 112 us vs 85 us at cfg2)
     int local_dmma_min_pe = 20;          // local blocks on the tensor-core path from this many basis functions per element
     int local_global_records = 1;        // wide systems: point records in an L2-resident scratch, one launch, E / D_d on DMMA
