@@ -358,11 +358,14 @@ inline __host__ __device__ HgfPlan hgf_plan(int pe, int pf, int qf) {
     return p;
 }
 
-template <int D>
-__device__ void hgf_dmma(const DiscView& dv, const LocalOut& out, int e, const FaceRec<1, D>* frec, const int* s_orient,
+template <int M, int D>
+__device__ void hgf_dmma(const DiscView& dv, const LocalOut& out, int e, const FaceRec<M, D>* frec, const int* s_orient,
                          double* buf) {
+    // Multi-component systems: one pass per component pair (m, mp) with the pair's coefficients
+    // dv_u[m M + mp], dv_q[(m M + mp) D + dp], dfh_uh[m M + mp]; rows / columns of the pair inside the blocks:
+    // H, G (nfl x npe): row lf mpf + m pf + b, column mp pe + j;  F (npe x nfl): row m pe + i, column lf mpf + mp pf + bp.
     const int pe = dv.pe, pf = dv.pf, qf = dv.qf, n_lfe = dv.n_lfe;
-    const int nfl = n_lfe * pf, npe = pe;
+    const int mpf = M * pf, nfl = n_lfe * mpf, npe = M * pe;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
     const int grp = lane >> 2, tig = lane & 3;
     const HgfPlan pl = hgf_plan(pe, pf, qf);
@@ -382,61 +385,69 @@ __device__ void hgf_dmma(const DiscView& dv, const LocalOut& out, int e, const F
     const int ksteps = pl.qfp / 4;
     for (int lf = 0; lf < n_lfe; ++lf) {
         const double* tp = dv.tphi + (static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf * pe;
-        const FaceRec<1, D>* fr = frec + lf * qf;
-        for (int w0 = 0; w0 < 1 + D; w0 += kHgfW) {  // coefficient sets [w0, w0 + nw): 0 = dv_u (H), 1 + dp = dv_q[dp] (G_dp)
-            const int nw = min(kHgfW, 1 + D - w0);
-            for (int t = tid; t < qf * pe; t += nt) {
-                const int gc = t / pe, j = t - gc * pe;
-                const double ph = __ldg(tp + t);
-                const FaceRec<1, D>& r = fr[gc];
-                const double wp = r.w * ph;
-                if (w0 == 0) Fs[gc * pl.lda + j] = ph;
-                for (int ww = 0; ww < nw; ++ww) {
-                    const int w = w0 + ww;
-                    Bh[(ww * pl.pep + j) * pl.ldk + gc] = wp * (w == 0 ? r.dv_u[0] : r.dv_q[w - 1]);
-                }
-            }
-            if (w0 == 0) {
-                for (int t = tid; t < qf * pf; t += nt) {
-                    const int gc = t / pf, bp = t - gc * pf;
-                    const FaceRec<1, D>& r = fr[gc];
-                    Bf[bp * pl.ldk + gc] = r.w * r.dfh_uh[0] * __ldg(dv.psi + bp + pf * gc);
-                }
-            }
-            __syncthreads();
-            const int ntile_h = nw * rt_h * ct_h;
-            for (int tile = warp; tile < ntile_h + (w0 == 0 ? ntile_f : 0); tile += nwarps) {
-                double c0 = 0.0, c1 = 0.0;
-                if (tile < ntile_h) {
-                    const int ww = tile / (rt_h * ct_h), rem = tile - ww * (rt_h * ct_h);
-                    const int rt = rem / ct_h, ct = rem - rt * ct_h;
-                    const double* as = Ps + rt * 8 + grp;
-                    const double* bs = Bh + (ww * pl.pep + ct * 8 + grp) * pl.ldk;
-                    for (int ks = 0; ks < ksteps; ++ks) dmma_8x8x4(c0, c1, as[(4 * ks + tig) * pl.ldp], bs[4 * ks + tig]);
-                    const int b = rt * 8 + grp, w = w0 + ww;
-                    double* dst = (w == 0 ? out.H : out.G[w - 1]) + static_cast<size_t>(e) * nfl * npe;
-                    if (b < pf) {
-                        const int j = ct * 8 + 2 * tig;
-                        if (j < pe) dst[static_cast<size_t>(j) * nfl + lf * pf + b] = c0;
-                        if (j + 1 < pe) dst[static_cast<size_t>(j + 1) * nfl + lf * pf + b] = c1;
-                    }
-                } else {
-                    const int tf = tile - ntile_h;
-                    const int rt = tf / rt_h, ct = tf - rt * rt_h;  // rt over i (pep / 8), ct over bp (pfp / 8)
-                    const double* as = Fs + rt * 8 + grp;
-                    const double* bs = Bf + (ct * 8 + grp) * pl.ldk;
-                    for (int ks = 0; ks < ksteps; ++ks) dmma_8x8x4(c0, c1, as[(4 * ks + tig) * pl.lda], bs[4 * ks + tig]);
-                    const int i = rt * 8 + grp;
-                    double* dst = out.F + static_cast<size_t>(e) * npe * nfl;
-                    if (i < pe) {
-                        const int bp = ct * 8 + 2 * tig;
-                        if (bp < pf) dst[static_cast<size_t>(lf * pf + bp) * npe + i] = c0;
-                        if (bp + 1 < pf) dst[static_cast<size_t>(lf * pf + bp + 1) * npe + i] = c1;
-                    }
-                }
-            }
-            __syncthreads();
+        const FaceRec<M, D>* fr = frec + lf * qf;
+        for (int t = tid; t < qf * pe; t += nt) {
+            const int gc = t / pe, j = t - gc * pe;
+            Fs[gc * pl.lda + j] = __ldg(tp + t);
         }
+        for (int pr = 0; pr < M * M; ++pr) {
+            const int mp = pr / M, m = pr - mp * M, mm = m * M + mp;
+            for (int w0 = 0; w0 < 1 + D; w0 += kHgfW) {  // coefficient sets [w0, w0 + nw): 0 = dv_u (H), 1 + dp = dv_q[dp] (G_dp)
+                const int nw = min(kHgfW, 1 + D - w0);
+                __syncthreads();  // Fs staged / previous tiles done with Bh, Bf
+                for (int t = tid; t < qf * pe; t += nt) {
+                    const int gc = t / pe, j = t - gc * pe;
+                    const FaceRec<M, D>& r = fr[gc];
+                    const double wp = r.w * Fs[gc * pl.lda + j];
+                    for (int ww = 0; ww < nw; ++ww) {
+                        const int w = w0 + ww;
+                        Bh[(ww * pl.pep + j) * pl.ldk + gc] = wp * (w == 0 ? r.dv_u[mm] : r.dv_q[mm * D + w - 1]);
+                    }
+                }
+                if (w0 == 0) {
+                    for (int t = tid; t < qf * pf; t += nt) {
+                        const int gc = t / pf, bp = t - gc * pf;
+                        const FaceRec<M, D>& r = fr[gc];
+                        Bf[bp * pl.ldk + gc] = r.w * r.dfh_uh[mm] * Ps[gc * pl.ldp + bp];
+                    }
+                }
+                __syncthreads();
+                const int ntile_h = nw * rt_h * ct_h;
+                for (int tile = warp; tile < ntile_h + (w0 == 0 ? ntile_f : 0); tile += nwarps) {
+                    double c0 = 0.0, c1 = 0.0;
+                    if (tile < ntile_h) {
+                        const int ww = tile / (rt_h * ct_h), rem = tile - ww * (rt_h * ct_h);
+                        const int rt = rem / ct_h, ct = rem - rt * ct_h;
+                        const double* as = Ps + rt * 8 + grp;
+                        const double* bs = Bh + (ww * pl.pep + ct * 8 + grp) * pl.ldk;
+                        for (int ks = 0; ks < ksteps; ++ks) dmma_8x8x4(c0, c1, as[(4 * ks + tig) * pl.ldp], bs[4 * ks + tig]);
+                        const int b = rt * 8 + grp, w = w0 + ww;
+                        double* dst = (w == 0 ? out.H : out.G[w - 1]) + static_cast<size_t>(e) * nfl * npe;
+                        if (b < pf) {
+                            const int j = ct * 8 + 2 * tig;
+                            const size_t row = lf * mpf + m * pf + b;
+                            if (j < pe) dst[static_cast<size_t>(mp * pe + j) * nfl + row] = c0;
+                            if (j + 1 < pe) dst[static_cast<size_t>(mp * pe + j + 1) * nfl + row] = c1;
+                        }
+                    } else {
+                        const int tf = tile - ntile_h;
+                        const int rt = tf / rt_h, ct = tf - rt * rt_h;  // rt over i (pep / 8), ct over bp (pfp / 8)
+                        const double* as = Fs + rt * 8 + grp;
+                        const double* bs = Bf + (ct * 8 + grp) * pl.ldk;
+                        for (int ks = 0; ks < ksteps; ++ks) dmma_8x8x4(c0, c1, as[(4 * ks + tig) * pl.lda], bs[4 * ks + tig]);
+                        const int i = rt * 8 + grp;
+                        double* dst = out.F + static_cast<size_t>(e) * npe * nfl;
+                        if (i < pe) {
+                            const int bp = ct * 8 + 2 * tig;
+                            const size_t row = m * pe + i;
+                            if (bp < pf) dst[static_cast<size_t>(lf * mpf + mp * pf + bp) * npe + row] = c0;
+                            if (bp + 1 < pf) dst[static_cast<size_t>(lf * mpf + mp * pf + bp + 1) * npe + row] = c1;
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();  // before the next face restages Fs
     }
 }
 
@@ -795,10 +806,10 @@ __global__ void __launch_bounds__(NT, (!GREC && Model::M == 1 && NT <= 256) ? 2 
         }
     }
     bool hgf_done = false;
-    if constexpr (ED && M == 1) {
-        if (ed_dmma_on == 2) {  // all face points in this launch
+    if constexpr (ED) {
+        if (ed_dmma_on == 2) {  // all face points in this launch, every output entry written exactly once
             double* opbuf = opbuf_base;
-            hgf_dmma<D>(dv, out, e, reinterpret_cast<const FaceRec<1, D>*>(frec), s_orient, opbuf);
+            hgf_dmma<M, D>(dv, out, e, frec, s_orient, opbuf);
             hgf_done = true;
         }
     }
@@ -905,7 +916,7 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
     if (all <= budget) {
         // E / D_d on the tensor-core path when the operand chunks fit next to the point records
         size_t ed_bytes = 2 * ed_plan(dv.pe, M, D, NTD / 32).doubles(D) * sizeof(double) + 16;
-        if (M == 1) ed_bytes = std::max(ed_bytes, hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D) * sizeof(double) + 16);
+        ed_bytes = std::max(ed_bytes, hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D) * sizeof(double) + 16);
         const bool ed = want_jac && tuning().use_dmma && ed_dmma_ok(dv.pe, M, D) && all + ed_bytes <= cap;
         if (ed) kern_d<<<dv.ne, NTD, all + ed_bytes, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2, nullptr, 0);
         else kern<<<dv.ne, 256, all, ctx->stream>>>(dv, mv, in, out, want_jac ? 1 : 0, 0, dv.qe, 0, nfp, 1, 0, nullptr, 0);
@@ -915,7 +926,7 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
     // wide systems with the Jacobian on the tensor-core path: records in a global (L2) scratch, one launch
     if constexpr (M > 1) {
         if (want_jac && tuning().use_dmma && tuning().local_global_records && ed_dmma_ok(dv.pe, M, D)) {
-            const size_t edb = 2 * ed_plan(dv.pe, M, D, 8).doubles(D) * sizeof(double) + 32;
+            const size_t edb = std::max(2 * ed_plan(dv.pe, M, D, 8).doubles(D), hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D)) * sizeof(double) + 32;
             const size_t rec_stride = (dv.qe * svr + nfp * sfr + 15) & ~static_cast<size_t>(15);
             if (fixed + edb <= cap) {
                 auto kern_g = local_assemble_kernel<Model, 256, true, true>;
@@ -925,7 +936,7 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
                     cfg_g = true;
                 }
                 DevBuf<char> scratch(rec_stride * static_cast<size_t>(dv.ne));
-                kern_g<<<dv.ne, 256, fixed + edb, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 1, scratch.p, rec_stride);
+                kern_g<<<dv.ne, 256, fixed + edb, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2, scratch.p, rec_stride);
                 HDGB_LAUNCH_CHECK(ctx);
                 return;
             }
