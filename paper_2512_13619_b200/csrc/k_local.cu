@@ -154,7 +154,16 @@ inline __host__ __device__ EdPlan ed_plan(int pe, int M, int D, int nwarps) {
 // usable when one pass's tiles fit the warps' accumulator slots
 inline bool ed_dmma_ok(int pe, int M, int D) { return pe <= 64 && pe >= tuning().local_dmma_min_pe; }
 
-template <int M, int D>
+// Point records in the global scratch (GREC) are read with ld.global.cg: an explicit global-space load that the
+// compiler may hoist above the shared-memory stores of the operand builder (a generic load may not be), coherent
+// at L2 with the records this CTA wrote earlier in the kernel.
+template <bool GREC>
+__device__ __forceinline__ double rec_ld(const double* p) {
+    if constexpr (GREC) return __ldcg(p);
+    else return *p;
+}
+
+template <int M, int D, bool GREC>
 __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& out, int e, const VolRec<M, D>* vrec,
                         const FaceRec<M, D>* frec, const int* s_orient, double* opbuf, int gv0, int gv1, int fp0, int fp1,
                         int first) {
@@ -208,13 +217,13 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
                         double dp_[D];
 #pragma unroll
                         for (int k = 0; k < D; ++k) dp_[k] = __ldg(dv.dphi[k] + i + pe * g);
-                        bval = r.w * ph;
+                        bval = rec_ld<GREC>(&r.w) * ph;
                         for (int pi = 0; pi < npair; ++pi) {
                             const int pr = pair0 + pi, mp = pr / M, m = pr - mp * M, mm = m * M + mp;
                             double fe = 0.0;
 #pragma unroll
-                            for (int k = 0; k < D; ++k) fe += r.cE[mm * D + k] * dp_[k];
-                            double eij = -fe - r.dSu[mm] * ph;
+                            for (int k = 0; k < D; ++k) fe += rec_ld<GREC>(&r.cE[mm * D + k]) * dp_[k];
+                            double eij = -fe - rec_ld<GREC>(&r.dSu[mm]) * ph;
                             if (transient && m == mp) eij += in.dt_inv * ph;
                             const int w0 = pi * (1 + D);
                             if (w0 >= wlo && w0 < whi) Ab[((w0 - wlo) * kEdKc + kk) * lda + i] = eij;
@@ -224,8 +233,8 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
                                 if (w < wlo || w >= whi) continue;
                                 double fd = 0.0;
 #pragma unroll
-                                for (int k = 0; k < D; ++k) fd += r.cD[(dq * M * M + mm) * D + k] * dp_[k];
-                                Ab[((w - wlo) * kEdKc + kk) * lda + i] = -fd - r.dSq[mm * D + dq] * ph;
+                                for (int k = 0; k < D; ++k) fd += rec_ld<GREC>(&r.cD[(dq * M * M + mm) * D + k]) * dp_[k];
+                                Ab[((w - wlo) * kEdKc + kk) * lda + i] = -fd - rec_ld<GREC>(&r.dSq[mm * D + dq]) * ph;
                             }
                         }
                     } else {
@@ -233,15 +242,15 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
                         const int lf = p / qf, gc = p - lf * qf;
                         const FaceRec<M, D>& r = frec[p0 + kk];
                         const double ph = __ldg(dv.tphi + ((static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf + gc) * pe + i);
-                        bval = r.w * ph;
+                        bval = rec_ld<GREC>(&r.w) * ph;
                         for (int pi = 0; pi < npair; ++pi) {
                             const int pr = pair0 + pi, mp = pr / M, m = pr - mp * M, mm = m * M + mp;
                             const int w0 = pi * (1 + D);
-                            if (w0 >= wlo && w0 < whi) Ab[((w0 - wlo) * kEdKc + kk) * lda + i] = (m == mp) ? r.tau * ph : 0.0;
+                            if (w0 >= wlo && w0 < whi) Ab[((w0 - wlo) * kEdKc + kk) * lda + i] = (m == mp) ? rec_ld<GREC>(&r.tau) * ph : 0.0;
 #pragma unroll
                             for (int dq = 0; dq < D; ++dq) {
                                 const int w = w0 + 1 + dq;
-                                if (w >= wlo && w < whi) Ab[((w - wlo) * kEdKc + kk) * lda + i] = r.dfh_q[mm * D + dq] * ph;
+                                if (w >= wlo && w < whi) Ab[((w - wlo) * kEdKc + kk) * lda + i] = rec_ld<GREC>(&r.dfh_q[mm * D + dq]) * ph;
                             }
                         }
                     }
@@ -358,7 +367,7 @@ inline __host__ __device__ HgfPlan hgf_plan(int pe, int pf, int qf) {
     return p;
 }
 
-template <int M, int D>
+template <int M, int D, bool GREC>
 __device__ void hgf_dmma(const DiscView& dv, const LocalOut& out, int e, const FaceRec<M, D>* frec, const int* s_orient,
                          double* buf) {
     // Multi-component systems: one pass per component pair (m, mp) with the pair's coefficients
@@ -398,17 +407,17 @@ __device__ void hgf_dmma(const DiscView& dv, const LocalOut& out, int e, const F
                 for (int t = tid; t < qf * pe; t += nt) {
                     const int gc = t / pe, j = t - gc * pe;
                     const FaceRec<M, D>& r = fr[gc];
-                    const double wp = r.w * Fs[gc * pl.lda + j];
+                    const double wp = rec_ld<GREC>(&r.w) * Fs[gc * pl.lda + j];
                     for (int ww = 0; ww < nw; ++ww) {
                         const int w = w0 + ww;
-                        Bh[(ww * pl.pep + j) * pl.ldk + gc] = wp * (w == 0 ? r.dv_u[mm] : r.dv_q[mm * D + w - 1]);
+                        Bh[(ww * pl.pep + j) * pl.ldk + gc] = wp * rec_ld<GREC>(w == 0 ? &r.dv_u[mm] : &r.dv_q[mm * D + w - 1]);
                     }
                 }
                 if (w0 == 0) {
                     for (int t = tid; t < qf * pf; t += nt) {
                         const int gc = t / pf, bp = t - gc * pf;
                         const FaceRec<M, D>& r = fr[gc];
-                        Bf[bp * pl.ldk + gc] = r.w * r.dfh_uh[mm] * Ps[gc * pl.ldp + bp];
+                        Bf[bp * pl.ldk + gc] = rec_ld<GREC>(&r.w) * rec_ld<GREC>(&r.dfh_uh[mm]) * Ps[gc * pl.ldp + bp];
                     }
                 }
                 __syncthreads();
@@ -708,7 +717,7 @@ __global__ void __launch_bounds__(NT, (!GREC && Model::M == 1 && NT <= 256) ? 2 
     if (ED && ed_dmma_on) {
         // operand chunks live behind the point records (16-byte aligned)
         double* opbuf = opbuf_base;
-        ed_dmma<M, D>(dv, in, out, e, vrec, frec, s_orient, opbuf, gv0, gv1, fp0, fp1, first);
+        ed_dmma<M, D, GREC>(dv, in, out, e, vrec, frec, s_orient, opbuf, gv0, gv1, fp0, fp1, first);
     } else {
         constexpr int TI = (M == 1) ? 2 : 1, TJ = (M == 1) ? 4 : 1;
         constexpr int Q = M * (1 + D);  // per row component m: E then D_0..D_{D-1}
@@ -809,7 +818,7 @@ __global__ void __launch_bounds__(NT, (!GREC && Model::M == 1 && NT <= 256) ? 2 
     if constexpr (ED) {
         if (ed_dmma_on == 2) {  // all face points in this launch, every output entry written exactly once
             double* opbuf = opbuf_base;
-            hgf_dmma<M, D>(dv, out, e, frec, s_orient, opbuf);
+            hgf_dmma<M, D, GREC>(dv, out, e, frec, s_orient, opbuf);
             hgf_done = true;
         }
     }
