@@ -68,10 +68,15 @@ hdgb_status hdgb_ctx_synchronize(hdgb_ctx* ctx);
 int64_t hdgb_ctx_launch_count(const hdgb_ctx* ctx);
 void hdgb_ctx_reset_launch_count(hdgb_ctx* ctx);
 const char* hdgb_version(void);
-/* Process-wide kernel-selection knobs for A/B measurements and tests: "use_stream" (0|1: route
- * large GEMVs through the TMA stream kernel), "stream_min_elems" (matrix entries below which the
- * team kernel is used).  Returns non-zero for an unknown key.  Results do not depend on them
- * beyond rounding. */
+/* Process-wide kernel-selection knobs for A/B measurements and tests (defaults in csrc/kernels.cuh):
+ *   GEMV:        "use_stream" (TMA stream kernel for large GEMVs), "stream_min_elems", "stream_packed" (several
+ *                small items per warp pass), "stream_packed_max_cols", "stream_packed_stage_bytes";
+ *   dense:       "use_dmma" (FP64 tensor-core GEMM / local blocks), "use_qelim_fused", "qelim_split_rows",
+ *                "qelim_wn", "qelim_stages", "gemm_wn_cap", "use_blocked_gj" (blocked Gauss-Jordan inverse),
+ *                "use_tile_lu" (register-tiled Gauss-Jordan, n <= 128, when the blocked one is off);
+ *   assembly:    "local_dmma_min_pe", "local_global_records", "local_dmma_chunked", "assemble_budget_kb";
+ *   GMRES:       "fused_cgs", "spin_sync".
+ * Returns non-zero for an unknown key.  Results do not depend on them beyond rounding. */
 int hdgb_set_tuning(const char* key, int64_t value);
 /* Caching-allocator diagnostics: device allocations / frees issued so far (no reference counterpart; the
  * reference allocates std::vector storage per call, newton.cpp:76-88). */
