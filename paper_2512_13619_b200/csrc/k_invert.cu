@@ -140,6 +140,111 @@ __global__ void gj_panel_kernel(int n, int j0, int64_t batch, const double* __re
         for (int r = lane; r < n; r += 32) W[static_cast<int64_t>(c) * n + r] = P[c * ldp + r];
 }
 
+// CTA variant for large blocks (n > 128): the n x NB panel of one block lives in the shared memory of a CTA of
+// kPanelCtaWarps warps (rows dealt round-robin to the threads), so the shared-memory-limited occupancy still leaves
+// 4x the warps of the one-warp-per-block kernel above to hide the per-pivot latency chain.  Two barriers per pivot:
+// after the per-warp pivot candidates are published, and after the row interchange.
+constexpr int kPanelCtaWarps = 4;
+
+__global__ void __launch_bounds__(kPanelCtaWarps * 32) gj_panel_cta_kernel(int n, int j0, const double* __restrict__ old,
+                                                                            double* __restrict__ nw,
+                                                                            const double* __restrict__ amax, int* __restrict__ piv,
+                                                                            int* __restrict__ src, int* flags, int ldp,
+                                                                            int64_t b_base) {
+    extern __shared__ double sm[];
+    __shared__ unsigned long long s_val[kPanelCtaWarps];
+    __shared__ int s_row[kPanelCtaWarps];
+    constexpr int NT = kPanelCtaWarps * 32;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t b = blockIdx.x;
+    double* P = sm;
+    const int64_t nn = static_cast<int64_t>(n) * n;
+    const int nbk = min(NB, n - j0);
+    const double* O = old + b * nn + static_cast<int64_t>(j0) * n;
+    for (int c = 0; c < nbk; ++c)
+        for (int r = tid; r < n; r += NT) P[c * ldp + r] = O[static_cast<int64_t>(c) * n + r];
+    int* S = src + b * n;
+    for (int r = tid; r < n; r += NT) S[r] = r;
+    const double tol = 1e-14 * amax[b];
+    bool bad = false;
+    __syncthreads();
+    for (int c = 0; c < nbk; ++c) {
+        const int k = j0 + c;
+        const double* col = P + c * ldp;
+        double best = -1.0;
+        int bi = INT_MAX;
+        for (int r = tid; r < n; r += NT) {
+            if (r < k) continue;
+            const double v = fabs(col[r]);
+            if (v > best || (v == best && r < bi)) { best = v; bi = r; }
+        }
+        // warp candidate: maximal modulus, lowest row on ties (|v| compares like its bit pattern)
+        const unsigned long long bits = best < 0.0 ? 0ull : static_cast<unsigned long long>(__double_as_longlong(best));
+        const unsigned hi = static_cast<unsigned>(bits >> 32), lo = static_cast<unsigned>(bits);
+        const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+        const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+        const bool win = (bi != INT_MAX) && hi == mhi && lo == mlo;
+        const unsigned wrow = __reduce_min_sync(0xffffffffu, win ? static_cast<unsigned>(bi) : 0xffffffffu);
+        if (lane == 0) {
+            s_val[warp] = (static_cast<unsigned long long>(mhi) << 32) | mlo;
+            s_row[warp] = static_cast<int>(wrow);
+        }
+        __syncthreads();
+        unsigned long long bv = 0ull;
+        int p = INT_MAX;
+#pragma unroll
+        for (int w = 0; w < kPanelCtaWarps; ++w) {
+            const unsigned long long v = s_val[w];
+            const int r = s_row[w];
+            if (r >= 0 && r < n && (v > bv || (v == bv && r < p))) { bv = v; p = r; }
+        }
+        const double dkk = col[k];
+        const double bestv = __longlong_as_double(static_cast<long long>(bv));
+        const bool ok = (dkk == dkk) && (bestv > tol) && p < n;
+        const int pp = ok ? p : k;
+        if (!ok) bad = true;
+        if (tid == 0) {
+            piv[b * n + k] = pp;
+            const int t = S[k];
+            S[k] = S[pp];
+            S[pp] = t;
+        }
+        if (tid < nbk && pp != k) {
+            double* q = P + tid * ldp;
+            const double t = q[k];
+            q[k] = q[pp];
+            q[pp] = t;
+        }
+        __syncthreads();
+        double rowk[NB];
+#pragma unroll
+        for (int c2 = 0; c2 < NB; ++c2) rowk[c2] = c2 < nbk ? P[c2 * ldp + k] : 0.0;
+        const double inv = 1.0 / (ok ? rowk[c] : 1.0);
+        // every thread eliminates its own rows; row k is rewritten by its owner only, and nobody reads another
+        // thread's rows before the next barrier (rowk was copied above -- but the owner of row k must not overwrite
+        // it before the others have read it)
+        __syncthreads();
+        for (int r = tid; r < n; r += NT) {
+            if (r == k) {
+#pragma unroll
+                for (int c2 = 0; c2 < NB; ++c2)
+                    if (c2 < nbk) P[c2 * ldp + r] = (c2 == c) ? inv : rowk[c2] * inv;
+            } else {
+                const double li = P[c * ldp + r] * inv;
+#pragma unroll
+                for (int c2 = 0; c2 < NB; ++c2)
+                    if (c2 < nbk) P[c2 * ldp + r] = (c2 == c) ? -li : fma(-li, rowk[c2], P[c2 * ldp + r]);
+            }
+        }
+        // (the next pivot search reads own rows only; the barrier after the candidates orders the rest)
+    }
+    if (bad && tid == 0) atomicMin(flags, static_cast<int>(b_base + b));
+    __syncthreads();
+    double* W = nw + b * nn + static_cast<int64_t>(j0) * n;
+    for (int c = 0; c < nbk; ++c)
+        for (int r = tid; r < n; r += NT) W[static_cast<int64_t>(c) * n + r] = P[c * ldp + r];
+}
+
 // Register variant for n <= 128: lane owns rows lane + 32 t (t < RT), the whole panel lives in registers and
 // only the two interchanged rows travel through a shared-memory scratch line per pivot.
 template <int RT>
@@ -417,6 +522,15 @@ void launch_gj_invert_batch(hdgb_ctx* ctx, int n, int64_t batch, const double* a
                     case 3: gj_panel_reg_kernel<3><<<pg, 128, 0, ctx->stream>>>(n, j0, nbt, old, nw, amax.p + done, pp, sp, flags, done); break;
                     default: gj_panel_reg_kernel<4><<<pg, 128, 0, ctx->stream>>>(n, j0, nbt, old, nw, amax.p + done, pp, sp, flags, done); break;
                 }
+            } else if (tuning().gj_panel_cta) {
+                const size_t csm = per_warp;  // one panel per CTA
+                static size_t cfg_cta = 0;
+                if (csm > 48 * 1024 && csm > cfg_cta) {
+                    HDGB_CUDA(cudaFuncSetAttribute(gj_panel_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(csm)));
+                    cfg_cta = csm;
+                }
+                gj_panel_cta_kernel<<<static_cast<unsigned>(nbt), kPanelCtaWarps * 32, csm, ctx->stream>>>(
+                    n, j0, old, nw, amax.p + done, piv.p + done * n, src.p + done * n, flags, ldp, done);
             } else
             gj_panel_kernel<<<ceil_div(nbt, wpc), wpc * 32, psm, ctx->stream>>>(n, j0, nbt, old, nw, amax.p + done,
                                                                                  piv.p + done * n, src.p + done * n, flags, ldp, done);

@@ -8,14 +8,17 @@ import paper_2512_13619_b200 as hdg
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["gj", "tile", "smem"])
+@pytest.fixture(params=["gj", "gj-cta", "tile", "smem"])
 def lu_kernel(request):
-    """gj: blocked Gauss-Jordan with DMMA rank-16 updates (the default for n > 24); tile: register-tiled
-    Gauss-Jordan (n <= 128); smem: one block per CTA in shared memory / the global-memory fallback."""
-    hdg.set_tuning("use_blocked_gj", 1 if request.param == "gj" else 0)
+    """gj: blocked Gauss-Jordan with DMMA rank-16 updates (the default for n > 24; gj-cta: its panel of large
+    blocks factored by a 4-warp CTA instead of one warp); tile: register-tiled Gauss-Jordan (n <= 128); smem: one
+    block per CTA in shared memory / the global-memory fallback."""
+    hdg.set_tuning("use_blocked_gj", 1 if request.param.startswith("gj") else 0)
+    hdg.set_tuning("gj_panel_cta", 1 if request.param == "gj-cta" else 0)
     hdg.set_tuning("use_tile_lu", 1 if request.param == "tile" else 0)
     yield request.param
     hdg.set_tuning("use_blocked_gj", 1)
+    hdg.set_tuning("gj_panel_cta", 0)
     hdg.set_tuning("use_tile_lu", 1)
 
 
@@ -23,8 +26,10 @@ def lu_kernel(request):
                                      (40, 11), (64, 9), (70, 5), (96, 7), (100, 3), (128, 2), (150, 2), (33, 300), (200, 3),
                                      (320, 2)])
 def test_lu_invert_batch(ctx, lu_kernel, n, batch):
-    if lu_kernel != "gj" and n > 150:
+    if not lu_kernel.startswith("gj") and n > 150:
         pytest.skip("the fallback kernels are slow at this size")
+    if lu_kernel == "gj-cta" and n <= 128:
+        pytest.skip("the CTA panel kernel is for n > 128")
     rng = np.random.default_rng(n)
     a = rng.standard_normal((batch, n, n)) + 0.1 * n * np.eye(n)[None]
     a[0] = np.eye(n)[rng.permutation(n)]                       # pure permutation: pivoting (test_dense_batch.cpp:88-96)
