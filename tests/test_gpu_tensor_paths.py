@@ -11,7 +11,12 @@ pytestmark = pytest.mark.gpu
 
 CASES = [("quad", 5, 2, 1, "poisson2d"), ("quad", 4, 3, 1, "burgers"), ("tri", 4, 4, 1, "burgers"), ("hex", 3, 3, 1, "poisson"),
          ("hex", 3, 2, 1, "reaction"), ("tet", 2, 2, 1, "poisson"), ("tet", 2, 2, 3, "elasticity"), ("quad", 4, 2, 2, "elasticity"),
-         ("hex", 2, 2, 5, "navier_stokes"), ("quad", 3, 3, 4, "navier_stokes")]
+         ("hex", 2, 2, 5, "navier_stokes"), ("quad", 3, 3, 4, "navier_stokes"),
+         # element sizes between the tensor-core threshold (pe = 20) and its limit (pe = 64), odd sizes included
+         ("quad", 4, 4, 1, "burgers"), ("quad", 3, 5, 1, "poisson2d"), ("tri", 3, 5, 1, "poisson2d"), ("tri", 3, 6, 1, "burgers"),
+         ("tet", 2, 3, 1, "poisson"), ("tet", 1, 4, 1, "poisson"), ("quad", 2, 6, 1, "poisson2d"),
+         # a wide system whose point records go through the L2 scratch (hex p = 3, three components)
+         ("hex", 2, 3, 3, "elasticity")]
 
 
 def rel(a, b):
