@@ -326,6 +326,13 @@ def run_ours(a):
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) * 1e-3 / reps
 
+    # FP64 pipe utilisation of static condensation (north star): one assemble_element_operators call =
+    # quadrature assembly of the local blocks + q-elimination + E-bar^-1 + Schur complement, algorithmic flops of
+    # SURVEY.md 8(d) against the DMMA peak measured with scripts/micro/fp64_peak.cu on this pool's B200s
+    D_, pe_, npe_, qe_, nfp_ = disc.dim, disc.pe, disc.npe, disc.qe, disc.n_lfe * disc.qf
+    fl_cond = D_ * (2 * npe_ ** 3 + 4 * npe_ ** 2 * nfl + 2 * npe_ * nfl ** 2) + 2 * npe_ ** 3 + 2 * npe_ ** 2 * nfl + 2 * npe_ * nfl ** 2
+    fl_local = 2 * (1 + D_) * npe_ * npe_ * (qe_ + nfp_) + 2 * (1 + D_) * nfl * npe_ * disc.qf + 2 * npe_ * nfl * disc.qf
+    t_cond = kernel_time(lambda: hdg.assemble_element_operators(disc, model, state), reps=5)
     t_mv = kernel_time(lambda: hdg.block_matvec(K, x, y))
     t_pc = kernel_time(lambda: P.apply_base(x, y))
     bytes_mv = 8 * nf * mpf * (mpf * nb + 2) + 8 * nf * nb          # K once + x + y + int64 neighbour table
@@ -368,6 +375,10 @@ def run_ours(a):
                          "in_solve_avg_launch_us": 1e6 * rep_t.t_mv / max(n_mv_calls, 1)},
             "precond_apply": {"kind": a.precond, "GBps": bytes_pc / t_pc / 1e9, "frac": bytes_pc / t_pc / 1e9 / peak,
                               "avg_us": 1e6 * t_pc, "algorithmic_bytes": bytes_pc},
+            "condensation": {"what": "assemble_element_operators: local blocks (DMMA) + fused q-elimination + blocked Gauss-Jordan E-bar^-1 + Schur complement",
+                             "ms": 1e3 * t_cond, "flops_per_element": fl_cond + fl_local, "achieved": (fl_cond + fl_local) * ne / t_cond / 1e12,
+                             "peak": 37.2, "unit": "TFLOP/s", "frac": (fl_cond + fl_local) * ne / t_cond / 1e12 / 37.2,
+                             "peak_source": "DMMA m8n8k4 peak measured with scripts/micro/fp64_peak.cu (DFMA pipe: 34.0)"},
             "newton_solve_s": t_res / a.steps, "n_newton": rep.n_newton, "n_gmres_total": rep.n_gmres_total,
             "gmres_ms_per_iter": 1e3 * (rep_t.t_mv + rep_t.t_prec + rep_t.t_orth) / n_it,
             "phase_s": {"t_ass": rep_t.t_ass, "t_mv": rep_t.t_mv, "t_prec": rep_t.t_prec, "t_orth": rep_t.t_orth,
