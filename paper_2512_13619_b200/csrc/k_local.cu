@@ -122,7 +122,8 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
 constexpr int kResParts = 8;   // thread groups sharing one basis function's point sweep in the residual phase
 constexpr int kEdKc = 16;      // points per chunk
 constexpr int kEdLdb = 20;     // leading dimension of the right operand chunk (= 4 mod 16)
-constexpr int kEdSlots = 2;    // 16 x 32 output tiles per warp
+constexpr int kEdSlotsMax = 4;  // 16 x 32 output tiles per warp: 2 for scalar systems (two CTAs per SM), 4 for wide ones (fewer passes)
+__host__ __device__ constexpr int ed_slots(int M) { return M == 1 ? 2 : kEdSlotsMax; }
 constexpr int kEdGroups = 32;  // ... of 16 warps
 
 struct EdPlan {
@@ -136,6 +137,7 @@ struct EdPlan {
     }
 };
 inline __host__ __device__ EdPlan ed_plan(int pe, int M, int D, int nwarps) {
+    const int kEdSlots = ed_slots(M);
     EdPlan p;
     p.rg = (pe + 15) / 16;
     p.cg = (pe + 31) / 32;
@@ -169,6 +171,7 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
                         int first) {
     // vrec / frec hold the records of volume points [gv0, gv1) and face points [fp0, fp1) (one chunk of a
     // point-chunked sweep, or all points); later chunks accumulate into the blocks (first == 0)
+    constexpr int kEdSlots = ed_slots(M);
     const int pe = dv.pe, qf = dv.qf, npe = M * pe;
     const int qe = gv1 - gv0, nfp = fp1 - fp0;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
