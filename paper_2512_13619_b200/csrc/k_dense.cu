@@ -1,6 +1,11 @@
 // Batched FP64 dense kernels: explicit inverses by partial-pivot LU
 // (dense_batch.cpp:19-99) and batched GEMM (dense_batch.cpp:101-136).
 //
+// Dispatch: n <= 24 -> lu_invert_warp_kernel (below); larger blocks -> the blocked Gauss-Jordan of k_invert.cu;
+// GEMMs with more than 256 output entries -> the DMMA kernels of k_gemm_dmma.cu.  The register-tiled
+// Gauss-Jordan, the shared-memory LU and the FMA GEMMs below are the previous generation, kept behind
+// hdgb_set_tuning switches as cross-checks for the tests.
+//
 // lu_invert: one block per warp (n <= 24) or per CTA (shared-memory resident up to n = 104;
 // larger blocks fall back to a global-memory workspace).  The factorisation follows the
 // reference step for step -- same pivot rule (first row of maximal modulus), same singularity

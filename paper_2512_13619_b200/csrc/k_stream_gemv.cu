@@ -14,6 +14,12 @@
 //   * multiplies (lanes own 1-2 consecutive rows x a column group; 128-bit LDS when the row count
 //     is even) keeping partial sums in registers across the chunks of an item,
 //   * combines the column groups with a fixed-order shuffle tree (deterministic) and writes y.
+// Small items (rows <= 32 after vectorisation, cols <= 32: triangle / quadrilateral blocks) use the PACKED
+// mode instead: 16 warps per CTA with stages of a few KB, a warp multiplies 32 / RL items side by side (lane =
+// item x row group, two independent accumulators, no cross-lane reduction), the x slices are gathered one
+// (item, slot) per lane and padded to an even stride so that two columns are read with one LDS.128.  At
+// 1 KB per item the per-item instruction count, not the byte stream, is what limits the kernel: ring
+// positions are carried incrementally in 32-bit counters (no 64-bit divisions on the per-item path).
 // HBM sees every matrix byte exactly once, as large sequential bulk reads; x / y traffic is served
 // from L2.  Roofline: HBM.  Algorithmic bytes per item: 8*(rows*cols + cols + rows) + 4*nslots.
 #include "kernels.cuh"
