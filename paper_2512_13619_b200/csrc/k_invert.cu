@@ -476,11 +476,230 @@ __global__ void gj_colperm_kernel(int n, const double* __restrict__ w, double* _
     }
 }
 
+// ---- single-kernel variant for n <= 128: the block stays in shared memory ---------------------------------------
+// Same blocked Gauss-Jordan, but the whole block lives in the shared memory of one CTA (column-major, leading
+// dimension = 4 mod 16), so each block is read from and written to HBM exactly once instead of once per panel:
+//   per panel: warp 0 factors the 16 pivot columns in registers (as gj_panel_reg_kernel) -> every thread applies the
+//   panel's row interchanges to one non-panel column and copies its pivot rows into the right-operand buffer ->
+//   all warps update their 8 x 8 tiles in place with DMMA (pivot rows: replaced, other rows: accumulated).
+// The column permutation happens on the way out.  Padding to a multiple of 16 is an identity block.
+template <int RT>
+__global__ void __launch_bounds__(256) gj_smem_kernel(int n, int64_t batch, const double* __restrict__ a_in,
+                                                      double* __restrict__ inv_out, int* flags, int64_t b_base) {
+    constexpr int NP = 32 * RT;  // padded order (rows lane + 32 t of the panel registers); n <= NP
+    constexpr int LDA = NP + 4;
+    extern __shared__ __align__(16) double sm[];
+    double* A = sm;                       // [NP][LDA] column-major
+    double* B1 = A + NP * LDA;            // [NP][LDB]: pivot rows of the non-panel columns, B operand
+    double* scr = B1 + NP * LDB;          // [2][NB] interchanged rows of the panel factorisation
+    int* s_piv = reinterpret_cast<int*>(scr + 2 * NB);  // [NP]
+    int* s_dst = s_piv + NP;                            // [NP]
+    __shared__ double s_red[8];
+    __shared__ int s_bad;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int grp = lane >> 2, tig = lane & 3;
+    const int npad = (n + NB - 1) / NB * NB;  // active order, multiple of NB (<= NP)
+    const int64_t nn = static_cast<int64_t>(n) * n;
+
+    for (int64_t blk = blockIdx.x; blk < batch; blk += gridDim.x) {
+        const double* Ag = a_in + blk * nn;
+        double amax = 0.0;
+        for (int t = tid; t < npad * npad; t += 256) {
+            const int c = t / npad, r = t - c * npad;
+            double v = (r == c) ? 1.0 : 0.0;  // identity padding
+            if (r < n && c < n) {
+                v = Ag[static_cast<int64_t>(c) * n + r];
+                amax = fmax(amax, fabs(v));
+            }
+            A[c * LDA + r] = v;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+        if (lane == 0) s_red[warp] = amax;
+        if (tid == 0) s_bad = 0;
+        __syncthreads();
+        amax = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) amax = fmax(amax, s_red[w]);
+        const double tol = 1e-14 * amax;
+
+        for (int j0 = 0; j0 < npad; j0 += NB) {
+            // ---- (a) panel factorisation by warp 0, register resident ----
+            if (warp == 0) {
+                double p_[RT][NB];
+#pragma unroll
+                for (int c = 0; c < NB; ++c)
+#pragma unroll
+                    for (int t = 0; t < RT; ++t) {
+                        const int r = lane + 32 * t;
+                        p_[t][c] = r < npad ? A[(j0 + c) * LDA + r] : 0.0;
+                    }
+                double* scr0 = scr;
+                double* scr1 = scr + NB;
+                bool bad = false;
+#pragma unroll
+                for (int c = 0; c < NB; ++c) {
+                    const int k = j0 + c;
+                    double best = -1.0, dkk = 0.0;
+                    int bi = INT_MAX;
+#pragma unroll
+                    for (int t = 0; t < RT; ++t) {
+                        const int r = lane + 32 * t;
+                        const double v = fabs(p_[t][c]);
+                        if (r >= k && r < npad && v > best) { best = v; bi = r; }
+                        if (r == k) dkk = p_[t][c];
+                    }
+                    const unsigned long long bits = best < 0.0 ? 0ull : static_cast<unsigned long long>(__double_as_longlong(best));
+                    const unsigned hi = static_cast<unsigned>(bits >> 32), lo = static_cast<unsigned>(bits);
+                    const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+                    const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+                    const bool win = (bi != INT_MAX) && hi == mhi && lo == mlo;
+                    const int p = static_cast<int>(__reduce_min_sync(0xffffffffu, win ? static_cast<unsigned>(bi) : 0xffffffffu));
+                    const bool nan_diag = __any_sync(0xffffffffu, dkk != dkk);
+                    const double bestv = __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(mhi) << 32) | mlo));
+                    // padding pivots (k >= n) are exact ones: never singular
+                    const bool ok = !nan_diag && (bestv > tol || k >= n) && p < npad;
+                    const int pp = ok ? p : k;
+                    if (!ok) bad = true;
+                    if (lane == 0) s_piv[k] = pp;
+#pragma unroll
+                    for (int t = 0; t < RT; ++t) {
+                        const int r = lane + 32 * t;
+                        if (r == pp) {
+#pragma unroll
+                            for (int c2 = 0; c2 < NB; ++c2) scr0[c2] = p_[t][c2];
+                        }
+                        if (r == k) {
+#pragma unroll
+                            for (int c2 = 0; c2 < NB; ++c2) scr1[c2] = p_[t][c2];
+                        }
+                    }
+                    __syncwarp();
+                    double rowk[NB];
+#pragma unroll
+                    for (int c2 = 0; c2 < NB; ++c2) rowk[c2] = scr0[c2];
+                    const double inv = 1.0 / (ok ? rowk[c] : 1.0);
+#pragma unroll
+                    for (int t = 0; t < RT; ++t) {
+                        const int r = lane + 32 * t;
+                        if (r == pp && pp != k) {
+#pragma unroll
+                            for (int c2 = 0; c2 < NB; ++c2) p_[t][c2] = scr1[c2];
+                        }
+                        if (r == k) {
+#pragma unroll
+                            for (int c2 = 0; c2 < NB; ++c2) p_[t][c2] = (c2 == c) ? inv : rowk[c2] * inv;
+                        } else {
+                            const double li = p_[t][c] * inv;
+#pragma unroll
+                            for (int c2 = 0; c2 < NB; ++c2) p_[t][c2] = (c2 == c) ? -li : fma(-li, rowk[c2], p_[t][c2]);
+                        }
+                    }
+                    __syncwarp();
+                }
+                if (bad && lane == 0) s_bad = 1;
+#pragma unroll
+                for (int c = 0; c < NB; ++c)
+#pragma unroll
+                    for (int t = 0; t < RT; ++t) {
+                        const int r = lane + 32 * t;
+                        if (r < npad) A[(j0 + c) * LDA + r] = p_[t][c];
+                    }
+            }
+            __syncthreads();
+            // ---- (b) row interchanges of the non-panel columns + right operand ----
+            const int ncol = npad - NB;
+            for (int ci = tid; ci < ncol; ci += 256) {
+                const int col = ci < j0 ? ci : ci + NB;
+                double* cp = A + col * LDA;
+#pragma unroll 4
+                for (int c = 0; c < NB; ++c) {
+                    const int k = j0 + c, p = s_piv[k];
+                    if (p != k) {
+                        const double t = cp[k];
+                        cp[k] = cp[p];
+                        cp[p] = t;
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < NB; ++c) B1[ci * LDB + c] = cp[j0 + c];
+            }
+            __syncthreads();
+            // ---- (c) rank-NB update of the 8 x 8 tiles, in place ----
+            const int tr = npad / 8, tc = ncol / 8;
+            for (int tile = warp; tile < tr * tc; tile += 8) {
+                const int ti = tile % tr, tj = tile / tr;
+                const int r0 = ti * 8, ci0 = tj * 8;
+                const int cidx = ci0 + 2 * tig;
+                const int col0 = cidx < j0 ? cidx : cidx + NB, col1 = (cidx + 1) < j0 ? cidx + 1 : cidx + 1 + NB;
+                const bool pivrow = (r0 >= j0 && r0 < j0 + NB);
+                double c0 = pivrow ? 0.0 : A[col0 * LDA + r0 + grp];
+                double c1 = pivrow ? 0.0 : A[col1 * LDA + r0 + grp];
+#pragma unroll
+                for (int kk = 0; kk < NB; kk += 4)
+                    dmma_8x8x4(c0, c1, A[(j0 + kk + tig) * LDA + r0 + grp], B1[(ci0 + grp) * LDB + kk + tig]);
+                A[col0 * LDA + r0 + grp] = c0;
+                A[col1 * LDA + r0 + grp] = c1;
+            }
+            __syncthreads();
+        }
+        // ---- column permutation on the way out: inverse[:, dst[j]] = W[:, j] ----
+        if (tid == 0) {
+            int* cmap = reinterpret_cast<int*>(B1);  // scratch
+            for (int j = 0; j < npad; ++j) cmap[j] = j;
+            for (int k = npad - 1; k >= 0; --k) {
+                const int p = s_piv[k];
+                const int t = cmap[k];
+                cmap[k] = cmap[p];
+                cmap[p] = t;
+            }
+            for (int j = 0; j < npad; ++j) s_dst[cmap[j]] = j;
+            if (s_bad) atomicMin(flags, static_cast<int>(b_base + blk));
+        }
+        __syncthreads();
+        if (!s_bad) {
+            double* Og = inv_out + blk * nn;
+            for (int t = tid; t < npad * npad; t += 256) {
+                const int c = t / npad, r = t - c * npad;
+                const int dc = s_dst[c];
+                if (r < n && dc < n) Og[static_cast<int64_t>(dc) * n + r] = A[c * LDA + r];
+            }
+        }
+        __syncthreads();
+    }
+}
+
 }  // namespace
 
 // inv may alias a.  Work buffers come from the context's caching allocator.
 void launch_gj_invert_batch(hdgb_ctx* ctx, int n, int64_t batch, const double* a, double* inv, int* flags) {
     if (batch <= 0) return;
+    if (n <= 128 && tuning().gj_smem) {
+        // single kernel, block resident in shared memory
+        const int rt = ceil_div(n, 32);
+        const int NP = 32 * rt;
+        const size_t smem = (static_cast<size_t>(NP) * (NP + 4) + static_cast<size_t>(NP) * LDB + 2 * NB) * sizeof(double) +
+                            2 * NP * sizeof(int);
+        const int per_sm = std::max<int>(1, static_cast<int>((220 * 1024) / (smem + 1024)));
+        const int64_t cap = static_cast<int64_t>(ctx->sm_count) * per_sm;
+        const unsigned grid = static_cast<unsigned>(batch < cap ? batch : cap);
+        auto launch = [&](auto kern) {
+            static size_t configured = 0;
+            if (smem > 48 * 1024 && smem > configured) {
+                HDGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+                configured = smem;
+            }
+            kern<<<grid, 256, smem, ctx->stream>>>(n, batch, a, inv, flags, 0);
+        };
+        switch (rt) {
+            case 1: launch(gj_smem_kernel<1>); break;
+            case 2: launch(gj_smem_kernel<2>); break;
+            case 3: launch(gj_smem_kernel<3>); break;
+            default: launch(gj_smem_kernel<4>); break;
+        }
+        HDGB_LAUNCH_CHECK(ctx);
+        return;
+    }
     const int64_t nn = static_cast<int64_t>(n) * n;
     const int steps = (n + NB - 1) / NB;
     DevBuf<double> tmp(static_cast<size_t>(nn) * batch);

@@ -8,17 +8,19 @@ import paper_2512_13619_b200 as hdg
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["gj", "gj-cta", "tile", "smem"])
+@pytest.fixture(params=["gj", "gj-cta", "gj-smem", "tile", "smem"])
 def lu_kernel(request):
     """gj: blocked Gauss-Jordan with DMMA rank-16 updates (the default for n > 24; gj-cta: its panel of large
     blocks factored by a 4-warp CTA instead of one warp); tile: register-tiled Gauss-Jordan (n <= 128); smem: one
     block per CTA in shared memory / the global-memory fallback."""
     hdg.set_tuning("use_blocked_gj", 1 if request.param.startswith("gj") else 0)
     hdg.set_tuning("gj_panel_cta", 1 if request.param == "gj-cta" else 0)
+    hdg.set_tuning("gj_smem", 1 if request.param == "gj-smem" else 0)   # single kernel, block in shared memory (n <= 128)
     hdg.set_tuning("use_tile_lu", 1 if request.param == "tile" else 0)
     yield request.param
     hdg.set_tuning("use_blocked_gj", 1)
     hdg.set_tuning("gj_panel_cta", 0)
+    hdg.set_tuning("gj_smem", 0)
     hdg.set_tuning("use_tile_lu", 1)
 
 
@@ -30,6 +32,8 @@ def test_lu_invert_batch(ctx, lu_kernel, n, batch):
         pytest.skip("the fallback kernels are slow at this size")
     if lu_kernel == "gj-cta" and n <= 128:
         pytest.skip("the CTA panel kernel is for n > 128")
+    if lu_kernel == "gj-smem" and (n > 128 or n <= 24):
+        pytest.skip("the shared-memory resident variant covers 24 < n <= 128")
     rng = np.random.default_rng(n)
     a = rng.standard_normal((batch, n, n)) + 0.1 * n * np.eye(n)[None]
     a[0] = np.eye(n)[rng.permutation(n)]                       # pure permutation: pivoting (test_dense_batch.cpp:88-96)
