@@ -717,11 +717,13 @@ __global__ void __launch_bounds__(NT, (!GREC && Model::M == 1 && NT <= 256) ? 2 
     // ---- phase 2b: E and D_d.  A thread owns a TI x TJ tile of scalar-basis pairs (i, j); per point it
     // forms the i-side values once and rank-1 updates the tile.  Component columns mp are swept one
     // at a time so that the accumulators (M (1 + D) per pair) stay in registers for wide systems ----
-    if (ED && ed_dmma_on) {
+    const int dbg_skip = ed_dmma_on >> 4;  // measurement aid (hdgb_set_tuning "local_debug_skip"): 1 = E/D_d, 2 = H/G_d/F
+    ed_dmma_on &= 15;
+    if (ED && ed_dmma_on && !(dbg_skip & 1)) {
         // operand chunks live behind the point records (16-byte aligned)
         double* opbuf = opbuf_base;
         ed_dmma<M, D, GREC>(dv, in, out, e, vrec, frec, s_orient, opbuf, gv0, gv1, fp0, fp1, first);
-    } else {
+    } else if (!(dbg_skip & 1)) {
         constexpr int TI = (M == 1) ? 2 : 1, TJ = (M == 1) ? 4 : 1;
         constexpr int Q = M * (1 + D);  // per row component m: E then D_0..D_{D-1}
         const int nti = (pe + TI - 1) / TI, ntj = (pe + TJ - 1) / TJ;
@@ -819,7 +821,8 @@ __global__ void __launch_bounds__(NT, (!GREC && Model::M == 1 && NT <= 256) ? 2 
     }
     bool hgf_done = false;
     if constexpr (ED) {
-        if (ed_dmma_on == 2) {  // all face points in this launch, every output entry written exactly once
+        if (ed_dmma_on == 2 && (dbg_skip & 2)) hgf_done = true;
+        else if (ed_dmma_on == 2) {  // all face points in this launch, every output entry written exactly once
             double* opbuf = opbuf_base;
             hgf_dmma<M, D, GREC>(dv, out, e, frec, s_orient, opbuf);
             hgf_done = true;
@@ -930,7 +933,7 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
         size_t ed_bytes = 2 * ed_plan(dv.pe, M, D, NTD / 32).doubles(D) * sizeof(double) + 16;
         ed_bytes = std::max(ed_bytes, hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D) * sizeof(double) + 16);
         const bool ed = want_jac && tuning().use_dmma && ed_dmma_ok(dv.pe, M, D) && all + ed_bytes <= cap;
-        if (ed) kern_d<<<dv.ne, NTD, all + ed_bytes, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2, nullptr, 0);
+        if (ed) kern_d<<<dv.ne, NTD, all + ed_bytes, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2 | (tuning().local_debug_skip << 4), nullptr, 0);
         else kern<<<dv.ne, 256, all, ctx->stream>>>(dv, mv, in, out, want_jac ? 1 : 0, 0, dv.qe, 0, nfp, 1, 0, nullptr, 0);
         HDGB_LAUNCH_CHECK(ctx);
         return;

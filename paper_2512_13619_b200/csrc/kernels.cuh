@@ -38,6 +38,7 @@ struct Tuning {
     int64_t stream_packed_stage_bytes = 6144;  // ... bytes per TMA stage of a warp in packed mode
     int spin_sync = 1;                   // GMRES: poll an event for the per-iteration Hessenberg column instead of a blocking sync
     int fused_cgs = 0;                   // CGS2: first update and second projection in one pass over the basis (measured slower: 112 us vs 85 us at cfg2)
+    int local_debug_skip = 0;            // measurement aid: skip phases of the local kernel (1 = E/D_d, 2 = H/G_d/F); results invalid
     int local_dmma_min_pe = 20;          // local blocks on the tensor-core path from this many basis functions per element
     int local_global_records = 1;        // wide systems: point records in an L2-resident scratch, one launch, E / D_d on DMMA
     int local_dmma_chunked = 0;          // E / D_d on the tensor-core path also in point-chunked sweeps (wide systems)
