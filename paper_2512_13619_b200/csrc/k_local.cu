@@ -988,6 +988,15 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
 
 }  // namespace
 
+// The model instantiations are split over three translation units (this file compiled with
+// -DHDGB_LOCAL_PART=0|1|2, see the Makefile) so that they build in parallel.
+#ifndef HDGB_LOCAL_PART
+#define HDGB_LOCAL_PART 0
+#endif
+void launch_local_assemble_part1(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, const LocalIn& in, const LocalOut& out, bool want_jac);
+void launch_local_assemble_part2(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, const LocalIn& in, const LocalOut& out, bool want_jac);
+
+#if HDGB_LOCAL_PART == 0
 void launch_local_factors(hdgb_ctx* ctx, const DiscView& dv, double* mass, double* const bmat[3], double* const cmat[3]) {
     mass_bmat_kernel<<<dv.ne, 128, 0, ctx->stream>>>(dv, mass, bmat[0], bmat[1], bmat[2]);
     HDGB_LAUNCH_CHECK(ctx);
@@ -1009,24 +1018,41 @@ void launch_local_assemble(hdgb_ctx* ctx, const DiscView& dv, const ModelView& m
             else launch_assemble_t<ReactionModel<3>>(ctx, dv, mv, in, out, want_jac);
             break;
         case HDGB_MODEL_BURGERS:
-            if (D == 2) launch_assemble_t<BurgersModel<2>>(ctx, dv, mv, in, out, want_jac);
-            else launch_assemble_t<BurgersModel<3>>(ctx, dv, mv, in, out, want_jac);
-            break;
         case HDGB_MODEL_CONVDIFF:
-            if (D == 2) launch_assemble_t<ConvDiffModel<2>>(ctx, dv, mv, in, out, want_jac);
-            else launch_assemble_t<ConvDiffModel<3>>(ctx, dv, mv, in, out, want_jac);
+            launch_local_assemble_part1(ctx, dv, mv, in, out, want_jac);
             break;
         case HDGB_MODEL_ELASTICITY:
-            if (D == 2) launch_assemble_t<ElasticityModel<2>>(ctx, dv, mv, in, out, want_jac);
-            else launch_assemble_t<ElasticityModel<3>>(ctx, dv, mv, in, out, want_jac);
-            break;
         case HDGB_MODEL_NAVIER_STOKES:
-            if (D == 2) launch_assemble_t<NavierStokesModel<2>>(ctx, dv, mv, in, out, want_jac);
-            else launch_assemble_t<NavierStokesModel<3>>(ctx, dv, mv, in, out, want_jac);
+            launch_local_assemble_part2(ctx, dv, mv, in, out, want_jac);
             break;
         default:
             throw Failure(HDGB_ERR_UNSUPPORTED, "unknown model kind " + std::to_string(mv.kind));
     }
 }
+#elif HDGB_LOCAL_PART == 1
+void launch_local_assemble_part1(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, const LocalIn& in,
+                                 const LocalOut& out, bool want_jac) {
+    const int D = dv.D;
+    if (mv.kind == HDGB_MODEL_BURGERS) {
+        if (D == 2) launch_assemble_t<BurgersModel<2>>(ctx, dv, mv, in, out, want_jac);
+        else launch_assemble_t<BurgersModel<3>>(ctx, dv, mv, in, out, want_jac);
+    } else {
+        if (D == 2) launch_assemble_t<ConvDiffModel<2>>(ctx, dv, mv, in, out, want_jac);
+        else launch_assemble_t<ConvDiffModel<3>>(ctx, dv, mv, in, out, want_jac);
+    }
+}
+#else
+void launch_local_assemble_part2(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, const LocalIn& in,
+                                 const LocalOut& out, bool want_jac) {
+    const int D = dv.D;
+    if (mv.kind == HDGB_MODEL_ELASTICITY) {
+        if (D == 2) launch_assemble_t<ElasticityModel<2>>(ctx, dv, mv, in, out, want_jac);
+        else launch_assemble_t<ElasticityModel<3>>(ctx, dv, mv, in, out, want_jac);
+    } else {
+        if (D == 2) launch_assemble_t<NavierStokesModel<2>>(ctx, dv, mv, in, out, want_jac);
+        else launch_assemble_t<NavierStokesModel<3>>(ctx, dv, mv, in, out, want_jac);
+    }
+}
+#endif
 
 }  // namespace hdgb
