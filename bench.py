@@ -125,7 +125,15 @@ class ClockSampler(threading.Thread):
     def _run_nvml(self):
         import pynvml as nv
         nv.nvmlInit()
-        h = nv.nvmlDeviceGetHandleByIndex(self.device)
+        h = None
+        try:  # CUDA ordinal -> NVML handle through the UUID (the ordinals differ under CUDA_VISIBLE_DEVICES)
+            import torch
+            uuid = str(torch.cuda.get_device_properties(self.device).uuid)
+            h = nv.nvmlDeviceGetHandleByUUID(("GPU-" + uuid) if not uuid.startswith("GPU-") else uuid)
+        except Exception:
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+            ids = [v for v in vis.split(",") if v.strip().isdigit()]
+            h = nv.nvmlDeviceGetHandleByIndex(int(ids[self.device]) if self.device < len(ids) else self.device)
         cmax = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
         bits = {"hw_slowdown": nv.nvmlClocksThrottleReasonHwSlowdown,
                 "hw_thermal_slowdown": nv.nvmlClocksThrottleReasonHwThermalSlowdown,
