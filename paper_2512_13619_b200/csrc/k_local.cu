@@ -425,36 +425,59 @@ __device__ void hgf_dmma(const DiscView& dv, const LocalOut& out, int e, const F
                 }
                 __syncthreads();
                 const int ntile_h = nw * rt_h * ct_h;
-                for (int tile = warp; tile < ntile_h + (w0 == 0 ? ntile_f : 0); tile += nwarps) {
-                    double c0 = 0.0, c1 = 0.0;
-                    if (tile < ntile_h) {
-                        const int ww = tile / (rt_h * ct_h), rem = tile - ww * (rt_h * ct_h);
-                        const int rt = rem / ct_h, ct = rem - rt * ct_h;
-                        const double* as = Ps + rt * 8 + grp;
-                        const double* bs = Bh + (ww * pl.pep + ct * 8 + grp) * pl.ldk;
-                        for (int ks = 0; ks < ksteps; ++ks) dmma_8x8x4(c0, c1, as[(4 * ks + tig) * pl.ldp], bs[4 * ks + tig]);
-                        const int b = rt * 8 + grp, w = w0 + ww;
-                        double* dst = (w == 0 ? out.H : out.G[w - 1]) + static_cast<size_t>(e) * nfl * npe;
-                        if (b < pf) {
-                            const int j = ct * 8 + 2 * tig;
+                const int ntot = ntile_h + (w0 == 0 ? ntile_f : 0);
+                // two tiles per warp trip: their DMMA chains (qf / 4 dependent steps each) interleave
+                for (int t0 = 2 * warp; t0 < ntot; t0 += 2 * nwarps) {
+                    const double* as[2];
+                    const double* bs[2];
+                    int lds[2];
+                    double* dst[2];
+                    size_t o0[2], o1[2];
+                    bool ok0[2], ok1[2];
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int tile = t0 + u;
+                        ok0[u] = ok1[u] = false;
+                        as[u] = Ps; bs[u] = Bh; lds[u] = pl.ldp; dst[u] = out.H; o0[u] = o1[u] = 0;
+                        if (tile >= ntot) continue;
+                        if (tile < ntile_h) {
+                            const int ww = tile / (rt_h * ct_h), rem = tile - ww * (rt_h * ct_h);
+                            const int rt = rem / ct_h, ct = rem - rt * ct_h;
+                            as[u] = Ps + rt * 8 + grp;
+                            lds[u] = pl.ldp;
+                            bs[u] = Bh + (ww * pl.pep + ct * 8 + grp) * pl.ldk;
+                            const int b = rt * 8 + grp, w = w0 + ww, j = ct * 8 + 2 * tig;
+                            dst[u] = (w == 0 ? out.H : out.G[w - 1]) + static_cast<size_t>(e) * nfl * npe;
                             const size_t row = lf * mpf + m * pf + b;
-                            if (j < pe) dst[static_cast<size_t>(mp * pe + j) * nfl + row] = c0;
-                            if (j + 1 < pe) dst[static_cast<size_t>(mp * pe + j + 1) * nfl + row] = c1;
-                        }
-                    } else {
-                        const int tf = tile - ntile_h;
-                        const int rt = tf / rt_h, ct = tf - rt * rt_h;  // rt over i (pep / 8), ct over bp (pfp / 8)
-                        const double* as = Fs + rt * 8 + grp;
-                        const double* bs = Bf + (ct * 8 + grp) * pl.ldk;
-                        for (int ks = 0; ks < ksteps; ++ks) dmma_8x8x4(c0, c1, as[(4 * ks + tig) * pl.lda], bs[4 * ks + tig]);
-                        const int i = rt * 8 + grp;
-                        double* dst = out.F + static_cast<size_t>(e) * npe * nfl;
-                        if (i < pe) {
-                            const int bp = ct * 8 + 2 * tig;
+                            o0[u] = static_cast<size_t>(mp * pe + j) * nfl + row;
+                            o1[u] = static_cast<size_t>(mp * pe + j + 1) * nfl + row;
+                            ok0[u] = b < pf && j < pe;
+                            ok1[u] = b < pf && j + 1 < pe;
+                        } else {
+                            const int tf = tile - ntile_h;
+                            const int rt = tf / rt_h, ct = tf - rt * rt_h;  // rt over i (pep / 8), ct over bp (pfp / 8)
+                            as[u] = Fs + rt * 8 + grp;
+                            lds[u] = pl.lda;
+                            bs[u] = Bf + (ct * 8 + grp) * pl.ldk;
+                            const int i = rt * 8 + grp, bp = ct * 8 + 2 * tig;
+                            dst[u] = out.F + static_cast<size_t>(e) * npe * nfl;
                             const size_t row = m * pe + i;
-                            if (bp < pf) dst[static_cast<size_t>(lf * mpf + mp * pf + bp) * npe + row] = c0;
-                            if (bp + 1 < pf) dst[static_cast<size_t>(lf * mpf + mp * pf + bp + 1) * npe + row] = c1;
+                            o0[u] = static_cast<size_t>(lf * mpf + mp * pf + bp) * npe + row;
+                            o1[u] = static_cast<size_t>(lf * mpf + mp * pf + bp + 1) * npe + row;
+                            ok0[u] = i < pe && bp < pf;
+                            ok1[u] = i < pe && bp + 1 < pf;
                         }
+                    }
+                    double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+                    for (int ks = 0; ks < ksteps; ++ks) {
+#pragma unroll
+                        for (int u = 0; u < 2; ++u)
+                            dmma_8x8x4(c[u][0], c[u][1], as[u][(4 * ks + tig) * lds[u]], bs[u][4 * ks + tig]);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        if (ok0[u]) dst[u][o0[u]] = c[u][0];
+                        if (ok1[u]) dst[u][o1[u]] = c[u][1];
                     }
                 }
             }
