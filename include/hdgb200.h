@@ -4,8 +4,8 @@
  * API in namespace hdg (proj/include/hdg/{dense_batch,local_ops,face_matrix,preconditioner,gmres,
  * newton}.hpp).  Each entry point below replaces one of those functions and cites it.  Signatures
  * use only plain pointers, sizes and POD structs; there are no torch / STL types.  The C++ header
- * layer include/hdg/ (namespace hdg) re-creates the reference's own signatures on top of this ABI,
- * and INTEGRATION.md shows the binding a reference maintainer would add.
+ * layer include/hdgb200.hpp (namespace hdg::b200) re-creates the reference's own names, option structs and
+ * exception hierarchy on top of this ABI, and INTEGRATION.md shows the binding a reference maintainer would add.
  *
  * Conventions
  *  - All floating-point data are FP64.  Dense blocks are column-major and stored back to back

@@ -1,0 +1,85 @@
+// Exercises include/hdgb200.hpp (the C++ mirror of the reference's namespace-hdg API) end to end on the GPU:
+// the same calls a reference test makes (tests/test_newton.cpp, test_face_matrix.cpp, test_dense_batch.cpp),
+// with the reference's error behaviour (exception type + offending batch index).
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+#include "hdgb200.hpp"
+
+using namespace hdg::b200;
+
+static int fails = 0;
+#define EXPECT(cond)                                                        \
+    do {                                                                    \
+        if (!(cond)) { std::printf("FAILED %s:%d  %s\n", __FILE__, __LINE__, #cond); ++fails; } \
+    } while (0)
+
+int main() {
+    Context ctx(0);
+    // ---- BASELINE config 1 in miniature: 2D Poisson, quads, p = 2, block-Jacobi GMRES ----
+    Discretization disc = Discretization::structured(ctx, HDGB_QUAD, 16, 2);
+    const auto xq = disc.table_f64("elem_coords");
+    const auto xf = disc.table_f64("face_coords");
+    const double pi = 3.14159265358979323846;
+    std::vector<double> forcing(xq.size() / 2), dirichlet(xf.size() / 2);
+    for (size_t i = 0; i < forcing.size(); ++i) forcing[i] = 2 * pi * pi * std::sin(pi * xq[2 * i]) * std::sin(pi * xq[2 * i + 1]);
+    for (size_t i = 0; i < dirichlet.size(); ++i) dirichlet[i] = std::sin(pi * xf[2 * i]) * std::sin(pi * xf[2 * i + 1]);
+    Model model(disc, HDGB_MODEL_POISSON, {1.0}, &forcing, &dirichlet);
+    StateFields state(disc);
+    PrecondSpec bj;  // default BJ
+    const SolveReport rep = newton_solve(model, disc, state, NewtonConfig{}, GmresConfig{}, bj);
+    EXPECT(rep.converged);
+    EXPECT(rep.n_newton == 1);
+    EXPECT(rep.final_residual <= 1e-8);
+    EXPECT(rep.gmres_per_newton.size() == 1 && rep.gmres_per_newton[0] == rep.n_gmres_total);
+    EXPECT(rep.residual_history.size() == 2);
+    std::printf("newton_solve: newton=%d gmres=%ld residual=%.3e\n", rep.n_newton, rep.n_gmres_total, rep.final_residual);
+
+    // ---- operators one by one ----
+    StateFields s2(disc);
+    ElementOperators ops = assemble_element_operators(model, s2, disc);
+    auto [K, rhs] = assemble_global(ops, disc);
+    EXPECT(K.n_dof() == disc.n_dof() && K.nb == disc.nb() && K.block_dim == disc.mpf());
+    const auto nbr = K.neighbor();
+    bool self_ok = true;
+    for (int f = 0; f < K.nf; ++f) self_ok = self_ok && nbr[static_cast<size_t>(f) * K.nb] == f;
+    EXPECT(self_ok);
+    std::vector<double> x(static_cast<size_t>(K.n_dof())), y(x.size());
+    for (size_t i = 0; i < x.size(); ++i) { x[i] = std::sin(0.37 * i); y[i] = std::cos(0.11 * i); }
+    const auto Kx = block_matvec(K, x), Ky = block_matvec(K, y);
+    std::vector<double> z(x.size());
+    for (size_t i = 0; i < x.size(); ++i) z[i] = 2 * x[i] - 3 * y[i];
+    const auto Kz = block_matvec(K, z);
+    double lin = 0.0, scale = 0.0;
+    for (size_t i = 0; i < x.size(); ++i) { lin = std::fmax(lin, std::fabs(Kz[i] - (2 * Kx[i] - 3 * Ky[i]))); scale = std::fmax(scale, std::fabs(Kx[i])); }
+    EXPECT(lin <= 1e-12 * scale);
+    Preconditioner P = build_preconditioner(bj, K, ops, disc);
+    auto [du, stats] = gmres_solve(K, P, rhs, {}, GmresConfig{});
+    EXPECT(stats.converged && stats.iters == rep.n_gmres_total);
+    // the Newton update of a linear problem from the zero state is the solution itself
+    const auto uh = state.get("uhat");
+    double diff = 0.0;
+    for (size_t i = 0; i < uh.size(); ++i) diff = std::fmax(diff, std::fabs(uh[i] - du[i]));
+    EXPECT(diff <= 1e-12);
+    const Residuals r0 = assemble_residual(model, state, disc);
+    EXPECT(std::fabs(r0.norm - rep.final_residual) <= 1e-14);
+
+    // ---- error behaviour ----
+    bool threw = false;
+    try { block_matvec(K, std::vector<double>(3)); } catch (const DimensionMismatch&) { threw = true; }
+    EXPECT(threw);
+    const int n = 5, batch = 4;
+    std::vector<double> a(static_cast<size_t>(n) * n * batch, 0.0);
+    for (int b = 0; b < batch; ++b)
+        for (int i = 0; i < n; ++i) a[static_cast<size_t>(b) * n * n + i * n + i] = (b == 2) ? 0.0 : 2.0 + b;  // block 2 singular
+    long bad = -1;
+    try { lu_invert_batch(ctx, a, n, batch); } catch (const SingularBlock& e) { bad = e.index; }
+    EXPECT(bad == 2);  // lowest failing batch index (dense_batch.cpp:84-97)
+    for (int i = 0; i < n; ++i) a[2 * n * n + i * n + i] = 4.0;
+    const auto inv = lu_invert_batch(ctx, a, n, batch);
+    EXPECT(std::fabs(inv[0] - 0.5) <= 1e-15 && std::fabs(inv[2 * n * n] - 0.25) <= 1e-15);
+
+    std::printf(fails ? "%d check(s) failed\n" : "all checks passed\n", fails);
+    return fails ? 1 : 0;
+}
