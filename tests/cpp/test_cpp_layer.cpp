@@ -65,6 +65,41 @@ int main() {
     const Residuals r0 = assemble_residual(model, state, disc);
     EXPECT(std::fabs(r0.norm - rep.final_residual) <= 1e-14);
 
+    // ---- 3D, additive Schwarz, one backward-Euler step through TimeContext (BASELINE config 2 in miniature) ----
+    {
+        Discretization d3 = Discretization::structured(ctx, HDGB_HEX, 3, 2);
+        const auto x3 = d3.table_f64("elem_coords");
+        const auto f3 = d3.table_f64("face_coords");
+        std::vector<double> fq(x3.size() / 3), dq(f3.size() / 3);
+        for (size_t i = 0; i < fq.size(); ++i)
+            fq[i] = 3 * pi * pi * std::sin(pi * x3[3 * i]) * std::sin(pi * x3[3 * i + 1]) * std::sin(pi * x3[3 * i + 2]);
+        for (size_t i = 0; i < dq.size(); ++i) dq[i] = std::sin(pi * f3[3 * i]) * std::sin(pi * f3[3 * i + 1]) * std::sin(pi * f3[3 * i + 2]);
+        Model m3(d3, HDGB_MODEL_POISSON, {1.0}, &fq, &dq);
+        StateFields s3(d3);
+        PrecondSpec as;
+        as.kind = PrecondKind::ASM;
+        const SolveReport r3 = newton_solve(m3, d3, s3, NewtonConfig{}, GmresConfig{}, as);
+        EXPECT(r3.converged && r3.final_residual <= 1e-8 && r3.n_gmres_total > 0);
+        StateFields s4(d3);
+        const std::vector<double> u_prev(static_cast<size_t>(d3.npe()) * d3.dims().ne, 0.0);
+        TimeContext tc;
+        tc.dt = 0.1;
+        tc.u_prev = &u_prev;
+        const SolveReport r4 = newton_solve(m3, d3, s4, NewtonConfig{}, GmresConfig{}, as, tc);
+        EXPECT(r4.converged);
+        // the transient solution after one step differs from the steady one
+        const auto ua = s3.get("u"), ub = s4.get("u");
+        double dmax = 0.0;
+        for (size_t i = 0; i < ua.size(); ++i) dmax = std::fmax(dmax, std::fabs(ua[i] - ub[i]));
+        EXPECT(dmax > 1e-3);
+        bool threw_t = false;
+        TimeContext bad_tc;
+        bad_tc.dt = 0.1;  // no previous solution
+        try { assemble_element_operators(m3, s4, d3, bad_tc); } catch (const InconsistentDimensions&) { threw_t = true; }
+        EXPECT(threw_t);
+        std::printf("hex ASM: steady newton=%d gmres=%ld, transient newton=%d\n", r3.n_newton, r3.n_gmres_total, r4.n_newton);
+    }
+
     // ---- error behaviour ----
     bool threw = false;
     try { block_matvec(K, std::vector<double>(3)); } catch (const DimensionMismatch&) { threw = true; }
