@@ -3,21 +3,35 @@
 
 Workload at N = 1: BASELINE configs[1] -- 3D Poisson, structured hex mesh 28^3 (1 091 328 trace
 DOFs), p = 3, additive Schwarz preconditioned GMRES (the reference's ASM; --precond ras selects the
-restricted variant), FP64.  One "step" = one complete
-newton_solve of that problem from the zero initial state: residual assembly, quadrature assembly +
-static condensation, face-block global assembly, preconditioner build, GMRES to 1e-6, local
-recovery, line search.  Metric: trace DOFs solved per second (whole job), plus the per-iteration
-GMRES time, the block-matvec / preconditioner-apply GB/s and the Newton solve time BASELINE names.
+restricted variant), FP64.  One "step" = one complete newton_solve of that problem from its initial
+state: residual assembly, quadrature assembly + static condensation, face-block global assembly,
+preconditioner build, GMRES to 1e-6, local recovery, line search.  Metric: trace DOFs solved per
+second (whole job), plus the per-iteration GMRES time, the block-matvec / preconditioner-apply GB/s
+and the Newton solve time BASELINE names.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config 1..5] [--scaling weak|strong] [--cells n]
+
+--gpus N > 1 launches N ranks itself (re-exec under torch.distributed.run on 127.0.0.1) unless the
+process already runs under torchrun (WORLD_SIZE set; it must then equal N).  One rank per GPU, domain
+decomposition (paper_2512_13619_b200/partition.py), NCCL halo exchange + all-reduce.  With fewer GPUs
+than ranks (a 1-GPU box) the ranks share devices and the exchanges go through a host-staged
+torch.distributed (gloo) transport -- a functional test of the multi-rank path, not a scaling number;
+the line says which transport ran.
+  --config 2 (default): --scaling weak  = one n^3 slab per GPU of an n x n x (n*N) box (default for N > 1)
+                        --scaling strong = the fixed 28^3 mesh cut into N slabs
+  --config 4 | 5: BASELINE's partitioned / strong-scaling cases (fixed global mesh; tet 6x32^3
+                  elasticity ASM, hex 24^3 Navier-Stokes BJ, one backward-Euler step).
+  --config 1 | 3: the remaining BASELINE configurations on one GPU.
 
 --impl reference times the CPU implementation of the same path (the tier-B oracle port: the
-reference itself is 2D-only and cannot run this 3D configuration) on the host cores, on a bounded
-sample (a smaller hex mesh of the same degree / model / preconditioner).
+reference itself is 2D-only and cannot run the 3D configurations) on the host cores, on a bounded
+sample (a smaller mesh of the same shape / degree / model / preconditioner, sized to the time limit).
 """
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -42,6 +56,23 @@ sys.path.insert(0, str(ROOT))
 METRIC = "newton_solve_trace_dofs_per_s"
 UNIT = "DOF/s"
 
+# BASELINE.json configs (SURVEY.md section 8 size table; synthetic meshes of section 8(d))
+CONFIGS = {
+    1: dict(text="2D Poisson, structured quad {n}^2, p={k}, BJ-GMRES(50)", shape="quad", n=64, degree=2, n_comp=1,
+            case="poisson2d", precond="bj", poly=0, poly_kind="gmres", dt=None, jitter=0.0, scaling="strong", cpu_n=64),
+    2: dict(text="3D Poisson, structured hex {n}^3, p={k}, {PC}-GMRES(50)", shape="hex", n=28, degree=3, n_comp=1,
+            case="poisson", precond="asm", poly=0, poly_kind="gmres", dt=None, jitter=0.0, scaling="weak", cpu_n=20),
+    3: dict(text="2D viscous Burgers, jittered triangle mesh 2x{n}^2, p={k}, Newton-GMRES(50), {PC} + Chebyshev(10)",
+            shape="tri", n=512, degree=4, n_comp=1, case="burgers", precond="asm", poly=10, poly_kind="chebyshev",
+            dt=None, jitter=0.2, scaling="strong", cpu_n=64),
+    4: dict(text="3D linear elasticity (M=3), jittered tet mesh 6x{n}^3, p={k}, {PC}-GMRES(50)", shape="tet", n=32,
+            degree=2, n_comp=3, case="elasticity", precond="asm", poly=0, poly_kind="gmres", dt=None, jitter=0.2,
+            scaling="strong", cpu_n=12),
+    5: dict(text="3D compressible Navier-Stokes (M=5), structured hex {n}^3, p={k}, Newton-GMRES(50) {PC}, one "
+                 "backward-Euler step dt=0.01", shape="hex", n=24, degree=3, n_comp=5, case="navier_stokes",
+            precond="bj", poly=0, poly_kind="gmres", dt=0.01, jitter=0.0, scaling="strong", cpu_n=6),
+}
+
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -49,64 +80,131 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cells", dest="n", type=int, default=28, help="hex cells per direction (28 -> 1.09 M trace DOFs)")
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
+                    help="N > 1: weak = one mesh slab per GPU (config 2 only, its default), strong = fixed global mesh")
+    ap.add_argument("--cells", dest="n", type=int, default=None, help="cells per direction (config 2: 28 -> 1.09 M trace DOFs)")
     ap.add_argument("--force-dd", action="store_true", help="use the domain-decomposition path even on one rank (testing)")
-    ap.add_argument("--degree", type=int, default=3)
-    ap.add_argument("--precond", default="asm", choices=["bj", "asm", "ras"])
-    ap.add_argument("--cpu-cells", dest="cpu_n", type=int, default=12, help="hex cells per direction of the bounded CPU sample")
+    ap.add_argument("--degree", type=int, default=None)
+    ap.add_argument("--precond", default=None, choices=["bj", "asm", "ras"])
+    ap.add_argument("--cpu-cells", dest="cpu_n", type=int, default=None,
+                    help="cells per direction of the bounded CPU sample (default: sized to the time budget)")
+    ap.add_argument("--cpu-budget-s", type=float, default=240.0, help="--impl reference: wall-clock budget of the whole run")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    return ap.parse_args()
+    ap.add_argument("--transport", default="auto", choices=["auto", "nccl", "host"])
+    a = ap.parse_args()
+    cfg = dict(CONFIGS[a.config])
+    if a.n is not None:
+        cfg["n"] = a.n
+    if a.degree is not None:
+        cfg["degree"] = a.degree
+    if a.precond is not None:
+        cfg["precond"] = a.precond
+    if a.scaling is not None:
+        if a.scaling == "weak" and a.config != 2:
+            ap.error("--scaling weak exists for --config 2 only (slabs of a structured hex box)")
+        cfg["scaling"] = a.scaling
+    a.cfg = cfg
+    return a
 
 
-def workload_name(n, k, pc):
-    return f"3D Poisson, structured hex {n}^3, p={k}, {pc.upper()}-GMRES(50) tol 1e-6, Newton tol 1e-8, FP64"
+def workload_name(cfg):
+    return (cfg["text"].format(n=cfg["n"], k=cfg["degree"], PC=cfg["precond"].upper())
+            + ", GMRES tol 1e-6, Newton tol 1e-8, FP64")
+
+
+def bench_config(cfg):
+    """The `config` object of the JSON line: identical in the GPU arm and the CPU (--impl reference) arm."""
+    return {"workload": workload_name(cfg), "baseline_config": next(k for k, v in CONFIGS.items() if v["text"] == cfg["text"]),
+            "shape": cfg["shape"], "cells_per_direction": cfg["n"], "degree": cfg["degree"], "components": cfg["n_comp"],
+            "preconditioner": cfg["precond"] + (f"+{cfg['poly_kind']}({cfg['poly']})" if cfg["poly"] else "")}
 
 
 # ---- CPU arm: the oracle port on the host cores ----------------------------------------------------
-def cpu_sample(n, k, pc, threads):
-    """One Newton solve of the bounded CPU sample; returns (seconds, n_dof, report, tables-setup seconds)."""
+def cpu_sample(cfg, n, threads):
+    """One Newton solve of the bounded CPU sample (same shape / degree / model / preconditioner on an n-cell
+    mesh); returns (seconds, n_dof, report).  Only the host-side setup tables come from the product library
+    (Discretization.structured(None, ...): mesh / basis / geometry, no GPU, no kernel); all arithmetic of the
+    solve is oracle/libhdgoracle.so."""
     from oracle import port
     import paper_2512_13619_b200 as hdg
-    hd = hdg.Discretization.structured(None, "hex", n=n, degree=k)  # host-only setup tables (no GPU involved)
+    hd = hdg.Discretization.structured(None, cfg["shape"], n=n, degree=cfg["degree"], n_comp=cfg["n_comp"],
+                                       jitter=cfg["jitter"])
     port.set_threads(threads)
-    t0 = time.perf_counter()
     oc = port.OraCase(port.tables_from_disc(hd))  # includes precompute_local_factors (setup, not part of the solve)
-    t_setup = time.perf_counter() - t0
-    xq, xf = hd.quad_coords()
-    sinprod = lambda x: np.prod(np.sin(np.pi * x), axis=-1)
-    oc.set_model("poisson", [1.0], 3 * np.pi * np.pi * sinprod(xq), sinprod(xf))
+    model = hdg.make_case_model(hd, cfg["case"], **({"mu": 0.02} if cfg["case"] == "navier_stokes" else {}))
+    oc.set_model_like(model)
+    u0 = hd.interpolate_volume(model.initial_state) if model.initial_state is not None else np.zeros(hd.npe * hd.ne)
+    uh0 = hd.interpolate_trace(model.initial_state) if model.initial_state is not None else np.zeros(hd.n_dof)
+    oc.set("u", u0)
+    oc.set("uhat", uh0)
+    kw = dict(precond=cfg["precond"], poly_degree=cfg["poly"], poly_kind=cfg["poly_kind"])
+    if cfg["dt"]:
+        kw.update(dt=cfg["dt"], u_prev=u0)
     t0 = time.perf_counter()
-    rep = oc.newton(precond=pc)
+    rep = oc.newton(**kw)
     dt = time.perf_counter() - t0
-    return dt, oc.n_dof, rep, t_setup
+    return dt, oc.n_dof, rep
+
+
+def cpu_cells_ladder(cfg):
+    top = cfg["n"]
+    ladder = [m for m in (4, 6, 8, 10, 12, 14, 16, 20, 24, 28, 32, 48, 64, 96, 128, 256, 512) if m <= top]
+    return ladder or [top]
 
 
 def run_reference(a):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    cfg = a.cfg
     threads = os.cpu_count() or 1
+    n_runs = a.warmup + a.steps
+    if a.cpu_n:
+        n = a.cpu_n
+    else:
+        # size the sample to the time budget: walk up the ladder while (warmup + steps) solves are predicted to fit
+        # (cost model: time ~ DOFs * iterations, iterations ~ cells per direction for these preconditioners)
+        ladder = cpu_cells_ladder(cfg)
+        n = ladder[0]
+        t_probe, nd, rp = cpu_sample(cfg, n, threads)
+        for m in ladder[1:]:
+            scale = (m / n) ** (cfg_dim(cfg) + 1)
+            if t_probe * scale * n_runs > a.cpu_budget_s:
+                break
+            t_probe, nd, rp = cpu_sample(cfg, m, threads)
+            n = m
     times, rep, n_dof = [], None, 0
-    for i in range(a.warmup + a.steps):
-        dt, n_dof, rep, _ = cpu_sample(a.cpu_n, a.degree, a.precond, threads)
+    for i in range(n_runs):
+        dt, n_dof, rep = cpu_sample(cfg, n, threads)
         if i >= a.warmup:
             times.append(dt)
     total = sum(times)
     value = n_dof * len(times) / total
-    sample = (f"hex {a.cpu_n}^3 p={a.degree} ({n_dof} trace DOFs), {rep['n_newton']} Newton / {rep['n_gmres_total']} GMRES "
-              f"iterations per solve, {threads} threads")
+    its = max(rep["n_gmres_total"], 1)
+    sample = (f"{cfg['shape']} {n} cells per direction, p={cfg['degree']} ({n_dof} trace DOFs), {rep['n_newton']} Newton / "
+              f"{rep['n_gmres_total']} GMRES iterations per solve, {threads} threads, {total / len(times):.2f} s per solve")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
-        "warmup": a.warmup, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
+        "warmup": a.warmup, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": cfg["scaling"],
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_name(a.n, a.degree, a.precond), "bounded_sample": sample},
+        "config": bench_config(cfg),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "gmres_ms_per_iter": 1e3 * (rep["t_mv"] + rep["t_prec"] + rep["t_orth"]) / max(rep["n_gmres_total"], 1),
+        "gmres_ms_per_iter": 1e3 * (rep["t_mv"] + rep["t_prec"] + rep["t_orth"]) / its,
+        "sample_trace_dofs": n_dof, "sample_gmres_iterations": rep["n_gmres_total"],
+        "gmres_us_per_iter_per_kdof": 1e6 * (rep["t_mv"] + rep["t_prec"] + rep["t_orth"]) / its / (n_dof / 1e3),
         "note": "the unmodified reference (oracle/_ref) is 2D/quad-only; this arm is the tier-B restatement "
-                "(oracle/hdg_oracle.cpp, bit-identical to the reference on 2D quads) run on all host threads",
+                "(oracle/hdg_oracle.cpp, bit-identical to the reference on 2D quads) run on all host threads on a bounded "
+                "sample of the workload; libhdgb200.so is mapped only for its host-side mesh / basis / geometry setup tables "
+                "(no CUDA context, no kernel launch); DOF/s on the smaller sample flatters the CPU (fewer GMRES iterations per "
+                "solve): compare gmres_us_per_iter_per_kdof for a size-independent figure",
     }
     emit(line)
+
+
+def cfg_dim(cfg):
+    return 3 if cfg["shape"] in ("hex", "tet") else 2
 
 
 # ---- GPU arm ---------------------------------------------------------------------------------------
@@ -196,84 +294,137 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
-def ncu_traffic(a):
+def ncu_traffic(cfg):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the matvec kernel from the committed
     ncu --set full capture of this workload (profiles/traffic.json), or None for other sizes."""
     try:
         t = json.loads((ROOT / "profiles" / "traffic.json").read_text())
-        return t.get(f"block_matvec hex {a.n}^3 p={a.degree}")
+        return t.get(f"block_matvec {cfg['shape']} {cfg['n']}^3 p={cfg['degree']}")
     except Exception:
         return None
+
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launch_ranks(a):
+    """--gpus N > 1 outside torchrun: re-exec this script under torch.distributed.run, one rank per GPU
+    (rendezvous on 127.0.0.1: the container hostname may not resolve)."""
+    os.dup2(_REAL_STDOUT, 1)  # the ranks inherit the real stdout; rank 0 prints the one JSON line
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), str(Path(__file__).resolve())] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
+
+def build_disc(a, ctx, world, rank, dist):
+    """The discretisation of this rank: the whole mesh on one GPU, otherwise a sub-domain (owned elements
+    + one ghost layer) with the halo plan and the communicator installed on the context."""
+    import paper_2512_13619_b200 as hdg
+    from paper_2512_13619_b200 import partition as P
+    cfg = a.cfg
+    if world == 1 and not a.force_dd:
+        disc = hdg.Discretization.structured(ctx, cfg["shape"], n=cfg["n"], degree=cfg["degree"], n_comp=cfg["n_comp"],
+                                             jitter=cfg["jitter"])
+        return disc, disc.n_dof, "1 GPU", None
+    if cfg["scaling"] == "weak":
+        # every rank owns an n^3 slab of an n x n x (n*world) box
+        lo, hi = (0.0, 0.0, 0.0), (1.0, 1.0, float(world))
+        coords, ev = P.box_hex_mesh(cfg["n"], cfg["n"], cfg["n"] * world, lo, hi)
+        gm = P.global_mesh("hex", coords, ev, lo=lo, hi=hi)
+        what = f"weak scaling: n x n x (n*{world}) box in z-slabs"
+    else:
+        # fixed global mesh (exactly the single-GPU mesh) cut into contiguous element-id slabs
+        gm = P.global_mesh_from_structured(cfg["shape"], cfg["n"], jitter=cfg["jitter"])
+        what = f"strong scaling: the fixed global mesh in {world} element-id slabs"
+    lm = P.build_my_local_mesh(gm, P.slab_partition(gm.ne, world), rank, dist if world > 1 else None)
+    disc = P.make_discretization(ctx, lm, cfg["shape"], cfg["degree"], n_comp=cfg["n_comp"])
+    n_dof_global = gm.nf * disc.mpf
+    return disc, n_dof_global, what, lm
 
 
 def run_ours(a):
     import torch
     import torch.distributed as dist
     import paper_2512_13619_b200 as hdg
+    from paper_2512_13619_b200 import partition as P
 
+    cfg = a.cfg
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    if world != a.gpus:
+        raise SystemExit(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}: launch with "
+                         f"`python -m torch.distributed.run --nproc-per-node {a.gpus} bench.py --gpus {a.gpus}` "
+                         f"(or without torchrun: bench.py starts the ranks itself)")
+    n_dev = torch.cuda.device_count()
+    if n_dev < 1:
+        raise SystemExit("bench.py: no CUDA device (this implementation has no CPU fallback; --impl reference times the CPU path)")
+    device = local % n_dev
+    oversubscribed = world > n_dev
+    transport = a.transport
+    if transport == "auto":
+        transport = "host" if oversubscribed else "nccl"
+    if transport == "nccl" and oversubscribed:
+        raise SystemExit(f"bench.py: {world} ranks on {n_dev} GPU(s): NCCL needs one GPU per rank (use --transport host)")
+    torch.cuda.set_device(device)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if transport == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+        else:
+            dist.init_process_group("gloo")
 
-    ctx = hdg.Context(local)
+    ctx = hdg.Context(device)
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)  # so torch.cuda.Event sees the launching stream
 
-    if world == 1 and not a.force_dd:
-        disc = hdg.Discretization.structured(ctx, "hex", n=a.n, degree=a.degree)
-        n_dof_global = disc.n_dof
-    else:
-        # weak scaling: every rank owns an n^3 slab of an n x n x (n*world) box, partitioned by domain
-        # decomposition (one ghost layer, halo exchange + all-reduce over NCCL)
-        from paper_2512_13619_b200 import partition as P
-        lo, hi = (0.0, 0.0, 0.0), (1.0, 1.0, float(world))
-        coords, ev = P.box_hex_mesh(a.n, a.n, a.n * world, lo, hi)
-        gm = P.global_mesh("hex", coords, ev, lo=lo, hi=hi)
-        lm = P.build_my_local_mesh(gm, P.slab_partition(gm.ne, world), rank, dist if world > 1 else None)
-        disc = P.make_discretization(ctx, lm, "hex", a.degree)
-        P.install_nccl_comm(ctx, lm, dist if world > 1 else None)
-        n_dof_global = gm.nf * disc.mpf
-        del gm, coords, ev
-    xq, xf = disc.quad_coords()
-    pi = np.pi
-    sinprod = lambda x: np.prod(np.sin(pi * x), axis=-1)
+    disc, n_dof_global, parallelism, lm = build_disc(a, ctx, world, rank, dist)
+    if lm is not None:
+        if transport == "nccl":
+            P.install_nccl_comm(ctx, lm, dist if world > 1 else None)
+        else:
+            P.install_host_comm(ctx, lm, dist) if world > 1 else P.install_nccl_comm(ctx, lm, None)
+    kw = {"mu": 0.02} if cfg["case"] == "navier_stokes" else {}
+    model = hdg.make_case_model(disc, cfg["case"], **kw)
+    exact = model.exact_solution
     # host-side model data and initial state in pinned memory: the step's inputs
-    forcing_h = torch.from_numpy(np.ascontiguousarray(3 * pi * pi * sinprod(xq))).pin_memory()
-    dirichlet_h = torch.from_numpy(np.ascontiguousarray(sinprod(xf))).pin_memory()
-    u0_h = torch.zeros(disc.npe * disc.ne, dtype=torch.float64).pin_memory()
-    uh0_h = torch.zeros(disc.n_dof, dtype=torch.float64).pin_memory()
-    u_out = torch.empty_like(u0_h).pin_memory()
-    uh_out = torch.empty_like(uh0_h).pin_memory()
-    h2d = 8 * (forcing_h.numel() + dirichlet_h.numel() + u0_h.numel() + uh0_h.numel())
+    pin = lambda arr: torch.from_numpy(np.array(arr, dtype=np.float64).ravel()).pin_memory()
+    forcing_h = pin(model.forcing_q) if model.forcing_q is not None else None
+    dirichlet_h = pin(model.dirichlet_q) if model.dirichlet_q is not None else None
+    if model.initial_state is not None:
+        u0_h, uh0_h = pin(disc.interpolate_volume(model.initial_state)), pin(disc.interpolate_trace(model.initial_state))
+    else:
+        u0_h, uh0_h = pin(np.zeros(disc.npe * disc.ne)), pin(np.zeros(disc.n_dof))
+    u_out, uh_out = torch.empty_like(u0_h).pin_memory(), torch.empty_like(uh0_h).pin_memory()
+    h2d = 8 * sum(t.numel() for t in (forcing_h, dirichlet_h, u0_h, uh0_h) if t is not None)
+    if cfg["dt"]:
+        h2d += 8 * u0_h.numel()  # u_prev
     d2h = 8 * (u_out.numel() + uh_out.numel())
-    pspec = hdg.PrecondSpec(a.precond)
+    pspec = hdg.PrecondSpec(cfg["precond"], poly_degree=cfg["poly"], poly_kind=cfg["poly_kind"])
     gcfg, ncfg = hdg.GmresConfig(), hdg.NewtonConfig()
 
-    def make_model(fq, dq):
-        return hdg.Model(disc, "poisson", [1.0], forcing=lambda x: fq, dirichlet=lambda x: dq, exact=sinprod)
-
-    # device-resident arm: model tables + state already in HBM
-    model = make_model(forcing_h.numpy(), dirichlet_h.numpy())
+    # device-resident arm: model tables + state (+ previous time level) already in HBM
     state = hdg.State(disc)
-    zeros_u = torch.zeros(disc.npe * disc.ne, dtype=torch.float64, device="cuda")
-    zeros_uh = torch.zeros(disc.n_dof, dtype=torch.float64, device="cuda")
+    u0_d, uh0_d = u0_h.cuda(), uh0_h.cuda()
+    tkw_res = dict(dt=cfg["dt"], u_prev=u0_d) if cfg["dt"] else {}
     reports = []
 
     def step_resident():
-        state.set("u", zeros_u)
-        state.set("uhat", zeros_uh)
-        reports.append(hdg.newton_solve(disc, model, state, ncfg, gcfg, pspec))
+        state.set("u", u0_d)
+        state.set("uhat", uh0_d)
+        reports.append(hdg.newton_solve(disc, model, state, ncfg, gcfg, pspec, **tkw_res))
 
     def step_e2e():
         # the public-API call a user makes with HOST arrays: model data + initial state in, solution out
-        m = make_model(forcing_h.numpy(), dirichlet_h.numpy())
+        m = hdg.Model(disc, model.kind, model.params, forcing_q=None if forcing_h is None else forcing_h.numpy(),
+                      dirichlet_q=None if dirichlet_h is None else dirichlet_h.numpy())
         s = hdg.State(disc)
         s.set("u", u0_h.numpy())
         s.set("uhat", uh0_h.numpy())
-        rep = hdg.newton_solve(disc, m, s, ncfg, gcfg, pspec)
+        tkw = dict(dt=cfg["dt"], u_prev=u0_h.numpy()) if cfg["dt"] else {}
+        rep = hdg.newton_solve(disc, m, s, ncfg, gcfg, pspec, **tkw)
         ctx.copy(u_out.numpy(), s.ptr("u"), u_out.numel())
         ctx.copy(uh_out.numpy(), s.ptr("uhat"), uh_out.numel())
         return rep
@@ -294,17 +445,17 @@ def run_ours(a):
             fn()
             if os.environ.get("BENCH_DEBUG"):
                 torch.cuda.synchronize()
-                print(f"[bench debug] step {1e3 * (time.perf_counter() - t_dbg):.1f} ms pool {hdg.hdg.pool_stats()}", file=sys.stderr)
+                print(f"[bench debug] rank {rank} step {1e3 * (time.perf_counter() - t_dbg):.1f} ms pool {hdg.hdg.pool_stats()}", file=sys.stderr)
         e1.record(stream)
         barrier()
-        ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda" if transport == "nccl" or world == 1 else "cpu")
         if world > 1:
             dist.all_reduce(ms, op=dist.ReduceOp.MAX)
         return float(ms.item()) * 1e-3
 
     for _ in range(a.warmup):
         step_resident()
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(device)
     sampler.start()
     reports.clear()
     t_res = timed(step_resident, a.steps, count_launches=True)
@@ -314,11 +465,13 @@ def run_ours(a):
     t_e2e = timed(step_e2e, a.steps)
     clocks = sampler.finish()
 
-    # ---- dominant-kernel roofline: the fused gather + block GEMV (team_gemv) of block_matvec --------
+    # ---- dominant-kernel roofline: the fused gather + block GEMV of block_matvec --------------------
     mpf, nb, nf, ne, nfl, n_dof = disc.mpf, disc.nb, getattr(disc, 'nf_owned', disc.nf), disc.ne, disc.nfl, disc.n_dof
-    ops = hdg.assemble_element_operators(disc, model, state)
+    state.set("u", u0_d)
+    state.set("uhat", uh0_d)
+    ops = hdg.assemble_element_operators(disc, model, state, **tkw_res)
     K, rhs = hdg.assemble_global(disc, ops)
-    P = hdg.build_preconditioner(pspec, K, ops, disc)
+    Pc = hdg.build_preconditioner(hdg.PrecondSpec(cfg["precond"]), K, ops, disc)
     x = torch.randn(n_dof, dtype=torch.float64, device="cuda")
     y = torch.empty_like(x)
 
@@ -326,7 +479,7 @@ def run_ours(a):
         for _ in range(3):
             fn()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
+        barrier()
         e0.record(stream)
         for _ in range(reps):
             fn()
@@ -337,72 +490,89 @@ def run_ours(a):
     # FP64 pipe utilisation of static condensation (north star): one assemble_element_operators call =
     # quadrature assembly of the local blocks + q-elimination + E-bar^-1 + Schur complement, algorithmic flops of
     # SURVEY.md 8(d) against the DMMA peak measured with scripts/micro/fp64_peak.cu on this pool's B200s
-    D_, pe_, npe_, qe_, nfp_ = disc.dim, disc.pe, disc.npe, disc.qe, disc.n_lfe * disc.qf
+    D_, npe_, qe_, nfp_ = disc.dim, disc.npe, disc.qe, disc.n_lfe * disc.qf
     fl_cond = D_ * (2 * npe_ ** 3 + 4 * npe_ ** 2 * nfl + 2 * npe_ * nfl ** 2) + 2 * npe_ ** 3 + 2 * npe_ ** 2 * nfl + 2 * npe_ * nfl ** 2
     fl_local = 2 * (1 + D_) * npe_ * npe_ * (qe_ + nfp_) + 2 * (1 + D_) * nfl * npe_ * disc.qf + 2 * npe_ * nfl * disc.qf
-    t_cond = kernel_time(lambda: hdg.assemble_element_operators(disc, model, state), reps=5)
-    t_mv = kernel_time(lambda: hdg.block_matvec(K, x, y))
-    t_pc = kernel_time(lambda: P.apply_base(x, y))
+    big = 8 * nf * mpf * mpf * nb > 400e6
+    t_cond = kernel_time(lambda: hdg.assemble_element_operators(disc, model, state, **tkw_res), reps=5 if not big or cfg["n_comp"] < 5 else 2)
+    t_mv = kernel_time(lambda: hdg.block_matvec(K, x, y), reps=30 if big else 200)
+    t_pc = kernel_time(lambda: Pc.apply_base(x, y), reps=30 if big else 200)
     bytes_mv = 8 * nf * mpf * (mpf * nb + 2) + 8 * nf * nb          # K once + x + y + int64 neighbour table
-    bytes_pc = (8 * ne * nfl * nfl + 8 * (2 * ne * nfl + 2 * nf * mpf)) if a.precond in ("asm", "ras") \
+    bytes_pc = (8 * ne * nfl * nfl + 8 * (2 * ne * nfl + 2 * nf * mpf)) if cfg["precond"] in ("asm", "ras") \
         else 8 * nf * mpf * (mpf + 2)
+    del Pc, K, rhs, ops
     # in-solve averages from one instrumented solve (CUDA events around every phase; adds syncs, so it
     # is NOT part of the timed steps above)
     ctx.enable_phase_timing(True)
-    state.set("u", zeros_u)
-    state.set("uhat", zeros_uh)
-    rep_t = hdg.newton_solve(disc, model, state, ncfg, gcfg, pspec)
+    state.set("u", u0_d)
+    state.set("uhat", uh0_d)
+    rep_t = hdg.newton_solve(disc, model, state, ncfg, gcfg, pspec, **tkw_res)
     ctx.enable_phase_timing(False)
     n_it = max(rep_t.n_gmres_total, 1)
-    n_mv_calls = rep_t.n_gmres_total + 2 * rep_t.n_newton + sum(1 for _ in rep_t.gmres_per_newton)  # + residual evaluations
+    n_mv_calls = rep_t.n_gmres_total + rep_t.n_inner_prec_ops + 2 * rep_t.n_newton + len(rep_t.gmres_per_newton)  # + residual evaluations
     peak, peak_src = peaks()
     achieved = bytes_mv / t_mv / 1e9
-    err = disc.l2_error(state.u, sinprod)
+    err = disc.l2_error(state.u, exact) if (exact is not None and lm is None) else None
+    gmres_ms_per_iter = 1e3 * (rep_t.t_mv + rep_t.t_prec + rep_t.t_orth) / n_it
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": n_dof_global * a.steps / t_res, "unit": UNIT, "n_gpus": world, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": 1e3 * t_res / a.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": a.warmup, "ms_per_step": 1e3 * t_res / a.steps, "higher_is_better": True,
+            "scaling": cfg["scaling"] if world > 1 or a.force_dd else CONFIGS[a.config]["scaling"],
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name(a.n, a.degree, a.precond), "trace_dofs_per_gpu": n_dof,
-                       "elements_per_gpu": ne, "faces_per_gpu": nf,
-                       "parallelism": "1 GPU" if world == 1 else
-                       f"domain decomposition over {world} GPUs: n x n x (n*{world}) box in z-slabs, one ghost layer, "
-                       f"NCCL halo exchange per operator application + all-reduce per Gram-Schmidt pass",
-                       "trace_dofs_global": n_dof_global,
-                       "l2_policy": "inputs larger than L2 (K = %.2f GB, ASM blocks = %.2f GB vs 126 MB L2)" %
-                                    (8e-9 * nf * mpf * mpf * nb, 8e-9 * ne * nfl * nfl)},
+            "config": bench_config(cfg),
+            "decomposition": {"parallelism": parallelism if world == 1 else
+                              f"domain decomposition over {world} ranks ({parallelism}), one ghost layer, halo exchange per "
+                              f"operator application + 2 all-reduces per Arnoldi step",
+                              "transport": "none (1 GPU)" if lm is None else
+                              ("NCCL (ncclSend/ncclRecv + ncclAllReduce)" if transport == "nccl" else
+                               f"host-staged torch.distributed gloo: {world} ranks share {n_dev} GPU(s) -- functional run of the "
+                               f"multi-rank path, NOT a scaling measurement"),
+                              "trace_dofs_rank0": n_dof, "elements_rank0": ne, "owned_faces_rank0": nf,
+                              "trace_dofs_global": n_dof_global},
+            "l2_policy": "inputs larger than L2 (K = %.2f GB, preconditioner blocks = %.2f GB vs 126 MB L2)" %
+                         (8e-9 * nf * mpf * mpf * nb, bytes_pc * 1e-9) if big else
+                         "operator fits L2 (K = %.1f MB): kernel timings are L2-resident, launch-latency bound" % (8e-6 * nf * mpf * mpf * nb),
             "e2e": {"value": n_dof_global * a.steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": 1e3 * t_e2e / a.steps},
             "gpu_launches": int(launches),
             "clocks": clocks,
-            "roofline": {"kernel": "stream_gemv_kernel<2,1> as block_matvec (fused neighbour gather + block-row GEMV, bulk-TMA ring)",
+            "roofline": {"kernel": "stream_gemv_kernel as block_matvec (fused neighbour gather + block-row GEMV, bulk-TMA ring)",
                          "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "peak_source": peak_src, "frac_of_8TBs": achieved / 8000.0,
-                         "algorithmic_bytes_per_launch": bytes_mv, "avg_launch_us": 1e6 * t_mv, "traffic": ncu_traffic(a),
-                         "in_solve_avg_launch_us": 1e6 * rep_t.t_mv / max(n_mv_calls, 1)},
-            "precond_apply": {"kind": a.precond, "GBps": bytes_pc / t_pc / 1e9, "frac": bytes_pc / t_pc / 1e9 / peak,
+                         "algorithmic_bytes_per_launch": bytes_mv, "avg_launch_us": 1e6 * t_mv, "traffic": ncu_traffic(cfg),
+                         "in_solve_avg_launch_us": 1e6 * rep_t.t_mv / max(n_mv_calls, 1) if not cfg["poly"] else None},
+            "precond_apply": {"kind": cfg["precond"], "GBps": bytes_pc / t_pc / 1e9, "frac": bytes_pc / t_pc / 1e9 / peak,
                               "avg_us": 1e6 * t_pc, "algorithmic_bytes": bytes_pc},
             "condensation": {"what": "assemble_element_operators: local blocks (DMMA) + fused q-elimination + blocked Gauss-Jordan E-bar^-1 + Schur complement",
                              "ms": 1e3 * t_cond, "flops_per_element": fl_cond + fl_local, "achieved": (fl_cond + fl_local) * ne / t_cond / 1e12,
                              "peak": 37.2, "unit": "TFLOP/s", "frac": (fl_cond + fl_local) * ne / t_cond / 1e12 / 37.2,
                              "peak_source": "DMMA m8n8k4 peak measured with scripts/micro/fp64_peak.cu (DFMA pipe: 34.0)"},
             "newton_solve_s": t_res / a.steps, "n_newton": rep.n_newton, "n_gmres_total": rep.n_gmres_total,
-            "gmres_ms_per_iter": 1e3 * (rep_t.t_mv + rep_t.t_prec + rep_t.t_orth) / n_it,
+            "n_inner_prec_ops": rep.n_inner_prec_ops,
+            "gmres_ms_per_iter": gmres_ms_per_iter,
+            "gmres_us_per_iter_per_kdof": 1e3 * gmres_ms_per_iter / (n_dof_global / 1e3),
             "phase_s": {"t_ass": rep_t.t_ass, "t_mv": rep_t.t_mv, "t_prec": rep_t.t_prec, "t_orth": rep_t.t_orth,
                         "t_total": rep_t.t_total},
             "final_residual": rep.final_residual, "l2_error_vs_exact": err,
         }
         if world == 1 and not a.no_cpu_baseline:
             threads = os.cpu_count() or 1
-            dt, nd, rc, _ = cpu_sample(a.cpu_n, a.degree, a.precond, threads)
+            cn = a.cpu_n or cfg["cpu_n"]
+            dt, nd, rc = cpu_sample(cfg, cn, threads)
+            cpu_it = 1e3 * (rc["t_mv"] + rc["t_prec"] + rc["t_orth"]) / max(rc["n_gmres_total"], 1)
+            cpu_norm = 1e3 * cpu_it / (nd / 1e3)
             line["cpu_baseline"] = {
                 "value": nd / dt, "unit": UNIT, "cores": threads, "kind": "port",
-                "sample": f"one Newton solve of hex {a.cpu_n}^3 p={a.degree} ({nd} trace DOFs, {rc['n_gmres_total']} GMRES "
-                          f"iterations), tier-B oracle port, {dt:.1f} s",
-                "gmres_ms_per_iter": 1e3 * (rc["t_mv"] + rc["t_prec"] + rc["t_orth"]) / max(rc["n_gmres_total"], 1)}
+                "sample": f"one Newton solve of {cfg['shape']} {cn} cells per direction, p={cfg['degree']} ({nd} trace DOFs, "
+                          f"{rc['n_newton']} Newton / {rc['n_gmres_total']} GMRES iterations; the GPU workload: {n_dof_global} DOFs, "
+                          f"{rep.n_newton} / {rep.n_gmres_total}), tier-B oracle port, {dt:.1f} s",
+                "gmres_ms_per_iter": cpu_it, "gmres_us_per_iter_per_kdof": cpu_norm,
+                "per_iter_per_dof_ratio": cpu_norm / line["gmres_us_per_iter_per_kdof"]}
         emit(line)
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
 
 
@@ -410,5 +580,7 @@ if __name__ == "__main__":
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        launch_ranks(args)
     else:
         run_ours(args)

@@ -9,7 +9,13 @@
 //   assemble_global      face_matrix.cpp:11-61     (n_lfe generalised from the hard-coded 4)
 //   block_matvec         face_matrix.cpp:83-107
 //   build/apply BJ, ASM  preconditioner.cpp:30-105
+//   compute_harmonic_ritz / leja_order   preconditioner.cpp:119-244 (the small dense solve and the
+//                        eigenvalues go through oracle/eigen_shim, the same stand-in the compiled
+//                        reference uses here: Eigen 3 is absent from this image)
 //   apply_poly           preconditioner.cpp:246-283
+//   Chebyshev nodes      NOT in the reference: the spec is DESIGN.md section 6 --
+//                        roots of T_P on [lo, hi] = range of the real parts of the harmonic Ritz values
+//                        (lo <= 0 -> hi / 30), Leja-ordered, applied by apply_poly's recurrence
 //   orthogonalize/GMRES  gmres.cpp:28-228
 //   newton_solve         newton.cpp:54-154
 //   lu_invert / gemm / gemv  dense_batch.cpp:19-160
@@ -24,12 +30,17 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <complex>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <functional>
+#include <random>
 #include <string>
 #include <thread>
 #include <vector>
+
+#include <Eigen/Dense>  // oracle/eigen_shim (stand-in, see its header)
 
 namespace {
 
@@ -874,6 +885,146 @@ struct Case {
         z = std::move(w);
     }
 
+    // leja_order (preconditioner.cpp:207-244)
+    static std::vector<std::complex<double>> leja_order(const std::vector<std::complex<double>>& theta) {
+        using C = std::complex<double>;
+        std::vector<C> cands;
+        for (const auto& t : theta)
+            if (t.imag() >= 0.0) cands.push_back(t);
+        std::vector<C> out;
+        std::vector<bool> used(cands.size(), false);
+        const auto better = [](const C& a, double ma, const C& b, double mb) {
+            if (ma != mb) return ma > mb;
+            if (a.real() != b.real()) return a.real() > b.real();
+            return a.imag() > b.imag();
+        };
+        for (size_t step = 0; step < cands.size(); ++step) {
+            int best = -1;
+            double best_metric = 0.0;
+            for (size_t c = 0; c < cands.size(); ++c) {
+                if (used[c]) continue;
+                double metric;
+                if (out.empty()) {
+                    metric = std::abs(cands[c]);
+                } else {
+                    metric = 0.0;
+                    for (const auto& chosen : out) metric += std::log(std::abs(cands[c] - chosen));
+                }
+                if (best < 0 || better(cands[c], metric, cands[best], best_metric)) {
+                    best = static_cast<int>(c);
+                    best_metric = metric;
+                }
+            }
+            used[best] = true;
+            out.push_back(cands[best]);
+            if (cands[best].imag() > 0.0) out.push_back(std::conj(cands[best]));
+        }
+        return out;
+    }
+
+    // compute_harmonic_ritz (preconditioner.cpp:119-205) on op = v -> base(K v)
+    int harmonic_ritz(int degree, uint64_t seed, std::vector<std::complex<double>>& out) {
+        const size_t n = static_cast<size_t>(mpf) * nf;
+        if (degree < 1) { err = "dimension mismatch: polynomial degree must be >= 1"; return 8; }
+        if (static_cast<size_t>(degree) > n) { err = "dimension mismatch: polynomial degree exceeds the operator dimension"; return 8; }
+        std::mt19937_64 rng(seed);
+        Vec v0(n);
+        for (double& x : v0) x = 2.0 * (static_cast<double>(rng() >> 11) * 0x1p-53) - 1.0;
+        const double nv = norm2(v0);
+        for (double& x : v0) x /= nv;
+        std::vector<Vec> basis;
+        basis.push_back(std::move(v0));
+        const int pmax = degree;
+        Vec hess(static_cast<size_t>(pmax + 1) * pmax, 0.0);
+        auto h = [&](int i, int j) -> double& { return hess[static_cast<size_t>(j) * (pmax + 1) + i]; };
+        int p_eff = 0;
+        double scale = 1.0;
+        Vec w(n), kv(n);
+        for (int j = 0; j < pmax; ++j) {
+            matvec(basis[j], kv);
+            apply_base(kv, w);
+            if (j == 0) scale = std::max(1.0, norm2(w));
+            for (int i = 0; i <= j; ++i) {
+                const double hij = dot(basis[i], w);
+                h(i, j) = hij;
+                for (size_t t = 0; t < n; ++t) w[t] -= hij * basis[i][t];
+            }
+            const double hn = norm2(w);
+            h(j + 1, j) = hn;
+            p_eff = j + 1;
+            if (!std::isfinite(hn)) { err = "NaN detected in harmonic Ritz Arnoldi"; return 6; }
+            if (hn < 1e-14 * scale) break;
+            if (j + 1 < pmax) {
+                Vec vn(n);
+                for (size_t t = 0; t < n; ++t) vn[t] = w[t] / hn;
+                basis.push_back(std::move(vn));
+            }
+        }
+        const int p = p_eff;
+        Eigen::MatrixXd hs(p, p);
+        for (int j = 0; j < p; ++j)
+            for (int i = 0; i < p; ++i) hs(i, j) = h(i, j);
+        const double hp1 = (p < pmax) ? 0.0 : h(p, p - 1);
+        if (hp1 != 0.0) {
+            Eigen::VectorXd ep = Eigen::VectorXd::Zero(p);
+            ep(p - 1) = 1.0;
+            Eigen::FullPivLU<Eigen::MatrixXd> lu(hs.transpose());
+            if (lu.isInvertible()) hs.col(p - 1) += hp1 * hp1 * lu.solve(ep);
+        }
+        Eigen::EigenSolver<Eigen::MatrixXd> es(hs, false);
+        std::vector<std::complex<double>> vals;
+        double max_abs = 0.0;
+        for (int i = 0; i < p; ++i) {
+            std::complex<double> t(es.eigenvalues()(i).real(), es.eigenvalues()(i).imag());
+            if (std::abs(t.imag()) < 1e-12 * std::abs(t)) t = {t.real(), 0.0};
+            vals.push_back(t);
+            max_abs = std::max(max_abs, std::abs(t));
+        }
+        std::vector<std::complex<double>> kept;
+        for (const auto& t : vals) {
+            if (std::abs(t) < 1e-12 * max_abs) continue;
+            if (t.imag() < 0.0) continue;
+            kept.push_back(t);
+            if (t.imag() > 0.0) kept.emplace_back(t.real(), -t.imag());
+        }
+        out = leja_order(kept);
+        return 0;
+    }
+
+    // Chebyshev variant (spec: DESIGN.md section 6; not in the reference): the P roots of T_P mapped to
+    // [lo, hi] = range of Re(theta) over the harmonic Ritz estimates, with lo <= 0 replaced by hi / 30 and a
+    // degenerate interval widened by 1e-8 relative; Leja-ordered; applied by apply_poly's recurrence.
+    static std::vector<std::complex<double>> chebyshev_nodes(const std::vector<std::complex<double>>& th, int degree) {
+        double lo = INFINITY, hi = -INFINITY;
+        for (const auto& t : th) {
+            lo = std::min(lo, t.real());
+            hi = std::max(hi, t.real());
+        }
+        if (!(lo > 0.0)) lo = hi / 30.0;
+        if (hi <= lo) hi = lo * (1.0 + 1e-8);
+        const double kPi = 3.14159265358979323846;
+        std::vector<std::complex<double>> nodes;
+        for (int j = 0; j < degree; ++j) {
+            const double x = std::cos(kPi * (2.0 * j + 1.0) / (2.0 * degree));
+            nodes.emplace_back(0.5 * (hi + lo) + 0.5 * (hi - lo) * x, 0.0);
+        }
+        return leja_order(nodes);
+    }
+
+    // the polynomial part of build_preconditioner (newton.cpp:38-50); poly_kind 0 = GMRES polynomial, 1 = Chebyshev
+    int build_poly(int degree, int poly_kind, uint64_t seed) {
+        ritz.clear();
+        if (degree <= 0) return 0;
+        const size_t n = static_cast<size_t>(mpf) * nf;
+        const int deg = static_cast<int>(std::min<size_t>(degree, n));
+        std::vector<std::complex<double>> th;
+        const int rc = harmonic_ritz(deg, seed, th);
+        if (rc) return rc;
+        if (poly_kind == 1 && !th.empty()) th = chebyshev_nodes(th, deg);
+        for (const auto& t : th) { ritz.push_back(t.real()); ritz.push_back(t.imag()); }
+        return 0;
+    }
+
     // orthogonalize (gmres.cpp:28-59)
     static Vec orthogonalize(const std::vector<Vec>& basis, Vec& w, bool mgs) {
         const size_t j = basis.size();
@@ -1196,6 +1347,11 @@ void ora_matvec(void* h, const double* x, double* y) {
 }
 
 int ora_build_precond(void* h, int kind) { return static_cast<Case*>(h)->build_precond(kind); }
+// polynomial wrapper on top of the base built by ora_build_precond: harmonic Ritz values of base(K .) (poly_kind 0)
+// or the Chebyshev nodes derived from them (poly_kind 1), left in "ritz"
+int ora_build_poly(void* h, int degree, int poly_kind, uint64_t seed) {
+    return static_cast<Case*>(h)->build_poly(degree, poly_kind, seed);
+}
 
 void ora_apply_base(void* h, const double* y, double* z) {
     Case* c = static_cast<Case*>(h);
@@ -1245,11 +1401,12 @@ int ora_gmres(void* h, const double* rhs, const double* x0, int restart, double 
     return 0;
 }
 
-// newton_solve (newton.cpp:54-154) without the polynomial wrapper's Ritz extraction (ritz values,
-// if any, must have been set with ora_set("ritz")).
+// newton_solve (newton.cpp:54-154).  poly_degree > 0: the polynomial wrapper is rebuilt every Newton step
+// (build_preconditioner, newton.cpp:30-52); poly_degree == 0 keeps whatever ritz values were set with
+// ora_set("ritz") (fixed interpolation nodes, used by the apply_poly parity tests); poly_degree < 0: none.
 // report: n_newton, n_gmres_total, n_inner, final_residual, converged, t_ass, t_mv, t_prec, t_orth, t_total
 int ora_newton(void* h, double newton_tol, int max_newton, double min_alpha, int restart, double gmres_tol,
-               int gmres_max_iters, int mgs, int pc_kind, double* report) {
+               int gmres_max_iters, int mgs, int pc_kind, int poly_degree, int poly_kind, uint64_t seed, double* report) {
     Case* c = static_cast<Case*>(h);
     const auto t_start = Clock::now();
     c->residual_history.clear();
@@ -1274,6 +1431,10 @@ int ora_newton(void* h, double newton_tol, int max_newton, double min_alpha, int
         rc = c->build_precond(pc_kind);
         c->ritz = keep_ritz;
         if (rc) return rc;
+        if (poly_degree > 0) {
+            rc = c->build_poly(poly_degree, poly_kind, seed);
+            if (rc) return rc;
+        }
         report[5] += since(t0);
         Vec duhat(n, 0.0);
         const Stats st = c->gmres(c->rhs, duhat, restart, gmres_tol, gmres_max_iters, mgs != 0);

@@ -20,6 +20,7 @@ _lib = None
 
 MODELS = {"poisson": 0, "burgers": 1, "convdiff": 2, "elasticity": 3, "reaction": 4, "navier_stokes": 5}
 PRECOND = {"none": 0, "identity": 0, "bj": 1, "asm": 2, "ras": 3}
+POLY = {"gmres": 0, "chebyshev": 1}
 
 
 class OracleError(RuntimeError):
@@ -67,7 +68,8 @@ def lib():
         L.ora_recover_local.argtypes = [C.c_void_p, _dp, _dp]
         L.ora_gmres.argtypes = [C.c_void_p, _dp, _dp, C.c_int, C.c_double, C.c_int, C.c_int, _dp, _dp]
         L.ora_newton.argtypes = [C.c_void_p, C.c_double, C.c_int, C.c_double, C.c_int, C.c_double, C.c_int, C.c_int,
-                                 C.c_int, _dp]
+                                 C.c_int, C.c_int, C.c_int, C.c_uint64, _dp]
+        L.ora_build_poly.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_uint64]
         L.ora_set_threads.argtypes = [C.c_int]
         L.ora_lu_invert_batch.argtypes = [C.c_int, C.c_int, _dp, _dp, C.POINTER(C.c_long)]
         _lib = L
@@ -224,8 +226,16 @@ class OraCase:
         lib().ora_matvec(self._h, _p(x), _p(y))
         return y
 
-    def build_precond(self, kind="bj"):
+    def build_precond(self, kind="bj", poly_degree=0, poly_kind="gmres", seed=12345):
+        """build_bj / build_asm (+ RAS) and, for poly_degree > 0, the harmonic-Ritz (or Chebyshev) nodes."""
         self._check(lib().ora_build_precond(self._h, PRECOND[kind]))
+        if poly_degree > 0:
+            self._check(lib().ora_build_poly(self._h, poly_degree, POLY[poly_kind], seed))
+
+    @property
+    def ritz(self):
+        r = self.get("ritz")
+        return r[0::2] + 1j * r[1::2]
 
     def set_ritz(self, theta):
         th = np.asarray(theta, dtype=np.complex128)
@@ -266,10 +276,13 @@ class OraCase:
                        t_mv=st[4], t_prec=st[5], t_orth=st[6])
 
     def newton(self, newton_tol=1e-8, max_newton=50, min_alpha=1.0 / 1024.0, restart=50, gmres_tol=1e-6,
-               gmres_max_iters=1000, mgs=False, precond="bj"):
+               gmres_max_iters=1000, mgs=False, precond="bj", poly_degree=0, poly_kind="gmres", seed=12345,
+               dt=None, u_prev=None):
+        if dt is not None:
+            self.set_dt(dt, u_prev)
         rep = np.zeros(10)
         self._check(lib().ora_newton(self._h, newton_tol, max_newton, min_alpha, restart, gmres_tol, gmres_max_iters,
-                                     int(mgs), PRECOND[precond], _p(rep)))
+                                     int(mgs), PRECOND[precond], poly_degree, POLY[poly_kind], seed, _p(rep)))
         keys = ["n_newton", "n_gmres_total", "n_inner_prec_ops", "final_residual", "converged", "t_ass", "t_mv",
                 "t_prec", "t_orth", "t_total"]
         d = dict(zip(keys, rep))

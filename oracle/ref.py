@@ -67,6 +67,7 @@ def lib():
         L.ref_case_build_precond.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_uint64]
         L.ref_case_apply_base.argtypes = [C.c_void_p, _dp, _dp]
         L.ref_case_apply_precond.argtypes = [C.c_void_p, _dp, _dp]
+        L.ref_case_set_ritz.argtypes = [C.c_void_p, _dp, C.c_int]
         L.ref_case_gather_element_trace.argtypes = [C.c_void_p, _dp, _dp]
         L.ref_case_recover_local.argtypes = [C.c_void_p, _dp, _dp]
         L.ref_case_gmres.argtypes = [C.c_void_p, _dp, _dp, C.c_int, C.c_double, C.c_int, C.c_int, _dp, _dp]
@@ -282,6 +283,12 @@ class RefCase:
 
     def build_precond(self, kind="bj", poly_degree=0, seed=12345):
         _check(lib().ref_case_build_precond(self._h, PRECOND[kind], poly_degree, seed))
+
+    def set_ritz(self, theta):
+        th = np.asarray(theta, dtype=np.complex128)
+        buf = np.empty(2 * len(th))
+        buf[0::2], buf[1::2] = th.real, th.imag
+        _check(lib().ref_case_set_ritz(self._h, _p(buf), len(th)))
 
     def apply_base(self, y):
         y = _f64(y)

@@ -485,6 +485,17 @@ int ref_case_build_precond(void* h, int kind, int poly_degree, std::uint64_t see
     });
 }
 
+// Overrides the interpolation nodes of the built preconditioner (interleaved re/im, already ordered): lets the
+// reference's own apply_poly run with externally supplied nodes (Chebyshev variant, fixed-node parity tests).
+int ref_case_set_ritz(void* h, const double* reim, int count) {
+    auto* c = static_cast<RefCase*>(h);
+    return guarded([&] {
+        c->prec.ritz.clear();
+        for (int i = 0; i < count; ++i) c->prec.ritz.emplace_back(reim[2 * i], reim[2 * i + 1]);
+        c->prec.poly_degree = count;
+    });
+}
+
 int ref_case_apply_base(void* h, const double* y, double* z) {
     auto* c = static_cast<RefCase*>(h);
     return guarded([&] {

@@ -552,24 +552,30 @@ class Model:
     """PdeModel (models.hpp:27-50) as a device functor tag + parameters + tabulated x-only data."""
 
     def __init__(self, disc: Discretization, kind: str, params, forcing=None, dirichlet=None, exact=None,
-                 initial=None, name=None):
+                 initial=None, name=None, forcing_q=None, dirichlet_q=None):
+        """forcing / dirichlet: callables of x, tabulated here at the quadrature points; forcing_q / dirichlet_q:
+        the same data already tabulated ([e][g][m] / [f][g][m] host arrays), uploaded as they are.  On a host-only
+        discretisation (ctx None) the model is a description only (used to feed the CPU oracle)."""
         self.disc, self.kind, self.params = disc, kind, list(params)
         self.exact_solution, self.initial_state, self.name = exact, initial, name or kind
         self._forcing, self._dirichlet = forcing, dirichlet
         ctx = disc.ctx
-        xq, xf = None, None
-        fq = dq = None
-        if forcing is not None or dirichlet is not None:
+        fq, dq = forcing_q, dirichlet_q
+        if (forcing is not None and fq is None) or (dirichlet is not None and dq is None):
             xq, xf = disc.quad_coords()
-        if forcing is not None:
-            fq = np.asarray(forcing(xq), dtype=np.float64)
-            fq = np.ascontiguousarray(np.broadcast_to(fq.reshape(disc.ne, disc.qe, -1), (disc.ne, disc.qe, disc.n_comp)))
-        if dirichlet is not None:
-            dq = np.asarray(dirichlet(xf), dtype=np.float64)
-            dq = np.ascontiguousarray(np.broadcast_to(dq.reshape(disc.nf, disc.qf, -1), (disc.nf, disc.qf, disc.n_comp)))
+            if forcing is not None and fq is None:
+                fq = np.asarray(forcing(xq), dtype=np.float64)
+                fq = np.ascontiguousarray(np.broadcast_to(fq.reshape(disc.ne, disc.qe, -1), (disc.ne, disc.qe, disc.n_comp)))
+            if dirichlet is not None and dq is None:
+                dq = np.asarray(dirichlet(xf), dtype=np.float64)
+                dq = np.ascontiguousarray(np.broadcast_to(dq.reshape(disc.nf, disc.qf, -1), (disc.nf, disc.qf, disc.n_comp)))
+        self.forcing_q, self.dirichlet_q = fq, dq
+        self._h = None
+        if ctx is None:
+            return
         p = np.asarray(self.params, dtype=np.float64)
         h = _vp()
-        ctx.check(ctx._L.hdgb_model_create(ctx._h, disc._h, MODELS[kind], _ptr(p), len(p), _ptr(fq), _ptr(dq), C.byref(h)))
+        ctx.check(ctx._L.hdgb_model_create(ctx._h, disc._h, MODELS[kind], _ptr(p), len(p), _ptr(_f64(fq)), _ptr(_f64(dq)), C.byref(h)))
         self._h = h
 
     def __del__(self):

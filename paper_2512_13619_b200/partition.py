@@ -106,6 +106,20 @@ def global_mesh(shape: str, coords, elem_verts, tags=None, lo=None, hi=None) -> 
     return gm
 
 
+def global_mesh_from_structured(shape: str, n: int, jitter: float = 0.0, seed: int = 12345, lo=None, hi=None) -> GlobalMesh:
+    """Connectivity of the library's own structured builder (host-only discretisation, no GPU): the
+    partitioned run then cuts exactly the mesh -- element / face numbering, orientation flags, boundary
+    tags, jittered vertices -- that Discretization.structured() gives the single-GPU run."""
+    d = H.Discretization.structured(None, shape, n=n, degree=1, jitter=jitter, seed=seed, lo=lo, hi=hi)
+    ne, nf = d.ne, d.nf
+    gm = GlobalMesh(shape, d.table("element_vertices").reshape(ne, -1), d.table("vertex_coords").reshape(-1, d.dim),
+                    d.table("element_to_face").reshape(ne, -1), d.table("face_to_elements").reshape(nf, 2),
+                    d.table("face_local_index").reshape(nf, 2), d.table("face_orient").reshape(nf, 2),
+                    d.table("face_vertices").reshape(nf, -1), d.table("boundary_tag"))
+    d.close()
+    return gm
+
+
 def slab_partition(n_elems: int, n_ranks: int) -> np.ndarray:
     """Contiguous element-id ranges (slabs of a structured mesh): rank of every element."""
     return (np.arange(n_elems, dtype=np.int64) * n_ranks // n_elems).astype(np.int32)
@@ -265,6 +279,66 @@ def install_nccl_comm(ctx, lm: LocalMesh, dist):
         dist.broadcast_object_list(box, src=0)
     ctx.check(L.hdgb_comm_create_nccl(ctx._h, box[0], lm.rank, lm.n_ranks))
     set_halo_plan(ctx, lm)
+
+
+class HostComm:
+    """Host-staged transport over any torch.distributed backend (gloo): the library's callback
+    communicator with the halo exchange and the all-reduce carried through host memory.  It exists for
+    boxes with fewer GPUs than ranks (several ranks sharing one device, where NCCL refuses to form a
+    communicator) and for tests; the production transport is install_nccl_comm."""
+
+    HALO_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int)
+    ALLRED_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int)
+
+    def __init__(self, ctx, lm: LocalMesh, dist):
+        import torch
+        self.ctx, self.lm, self.dist, self.torch = ctx, lm, dist, torch
+        self._halo = self.HALO_FN(self.halo)
+        self._allred = self.ALLRED_FN(self.allreduce)
+        L = H.load_library()
+        ctx.check(L.hdgb_comm_set_callbacks(ctx._h, lm.rank, lm.n_ranks, C.cast(self._halo, C.c_void_p),
+                                            C.cast(self._allred, C.c_void_p), None))
+
+    def halo(self, user, vec, width):
+        try:
+            lm, torch, dist = self.lm, self.torch, self.dist
+            own = np.empty(lm.nf_owned * width)
+            self.ctx.copy(own, vec, own.size)
+            own = own.reshape(lm.nf_owned, width)
+            reqs, recvs = [], []
+            for k, s in enumerate(lm.nbr_ranks):
+                if len(lm.send_ids[k]):
+                    reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(own[lm.send_ids[k]])), int(s)))
+                if lm.recv_cnt[k]:
+                    buf = torch.empty(int(lm.recv_cnt[k]) * width, dtype=torch.float64)
+                    recvs.append((k, buf))
+                    reqs.append(dist.irecv(buf, int(s)))
+            for r in reqs:
+                r.wait()
+            for k, buf in recvs:
+                self.ctx.copy(vec + int(lm.recv_off[k]) * width * 8, buf.numpy(), buf.numel())
+            return 0
+        except Exception as e:  # pragma: no cover
+            print("host halo exchange failed:", repr(e), flush=True)
+            return 1
+
+    def allreduce(self, user, buf, n):
+        try:
+            t = self.torch.empty(n, dtype=self.torch.float64)
+            self.ctx.copy(t.numpy(), buf, n)
+            self.dist.all_reduce(t)
+            self.ctx.copy(buf, t.numpy(), n)
+            return 0
+        except Exception as e:  # pragma: no cover
+            print("host all-reduce failed:", repr(e), flush=True)
+            return 1
+
+
+def install_host_comm(ctx, lm: LocalMesh, dist) -> HostComm:
+    """Callback communicator carried by torch.distributed point-to-point / all-reduce on host tensors."""
+    hc = HostComm(ctx, lm, dist)
+    ctx._host_comm = hc  # keep the ctypes thunks alive as long as the context
+    return hc
 
 
 def set_halo_plan(ctx, lm: LocalMesh):

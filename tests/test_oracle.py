@@ -83,6 +83,65 @@ def test_tier_b_polynomial_apply_bitwise(ref):
     assert np.array_equal(oc.apply_precond(y), rc.apply_precond(y))
 
 
+@pytest.mark.parametrize("kind,deg", [("asm", 8), ("bj", 5), ("asm", 50)])
+def test_tier_b_harmonic_ritz_and_leja_bitwise(ref, kind, deg):
+    """compute_harmonic_ritz + leja_order of tier B (preconditioner.cpp:119-244 restated, same eigen stand-in)
+    give the reference's Ritz values bit for bit, and so does the polynomial apply built on them."""
+    rc = ref.RefCase("burgers2d", k=1, n=8)
+    oc = tier_b_from_ref(rc, "burgers2d")
+    rc.assemble()
+    oc.assemble()
+    rc.build_precond(kind, poly_degree=deg)
+    oc.build_precond(kind, poly_degree=deg)
+    assert np.array_equal(oc.get("ritz"), rc.get("ritz"))
+    y = ref.random_vector(oc.n_dof, 4)
+    assert np.array_equal(oc.apply_precond(y), rc.apply_precond(y))
+
+
+@pytest.mark.parametrize("case,k,n,kind,deg", [("burgers2d", 1, 8, "asm", 6), ("poisson2d", 2, 6, "bj", 10)])
+def test_tier_b_polynomial_newton_equals_reference(ref, case, k, n, kind, deg):
+    rc = ref.RefCase(case, k=k, n=n)
+    oc = tier_b_from_ref(rc, case)
+    rr = rc.newton(precond=kind, poly_degree=deg)
+    ro = oc.newton(precond=kind, poly_degree=deg)
+    assert ro["n_newton"] == rr["n_newton"] and ro["n_gmres_total"] == rr["n_gmres_total"]
+    assert ro["n_inner_prec_ops"] == rr["n_inner_prec_ops"]
+    assert np.array_equal(ro["residual_history"], rr["residual_history"])
+    assert np.array_equal(oc.get("uhat"), rc.get("uhat")) and np.array_equal(oc.get("u"), rc.get("u"))
+
+
+def test_tier_b_chebyshev_nodes_spec(ref):
+    """The Chebyshev variant is not in the reference: tier B restates the spec of DESIGN.md section 6 on top of the
+    (reference-pinned) harmonic Ritz values -- roots of T_P on [min Re, max Re], Leja-ordered by the reference's
+    leja_order -- and applies them with the reference's own recurrence (apply_poly with those nodes injected)."""
+    rc = ref.RefCase("burgers2d", k=2, n=6)
+    oc = tier_b_from_ref(rc, "burgers2d")
+    rc.assemble()
+    oc.assemble()
+    deg = 7
+    rc.build_precond("asm", poly_degree=deg)
+    th = rc.get("ritz")[0::2]
+    lo, hi = th.min(), th.max()
+    assert lo > 0
+    nodes = 0.5 * (hi + lo) + 0.5 * (hi - lo) * np.cos(np.pi * (2.0 * np.arange(deg) + 1.0) / (2.0 * deg))
+    want = ref.leja_order(nodes)
+    oc.build_precond("asm", poly_degree=deg, poly_kind="chebyshev")
+    got = oc.ritz
+    assert np.all(got.imag == 0.0) and np.allclose(got.real, want.real, rtol=1e-15, atol=0.0)
+    # the reference's apply_poly with the same nodes injected
+    rc.set_ritz(got)
+    y = ref.random_vector(oc.n_dof, 9)
+    assert np.array_equal(oc.apply_precond(y), rc.apply_precond(y))
+    # residual polynomial property: w = p(A) y with 1 - t p(t) = prod (1 - t / theta_j)  =>  y - A w = prod (I - A/theta_j) y
+    A = lambda v: oc.apply_base(oc.matvec(v))
+    oc2 = oc.apply_precond(y)
+    r = oc.apply_base(y)
+    for t in got.real:
+        r = r - A(r) / t
+    lhs = oc.apply_base(y) - A(oc2)
+    assert np.max(np.abs(lhs - r)) <= 1e-10 * np.max(np.abs(y))
+
+
 @pytest.mark.parametrize("case,k,n,kind", [("poisson2d", 2, 8, "bj"), ("burgers2d", 1, 8, "asm")])
 def test_tier_b_newton_equals_reference(ref, case, k, n, kind):
     rc = ref.RefCase(case, k=k, n=n)
