@@ -35,8 +35,8 @@ CONFIGS = {
             n_comp=1, case="burgers", precond=("asm", 10, "chebyshev"), dt=None, jitter=0.2),
     4: dict(name="3D elasticity, jittered tet 6x32^3, p=2, M=3, ASM-GMRES", shape="tet", n=32, degree=2, n_comp=3,
             case="elasticity", precond=("asm", 0, "gmres"), dt=None, jitter=0.2),
-    5: dict(name="3D compressible Navier-Stokes, hex 16^3, p=3, M=5, Newton-GMRES BJ, one backward-Euler step",
-            shape="hex", n=16, degree=3, n_comp=5, case="navier_stokes", precond=("bj", 0, "gmres"), dt=0.01),
+    5: dict(name="3D compressible Navier-Stokes, hex 24^3, p=3, M=5, Newton-GMRES BJ, one backward-Euler step",
+            shape="hex", n=24, degree=3, n_comp=5, case="navier_stokes", precond=("bj", 0, "gmres"), dt=0.01),
 }
 
 
