@@ -29,6 +29,7 @@ int hdgb_set_tuning(const char* key, int64_t value) {
     if (k == "use_blocked_gj") { hdgb::tuning().use_blocked_gj = static_cast<int>(value); return 0; }
     if (k == "qelim_split_rows") { hdgb::tuning().qelim_split_rows = static_cast<int>(value); return 0; }
     if (k == "spin_sync") { hdgb::tuning().spin_sync = static_cast<int>(value); return 0; }
+    if (k == "cgs_stream") { hdgb::tuning().cgs_stream = static_cast<int>(value); return 0; }
     if (k == "fused_cgs") { hdgb::tuning().fused_cgs = static_cast<int>(value); return 0; }
     if (k == "local_debug_skip") { hdgb::tuning().local_debug_skip = static_cast<int>(value); return 0; }
     if (k == "local_dmma_min_pe") { hdgb::tuning().local_dmma_min_pe = static_cast<int>(value); return 0; }
@@ -166,6 +167,19 @@ void free_all_locked(Pool& P) {
     P.parked_bytes = 0;
 }
 }  // namespace
+
+void ensure_dynamic_smem_raw(const void* func, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> granted;
+    int dev = 0;
+    HDGB_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& have = granted[{func, dev}];
+    if (bytes > have) {
+        HDGB_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+        have = bytes;
+    }
+}
 
 void pool_set_current(cudaStream_t s) { tl_stream = s; tl_stream_set = true; }
 

@@ -28,25 +28,63 @@ GmresWork& gmres_work(hdgb_matrix* k, int restart) {
         w.basis.alloc(static_cast<size_t>(restart + 1) * ld);
         w.kv.alloc(ld);
         w.r.alloc(ld);
-        w.coef.alloc(2 * static_cast<size_t>(restart + 1) + 2);
+        w.coef.alloc(2 * static_cast<size_t>(restart + 1) + 4);
         w.partial.alloc(multi_dot_workspace_doubles(n, restart + 1));
         w.ycoef.alloc(restart + 1);
+        w.cgs.alloc(cgs_workspace_doubles(k->ctx));
+        w.cgs.zero(k->ctx->stream);
     }
     return *k->work;
 }
 
 // orthogonalize (gmres.cpp:28-59) of w against V[0..nvec); h (host) gets nvec + 1 entries.
-// CGS mode: both projection passes are batched (c = V^T w; w -= V c; d = V^T w; w -= V d) with the
-// norm fused into the second update; the reference's second pass interleaves dot and update, which
-// differs at O(eps^2) relative.  MGS mode follows the reference sequence exactly.
-// n = owned unknowns (what the sums run over), ldv = distance between basis vectors; with a
-// communicator every projection pass is completed by one small all-reduce.
+// CGS mode: both projection passes are batched (c = V^T w; w -= V c; d = V^T w; w -= V d); the reference's second
+// pass interleaves dot and update, which differs at O(eps^2) relative.  Three streamed passes over the basis
+// (k_orth.cu: the first update and the second projection share one read of V), the four-pass kernels of k_vec.cu
+// for shapes the streamed kernel declines.  MGS mode follows the reference sequence exactly.
+// n = owned unknowns (what the sums run over), ldv = distance between basis vectors.
+// With a communicator (domain decomposition) an Arnoldi step costs TWO all-reduces: c, then [d, ||w1||^2] together --
+// the norm of the twice-projected vector follows from Pythagoras, ||w2||^2 = ||w1||^2 - ||d||^2 (V orthonormal), so
+// the last pass already writes the normalised vector; if that difference cancels badly (w almost in span V: the
+// happy-breakdown regime) the norm is re-measured explicitly.
+// coef: 2 nvec + 2 device scalars  c | d | s0 | s1 ;  cgs: workspace of the streamed passes or nullptr.
 void orthogonalize_device(hdgb_ctx* c, const double* V, int64_t ldv, int nvec, int64_t n, double* w, int orth,
-                          double* coef, double* partial, double* h) {
+                          double* coef, double* partial, double* cgs, double* h) {
     double* dc = coef;
     double* dd = coef + nvec;
-    double* dn = coef + 2 * nvec;
+    double* s0 = coef + 2 * nvec;
+    double* s1 = s0 + 1;
+    double* stage = c->pinned;
     auto reduce = [&](double* dev, int cnt) { if (c->comm) c->comm->allreduce(c, dev, cnt); };
+    auto wait = [&] {
+        if (tuning().spin_sync) host_wait(c);
+        else HDGB_CUDA(cudaStreamSynchronize(c->stream));
+    };
+    const bool streamed = orth != 1 && cgs && tuning().cgs_stream && cgs_pass_supported(V, ldv, nvec, w, n);
+    if (streamed && c->comm) {
+        launch_cgs_pass(c, 0, V, ldv, nvec, w, n, nullptr, dc, cgs);
+        reduce(dc, nvec);
+        launch_cgs_pass(c, 1, V, ldv, nvec, w, n, dc, dd, cgs);  // dd[nvec] == s0 = ||w1||^2 (owned rows)
+        reduce(dd, nvec + 1);
+        launch_cgs_pass(c, 3, V, ldv, nvec, w, n, dd, s1, cgs);  // w normalised, s1 = ||w1||^2 - ||d||^2
+        HDGB_CUDA(cudaMemcpyAsync(stage, coef, (2 * nvec + 2) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        wait();
+        double w1n2 = stage[2 * nvec], t = stage[2 * nvec + 1];
+        double hn = std::sqrt(t);
+        if (!(t > 1e-3 * w1n2)) {
+            // severe cancellation: measure ||w|| of what pass 3 left (w2 * s, or w2 itself when t <= 0)
+            launch_sumsq(c, w, n, s0, partial);
+            reduce(s0, 1);
+            HDGB_CUDA(cudaMemcpyAsync(stage + 2 * nvec, s0, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+            launch_scale_dev(c, w, s0, 0, w, n);
+            wait();
+            const double m2 = stage[2 * nvec];  // ||w2||^2 * s^2
+            hn = t > 0.0 ? std::sqrt(m2 * t) : std::sqrt(m2);
+        }
+        for (int i = 0; i < nvec; ++i) h[i] = stage[i] + stage[nvec + i];
+        h[nvec] = hn;
+        return;
+    }
     if (orth == 1) {
         for (int i = 0; i < nvec; ++i) {
             const double* vi = V + static_cast<size_t>(i) * ldv;
@@ -54,9 +92,13 @@ void orthogonalize_device(hdgb_ctx* c, const double* V, int64_t ldv, int nvec, i
             reduce(dc + i, 1);
             launch_multi_axpy(c, vi, ldv, 1, dc + i, -1.0, w, n, nullptr, partial);
         }
-        launch_sumsq(c, w, n, dn, partial);
-        reduce(dn, 1);
+        launch_sumsq(c, w, n, s0, partial);
+        reduce(s0, 1);
         HDGB_CUDA(cudaMemsetAsync(dd, 0, nvec * sizeof(double), c->stream));
+    } else if (streamed) {
+        launch_cgs_pass(c, 0, V, ldv, nvec, w, n, nullptr, dc, cgs);
+        launch_cgs_pass(c, 1, V, ldv, nvec, w, n, dc, dd, cgs);
+        launch_cgs_pass(c, 2, V, ldv, nvec, w, n, dd, s0, cgs);
     } else {
         launch_multi_dot(c, V, ldv, nvec, w, n, dc, partial);
         reduce(dc, nvec);
@@ -65,16 +107,14 @@ void orthogonalize_device(hdgb_ctx* c, const double* V, int64_t ldv, int nvec, i
             launch_multi_dot(c, V, ldv, nvec, w, n, dd, partial);
         }
         reduce(dd, nvec);
-        launch_multi_axpy(c, V, ldv, nvec, dd, -1.0, w, n, dn, partial);
-        reduce(dn, 1);
+        launch_multi_axpy(c, V, ldv, nvec, dd, -1.0, w, n, s0, partial);
+        reduce(s0, 1);
     }
     // normalise on the device (no-op when the norm is zero, gmres.cpp:54-57) while the column
     // travels to the host
-    double* stage = c->pinned;
     HDGB_CUDA(cudaMemcpyAsync(stage, coef, (2 * nvec + 1) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    launch_scale_dev(c, w, dn, 0, w, n);
-    if (tuning().spin_sync) host_wait(c);
-    else HDGB_CUDA(cudaStreamSynchronize(c->stream));
+    launch_scale_dev(c, w, s0, 0, w, n);
+    wait();
     for (int i = 0; i < nvec; ++i) h[i] = stage[i] + stage[nvec + i];
     h[nvec] = std::sqrt(stage[2 * nvec]);
 }
@@ -88,7 +128,7 @@ void gmres_device(hdgb_matrix* k, hdgb_precond* p, const double* rhs, double* x,
     const int64_t ld = k->n_local(); // vector length incl. the halo part
     const int m = cfg.restart;
     if (m < 1) throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: GMRES restart length must be >= 1");
-    if (2 * static_cast<size_t>(m + 1) + 2 > c->pinned_doubles) throw Failure(HDGB_ERR_UNSUPPORTED, "GMRES restart length too large");
+    if (2 * static_cast<size_t>(m + 1) + 4 > c->pinned_doubles) throw Failure(HDGB_ERR_UNSUPPORTED, "GMRES restart length too large");
     GmresWork& W = gmres_work(k, m);
     std::memset(st, 0, sizeof(*st));
     double* kv = W.kv.p;
@@ -156,7 +196,7 @@ void gmres_device(hdgb_matrix* k, hdgb_precond* p, const double* rhs, double* x,
             }
             {
                 PhaseTimer to(c, &st->t_orth);
-                orthogonalize_device(c, V, ld, nbasis, n, w, cfg.orth, W.coef.p, W.partial.p, h.data());
+                orthogonalize_device(c, V, ld, nbasis, n, w, cfg.orth, W.coef.p, W.partial.p, W.cgs.p, h.data());
                 to.stop();
             }
             for (int i = 0; i <= nbasis; ++i)
@@ -289,9 +329,11 @@ hdgb_status hdgb_gmres_solve(hdgb_matrix* k, hdgb_precond* p, const double* rhs,
 
 hdgb_status hdgb_orthogonalize(hdgb_ctx* c, const double* basis, int nvec, int64_t n, double* w, int orth, double* h) {
     return guarded(c, [&] {
-        if (2 * static_cast<size_t>(nvec) + 2 > c->pinned_doubles) throw Failure(HDGB_ERR_UNSUPPORTED, "too many basis vectors");
-        DevBuf<double> coef(2 * static_cast<size_t>(nvec) + 2), partial(multi_dot_workspace_doubles(n, std::max(nvec, 1)));
-        orthogonalize_device(c, basis, n, nvec, n, w, orth, coef.p, partial.p, h);
+        if (2 * static_cast<size_t>(nvec) + 4 > c->pinned_doubles) throw Failure(HDGB_ERR_UNSUPPORTED, "too many basis vectors");
+        DevBuf<double> coef(2 * static_cast<size_t>(nvec) + 4), partial(multi_dot_workspace_doubles(n, std::max(nvec, 1)));
+        DevBuf<double> cgs(cgs_workspace_doubles(c));
+        cgs.zero(c->stream);
+        orthogonalize_device(c, basis, n, nvec, n, w, orth, coef.p, partial.p, cgs.p, h);
     });
 }
 
@@ -420,28 +462,20 @@ hdgb_status hdgb_time_march(hdgb_disc* d, const hdgb_model* m, hdgb_state* s, do
                             const hdgb_newton_config* ncfg, const hdgb_gmres_config* gcfg,
                             const hdgb_precond_spec* pspec, hdgb_solve_report* reports) {
     hdgb_ctx* c = d->ctx;
-    if (!(dt > 0.0)) {
-        c->err = "time_march requires a positive dt";
-        return HDGB_ERR_GENERIC;
-    }
-    hdgb_status st = HDGB_OK;
-    try {
+    // a failing step leaves defined (zeroed) reports behind it
+    if (reports && n_steps > 0) std::memset(reports, 0, sizeof(hdgb_solve_report) * static_cast<size_t>(n_steps));
+    return guarded(c, [&] {
+        if (!(dt > 0.0)) throw Failure(HDGB_ERR_GENERIC, "time_march requires a positive dt");
         DevBuf<double> u_prev(s->u.n);
         for (int step = 0; step < n_steps; ++step) {
             HDGB_CUDA(cudaMemcpyAsync(u_prev.p, s->u.p, s->u.n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
             hdgb_time t{dt, u_prev.p};
             hdgb_solve_report local;
-            st = hdgb_newton_solve(d, m, s, ncfg, gcfg, pspec, &t, reports ? &reports[step] : &local);
-            if (st != HDGB_OK) {
-                c->err = "time step " + std::to_string(step) + ": " + c->err;
-                return st;
-            }
+            const hdgb_status st = hdgb_newton_solve(d, m, s, ncfg, gcfg, pspec, &t, reports ? &reports[step] : &local);
+            pool_set_current(c->stream);
+            if (st != HDGB_OK) throw Failure(st, "time step " + std::to_string(step) + ": " + c->err, c->err_index);
         }
-    } catch (const Failure& f) {
-        c->err = f.what();
-        return f.code;
-    }
-    return st;
+    });
 }
 
 }  // extern "C"

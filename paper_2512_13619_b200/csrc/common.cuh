@@ -225,6 +225,15 @@ hdgb_status guarded(hdgb_ctx* ctx, F&& fn) {
     }
 }
 
+// Opt-in to more than 48 KB of dynamic shared memory for a kernel.  The attribute is per function AND per device
+// (hdgb_ctx_create(device) allows several devices in one process), so what has been granted is tracked per
+// (function, current device) under a mutex (api_core.cu); cheap enough to call at every launch site.
+void ensure_dynamic_smem_raw(const void* func, size_t bytes);
+template <class K>
+inline void ensure_dynamic_smem(K kernel, size_t bytes) {
+    if (bytes > 48 * 1024) ensure_dynamic_smem_raw(reinterpret_cast<const void*>(kernel), bytes);
+}
+
 inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
 
 }  // namespace hdgb

@@ -98,6 +98,7 @@ struct GmresWork {
     DevBuf<double> coef;     // 2*(restart+1) + 2 device scalars: c | d | norm2
     DevBuf<double> partial;  // reduction workspace
     DevBuf<double> ycoef;    // restart device coefficients for the solution update
+    DevBuf<double> cgs;      // workspace of the streamed CGS2 passes (ticket word + per-CTA partials)
 };
 }  // namespace hdgb
 

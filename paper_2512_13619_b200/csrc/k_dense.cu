@@ -477,8 +477,7 @@ void launch_lu_invert_batch(hdgb_ctx* ctx, int n, int64_t batch, const double* a
     if (n <= 24) {
         const int wpc = 4;
         const size_t smem = per * wpc * sizeof(double);
-        if (smem > 48 * 1024)
-            HDGB_CUDA(cudaFuncSetAttribute(lu_invert_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        ensure_dynamic_smem(lu_invert_warp_kernel, smem);
         lu_invert_warp_kernel<<<ceil_div(batch, wpc), wpc * 32, smem, ctx->stream>>>(n, batch, a, inv, flags, wpc);
         HDGB_LAUNCH_CHECK(ctx);
         return;
@@ -503,8 +502,7 @@ void launch_lu_invert_batch(hdgb_ctx* ctx, int n, int64_t batch, const double* a
     if (threads < 64) threads = 64;
     if (threads > 512) threads = 512;
     if (smem <= 200 * 1024) {
-        if (smem > 48 * 1024)
-            HDGB_CUDA(cudaFuncSetAttribute(lu_invert_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        ensure_dynamic_smem(lu_invert_cta_kernel, smem);
         const int64_t grid = batch < (1 << 20) ? batch : (1 << 20);
         lu_invert_cta_kernel<<<static_cast<unsigned>(grid), threads, smem, ctx->stream>>>(n, batch, a, inv, flags, nullptr);
         HDGB_LAUNCH_CHECK(ctx);

@@ -168,14 +168,8 @@ void launch_wmwn(hdgb_ctx* ctx, const GemmArgs& g, int64_t batch, bool vec) {
     const size_t smem = (2 * KC * (BM + 4) + 2 * BN * LDB) * sizeof(double);
     auto kv = gemm_dmma_kernel<WM, WN, true>;
     auto ks = gemm_dmma_kernel<WM, WN, false>;
-    static bool configured = false;
-    if (!configured) {
-        if (smem > 48 * 1024) {
-            HDGB_CUDA(cudaFuncSetAttribute(kv, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-            HDGB_CUDA(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        }
-        configured = true;
-    }
+    ensure_dynamic_smem(kv, smem);
+    ensure_dynamic_smem(ks, smem);
     int64_t done = 0;
     while (done < batch) {  // gridDim.z limit
         const int64_t nb = (batch - done) < 65535 ? (batch - done) : 65535;
@@ -411,14 +405,10 @@ bool launch_qelim_fused(hdgb_ctx* ctx, int m0, int m1, int n, int k, int nterm, 
     g.c_colstride = c_colw > 0 ? c_colstride : n;
     const int NS = tuning().qelim_stages >= 3 ? 3 : 2;
     const size_t smem = static_cast<size_t>(NS) * (KC * (32 * WM + 4) + 32 * WN * LDB) * sizeof(double);
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-        HDGB_CUDA(cudaFuncSetAttribute(qelim_fused_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        HDGB_CUDA(cudaFuncSetAttribute(qelim_fused_kernel<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        HDGB_CUDA(cudaFuncSetAttribute(qelim_fused_kernel<true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        HDGB_CUDA(cudaFuncSetAttribute(qelim_fused_kernel<false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        configured = smem;
-    }
+    ensure_dynamic_smem(qelim_fused_kernel<true, 2>, smem);
+    ensure_dynamic_smem(qelim_fused_kernel<false, 2>, smem);
+    ensure_dynamic_smem(qelim_fused_kernel<true, 3>, smem);
+    ensure_dynamic_smem(qelim_fused_kernel<false, 3>, smem);
     int64_t done = 0;
     while (done < batch) {
         const int64_t nb = (batch - done) < 65535 ? (batch - done) : 65535;

@@ -142,12 +142,10 @@ void launch_team_gemv(hdgb_ctx* ctx, const GemvArgs& g) {
     const int64_t grid = (g.batch + FPB - 1) / FPB;
     if (grid > 2147483647LL) throw Failure(HDGB_ERR_UNSUPPORTED, "team_gemv: batch too large");
     if (vec2) {
-        if (smem > 48 * 1024)
-            HDGB_CUDA(cudaFuncSetAttribute(team_gemv_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        ensure_dynamic_smem(team_gemv_kernel<2>, smem);
         team_gemv_kernel<2><<<static_cast<unsigned>(grid), threads, smem, ctx->stream>>>(g, RL, CG, TS, FPB);
     } else {
-        if (smem > 48 * 1024)
-            HDGB_CUDA(cudaFuncSetAttribute(team_gemv_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        ensure_dynamic_smem(team_gemv_kernel<1>, smem);
         team_gemv_kernel<1><<<static_cast<unsigned>(grid), threads, smem, ctx->stream>>>(g, RL, CG, TS, FPB);
     }
     HDGB_LAUNCH_CHECK(ctx);

@@ -684,11 +684,7 @@ void launch_gj_invert_batch(hdgb_ctx* ctx, int n, int64_t batch, const double* a
         const int64_t cap = static_cast<int64_t>(ctx->sm_count) * per_sm;
         const unsigned grid = static_cast<unsigned>(batch < cap ? batch : cap);
         auto launch = [&](auto kern) {
-            static size_t configured = 0;
-            if (smem > 48 * 1024 && smem > configured) {
-                HDGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-                configured = smem;
-            }
+            ensure_dynamic_smem(kern, smem);
             kern<<<grid, 256, smem, ctx->stream>>>(n, batch, a, inv, flags, 0);
         };
         switch (rt) {
@@ -721,11 +717,7 @@ void launch_gj_invert_batch(hdgb_ctx* ctx, int n, int64_t batch, const double* a
         if (wpc < 1) throw Failure(HDGB_ERR_UNSUPPORTED, "lu_invert_batch: block too large for the panel kernel");
         if (wpc > 8) wpc = 8;
         const size_t psm = per_warp * wpc;
-        static size_t configured = 0;
-        if (psm > 48 * 1024 && psm > configured) {
-            HDGB_CUDA(cudaFuncSetAttribute(gj_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(psm)));
-            configured = psm;
-        }
+        ensure_dynamic_smem(gj_panel_kernel, psm);
         for (int s = 0; s < steps; ++s) {
             const int j0 = s * NB;
             const double* old = x[s & 1] + off;
@@ -743,11 +735,7 @@ void launch_gj_invert_batch(hdgb_ctx* ctx, int n, int64_t batch, const double* a
                 }
             } else if (tuning().gj_panel_cta) {
                 const size_t csm = per_warp;  // one panel per CTA
-                static size_t cfg_cta = 0;
-                if (csm > 48 * 1024 && csm > cfg_cta) {
-                    HDGB_CUDA(cudaFuncSetAttribute(gj_panel_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(csm)));
-                    cfg_cta = csm;
-                }
+                ensure_dynamic_smem(gj_panel_cta_kernel, csm);
                 gj_panel_cta_kernel<<<static_cast<unsigned>(nbt), kPanelCtaWarps * 32, csm, ctx->stream>>>(
                     n, j0, old, nw, amax.p + done, piv.p + done * n, src.p + done * n, flags, ldp, done);
             } else

@@ -944,12 +944,8 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
     auto kern = local_assemble_kernel<Model, 256, false, false>;
     constexpr int NTD = 256;  // tensor-core mode: 8 warps, two CTAs per SM for scalar systems (their phases overlap)
     auto kern_d = local_assemble_kernel<Model, NTD, true, false>;
-    static bool configured = false;
-    if (!configured) {
-        HDGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cap)));
-        HDGB_CUDA(cudaFuncSetAttribute(kern_d, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cap)));
-        configured = true;
-    }
+    ensure_dynamic_smem(kern, cap);
+    ensure_dynamic_smem(kern_d, cap);
     const size_t all = fixed + dv.qe * svr + nfp * sfr;
     if (all <= budget) {
         // E / D_d on the tensor-core path when the operand chunks fit next to the point records
@@ -968,11 +964,7 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
             const size_t rec_stride = (dv.qe * svr + nfp * sfr + 15) & ~static_cast<size_t>(15);
             if (fixed + edb <= cap) {
                 auto kern_g = local_assemble_kernel<Model, 256, true, true>;
-                static bool cfg_g = false;
-                if (!cfg_g) {
-                    HDGB_CUDA(cudaFuncSetAttribute(kern_g, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cap)));
-                    cfg_g = true;
-                }
+                ensure_dynamic_smem(kern_g, cap);
                 DevBuf<char> scratch(rec_stride * static_cast<size_t>(dv.ne));
                 kern_g<<<dv.ne, 256, fixed + edb, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2, scratch.p, rec_stride);
                 HDGB_LAUNCH_CHECK(ctx);

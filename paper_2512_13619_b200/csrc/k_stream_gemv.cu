@@ -23,6 +23,7 @@
 // HBM sees every matrix byte exactly once, as large sequential bulk reads; x / y traffic is served
 // from L2.  Roofline: HBM.  Algorithmic bytes per item: 8*(rows*cols + cols + rows) + 4*nslots.
 #include "kernels.cuh"
+#include "tma.cuh"
 
 namespace hdgb {
 
@@ -53,37 +54,6 @@ struct StreamPlan {
     int xstride;          // doubles between the x slices of consecutive items of a chunk (cols, or cols + 1 in packed mode with odd cols)
     float inv_cols, inv_width, inv_nslots;  // reciprocals for the gather's index arithmetic
 };
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "LAB_WAIT:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-        "@P1 bra DONE;\n"
-        "bra LAB_WAIT;\n"
-        "DONE:\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-// 1D bulk TMA copy global -> shared, completion counted in bytes on the mbarrier.
-__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
 
 template <int V>
 __device__ __forceinline__ void lds_rows(const double* p, double (&v)[V]);
@@ -134,7 +104,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) stream_gemv_kernel(GemvArgs g,
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.stages; ++s) mbar_init(full + s, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_fence_init();
     }
     __syncthreads();
 
@@ -418,11 +388,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) stream_gemv_kernel(GemvArgs g,
 template <int V, int RT>
 void launch_t(hdgb_ctx* ctx, const GemvArgs& g, const StreamPlan& p, int grid, size_t smem) {
     auto kern = stream_gemv_kernel<V, RT>;
-    static size_t configured = 0;  // per instantiation
-    if (smem > configured) {
-        HDGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        configured = smem;
-    }
+    ensure_dynamic_smem(kern, smem);
     kern<<<grid, p.warps * 32, smem, ctx->stream>>>(g, p);
     HDGB_LAUNCH_CHECK(ctx);
 }

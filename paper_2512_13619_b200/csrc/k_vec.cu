@@ -269,11 +269,19 @@ void launch_multi_dot(hdgb_ctx* ctx, const double* V, int64_t ldv, int nvec, con
                       double* out, double* partial, bool sqrt_last) {
     if (nvec <= 0 || n <= 0) return;
     const int nblocks = static_cast<int>((n + kDotChunk - 1) / kDotChunk);
-    const size_t smem = static_cast<size_t>(kDotThreads / 32) * nvec * sizeof(double);
-    multi_dot_partial_kernel<<<nblocks, kDotThreads, smem, ctx->stream>>>(V, ldv, nvec, w, n, partial, nblocks);
-    HDGB_LAUNCH_CHECK(ctx);
-    reduce_partials_kernel<<<nvec, 128, 0, ctx->stream>>>(partial, nblocks, out, sqrt_last ? nvec - 1 : -1);
-    HDGB_LAUNCH_CHECK(ctx);
+    // groups of at most kGroup vectors per launch: the per-warp reduction slots (64 B per vector) stay inside the
+    // default 48 KB of dynamic shared memory for any restart length (the reference accepts any, gmres.hpp:15)
+    constexpr int kGroup = 512;
+    for (int j0 = 0; j0 < nvec; j0 += kGroup) {
+        const int nv = nvec - j0 < kGroup ? nvec - j0 : kGroup;
+        const size_t smem = static_cast<size_t>(kDotThreads / 32) * nv * sizeof(double);
+        multi_dot_partial_kernel<<<nblocks, kDotThreads, smem, ctx->stream>>>(V + static_cast<int64_t>(j0) * ldv, ldv, nv, w, n, partial,
+                                                                             nblocks);
+        HDGB_LAUNCH_CHECK(ctx);
+        const bool last = j0 + nv == nvec;
+        reduce_partials_kernel<<<nv, 128, 0, ctx->stream>>>(partial, nblocks, out + j0, (sqrt_last && last) ? nv - 1 : -1);
+        HDGB_LAUNCH_CHECK(ctx);
+    }
 }
 
 void launch_multi_axpy(hdgb_ctx* ctx, const double* V, int64_t ldv, int nvec, const double* c, double sign,
@@ -281,10 +289,17 @@ void launch_multi_axpy(hdgb_ctx* ctx, const double* V, int64_t ldv, int nvec, co
     if (n <= 0) return;
     const int per = kAxpyThreads * kAxpyPerThread;
     const int nblocks = static_cast<int>((n + per - 1) / per);
-    const size_t smem = (static_cast<size_t>(nvec) + 8) * sizeof(double);
-    multi_axpy_kernel<<<nblocks, kAxpyThreads, smem, ctx->stream>>>(V, ldv, nvec, c, sign, w, n,
-                                                                    norm2_out ? partial : nullptr);
-    HDGB_LAUNCH_CHECK(ctx);
+    constexpr int kGroup = 4096;  // coefficients staged in shared memory per launch
+    int j0 = 0;
+    do {
+        const int nv = nvec - j0 < kGroup ? nvec - j0 : kGroup;
+        const bool last = j0 + nv >= nvec;
+        const size_t smem = (static_cast<size_t>(nv) + 8) * sizeof(double);
+        multi_axpy_kernel<<<nblocks, kAxpyThreads, smem, ctx->stream>>>(V + static_cast<int64_t>(j0) * ldv, ldv, nv, c + j0, sign, w, n,
+                                                                        (norm2_out && last) ? partial : nullptr);
+        HDGB_LAUNCH_CHECK(ctx);
+        j0 += nv;
+    } while (j0 < nvec);
     if (norm2_out) {
         reduce_partials_kernel<<<1, 128, 0, ctx->stream>>>(partial, nblocks, norm2_out, -1);
         HDGB_LAUNCH_CHECK(ctx);

@@ -37,7 +37,8 @@ struct Tuning {
     int stream_packed_max_cols = 32;     // ... for items with at most this many columns
     int64_t stream_packed_stage_bytes = 6144;  // ... bytes per TMA stage of a warp in packed mode
     int spin_sync = 1;                   // GMRES: poll an event for the per-iteration Hessenberg column instead of a blocking sync
-    int fused_cgs = 0;                   // CGS2: first update and second projection in one pass over the basis (measured slower: 112 us vs 85 us at cfg2)
+    int fused_cgs = 0;                   // round-1 register-resident fused CGS2 pass (measured slower: 112 us vs 85 us at cfg2)
+    int cgs_stream = 1;                  // CGS2 as three TMA-streamed passes over the basis (k_orth.cu) instead of four
     int local_debug_skip = 0;            // measurement aid: skip phases of the local kernel (1 = E/D_d, 2 = H/G_d/F); results invalid
     int local_dmma_min_pe = 20;          // local blocks on the tensor-core path from this many basis functions per element
     int local_global_records = 1;        // wide systems: point records in an L2-resident scratch, one launch, E / D_d on DMMA
@@ -76,6 +77,14 @@ size_t multi_dot_workspace_doubles(int64_t n, int nvec);
 // CGS2 middle step fused: w -= V c ; d = V^T w in one pass over V.  false = nvec too large (use the two kernels).
 bool launch_multi_axpy_dot(hdgb_ctx* ctx, const double* V, int64_t ldv, int nvec, const double* c, double* w, int64_t n,
                            double* d_out, double* partial);
+// CGS2 as three streaming passes over the basis (k_orth.cu).  mode 0: out[0..nvec) = V^T w;  mode 1: w -= V coef,
+// out[0..nvec) = V^T w, out[nvec] = ||w||^2;  mode 2: w -= V coef, out[0] = ||w||^2;  mode 3: w = (w - V coef) * s with
+// s = 1/sqrt(t), t = coef[nvec] - sum coef[j]^2, out[0] = max(t, 0).  `work` = cgs_workspace_doubles() doubles, zeroed once.
+constexpr int kOrthMaxVec = 56;  // 7 columns per consumer warp; two stages of 51 columns fit shared memory (restart 50)
+size_t cgs_workspace_doubles(hdgb_ctx* ctx);
+bool cgs_pass_supported(const double* V, int64_t ldv, int nvec, const double* w, int64_t n);
+void launch_cgs_pass(hdgb_ctx* ctx, int mode, const double* V, int64_t ldv, int nvec, double* w, int64_t n, const double* coef,
+                     double* out, double* work);
 // w[i] += sign * sum_j c[j] * V[j*ldv + i]  (ascending j).  If norm2_out != nullptr, also reduces
 // sum_i w_new[i]^2 into *norm2_out (device) using `partial`.
 void launch_multi_axpy(hdgb_ctx* ctx, const double* V, int64_t ldv, int nvec, const double* c /*device*/,
