@@ -183,6 +183,11 @@ hdgb_status hdgb_compute_q(hdgb_disc* d, hdgb_state* s);
  * keep_raw != 0 keeps the uncondensed blocks (test oracles, local_ops.cpp:420-428). */
 hdgb_status hdgb_assemble_element_operators(hdgb_disc* d, const hdgb_model* m, hdgb_state* s,
                                             const hdgb_time* t, int keep_raw, hdgb_ops** out);
+/* ElementOperators (local_ops.hpp:40-62) from caller data (host|device; NULL = zeros): lets a caller that holds the
+ * reference's value-type operators hand them to assemble_global / build_asm / recover_local. */
+hdgb_status hdgb_ops_create(hdgb_disc* d, const double* kbar, const double* ebar_inv, const double* fbar,
+                            const double* hbar, const double* rbar, const double* ru, const double* ruhat_e,
+                            hdgb_ops** out);
 void hdgb_ops_destroy(hdgb_ops* o);
 /* name: kbar, ebar_inv, fbar, hbar, rbar, ru, ruhat_e, and with keep_raw: e_raw, f_raw, h_raw,
  * j_raw, d_raw0.., g_raw0.. */
@@ -264,6 +269,37 @@ hdgb_status hdgb_precond_apply_base(hdgb_precond* p, const double* y, double* z)
 /* make_preconditioner_apply (preconditioner.cpp:301-308) incl. apply_poly (:246-283). */
 hdgb_status hdgb_precond_apply(hdgb_precond* p, hdgb_matrix* k, const double* y, double* z);
 int64_t hdgb_precond_inner_ops(const hdgb_precond* p); /* SolveReport::n_inner_prec_ops */
+
+/* The reference's per-function preconditioner API (preconditioner.hpp:31-76), one entry point each.
+ * hdgb_build_preconditioner above is newton.cpp:30-52 (which calls these); the functions below are for
+ * callers that drive the pieces themselves, as the reference's tests do. */
+/* build_bj (preconditioner.cpp:30-46): inverts the diagonal face blocks; SingularBlock(face). */
+hdgb_status hdgb_build_bj(hdgb_matrix* k, hdgb_precond** out);
+/* apply_bj (preconditioner.cpp:48-52). */
+hdgb_status hdgb_apply_bj(hdgb_precond* p, const double* y /*host|device*/, double* z /*host|device*/);
+/* build_asm (preconditioner.cpp:54-84): from the element operators and the mesh alone (no K needed: the two-sided
+ * diagonal sub-block sums are formed from K-bar, side 0 first, :59-75); SingularBlock(element). */
+hdgb_status hdgb_build_asm(const hdgb_ops* o, hdgb_disc* d, hdgb_precond** out);
+/* apply_asm (preconditioner.cpp:86-105). */
+hdgb_status hdgb_apply_asm(hdgb_precond* p, const double* y, double* z);
+/* A Preconditioner (preconditioner.hpp:19-29) from caller data: kind, the inverse blocks of that kind (bj_inv:
+ * mpf^2 per face | asm_inv: nfl^2 per element, needs d | NULL for identity; host|device) and optional Ritz values
+ * (interleaved re/im in application order). */
+hdgb_status hdgb_precond_create(hdgb_ctx* ctx, int kind, int mpf, int nf, hdgb_disc* d, const double* inv,
+                                const double* ritz_reim, int n_ritz, hdgb_precond** out);
+
+/* A linear operator as a C callback on DEVICE vectors of n doubles (the reference's LinearOp / OpFn closures,
+ * preconditioner.hpp:50, gmres.hpp:43): out = op(in).  The callback must enqueue its work on hdgb_ctx_stream(ctx)
+ * or synchronise before returning; in and out never alias.  Non-zero return = failure (-> HDGB_ERR_GENERIC). */
+typedef int (*hdgb_op_fn)(void* user, const double* in, double* out, int64_t n);
+/* compute_harmonic_ritz (preconditioner.cpp:119-205) of an arbitrary operator: seeded start vector, MGS Arnoldi
+ * on the device, harmonic correction + eigenvalues + Leja order on the host.  out_reim: 2*degree doubles. */
+hdgb_status hdgb_compute_harmonic_ritz(hdgb_ctx* ctx, hdgb_op_fn op, void* user, int64_t n_dof, int degree,
+                                       uint64_t seed, double* out_reim, int* n_out);
+/* apply_poly (preconditioner.cpp:246-283): z = poly(base K) base y with p's Ritz values; base_apply == NULL uses
+ * p's own base (make_base_apply, :285-299).  *inner_ops (may be NULL) is incremented by the operator count. */
+hdgb_status hdgb_apply_poly(hdgb_precond* p, hdgb_op_fn base_apply, void* user, hdgb_matrix* k, const double* y,
+                            double* z, int64_t* inner_ops);
 /* leja_order (preconditioner.cpp:207-244) on interleaved (re, im); returns count in *n_out. */
 hdgb_status hdgb_leja_order(const double* reim, int n, double* out_reim, int* n_out);
 /* Harmonic Ritz values of a small dense Hessenberg-type matrix (host, column-major (p+1) x p):
@@ -296,6 +332,12 @@ void hdgb_gmres_config_default(hdgb_gmres_config* cfg);
 hdgb_status hdgb_gmres_solve(hdgb_matrix* k, hdgb_precond* p, const double* rhs /*host|device*/,
                              const double* x0 /*host|device|NULL*/, const hdgb_gmres_config* cfg,
                              double* x /*host|device*/, hdgb_gmres_stats* stats, double* residual_trace);
+/* gmres_solve (gmres.cpp:61-228), closure form of gmres.hpp:50-53: operator and preconditioner are callbacks on
+ * device vectors of n doubles (precond NULL = identity); same control flow, statistics and errors. */
+hdgb_status hdgb_gmres_solve_fn(hdgb_ctx* ctx, int64_t n, hdgb_op_fn matvec, void* matvec_user, hdgb_op_fn precond,
+                                void* precond_user, const double* rhs /*host|device*/, const double* x0 /*host|device|NULL*/,
+                                const hdgb_gmres_config* cfg, double* x /*host|device*/, hdgb_gmres_stats* stats,
+                                double* residual_trace);
 /* orthogonalize (gmres.cpp:28-59) on device vectors: basis is nvec contiguous vectors of length n;
  * h receives nvec+1 values (host). */
 hdgb_status hdgb_orthogonalize(hdgb_ctx* ctx, const double* basis /*device*/, int nvec, int64_t n,

@@ -12,8 +12,11 @@
 #ifndef HDGB200_HPP
 #define HDGB200_HPP
 
+#include <algorithm>
 #include <complex>
 #include <cstdint>
+#include <exception>
+#include <functional>
 #include <memory>
 #include <optional>
 #include <stdexcept>
@@ -367,6 +370,123 @@ inline std::vector<double> apply_preconditioner(Preconditioner& p, const FaceBlo
     std::vector<double> z(y.size());
     check(k.ctx().get(), hdgb_precond_apply(p.handle(), k.handle(), y.data(), z.data()));
     return z;
+}
+// ---- preconditioner.hpp:31-76, one function each --------------------------------------------------------------
+// build_bj (preconditioner.hpp:33) / apply_bj (:36)
+inline Preconditioner build_bj(const FaceBlockMatrix& k) {
+    hdgb_precond* p = nullptr;
+    check(k.ctx().get(), hdgb_build_bj(k.handle(), &p));
+    return Preconditioner(k.ctx(), p);
+}
+inline std::vector<double> apply_bj(Context& c, Preconditioner& p, const std::vector<double>& y) {
+    std::vector<double> z(y.size());
+    check(c.get(), hdgb_apply_bj(p.handle(), y.data(), z.data()));
+    return z;
+}
+// build_asm (preconditioner.hpp:42) / apply_asm (:47); the mesh argument of the reference is the discretisation
+inline Preconditioner build_asm(const ElementOperators& ops, const Discretization& d) {
+    hdgb_precond* p = nullptr;
+    check(d.ctx().get(), hdgb_build_asm(ops.handle(), d.get(), &p));
+    return Preconditioner(d.ctx(), p);
+}
+inline std::vector<double> apply_asm(Context& c, Preconditioner& p, const std::vector<double>& y) {
+    std::vector<double> z(y.size());
+    check(c.get(), hdgb_apply_asm(p.handle(), y.data(), z.data()));
+    return z;
+}
+
+// A linear operator on DEVICE vectors of n doubles: out = op(in), enqueued on the context's stream (or synchronised
+// before returning).  The reference's LinearOp / OpFn (preconditioner.hpp:50, gmres.hpp:43) with device pointers.
+using DeviceOp = std::function<void(const double* in, double* out, std::int64_t n)>;
+
+namespace detail {
+struct OpThunk {
+    const DeviceOp* fn;
+    std::exception_ptr error;
+    static int call(void* user, const double* in, double* out, std::int64_t n) {
+        OpThunk* t = static_cast<OpThunk*>(user);
+        try {
+            (*t->fn)(in, out, n);
+            return 0;
+        } catch (...) {
+            t->error = std::current_exception();
+            return 1;
+        }
+    }
+};
+inline std::vector<std::complex<double>> unpack(const std::vector<double>& reim, int n) {
+    std::vector<std::complex<double>> o;
+    for (int i = 0; i < n; ++i) o.emplace_back(reim[2 * i], reim[2 * i + 1]);
+    return o;
+}
+}  // namespace detail
+
+// compute_harmonic_ritz (preconditioner.hpp:57-58)
+inline std::vector<std::complex<double>> compute_harmonic_ritz(Context& c, const DeviceOp& op, std::size_t n_dof, int degree,
+                                                               std::uint64_t seed) {
+    detail::OpThunk t{&op, nullptr};
+    std::vector<double> reim(2 * static_cast<size_t>(degree > 0 ? degree : 1));
+    int n = 0;
+    const hdgb_status st = hdgb_compute_harmonic_ritz(c.get(), detail::OpThunk::call, &t, static_cast<std::int64_t>(n_dof), degree,
+                                                      seed, reim.data(), &n);
+    if (t.error) std::rethrow_exception(t.error);
+    check(c.get(), st);
+    return detail::unpack(reim, n);
+}
+// leja_order (preconditioner.hpp:64)
+inline std::vector<std::complex<double>> leja_order(const std::vector<std::complex<double>>& theta) {
+    std::vector<double> in, out(2 * theta.size() + 2);
+    for (const auto& t : theta) { in.push_back(t.real()); in.push_back(t.imag()); }
+    int n = 0;
+    if (hdgb_leja_order(in.data(), static_cast<int>(theta.size()), out.data(), &n) != HDGB_OK) throw Error("leja_order failed");
+    return detail::unpack(out, n);
+}
+// make_base_apply (preconditioner.hpp:70) / make_preconditioner_apply (:73-74) as device operators
+inline DeviceOp make_base_apply(Context& c, Preconditioner& p) {
+    return [&c, &p](const double* in, double* out, std::int64_t) { check(c.get(), hdgb_precond_apply_base(p.handle(), in, out)); };
+}
+inline DeviceOp make_preconditioner_apply(Preconditioner& p, const FaceBlockMatrix& k) {
+    return [&p, &k](const double* in, double* out, std::int64_t) { check(k.ctx().get(), hdgb_precond_apply(p.handle(), k.handle(), in, out)); };
+}
+// block_matvec as a device operator (the closure the reference's tests build around block_matvec)
+inline DeviceOp make_matvec(const FaceBlockMatrix& k) {
+    return [&k](const double* in, double* out, std::int64_t) { check(k.ctx().get(), hdgb_block_matvec(k.handle(), in, out)); };
+}
+// apply_poly (preconditioner.hpp:66-67): p supplies the Ritz values; base == nullptr uses p's own base
+inline std::vector<double> apply_poly(Preconditioner& p, const DeviceOp* base, const FaceBlockMatrix& k, const std::vector<double>& y,
+                                      long* inner_ops = nullptr) {
+    if (y.size() != static_cast<size_t>(k.n_dof())) throw DimensionMismatch("apply_poly: vector size does not match the matrix");
+    std::vector<double> z(y.size());
+    std::int64_t ops = 0;
+    detail::OpThunk t{base, nullptr};
+    const hdgb_status st = hdgb_apply_poly(p.handle(), base ? detail::OpThunk::call : nullptr, base ? &t : nullptr, k.handle(), y.data(),
+                                           z.data(), &ops);
+    if (t.error) std::rethrow_exception(t.error);
+    check(k.ctx().get(), st);
+    if (inner_ops) *inner_ops += static_cast<long>(ops);
+    return z;
+}
+// gmres.hpp:50-53, closure form: operator and preconditioner are device operators (precond empty = identity)
+inline std::pair<std::vector<double>, GmresStats> gmres_solve(Context& c, const DeviceOp& matvec, const DeviceOp& precond,
+                                                              const std::vector<double>& rhs, const std::vector<double>& x0,
+                                                              const GmresConfig& cfg = {}, std::vector<double>* residual_trace = nullptr) {
+    std::vector<double> x(rhs.size());
+    const hdgb_gmres_config cc = detail::to_c(cfg);
+    hdgb_gmres_stats st{};
+    detail::OpThunk mv{&matvec, nullptr}, pc{&precond, nullptr};
+    std::vector<double> trace(residual_trace ? static_cast<size_t>(cfg.max_iters > 0 ? cfg.max_iters : 1) : 0);
+    const hdgb_status rc = hdgb_gmres_solve_fn(c.get(), static_cast<std::int64_t>(rhs.size()), detail::OpThunk::call, &mv,
+                                               precond ? detail::OpThunk::call : nullptr, precond ? &pc : nullptr, rhs.data(),
+                                               x0.empty() ? nullptr : x0.data(), &cc, x.data(), &st, residual_trace ? trace.data() : nullptr);
+    if (mv.error) std::rethrow_exception(mv.error);
+    if (pc.error) std::rethrow_exception(pc.error);
+    check(c.get(), rc);
+    GmresStats o;
+    o.iters = st.iters; o.restarts = st.restarts; o.final_rel_residual = st.final_rel_residual;
+    o.t_mv = st.t_mv; o.t_prec = st.t_prec; o.t_orth = st.t_orth; o.converged = st.converged != 0;
+    o.max_orth_error = st.max_orth_error; o.max_residual_gap = st.max_residual_gap;
+    if (residual_trace) residual_trace->assign(trace.begin(), trace.begin() + std::min<size_t>(trace.size(), static_cast<size_t>(st.iters)));
+    return {std::move(x), o};
 }
 // gmres.hpp:50-53 in the data form of SPEC.md:557
 inline std::pair<std::vector<double>, GmresStats> gmres_solve(const FaceBlockMatrix& k, Preconditioner& p, const std::vector<double>& rhs,

@@ -674,6 +674,32 @@ hdgb_status hdgb_assemble_element_operators(hdgb_disc* d, const hdgb_model* m, h
     });
 }
 
+hdgb_status hdgb_ops_create(hdgb_disc* d, const double* kbar, const double* ebar_inv, const double* fbar, const double* hbar,
+                            const double* rbar, const double* ru, const double* ruhat_e, hdgb_ops** out) {
+    *out = nullptr;
+    hdgb_ctx* c = d->ctx;
+    return guarded(c, [&] {
+        const DiscView& v = d->view;
+        std::unique_ptr<hdgb_ops> o(new hdgb_ops());
+        o->ctx = c; o->npe = v.npe; o->nfl = v.nfl; o->ne = v.ne; o->D = v.D;
+        const size_t ne = v.ne, npe = v.npe, nfl = v.nfl;
+        auto fill = [&](DevBuf<double>& b, const double* src, size_t n) {
+            b.alloc(n);
+            if (src) HDGB_CUDA(cudaMemcpyAsync(b.p, src, n * sizeof(double), cudaMemcpyDefault, c->stream));
+            else b.zero(c->stream);
+        };
+        fill(o->kbar, kbar, nfl * nfl * ne);
+        fill(o->ebar_inv, ebar_inv, npe * npe * ne);
+        fill(o->fbar, fbar, npe * nfl * ne);
+        fill(o->hbar, hbar, nfl * npe * ne);
+        fill(o->rbar, rbar, nfl * ne);
+        fill(o->ru, ru, npe * ne);
+        fill(o->ruhat_e, ruhat_e, nfl * ne);
+        HDGB_CUDA(cudaStreamSynchronize(c->stream));
+        *out = o.release();
+    });
+}
+
 void hdgb_ops_destroy(hdgb_ops* o) { delete o; }
 
 static hdgb::DevBuf<double>* ops_field(hdgb_ops* o, const char* name) {

@@ -66,16 +66,18 @@ void apply_base_device(hdgb_precond* p, const double* y, double* z) {
 }
 
 // apply_poly (preconditioner.cpp:246-283); op = v -> base(K v).
-static void apply_poly_device(hdgb_precond* p, hdgb_matrix* k, const double* y, double* z) {
+void apply_poly_op(hdgb_precond* p, const DevOp& base, hdgb_matrix* k, const double* y, double* z) {
     hdgb_ctx* c = p->ctx;
-    const int64_t n = static_cast<int64_t>(p->mpf) * p->nf;
+    const int64_t n = k->n_dof();
+    const size_t ld = static_cast<size_t>(k->n_local());
+    if (p->wq.n != ld) { p->wq.alloc(ld); p->wt.alloc(ld); p->ws.alloc(ld); p->wkv.alloc(ld); }
     double *q = p->wq.p, *t = p->wt.p, *s = p->ws.p, *kv = p->wkv.p;
     double* w = z;
-    apply_base_device(p, y, q);
+    base(y, q);
     launch_fill(c, w, 0.0, n);
     auto op = [&](const double* in, double* out) {
         matvec_device(k, in, kv);
-        apply_base_device(p, kv, out);
+        base(kv, out);
         ++p->inner_ops;
     };
     const size_t cnt = p->ritz.size() / 2;
@@ -99,6 +101,10 @@ static void apply_poly_device(hdgb_precond* p, hdgb_matrix* k, const double* y, 
     }
 }
 
+static void apply_poly_device(hdgb_precond* p, hdgb_matrix* k, const double* y, double* z) {
+    apply_poly_op(p, [p](const double* in, double* out) { apply_base_device(p, in, out); }, k, y, z);
+}
+
 void apply_precond_device(hdgb_precond* p, hdgb_matrix* k, const double* y, double* z) {
     if (!p) {
         if (y != z)
@@ -111,16 +117,12 @@ void apply_precond_device(hdgb_precond* p, hdgb_matrix* k, const double* y, doub
 
 // compute_harmonic_ritz (preconditioner.cpp:119-205): seeded start vector, MGS Arnoldi on the
 // device, small eigen-solve and Leja ordering on the host.
-static std::vector<std::complex<double>> harmonic_ritz_device(hdgb_precond* p, hdgb_matrix* k, int degree,
-                                                              uint64_t seed, bool* breakdown_out) {
-    hdgb_ctx* c = p->ctx;
-    const int64_t n = k->n_dof();
+std::vector<std::complex<double>> harmonic_ritz_op(hdgb_ctx* c, const DevOp& op, int64_t n, int64_t ld, int degree,
+                                                   uint64_t seed, const int64_t* face_gid, int nf_local, int mpf,
+                                                   int64_t n_global, bool* breakdown_out) {
     if (degree < 1) throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: polynomial degree must be >= 1");
     // Seeded start vector over the GLOBAL unknowns (preconditioner.cpp:128-132); a rank keeps the
     // entries of its local faces, so the sequence does not depend on the partition.
-    const int mpf = k->mpf();
-    const int64_t ld = k->n_local();
-    const int64_t n_global = p->disc && !p->disc->face_gid.empty() ? p->disc->nf_global * mpf : n;
     if (degree > n_global) throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: polynomial degree exceeds the operator dimension");
     std::mt19937_64 rng(seed);
     std::vector<double> vg(n_global);
@@ -129,17 +131,17 @@ static std::vector<std::complex<double>> harmonic_ritz_device(hdgb_precond* p, h
     for (double x : vg) acc += x * x;  // same ascending order as the reference's dot
     const double nv = std::sqrt(acc);
     std::vector<double> v0(ld, 0.0);
-    if (n_global == n && ld == n) {
+    if (!face_gid) {
         for (int64_t i = 0; i < n; ++i) v0[i] = vg[i] / nv;
     } else {
-        for (int f = 0; f < k->nf_local; ++f) {
-            const int64_t gf = p->disc->face_gid[f];
+        for (int f = 0; f < nf_local; ++f) {
+            const int64_t gf = face_gid[f];
             for (int r = 0; r < mpf; ++r) v0[static_cast<int64_t>(f) * mpf + r] = vg[gf * mpf + r] / nv;
         }
     }
 
     const int pmax = degree;
-    DevBuf<double> basis(static_cast<size_t>(pmax) * ld), w(ld), kv(ld), sc(pmax + 4);
+    DevBuf<double> basis(static_cast<size_t>(pmax) * ld), w(ld), sc(pmax + 4);
     DevBuf<double> partial(multi_dot_workspace_doubles(n, 1));
     HDGB_CUDA(cudaMemcpyAsync(basis.p, v0.data(), ld * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     std::vector<double> hess(static_cast<size_t>(pmax + 1) * pmax, 0.0);
@@ -155,8 +157,7 @@ static std::vector<std::complex<double>> harmonic_ritz_device(hdgb_precond* p, h
     double scale = 1.0;
     std::vector<double> col(pmax + 2);
     for (int j = 0; j < pmax; ++j) {
-        matvec_device(k, basis.p + static_cast<size_t>(j) * ld, kv.p);
-        apply_base_device(p, kv.p, w.p);
+        op(basis.p + static_cast<size_t>(j) * ld, w.p);
         if (j == 0) {
             launch_sumsq(c, w.p, n, sc.p, partial.p);
             reduce(sc.p, 1);
@@ -185,6 +186,19 @@ static std::vector<std::complex<double>> harmonic_ritz_device(hdgb_precond* p, h
     return harmonic_ritz_from_hessenberg(hess.data(), pmax, p_eff);
 }
 
+static std::vector<std::complex<double>> harmonic_ritz_device(hdgb_precond* p, hdgb_matrix* k, int degree,
+                                                              uint64_t seed, bool* breakdown_out) {
+    const int64_t n = k->n_dof(), ld = k->n_local();
+    const bool dd = p->disc && !p->disc->face_gid.empty();
+    DevBuf<double> kv(ld);
+    return harmonic_ritz_op(p->ctx, [&](const double* in, double* out) {
+                                matvec_device(k, in, kv.p);
+                                apply_base_device(p, kv.p, out);
+                            },
+                            n, ld, degree, seed, dd ? p->disc->face_gid.data() : nullptr, k->nf_local, k->mpf(),
+                            dd ? p->disc->nf_global * k->mpf() : n, breakdown_out);
+}
+
 // Chebyshev nodes of the real interval covering the Ritz estimates, Leja-ordered.
 static std::vector<std::complex<double>> chebyshev_nodes(const std::vector<std::complex<double>>& ritz, int degree) {
     double lo = INFINITY, hi = -INFINITY;
@@ -203,45 +217,73 @@ static std::vector<std::complex<double>> chebyshev_nodes(const std::vector<std::
     return leja_order(nodes);
 }
 
-hdgb_precond* build_preconditioner_spec(hdgb_matrix* k, const hdgb_ops* o, hdgb_disc* d, const hdgb_precond_spec& spec) {
-    hdgb_ctx* c = k->ctx;
+static std::unique_ptr<hdgb_precond> new_precond(hdgb_ctx* c, int kind, int mpf, int nf, int nf_local, int n_lfe, hdgb_disc* d) {
     std::unique_ptr<hdgb_precond> p(new hdgb_precond());
     p->ctx = c;
-    p->kind = spec.kind;
-    p->mpf = k->mpf();
-    p->nf = k->nf;
-    p->nf_local = k->nf_local;
-    p->n_lfe = k->n_lfe;
+    p->kind = kind;
+    p->mpf = mpf;
+    p->nf = nf;
+    p->nf_local = nf_local;
+    p->n_lfe = n_lfe;
     p->disc = d;
+    return p;
+}
+
+// build_bj (preconditioner.cpp:30-46)
+hdgb_precond* build_bj_device(hdgb_matrix* k) {
+    hdgb_ctx* c = k->ctx;
+    auto p = new_precond(c, HDGB_PC_BJ, k->mpf(), k->nf, k->nf_local, k->n_lfe, nullptr);
+    const int mpf = p->mpf;
+    p->bj_inv.alloc(static_cast<size_t>(mpf) * mpf * k->nf);
+    launch_extract_diag(c, k->blocks.p, k->nf, mpf, k->nb(), p->bj_inv.p);
+    device_lu_invert(c, mpf, k->nf, p->bj_inv.p, p->bj_inv.p, "build_bj (face block)", HDGB_ERR_SINGULAR_BLOCK);
+    return p.release();
+}
+
+// build_asm (preconditioner.cpp:54-84).  The enriched diagonal sub-block of a face (both sides' K-bar_ll summed,
+// side 0 first, :59-75) IS the face's self block K_ff of the assembled operator: diag_from_k (mpf^2 per local
+// face, owned part filled) passes it in when K exists; nullptr sums it from K-bar directly, as the reference does.
+// Halo faces receive theirs from the owner, so ghost elements are enriched without a second ghost layer.
+hdgb_precond* build_asm_device(const hdgb_ops* o, hdgb_disc* d, int kind, const double* diag_from_k) {
+    if (!o || !d) throw Failure(HDGB_ERR_GENERIC, "build_asm needs the element operators and the discretisation");
+    hdgb_ctx* c = d->ctx;
+    const DiscView& v = d->view;
+    if (o->ne != v.ne || o->nfl != v.nfl) throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: build_asm operators / mesh");
+    auto p = new_precond(c, kind, v.mpf, v.nf_owned, v.nf, v.n_lfe, d);
+    p->ne = v.ne;
+    p->asm_inv.alloc(static_cast<size_t>(v.nfl) * v.nfl * v.ne);
+    DevBuf<double> diag;
+    double* dg = const_cast<double*>(diag_from_k);
+    if (!dg) {
+        diag.alloc(static_cast<size_t>(v.mpf) * v.mpf * v.nf);
+        launch_face_diag(c, v, o->kbar.p, diag.p);
+        dg = diag.p;
+    }
+    if (c->comm) c->comm->halo(c, dg, v.mpf * v.mpf);
+    launch_asm_enrich(c, v, o->kbar.p, dg, p->asm_inv.p);
+    device_lu_invert(c, v.nfl, v.ne, p->asm_inv.p, p->asm_inv.p, "build_asm (element block)", HDGB_ERR_SINGULAR_BLOCK);
+    p->ze.alloc(static_cast<size_t>(v.nfl) * v.ne);
+    return p.release();
+}
+
+hdgb_precond* build_preconditioner_spec(hdgb_matrix* k, const hdgb_ops* o, hdgb_disc* d, const hdgb_precond_spec& spec) {
+    hdgb_ctx* c = k->ctx;
+    std::unique_ptr<hdgb_precond> p;
     const int64_t n = k->n_dof();
     switch (spec.kind) {
-        case HDGB_PC_IDENTITY: break;
-        case HDGB_PC_BJ: {
-            // build_bj (preconditioner.cpp:30-46)
-            const int mpf = p->mpf;
-            p->bj_inv.alloc(static_cast<size_t>(mpf) * mpf * k->nf);
-            launch_extract_diag(c, k->blocks.p, k->nf, mpf, k->nb(), p->bj_inv.p);
-            device_lu_invert(c, mpf, k->nf, p->bj_inv.p, p->bj_inv.p, "build_bj (face block)", HDGB_ERR_SINGULAR_BLOCK);
+        case HDGB_PC_IDENTITY: p = new_precond(c, HDGB_PC_IDENTITY, k->mpf(), k->nf, k->nf_local, k->n_lfe, d); break;
+        case HDGB_PC_BJ:
+            p.reset(build_bj_device(k));
+            p->disc = d;
             break;
-        }
         case HDGB_PC_ASM:
         case HDGB_PC_RAS: {
-            // build_asm (preconditioner.cpp:54-84)
             if (!o || !d) throw Failure(HDGB_ERR_GENERIC, "build_asm needs the element operators and the discretisation");
-            const DiscView& v = d->view;
-            if (v.mpf != p->mpf || v.nf_owned != p->nf)
+            if (d->view.mpf != k->mpf() || d->view.nf_owned != k->nf)
                 throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: build_asm matrix / mesh");
-            p->ne = v.ne;
-            p->asm_inv.alloc(static_cast<size_t>(v.nfl) * v.nfl * v.ne);
-            // The enriched diagonal sub-block of a face (both sides' K-bar_ll summed, side 0 first,
-            // preconditioner.cpp:59-75) IS the face's self block K_ff of the assembled operator; halo
-            // faces receive theirs from the owner, so ghost elements are enriched without a 2nd layer.
-            DevBuf<double> diag(static_cast<size_t>(p->mpf) * p->mpf * v.nf);
-            launch_extract_diag(c, k->blocks.p, k->nf, p->mpf, k->nb(), diag.p);
-            if (c->comm) c->comm->halo(c, diag.p, p->mpf * p->mpf);
-            launch_asm_enrich(c, v, o->kbar.p, diag.p, p->asm_inv.p);
-            device_lu_invert(c, v.nfl, v.ne, p->asm_inv.p, p->asm_inv.p, "build_asm (element block)", HDGB_ERR_SINGULAR_BLOCK);
-            p->ze.alloc(static_cast<size_t>(v.nfl) * v.ne);
+            DevBuf<double> diag(static_cast<size_t>(k->mpf()) * k->mpf() * d->view.nf);
+            launch_extract_diag(c, k->blocks.p, k->nf, k->mpf(), k->nb(), diag.p);
+            p.reset(build_asm_device(o, d, spec.kind, diag.p));
             break;
         }
         default: throw Failure(HDGB_ERR_UNSUPPORTED, "unknown preconditioner kind");
@@ -521,6 +563,116 @@ hdgb_status hdgb_precond_apply(hdgb_precond* p, hdgb_matrix* k, const double* y,
         apply_precond_device(p, k, Y.dev, Z.dev);
         Z.commit();
         if (!Y.tmp.p && !Z.host) return;
+        HDGB_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+// ---- per-function entry points of preconditioner.hpp:31-76 ------------------------------------------------
+hdgb_status hdgb_build_bj(hdgb_matrix* k, hdgb_precond** out) {
+    *out = nullptr;
+    return guarded(k->ctx, [&] {
+        *out = build_bj_device(k);
+        HDGB_CUDA(cudaStreamSynchronize(k->ctx->stream));
+    });
+}
+
+hdgb_status hdgb_build_asm(const hdgb_ops* o, hdgb_disc* d, hdgb_precond** out) {
+    *out = nullptr;
+    return guarded(d->ctx, [&] {
+        *out = build_asm_device(o, d, HDGB_PC_ASM, nullptr);
+        HDGB_CUDA(cudaStreamSynchronize(d->ctx->stream));
+    });
+}
+
+static hdgb_status apply_kind(hdgb_precond* p, int kind_a, int kind_b, const char* what, const double* y, double* z) {
+    hdgb_ctx* c = p->ctx;
+    return guarded(c, [&] {
+        if (p->kind != kind_a && p->kind != kind_b)
+            throw Failure(HDGB_ERR_DIMENSION_MISMATCH, std::string("dimension mismatch: ") + what + " on a preconditioner of another kind");
+        const size_t n = static_cast<size_t>(p->mpf) * std::max(p->nf, p->nf_local);
+        InArg Y(c, y, n);
+        OutArg Z(c, z, n);
+        apply_base_device(p, Y.dev, Z.dev);
+        Z.commit();
+        if (!Y.tmp.p && !Z.host) return;
+        HDGB_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+hdgb_status hdgb_apply_bj(hdgb_precond* p, const double* y, double* z) { return apply_kind(p, HDGB_PC_BJ, HDGB_PC_BJ, "apply_bj", y, z); }
+hdgb_status hdgb_apply_asm(hdgb_precond* p, const double* y, double* z) { return apply_kind(p, HDGB_PC_ASM, HDGB_PC_RAS, "apply_asm", y, z); }
+
+hdgb_status hdgb_precond_create(hdgb_ctx* c, int kind, int mpf, int nf, hdgb_disc* d, const double* inv,
+                                const double* ritz_reim, int n_ritz, hdgb_precond** out) {
+    *out = nullptr;
+    return guarded(c, [&] {
+        if (mpf < 1 || nf < 0 || n_ritz < 0) throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: invalid preconditioner dimensions");
+        std::unique_ptr<hdgb_precond> p;
+        switch (kind) {
+            case HDGB_PC_IDENTITY: p = new_precond(c, kind, mpf, nf, nf, 0, d); break;
+            case HDGB_PC_BJ: {
+                if (!inv) throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: block-Jacobi inverses missing");
+                p = new_precond(c, kind, mpf, nf, nf, 0, d);
+                p->bj_inv.alloc(static_cast<size_t>(mpf) * mpf * nf);
+                HDGB_CUDA(cudaMemcpyAsync(p->bj_inv.p, inv, p->bj_inv.n * sizeof(double), cudaMemcpyDefault, c->stream));
+                break;
+            }
+            case HDGB_PC_ASM:
+            case HDGB_PC_RAS: {
+                if (!inv || !d) throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: additive Schwarz needs the inverses and the discretisation");
+                const DiscView& v = d->view;
+                if (v.mpf != mpf || v.nf_owned != nf) throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: preconditioner / mesh");
+                p = new_precond(c, kind, mpf, v.nf_owned, v.nf, v.n_lfe, d);
+                p->ne = v.ne;
+                p->asm_inv.alloc(static_cast<size_t>(v.nfl) * v.nfl * v.ne);
+                HDGB_CUDA(cudaMemcpyAsync(p->asm_inv.p, inv, p->asm_inv.n * sizeof(double), cudaMemcpyDefault, c->stream));
+                p->ze.alloc(static_cast<size_t>(v.nfl) * v.ne);
+                break;
+            }
+            default: throw Failure(HDGB_ERR_UNSUPPORTED, "unknown preconditioner kind");
+        }
+        if (n_ritz > 0) {
+            p->ritz.assign(ritz_reim, ritz_reim + 2 * static_cast<size_t>(n_ritz));
+            p->poly_degree = n_ritz;
+        }
+        HDGB_CUDA(cudaStreamSynchronize(c->stream));
+        *out = p.release();
+    });
+}
+
+// Wraps a C callback as a device operator; a non-zero return aborts the calling algorithm.
+static DevOp wrap_op(hdgb_op_fn fn, void* user, int64_t n, const char* what) {
+    return [fn, user, n, what](const double* in, double* out) {
+        if (fn(user, in, out, n) != 0) throw Failure(HDGB_ERR_GENERIC, std::string(what) + ": operator callback failed");
+    };
+}
+
+hdgb_status hdgb_compute_harmonic_ritz(hdgb_ctx* c, hdgb_op_fn op, void* user, int64_t n_dof, int degree, uint64_t seed,
+                                       double* out_reim, int* n_out) {
+    if (n_out) *n_out = 0;
+    return guarded(c, [&] {
+        if (!op) throw Failure(HDGB_ERR_GENERIC, "compute_harmonic_ritz: operator callback missing");
+        const auto th = harmonic_ritz_op(c, wrap_op(op, user, n_dof, "compute_harmonic_ritz"), n_dof, n_dof, degree, seed,
+                                         nullptr, 0, 1, n_dof, nullptr);
+        for (size_t i = 0; i < th.size(); ++i) { out_reim[2 * i] = th[i].real(); out_reim[2 * i + 1] = th[i].imag(); }
+        if (n_out) *n_out = static_cast<int>(th.size());
+    });
+}
+
+hdgb_status hdgb_apply_poly(hdgb_precond* p, hdgb_op_fn base_apply, void* user, hdgb_matrix* k, const double* y, double* z,
+                            int64_t* inner_ops) {
+    hdgb_ctx* c = p->ctx;
+    return guarded(c, [&] {
+        if (static_cast<int64_t>(p->mpf) * p->nf != k->n_dof())
+            throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: preconditioner / operator size");
+        const size_t n = static_cast<size_t>(k->n_local());
+        InArg Y(c, y, n);
+        OutArg Z(c, z, n);
+        const int64_t before = p->inner_ops;
+        if (base_apply) apply_poly_op(p, wrap_op(base_apply, user, k->n_dof(), "apply_poly"), k, Y.dev, Z.dev);
+        else apply_poly_op(p, [p](const double* in, double* out) { apply_base_device(p, in, out); }, k, Y.dev, Z.dev);
+        if (inner_ops) *inner_ops += p->inner_ops - before;
+        Z.commit();
         HDGB_CUDA(cudaStreamSynchronize(c->stream));
     });
 }

@@ -19,21 +19,7 @@ namespace {
 
 GmresWork& gmres_work(hdgb_matrix* k, int restart) {
     const int64_t n = k->n_dof();
-    const int64_t ld = k->n_local();
-    if (!k->work || k->work->restart < restart || k->work->n != n) {
-        k->work.reset(new GmresWork());
-        GmresWork& w = *k->work;
-        w.restart = restart;
-        w.n = n;
-        w.basis.alloc(static_cast<size_t>(restart + 1) * ld);
-        w.kv.alloc(ld);
-        w.r.alloc(ld);
-        w.coef.alloc(2 * static_cast<size_t>(restart + 1) + 4);
-        w.partial.alloc(multi_dot_workspace_doubles(n, restart + 1));
-        w.ycoef.alloc(restart + 1);
-        w.cgs.alloc(cgs_workspace_doubles(k->ctx));
-        w.cgs.zero(k->ctx->stream);
-    }
+    if (!k->work || k->work->restart < restart || k->work->n != n) k->work = make_gmres_work(k->ctx, n, k->n_local(), restart);
     return *k->work;
 }
 
@@ -121,19 +107,43 @@ void orthogonalize_device(hdgb_ctx* c, const double* V, int64_t ldv, int nvec, i
 
 }  // namespace
 
+std::unique_ptr<GmresWork> make_gmres_work(hdgb_ctx* c, int64_t n, int64_t ld, int restart) {
+    std::unique_ptr<GmresWork> work(new GmresWork());
+    GmresWork& w = *work;
+    w.restart = restart;
+    w.n = n;
+    w.basis.alloc(static_cast<size_t>(restart + 1) * ld);
+    w.kv.alloc(ld);
+    w.r.alloc(ld);
+    w.coef.alloc(2 * static_cast<size_t>(restart + 1) + 4);
+    w.partial.alloc(multi_dot_workspace_doubles(n, restart + 1));
+    w.ycoef.alloc(restart + 1);
+    w.cgs.alloc(cgs_workspace_doubles(c));
+    w.cgs.zero(c->stream);
+    return work;
+}
+
 void gmres_device(hdgb_matrix* k, hdgb_precond* p, const double* rhs, double* x, const hdgb_gmres_config& cfg,
                   hdgb_gmres_stats* st, double* residual_trace) {
-    hdgb_ctx* c = k->ctx;
-    const int64_t n = k->n_dof();    // owned unknowns: rows, sums
-    const int64_t ld = k->n_local(); // vector length incl. the halo part
+    if (cfg.restart < 1) throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: GMRES restart length must be >= 1");
+    GmresWork& W = gmres_work(k, cfg.restart);
+    gmres_core(k->ctx, k->n_dof(), k->n_local(), W, [k](const double* in, double* out) { matvec_device(k, in, out); },
+               [k, p](const double* in, double* out) { apply_precond_device(p, k, in, out); }, rhs, x, cfg, st, residual_trace);
+}
+
+void gmres_core(hdgb_ctx* c, int64_t n, int64_t ld, GmresWork& W, const DevOp& matvec, const DevOp& precond,
+                const double* rhs, double* x, const hdgb_gmres_config& cfg, hdgb_gmres_stats* st, double* residual_trace) {
     const int m = cfg.restart;
     if (m < 1) throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: GMRES restart length must be >= 1");
     if (2 * static_cast<size_t>(m + 1) + 4 > c->pinned_doubles) throw Failure(HDGB_ERR_UNSUPPORTED, "GMRES restart length too large");
-    GmresWork& W = gmres_work(k, m);
     std::memset(st, 0, sizeof(*st));
     double* kv = W.kv.p;
     double* r = W.r.p;
     double* V = W.basis.p;
+    auto apply_prec = [&](const double* in, double* out) {
+        if (precond) precond(in, out);
+        else if (in != out) HDGB_CUDA(cudaMemcpyAsync(out, in, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    };
 
     auto norm_of = [&](const double* v) {
         launch_sumsq(c, v, n, W.coef.p, W.partial.p);
@@ -146,11 +156,11 @@ void gmres_device(hdgb_matrix* k, hdgb_precond* p, const double* rhs, double* x,
     // r = P^-1 (rhs - K x)   (gmres.cpp:73-81)
     auto residual = [&](double* out) {
         PhaseTimer tm(c, &st->t_mv);
-        matvec_device(k, x, kv);
+        matvec(x, kv);
         launch_lincomb(c, 1.0, rhs, -1.0, kv, kv, n);
         tm.stop();
         PhaseTimer tp(c, &st->t_prec);
-        apply_precond_device(p, k, kv, out);
+        apply_prec(kv, out);
         tp.stop();
     };
 
@@ -188,10 +198,10 @@ void gmres_device(hdgb_matrix* k, hdgb_precond* p, const double* rhs, double* x,
             double* w = V + static_cast<size_t>(j + 1) * ld;  // the candidate lands in its basis slot
             {
                 PhaseTimer tm(c, &st->t_mv);
-                matvec_device(k, V + static_cast<size_t>(j) * ld, kv);
+                matvec(V + static_cast<size_t>(j) * ld, kv);
                 tm.stop();
                 PhaseTimer tp(c, &st->t_prec);
-                apply_precond_device(p, k, kv, w);
+                apply_prec(kv, w);
                 tp.stop();
             }
             {
@@ -322,6 +332,39 @@ hdgb_status hdgb_gmres_solve(hdgb_matrix* k, hdgb_precond* p, const double* rhs,
         else if (X.host) HDGB_CUDA(cudaMemcpyAsync(X.dev, x0, n * sizeof(double), cudaMemcpyDefault, c->stream));
         hdgb_gmres_stats local;
         gmres_device(k, p, B.dev, X.dev, cf, stats ? stats : &local, residual_trace);
+        X.commit();
+        HDGB_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+hdgb_status hdgb_gmres_solve_fn(hdgb_ctx* c, int64_t n, hdgb_op_fn matvec, void* mv_user, hdgb_op_fn precond, void* pc_user,
+                                const double* rhs, const double* x0, const hdgb_gmres_config* cfg, double* x,
+                                hdgb_gmres_stats* stats, double* residual_trace) {
+    return guarded(c, [&] {
+        hdgb_gmres_config cf;
+        hdgb_gmres_config_default(&cf);
+        if (cfg) cf = *cfg;
+        if (!matvec) throw Failure(HDGB_ERR_GENERIC, "gmres_solve: operator callback missing");
+        if (n < 0 || cf.restart < 1) throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: GMRES size / restart length");
+        const size_t sz = static_cast<size_t>(n);
+        InArg B(c, rhs, sz);
+        OutArg X(c, x, sz);
+        if (x0 && x0 != x) HDGB_CUDA(cudaMemcpyAsync(X.dev, x0, sz * sizeof(double), cudaMemcpyDefault, c->stream));
+        else if (!x0) HDGB_CUDA(cudaMemsetAsync(X.dev, 0, sz * sizeof(double), c->stream));
+        else if (X.host) HDGB_CUDA(cudaMemcpyAsync(X.dev, x0, sz * sizeof(double), cudaMemcpyDefault, c->stream));
+        auto wrap = [n](hdgb_op_fn fn, void* user, const char* what) -> DevOp {
+            if (!fn) return DevOp();
+            return [fn, user, n, what](const double* in, double* out) {
+                if (fn(user, in, out, n) != 0) throw Failure(HDGB_ERR_GENERIC, std::string("gmres_solve: ") + what + " callback failed");
+            };
+        };
+        // the restart length never needs to exceed the iteration cap (basis storage)
+        hdgb_gmres_config run = cf;
+        std::unique_ptr<GmresWork> W = make_gmres_work(c, n, n, std::max(1, std::min(cf.restart, cf.max_iters)));
+        run.restart = W->restart;
+        hdgb_gmres_stats local;
+        gmres_core(c, n, n, *W, wrap(matvec, mv_user, "matvec"), wrap(precond, pc_user, "preconditioner"), B.dev, X.dev, run,
+                   stats ? stats : &local, residual_trace);
         X.commit();
         HDGB_CUDA(cudaStreamSynchronize(c->stream));
     });

@@ -3,7 +3,7 @@
 // extraction (preconditioner.cpp:33-37) and the additive-Schwarz enrichment (:54-75).
 // Every face (row) is owned by one CTA: no atomics, side 0 is accumulated before side 1 exactly
 // like the reference.  Roofline: HBM (pure data movement, K written once).
-#include "kernels_local.cuh"
+#include "solver.cuh"
 
 namespace hdgb {
 
@@ -77,6 +77,22 @@ __global__ void extract_diag_kernel(const double* __restrict__ blocks, int64_t t
     diag[i] = blocks[f * bsz * nb + (i - f * bsz)];
 }
 
+// diag[f] = K-bar^{e0}_{l0 l0} + K-bar^{e1}_{l1 l1}: the self-block accumulation of assemble_global (side 0 first,
+// preconditioner.cpp:59-75) without forming K -- build_asm(ops, mesh) as a stand-alone entry point.
+__global__ void face_diag_kernel(DiscView dv, const double* __restrict__ kbar, double* __restrict__ diag) {
+    const int f = blockIdx.x;
+    const int mpf = dv.mpf, nfl = dv.nfl;
+    const int e0 = dv.face_elems[2 * f], e1 = dv.face_elems[2 * f + 1];
+    const int l0 = dv.face_lidx[2 * f], l1 = dv.face_lidx[2 * f + 1];
+    for (int t = threadIdx.x; t < mpf * mpf; t += blockDim.x) {
+        const int c = t / mpf, r = t - c * mpf;
+        double v = 0.0;
+        if (e0 >= 0) v += kbar[static_cast<size_t>(e0) * nfl * nfl + static_cast<size_t>(l0 * mpf + c) * nfl + (l0 * mpf + r)];
+        if (e1 >= 0) v += kbar[static_cast<size_t>(e1) * nfl * nfl + static_cast<size_t>(l1 * mpf + c) * nfl + (l1 * mpf + r)];
+        diag[static_cast<size_t>(f) * mpf * mpf + t] = v;
+    }
+}
+
 // One CTA per element: copy K-bar and overwrite the diagonal sub-block of every face with the
 // two-sided sum (side 0 + side 1, preconditioner.cpp:67-71), which the assembled operator already
 // holds as the face's self block diag[f] (face_matrix.cpp:29-39: same terms, same order).
@@ -120,6 +136,13 @@ void launch_extract_diag(hdgb_ctx* ctx, const double* blocks, int nf, int mpf, i
     const int64_t total = static_cast<int64_t>(nf) * mpf * mpf;
     if (total == 0) return;
     extract_diag_kernel<<<ceil_div(total, 256), 256, 0, ctx->stream>>>(blocks, total, mpf * mpf, nb, diag);
+    HDGB_LAUNCH_CHECK(ctx);
+}
+
+void launch_face_diag(hdgb_ctx* ctx, const DiscView& dv, const double* kbar, double* diag) {
+    if (dv.nf_owned == 0) return;
+    const int work = dv.mpf * dv.mpf;
+    face_diag_kernel<<<dv.nf_owned, work < 256 ? ((work + 31) / 32) * 32 : 256, 0, ctx->stream>>>(dv, kbar, diag);
     HDGB_LAUNCH_CHECK(ctx);
 }
 

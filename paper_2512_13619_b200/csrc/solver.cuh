@@ -2,6 +2,9 @@
 // api_solve.cu).  Everything here enqueues on ctx->stream; functions that return host values
 // synchronise.
 #pragma once
+#include <complex>
+#include <functional>
+
 #include "kernels_local.cuh"
 
 namespace hdgb {
@@ -28,6 +31,30 @@ void recover_local_device(hdgb_disc* d, const hdgb_ops* o, const double* duhat, 
 
 // compute_q (local_ops.cpp:367-374) on the device state
 void compute_q_device(hdgb_disc* d, hdgb_state* s);
+
+// A linear operator on device vectors (the reference's OpFn / LinearOp, gmres.hpp:43, preconditioner.hpp:50, with
+// device pointers): out = op(in), enqueued on ctx->stream.
+using DevOp = std::function<void(const double* in, double* out)>;
+
+// gmres_solve (gmres.cpp:61-228) for arbitrary operators: n owned unknowns (rows, sums), ld = vector length
+// incl. the halo part; precond empty = identity.  W is sized by make_gmres_work.
+std::unique_ptr<GmresWork> make_gmres_work(hdgb_ctx* c, int64_t n, int64_t ld, int restart);
+void gmres_core(hdgb_ctx* c, int64_t n, int64_t ld, GmresWork& W, const DevOp& matvec, const DevOp& precond,
+                const double* rhs, double* x, const hdgb_gmres_config& cfg, hdgb_gmres_stats* stats,
+                double* residual_trace);
+// compute_harmonic_ritz (preconditioner.cpp:119-205) of op on n owned unknowns (ld vector length): seeded start
+// vector over n_global unknowns (face_gid maps local faces of width mpf to global ones, nullptr = identity),
+// MGS Arnoldi on the device, eigen-solve + Leja order on the host.
+std::vector<std::complex<double>> harmonic_ritz_op(hdgb_ctx* c, const DevOp& op, int64_t n, int64_t ld, int degree,
+                                                   uint64_t seed, const int64_t* face_gid, int nf_local, int mpf,
+                                                   int64_t n_global, bool* breakdown_out);
+// apply_poly (preconditioner.cpp:246-283) with an arbitrary base application: z = poly(base K) base y.
+void apply_poly_op(hdgb_precond* p, const DevOp& base, hdgb_matrix* k, const double* y, double* z);
+// the two-sided diagonal sub-block sums of build_asm (preconditioner.cpp:59-75) straight from K-bar
+void launch_face_diag(hdgb_ctx* ctx, const DiscView& dv, const double* kbar, double* diag);
+// build_bj (preconditioner.cpp:30-46) / build_asm (:54-84) as separate entry points
+hdgb_precond* build_bj_device(hdgb_matrix* k);
+hdgb_precond* build_asm_device(const hdgb_ops* o, hdgb_disc* d, int kind, const double* diag_from_k);
 
 // gmres_solve (gmres.cpp:61-228) on device vectors rhs / x (x holds x0 on entry).
 void gmres_device(hdgb_matrix* k, hdgb_precond* p, const double* rhs, double* x, const hdgb_gmres_config& cfg,

@@ -32,6 +32,8 @@ __all__ = [
     "lu_invert_batch", "gemm_batch", "gemv_strided_batch", "compute_q", "assemble_element_operators",
     "assemble_residual", "gather_element_trace", "recover_local", "assemble_global", "block_matvec",
     "gather_extended", "write_matrix", "read_matrix", "build_preconditioner", "leja_order",
+    "build_bj", "apply_bj", "build_asm", "apply_asm", "compute_harmonic_ritz", "apply_poly", "gmres_solve_fn",
+    "precond_from_host", "ops_from_host",
     "harmonic_ritz_from_hessenberg", "gmres_solve", "orthogonalize", "newton_solve", "time_march",
     "make_case_model", "make_initial_state", "library_path", "load_library", "random_vector", "set_tuning",
     "SHAPES", "MODELS", "PRECONDS",
@@ -157,6 +159,9 @@ class SolveReport:
                 f"final_residual={self.final_residual:.6e}, converged={self.converged})")
 
 
+# hdgb_op_fn: int (*)(void* user, const double* in, double* out, int64_t n) on DEVICE vectors
+OP_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64)
+
 _lib = None
 
 
@@ -229,6 +234,14 @@ def load_library():
         "hdgb_comm_rank": (i, [_vp]), "hdgb_comm_size": (i, [_vp]),
         "hdgb_device_alloc": (i, [_vp, i64, pp]), "hdgb_device_free": (None, [_vp, _vp]),
         "hdgb_copy": (i, [_vp, _vp, _vp, i64]),
+        "hdgb_ops_create": (i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, pp]),
+        "hdgb_build_bj": (i, [_vp, pp]), "hdgb_apply_bj": (i, [_vp, _vp, _vp]),
+        "hdgb_build_asm": (i, [_vp, _vp, pp]), "hdgb_apply_asm": (i, [_vp, _vp, _vp]),
+        "hdgb_precond_create": (i, [_vp, i, i, i, _vp, _vp, _vp, i, pp]),
+        "hdgb_compute_harmonic_ritz": (i, [_vp, OP_FN, _vp, i64, i, u64, _vp, C.POINTER(i)]),
+        "hdgb_apply_poly": (i, [_vp, OP_FN, _vp, _vp, _vp, _vp, C.POINTER(i64)]),
+        "hdgb_gmres_solve_fn": (i, [_vp, i64, OP_FN, _vp, OP_FN, _vp, _vp, _vp, C.POINTER(GmresConfig), _vp,
+                                    C.POINTER(GmresStats), _vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)  # AttributeError = the library does not export what the header declares
@@ -922,6 +935,10 @@ class Preconditioner:
     def __init__(self, ctx, handle, k):
         self.ctx, self._h, self.k = ctx, handle, k
 
+    @property
+    def _n_vec(self):
+        return self.k.n_vec if hasattr(self.k, "n_vec") else self.k.n_dof
+
     def __del__(self):
         try:
             if getattr(self, "_h", None):
@@ -951,14 +968,14 @@ class Preconditioner:
     def apply_base(self, y, z=None):
         """make_base_apply (preconditioner.cpp:285-299)."""
         y = _f64(y)
-        out = np.empty(self.k.n_vec) if z is None else z
+        out = np.empty(self._n_vec) if z is None else z
         self.ctx.check(self.ctx._L.hdgb_precond_apply_base(self._h, _ptr(y), _ptr(out)))
         return out
 
     def apply(self, y, z=None):
         """make_preconditioner_apply (preconditioner.cpp:301-308)."""
         y = _f64(y)
-        out = np.empty(self.k.n_vec) if z is None else z
+        out = np.empty(self._n_vec) if z is None else z
         self.ctx.check(self.ctx._L.hdgb_precond_apply(self._h, self.k._h, _ptr(y), _ptr(out)))
         return out
 
@@ -975,6 +992,123 @@ def build_preconditioner(spec, k: FaceBlockMatrix, ops: ElementOperators = None,
     k.ctx.check(k.ctx._L.hdgb_build_preconditioner(k._h, ops._h if ops else None, disc._h if disc else None,
                                                    C.byref(spec), C.byref(h)))
     return Preconditioner(k.ctx, h, k)
+
+
+def build_bj(k: FaceBlockMatrix) -> Preconditioner:
+    """build_bj (preconditioner.cpp:30-46)."""
+    h = _vp()
+    k.ctx.check(k.ctx._L.hdgb_build_bj(k._h, C.byref(h)))
+    return Preconditioner(k.ctx, h, k)
+
+
+def build_asm(ops: ElementOperators, disc: Discretization, k: FaceBlockMatrix = None) -> Preconditioner:
+    """build_asm (preconditioner.cpp:54-84) from the element operators and the mesh alone; k is only kept for the
+    vector size of Preconditioner.apply*."""
+    h = _vp()
+    disc.ctx.check(disc.ctx._L.hdgb_build_asm(ops._h, disc._h, C.byref(h)))
+    return Preconditioner(disc.ctx, h, k if k is not None else disc)
+
+
+def apply_bj(p: Preconditioner, y, z=None):
+    """apply_bj (preconditioner.cpp:48-52)."""
+    y = _f64(y)
+    out = np.empty(len(y)) if z is None else z
+    p.ctx.check(p.ctx._L.hdgb_apply_bj(p._h, _ptr(y), _ptr(out)))
+    return out
+
+
+def apply_asm(p: Preconditioner, y, z=None):
+    """apply_asm (preconditioner.cpp:86-105)."""
+    y = _f64(y)
+    out = np.empty(len(y)) if z is None else z
+    p.ctx.check(p.ctx._L.hdgb_apply_asm(p._h, _ptr(y), _ptr(out)))
+    return out
+
+
+def precond_from_host(ctx: Context, kind, mpf, nf, inv=None, disc: Discretization = None, ritz=None, k=None) -> Preconditioner:
+    """A Preconditioner from caller data (hdgb_precond_create): the reference's value type handed to the device."""
+    kd = PRECONDS[kind] if isinstance(kind, str) else int(kind)
+    buf, n = None, 0
+    if ritz is not None and len(ritz):
+        th = np.asarray(ritz, dtype=np.complex128)
+        buf = np.empty(2 * len(th))
+        buf[0::2], buf[1::2] = th.real, th.imag
+        n = len(th)
+    h = _vp()
+    inv = _f64(inv)
+    ctx.check(ctx._L.hdgb_precond_create(ctx._h, kd, mpf, nf, disc._h if disc else None, _ptr(inv), _ptr(buf), n, C.byref(h)))
+    return Preconditioner(ctx, h, k)
+
+
+def ops_from_host(disc: Discretization, kbar, ebar_inv, fbar, hbar, rbar, ru, ruhat_e=None) -> ElementOperators:
+    """ElementOperators from caller data (hdgb_ops_create)."""
+    arrs = [_f64(a) for a in (kbar, ebar_inv, fbar, hbar, rbar, ru, ruhat_e)]
+    h = _vp()
+    disc.ctx.check(disc.ctx._L.hdgb_ops_create(disc._h, *[_ptr(a) for a in arrs], C.byref(h)))
+    return ElementOperators(disc, h)
+
+
+def _wrap_op(fn, errors):
+    """Python callable (in_ptr, out_ptr, n) on device addresses -> hdgb_op_fn; exceptions are parked in `errors`."""
+    if fn is None:
+        return C.cast(None, OP_FN)
+
+    def thunk(_user, din, dout, n):
+        try:
+            fn(din, dout, n)
+            return 0
+        except BaseException as e:  # must not propagate through the C frames
+            errors.append(e)
+            return 1
+    return OP_FN(thunk)
+
+
+def compute_harmonic_ritz(ctx: Context, op, n_dof: int, degree: int, seed: int = 12345) -> np.ndarray:
+    """compute_harmonic_ritz (preconditioner.cpp:119-205) of a callable op(in_ptr, out_ptr, n) on device vectors."""
+    errors = []
+    cb = _wrap_op(op, errors)
+    out = np.empty(2 * max(degree, 1))
+    n = C.c_int()
+    st = ctx._L.hdgb_compute_harmonic_ritz(ctx._h, cb, None, n_dof, degree, seed, _ptr(out), C.byref(n))
+    if errors:
+        raise errors[0]
+    ctx.check(st)
+    return out[0:2 * n.value:2] + 1j * out[1:2 * n.value:2]
+
+
+def apply_poly(p: Preconditioner, k: FaceBlockMatrix, y, base=None, z=None):
+    """apply_poly (preconditioner.cpp:246-283); base = callable(in_ptr, out_ptr, n) on device vectors or None (p's own
+    base).  Returns (z, inner operator applications)."""
+    errors = []
+    cb = _wrap_op(base, errors)
+    y = _f64(y)
+    out = np.empty(k.n_vec) if z is None else z
+    ops = C.c_int64(0)
+    st = p.ctx._L.hdgb_apply_poly(p._h, cb, None, k._h, _ptr(y), _ptr(out), C.byref(ops))
+    if errors:
+        raise errors[0]
+    p.ctx.check(st)
+    return out, ops.value
+
+
+def gmres_solve_fn(ctx: Context, n: int, matvec, precond, rhs, x0=None, cfg: GmresConfig = None, x=None):
+    """gmres_solve (gmres.cpp:61-228), closure form of gmres.hpp:50-53: matvec / precond are callables
+    (in_ptr, out_ptr, n) on device vectors (precond None = identity).  Returns (x, GmresStats)."""
+    cfg = cfg or GmresConfig()
+    errors = []
+    mv, pc = _wrap_op(matvec, errors), _wrap_op(precond, errors)
+    rhs, x0 = _f64(rhs), _f64(x0)
+    out = np.empty(n) if x is None else x
+    st = GmresStats()
+    trace = np.zeros(max(cfg.max_iters, 1)) if cfg.track_diagnostics else None
+    rc = ctx._L.hdgb_gmres_solve_fn(ctx._h, n, mv, None, pc, None, _ptr(rhs), _ptr(x0), C.byref(cfg), _ptr(out), C.byref(st),
+                                    _ptr(trace))
+    if errors:
+        raise errors[0]
+    ctx.check(rc)
+    if trace is not None:
+        st.residual_trace = trace[: st.iters]
+    return out, st
 
 
 def leja_order(theta) -> np.ndarray:

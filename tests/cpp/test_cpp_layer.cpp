@@ -3,6 +3,8 @@
 // with the reference's error behaviour (exception type + offending batch index).
 #include <cmath>
 #include <cstdio>
+#include <stdexcept>
+#include <string>
 #include <vector>
 
 #include "hdgb200.hpp"
@@ -98,6 +100,71 @@ int main() {
         try { assemble_element_operators(m3, s4, d3, bad_tc); } catch (const InconsistentDimensions&) { threw_t = true; }
         EXPECT(threw_t);
         std::printf("hex ASM: steady newton=%d gmres=%ld, transient newton=%d\n", r3.n_newton, r3.n_gmres_total, r4.n_newton);
+    }
+
+    // ---- the per-function preconditioner API and the closure forms (preconditioner.hpp:31-76, gmres.hpp:50-53) ----
+    {
+        Preconditioner pbj = build_bj(K);
+        Preconditioner pspec = build_preconditioner(bj, K, ops, disc);
+        const std::vector<double> yv = rhs;
+        const auto z1 = apply_bj(ctx, pbj, yv), z2 = apply_preconditioner(pspec, K, yv);
+        double dz = 0.0;
+        for (size_t i = 0; i < z1.size(); ++i) dz = std::fmax(dz, std::fabs(z1[i] - z2[i]));
+        EXPECT(dz == 0.0);  // same kernels, same data: bit-identical
+        Preconditioner pasm = build_asm(ops, disc);
+        PrecondSpec as_spec;
+        as_spec.kind = PrecondKind::ASM;
+        Preconditioner pasm2 = build_preconditioner(as_spec, K, ops, disc);
+        const auto a1 = apply_asm(ctx, pasm, yv), a2 = apply_preconditioner(pasm2, K, yv);
+        double da = 0.0, amax = 0.0;
+        for (size_t i = 0; i < a1.size(); ++i) { da = std::fmax(da, std::fabs(a1[i] - a2[i])); amax = std::fmax(amax, std::fabs(a2[i])); }
+        EXPECT(da <= 1e-12 * std::fmax(1.0, amax));  // enrichment summed from K-bar vs read from K: same terms, same order
+        bool wrong_kind = false;
+        try { apply_asm(ctx, pbj, yv); } catch (const DimensionMismatch&) { wrong_kind = true; }
+        EXPECT(wrong_kind);
+
+        // closure-form GMRES == handle-form GMRES (identical operators, identical control flow)
+        GmresConfig gc;
+        gc.tol = 1e-10;
+        const DeviceOp mv = make_matvec(K), pc = make_base_apply(ctx, pbj);
+        std::vector<double> trace;
+        const auto [xc, sc] = gmres_solve(ctx, mv, pc, rhs, {}, gc, &trace);
+        const auto [xh, sh] = gmres_solve(K, pbj, rhs, {}, gc);
+        EXPECT(sc.converged && sh.converged && sc.iters == sh.iters);
+        EXPECT(trace.size() == static_cast<size_t>(sc.iters));
+        double dx = 0.0;
+        for (size_t i = 0; i < xc.size(); ++i) dx = std::fmax(dx, std::fabs(xc[i] - xh[i]));
+        EXPECT(dx == 0.0);
+        // a throwing closure surfaces as the caller's exception, not as a crash across the C boundary
+        bool surfaced = false;
+        const DeviceOp bad = [](const double*, double*, std::int64_t) { throw std::runtime_error("boom"); };
+        try { gmres_solve(ctx, bad, DeviceOp(), rhs, {}, gc); } catch (const std::runtime_error& e) { surfaced = std::string(e.what()) == "boom"; }
+        EXPECT(surfaced);
+
+        // harmonic Ritz values of the BJ-preconditioned operator through the closure form == the spec form
+        PrecondSpec poly = bj;
+        poly.poly_degree = 6;
+        Preconditioner ppoly = build_preconditioner(poly, K, ops, disc);
+        double* tmp = nullptr;
+        check(ctx.get(), hdgb_device_alloc(ctx.get(), K.n_dof(), &tmp));
+        const DeviceOp op = [&](const double* in, double* out, std::int64_t n) { mv(in, tmp, n); pc(tmp, out, n); };
+        const auto th = compute_harmonic_ritz(ctx, op, static_cast<size_t>(K.n_dof()), 6, 12345);
+        std::int64_t nr = 0;
+        check(ctx.get(), hdgb_precond_get(ppoly.handle(), "ritz", nullptr, 0, &nr));
+        std::vector<double> reim(static_cast<size_t>(nr));
+        check(ctx.get(), hdgb_precond_get(ppoly.handle(), "ritz", reim.data(), nr, &nr));
+        EXPECT(th.size() * 2 == reim.size());
+        for (size_t i = 0; i < th.size() && 2 * i + 1 < reim.size(); ++i) EXPECT(th[i].real() == reim[2 * i] && th[i].imag() == reim[2 * i + 1]);
+        // apply_poly with the closure base == the wrapped application
+        long inner = 0;
+        const auto w1 = apply_poly(ppoly, &pc, K, yv, &inner), w2 = apply_preconditioner(ppoly, K, yv);
+        double dw = 0.0;
+        for (size_t i = 0; i < w1.size(); ++i) dw = std::fmax(dw, std::fabs(w1[i] - w2[i]));
+        EXPECT(dw == 0.0 && inner == static_cast<long>(th.size()));
+        hdgb_device_free(ctx.get(), tmp);
+        const auto lj = leja_order({{1, 0}, {10, 0}, {5, 0}});
+        EXPECT(lj.size() == 3 && lj[0].real() == 10 && lj[1].real() == 1 && lj[2].real() == 5);  // test_precond.cpp Leja unit case
+        std::printf("closure forms: gmres iters=%d (handle form %d), ritz=%zu, inner ops=%ld\n", sc.iters, sh.iters, th.size(), inner);
     }
 
     // ---- error behaviour ----
