@@ -510,11 +510,17 @@ hdgb_ops* assemble_element_operators_device(hdgb_disc* d, const hdgb_model* m, h
     // Raw-block workspace: bounded chunk of elements (whole mesh when the raw blocks are kept).
     const size_t per_elem = sEE * (1 + D) + sEF * (2 + D) + sFF;
     // the workspace may take up to a third of the free HBM (180 GB parts: config 2 runs in one chunk)
-    size_t free_b = 0, total_b = 0;
-    HDGB_CUDA(cudaMemGetInfo(&free_b, &total_b));
     // parked blocks of the caching allocator count as free: the chunking must not depend on what earlier calls left
-    // cached, or buffer sizes change from call to call and every allocation misses the cache
-    const double budget = std::max(2.0e9, static_cast<double>(free_b + pool_parked_bytes()) / 3.0);
+    // cached, or buffer sizes change from call to call and every allocation misses the cache.  The budget is fixed
+    // at the first assembly on this discretisation: cudaMemGetInfo is a resource-manager call that queues behind
+    // any concurrent nvidia-smi / NVML query on the box (measured: sporadic +15..55 ms per Newton iteration while a
+    // monitor polls the GPU), so it stays out of the steady-state path.
+    if (d->assemble_budget <= 0.0) {
+        size_t free_b = 0, total_b = 0;
+        HDGB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        d->assemble_budget = std::max(2.0e9, static_cast<double>(free_b + pool_parked_bytes()) / 3.0);
+    }
+    const double budget = d->assemble_budget;
     size_t chunk = keep_raw ? ne : static_cast<size_t>(budget / (per_elem * sizeof(double)));
     if (chunk < 1) chunk = 1;
     if (chunk > static_cast<size_t>(ne)) chunk = ne;

@@ -63,6 +63,7 @@ struct hdgb_disc {
     hdgb::DevBuf<double> elem_detjac, elem_invjac, elem_coords, face_detjac, face_coords, face_normal;
     hdgb::DevBuf<double> mass, mass_inv, bmat[3], cmat[3], minv_b[3], minv_c[3];
     hdgb::DiscView view{};
+    double assemble_budget = 0.0;  // bytes of raw-block workspace per assembly chunk, fixed at the first assembly
     // residual-assembly workspace (assemble_residual runs once per line-search trial)
     hdgb::DevBuf<double> res_ruhat_e, res_partial, res_sums;
 };
