@@ -121,19 +121,22 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
 
 constexpr int kResParts = 8;   // thread groups sharing one basis function's point sweep in the residual phase
 constexpr int kEdKc = 16;      // points per chunk
-constexpr int kEdLdb = 20;     // leading dimension of the right operand chunk (= 4 mod 16)
 constexpr int kEdSlotsMax = 4;  // 16 x 32 output tiles per warp: 2 for scalar systems (two CTAs per SM), 4 for wide ones (fewer passes)
 __host__ __device__ constexpr int ed_slots(int M) { return M == 1 ? 2 : kEdSlotsMax; }
 constexpr int kEdGroups = 32;  // ... of 16 warps
 
+// Operand chunks are stored POINT-major ([point in chunk][basis function], leading dimensions = 4 mod 16): the
+// builder's half-warps write 16 consecutive basis functions of one point (conflict-free stores) and both DMMA
+// fragment loads -- A: (row grp, k tig) -> [k][row], B: (k tig, column grp) -> [k][column] -- hit 16 distinct
+// 8-byte banks per half-warp.
 struct EdPlan {
     int rg, cg;   // 16-row / 32-column tile groups covering pe
     int pp;       // component pairs per pass
     int lda;      // leading dimension of a V_w chunk (= 4 mod 16)
+    int ldb;      // leading dimension of the weighted-basis chunk (= 4 mod 16)
     int wsub;     // V_w matrices resident per sub-pass (the warps' accumulator slots cover that many at a time)
-    __host__ __device__ int qp(int D) const { return pp * (1 + D); }
     __host__ __device__ size_t doubles(int D) const {
-        return static_cast<size_t>(wsub) * kEdKc * lda + static_cast<size_t>(cg) * 32 * kEdLdb;
+        return static_cast<size_t>(wsub) * kEdKc * lda + static_cast<size_t>(kEdKc) * ldb;
     }
 };
 inline __host__ __device__ EdPlan ed_plan(int pe, int M, int D, int nwarps) {
@@ -142,6 +145,7 @@ inline __host__ __device__ EdPlan ed_plan(int pe, int M, int D, int nwarps) {
     p.rg = (pe + 15) / 16;
     p.cg = (pe + 31) / 32;
     p.lda = p.rg * 16 + 4;
+    p.ldb = p.cg * 32 + 4;
     const int per_pair = (1 + D) * p.rg * p.cg;
     int pp = kEdGroups / per_pair;
     if (pp < 1) pp = 1;
@@ -155,6 +159,7 @@ inline __host__ __device__ EdPlan ed_plan(int pe, int M, int D, int nwarps) {
 }
 // usable when one pass's tiles fit the warps' accumulator slots
 inline bool ed_dmma_ok(int pe, int M, int D) { return pe <= 64 && pe >= tuning().local_dmma_min_pe; }
+
 
 // Point records in the global scratch (GREC) are read with ld.global.cg: an explicit global-space load that the
 // compiler may hoist above the shared-memory stores of the operand builder (a generic load may not be), coherent
@@ -172,30 +177,27 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
     // vrec / frec hold the records of volume points [gv0, gv1) and face points [fp0, fp1) (one chunk of a
     // point-chunked sweep, or all points); later chunks accumulate into the blocks (first == 0)
     constexpr int kEdSlots = ed_slots(M);
+    constexpr int kEdRes = (M == 1) ? 2 : 4;  // resident matrices whose coefficient rows the cached builder keeps in registers
+    constexpr int kEdIt = 4;                  // strips of 16 basis functions covering the padded columns (pe <= 64)
     const int pe = dv.pe, qf = dv.qf, npe = M * pe;
     const int qe = gv1 - gv0, nfp = fp1 - fp0;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
     const int grp = lane >> 2, tig = lane & 3;
     const EdPlan pl = ed_plan(pe, M, D, nwarps);
     const int lda = pl.lda;
-    const int bufd = static_cast<int>(pl.doubles(D));  // one operand buffer: [wsub][kc][lda] then [cg*32][kEdLdb]; two of them
+    const int bufd = static_cast<int>(pl.doubles(D));  // one operand buffer: [wsub][kc][lda] then [kc][ldb]; two of them
     const int boff0 = pl.wsub * kEdKc * lda;
     const int rc = pl.rg * pl.cg;
     const bool transient = in.dt_inv > 0.0;
-    const int cols_pad = pl.cg * 32;
     const int gpp = (1 + D) * pl.rg * pl.cg;  // tile groups per component pair
     const int nchunk_v = (qe + kEdKc - 1) / kEdKc, nchunk_f = (nfp + kEdKc - 1) / kEdKc;
     const int nchunk = nchunk_v + nchunk_f;
 
-    // the (point-in-chunk, basis function) pairs this thread builds are the same for every chunk
-    constexpr int kMaxBuild = 4;  // 16 * pe / nt with pe <= 64, nt >= 256
-    int bkk[kMaxBuild], bi[kMaxBuild];
-#pragma unroll
-    for (int it = 0; it < kMaxBuild; ++it) {
-        const int t = tid + it * nt;
-        bkk[it] = (t < kEdKc * pe) ? t / pe : -1;
-        bi[it] = t - (t / pe) * pe;
-    }
+    // Builder mapping (blockDim.x == 256 = 16 half-warps): half-warp <-> point of the chunk, lanes <-> basis functions
+    // i0, i0 + 16, ...  A thread reads its point's coefficients once per chunk and the basis tables with 128-byte
+    // half-warp loads; every operand entry the products read (incl. the zero padding) is written by exactly one thread.
+    const int bkk = tid >> 4, bi0 = tid & 15;
+    const int irows = pl.rg * 16, icols = pl.cg * 32, ldb = pl.ldb;
     for (int pair0 = 0; pair0 < M * M; pair0 += pl.pp) {
         const int npair = min(pl.pp, M * M - pair0);
         const int ngroups = npair * gpp;
@@ -207,60 +209,193 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
             const bool vol = ch < nchunk_v;
             const int p0 = vol ? ch * kEdKc : (ch - nchunk_v) * kEdKc;
             const int np = min(kEdKc, (vol ? qe : nfp) - p0);
+            const bool live = bkk < np;
+            const int pt = live ? p0 + bkk : 0;
+            if (vol) {
+                const int g = gv0 + pt;
+                const VolRec<M, D>& r = vrec[pt];
+                const double wq = live ? rec_ld<GREC>(&r.w) : 0.0;
+                const double* php = dv.phi + static_cast<size_t>(pe) * g;
+                const double* dpp[D];
 #pragma unroll
-            for (int it = 0; it < kMaxBuild; ++it) {
-                const int kk = bkk[it], i = bi[it];
-                if (kk < 0) break;
-                double bval = 0.0;
-                if (kk < np) {
-                    if (vol) {
-                        const int g = gv0 + p0 + kk;
-                        const VolRec<M, D>& r = vrec[p0 + kk];
-                        const double ph = __ldg(dv.phi + i + pe * g);
+                for (int k = 0; k < D; ++k) dpp[k] = dv.dphi[k] + static_cast<size_t>(pe) * g;
+                for (int pi = 0; pi < npair; ++pi) {
+                    const int pr = pair0 + pi, mp = pr / M, m = pr - mp * M, mm = m * M + mp;
+                    const int w0 = pi * (1 + D);
+                    // coefficient rows of this pair's matrices that are resident in the sub-pass
+                    bool on[1 + D];
+                    double cph[1 + D], cdp[1 + D][D];
+#pragma unroll
+                    for (int w = 0; w <= D; ++w) {
+                        on[w] = w0 + w >= wlo && w0 + w < whi;
+                        cph[w] = 0.0;
+#pragma unroll
+                        for (int k = 0; k < D; ++k) cdp[w][k] = 0.0;
+                    }
+                    if (on[0]) {
+                        cph[0] = rec_ld<GREC>(&r.dSu[mm]);
+#pragma unroll
+                        for (int k = 0; k < D; ++k) cdp[0][k] = rec_ld<GREC>(&r.cE[mm * D + k]);
+                    }
+#pragma unroll
+                    for (int dq = 0; dq < D; ++dq)
+                        if (on[1 + dq]) {
+                            cph[1 + dq] = rec_ld<GREC>(&r.dSq[mm * D + dq]);
+#pragma unroll
+                            for (int k = 0; k < D; ++k) cdp[1 + dq][k] = rec_ld<GREC>(&r.cD[(dq * M * M + mm) * D + k]);
+                        }
+                    const bool tdiag = transient && m == mp;
+                    for (int i = bi0; i < icols; i += 16) {
+                        const bool inb = live && i < pe;  // outside: exact zero padding
+                        const double ph = inb ? __ldg(php + i) : 0.0;
                         double dp_[D];
 #pragma unroll
-                        for (int k = 0; k < D; ++k) dp_[k] = __ldg(dv.dphi[k] + i + pe * g);
-                        bval = rec_ld<GREC>(&r.w) * ph;
-                        for (int pi = 0; pi < npair; ++pi) {
-                            const int pr = pair0 + pi, mp = pr / M, m = pr - mp * M, mm = m * M + mp;
-                            double fe = 0.0;
+                        for (int k = 0; k < D; ++k) dp_[k] = inb ? __ldg(dpp[k] + i) : 0.0;
+                        if (i < irows) {
 #pragma unroll
-                            for (int k = 0; k < D; ++k) fe += rec_ld<GREC>(&r.cE[mm * D + k]) * dp_[k];
-                            double eij = -fe - rec_ld<GREC>(&r.dSu[mm]) * ph;
-                            if (transient && m == mp) eij += in.dt_inv * ph;
-                            const int w0 = pi * (1 + D);
-                            if (w0 >= wlo && w0 < whi) Ab[((w0 - wlo) * kEdKc + kk) * lda + i] = eij;
+                            for (int w = 0; w <= D; ++w) {
+                                if (!on[w]) continue;
+                                double fs = 0.0;
 #pragma unroll
-                            for (int dq = 0; dq < D; ++dq) {
-                                const int w = w0 + 1 + dq;
-                                if (w < wlo || w >= whi) continue;
-                                double fd = 0.0;
-#pragma unroll
-                                for (int k = 0; k < D; ++k) fd += rec_ld<GREC>(&r.cD[(dq * M * M + mm) * D + k]) * dp_[k];
-                                Ab[((w - wlo) * kEdKc + kk) * lda + i] = -fd - rec_ld<GREC>(&r.dSq[mm * D + dq]) * ph;
+                                for (int k = 0; k < D; ++k) fs += cdp[w][k] * dp_[k];
+                                double v = -fs - cph[w] * ph;
+                                if (w == 0 && tdiag) v += in.dt_inv * ph;
+                                Ab[((w0 + w - wlo) * kEdKc + bkk) * lda + i] = inb ? v : 0.0;
                             }
                         }
-                    } else {
-                        const int p = fp0 + p0 + kk;
-                        const int lf = p / qf, gc = p - lf * qf;
-                        const FaceRec<M, D>& r = frec[p0 + kk];
-                        const double ph = __ldg(dv.tphi + ((static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf + gc) * pe + i);
-                        bval = rec_ld<GREC>(&r.w) * ph;
-                        for (int pi = 0; pi < npair; ++pi) {
-                            const int pr = pair0 + pi, mp = pr / M, m = pr - mp * M, mm = m * M + mp;
-                            const int w0 = pi * (1 + D);
-                            if (w0 >= wlo && w0 < whi) Ab[((w0 - wlo) * kEdKc + kk) * lda + i] = (m == mp) ? rec_ld<GREC>(&r.tau) * ph : 0.0;
+                        if (pi == 0) Bb[bkk * ldb + i] = wq * ph;
+                    }
+                }
+            } else {
+                const int p = fp0 + pt;
+                const int lf = p / qf, gc = p - lf * qf;
+                const FaceRec<M, D>& r = frec[pt];
+                const double wq = live ? rec_ld<GREC>(&r.w) : 0.0;
+                const double* php = dv.tphi + ((static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf + gc) * pe;
+                for (int pi = 0; pi < npair; ++pi) {
+                    const int pr = pair0 + pi, mp = pr / M, m = pr - mp * M, mm = m * M + mp;
+                    const int w0 = pi * (1 + D);
+                    bool on[1 + D];
+                    double cf[1 + D];
 #pragma unroll
-                            for (int dq = 0; dq < D; ++dq) {
-                                const int w = w0 + 1 + dq;
-                                if (w >= wlo && w < whi) Ab[((w - wlo) * kEdKc + kk) * lda + i] = rec_ld<GREC>(&r.dfh_q[mm * D + dq]) * ph;
-                            }
+                    for (int w = 0; w <= D; ++w) {
+                        on[w] = w0 + w >= wlo && w0 + w < whi;
+                        cf[w] = 0.0;
+                    }
+                    if (on[0] && m == mp) cf[0] = rec_ld<GREC>(&r.tau);
+#pragma unroll
+                    for (int dq = 0; dq < D; ++dq)
+                        if (on[1 + dq]) cf[1 + dq] = rec_ld<GREC>(&r.dfh_q[mm * D + dq]);
+                    for (int i = bi0; i < icols; i += 16) {
+                        const bool inb = live && i < pe;
+                        const double ph = inb ? __ldg(php + i) : 0.0;
+                        if (i < irows) {
+#pragma unroll
+                            for (int w = 0; w <= D; ++w)
+                                if (on[w]) Ab[((w0 + w - wlo) * kEdKc + bkk) * lda + i] = inb ? cf[w] * ph : 0.0;
+                        }
+                        if (pi == 0) Bb[bkk * ldb + i] = wq * ph;
+                    }
+                }
+            }
+        };
+        // The same builder with everything hoisted for the common shapes (the resident matrices of a sub-pass fit
+        // kEdRes coefficient rows in registers: scalar systems with pe in 49..64, wide systems one pair per pass):
+        // coefficient rows read once per chunk, the basis-function strips unrolled with constant offsets.
+        auto build_cached = [&](int ch, int buf) {
+            double* Ab = opbuf + buf * bufd + bkk * lda + bi0;       // this thread's entry of resident matrix 0, strip 0
+            double* Bb = opbuf + buf * bufd + boff0 + bkk * ldb + bi0;
+            const bool vol = ch < nchunk_v;
+            const int p0 = vol ? ch * kEdKc : (ch - nchunk_v) * kEdKc;
+            const int np = min(kEdKc, (vol ? qe : nfp) - p0);
+            const bool live = bkk < np;
+            const int pt = live ? p0 + bkk : 0;
+            const int nres = whi - wlo;
+            const int qstride = kEdKc * lda;
+            if (vol) {
+                const int g = gv0 + pt;
+                const VolRec<M, D>& r = vrec[pt];
+                const double wq = rec_ld<GREC>(&r.w);
+                double c0[kEdRes], ck[kEdRes][D];
+                bool td[kEdRes];
+#pragma unroll
+                for (int q = 0; q < kEdRes; ++q) {
+                    c0[q] = 0.0;
+                    td[q] = false;
+#pragma unroll
+                    for (int k = 0; k < D; ++k) ck[q][k] = 0.0;
+                    if (q < nres) {
+                        const int wg = wlo + q, pi = wg / (1 + D), w = wg - pi * (1 + D);
+                        const int pr = pair0 + pi, mp = pr / M, m = pr - mp * M, mm = m * M + mp;
+                        if (w == 0) {
+                            c0[q] = rec_ld<GREC>(&r.dSu[mm]);
+#pragma unroll
+                            for (int k = 0; k < D; ++k) ck[q][k] = rec_ld<GREC>(&r.cE[mm * D + k]);
+                            td[q] = transient && m == mp;
+                        } else {
+                            c0[q] = rec_ld<GREC>(&r.dSq[mm * D + w - 1]);
+#pragma unroll
+                            for (int k = 0; k < D; ++k) ck[q][k] = rec_ld<GREC>(&r.cD[((w - 1) * M * M + mm) * D + k]);
                         }
                     }
-                } else {
-                    for (int w = wlo; w < whi; ++w) Ab[((w - wlo) * kEdKc + kk) * lda + i] = 0.0;
                 }
-                Bb[i * kEdLdb + kk] = bval;
+                const double* php = dv.phi + static_cast<size_t>(pe) * g + bi0;
+                const double* dpp[D];
+#pragma unroll
+                for (int k = 0; k < D; ++k) dpp[k] = dv.dphi[k] + static_cast<size_t>(pe) * g + bi0;
+#pragma unroll
+                for (int it = 0; it < kEdIt; ++it) {
+                    if (16 * it >= icols) break;
+                    const bool inb = live && bi0 + 16 * it < pe;  // outside: exact zero padding
+                    const double ph = inb ? __ldg(php + 16 * it) : 0.0;
+                    double dp_[D];
+#pragma unroll
+                    for (int k = 0; k < D; ++k) dp_[k] = inb ? __ldg(dpp[k] + 16 * it) : 0.0;
+                    if (16 * it < irows) {
+#pragma unroll
+                        for (int q = 0; q < kEdRes; ++q) {
+                            if (q >= nres) break;
+                            double fs = 0.0;
+#pragma unroll
+                            for (int k = 0; k < D; ++k) fs += ck[q][k] * dp_[k];
+                            double v = -fs - c0[q] * ph;
+                            if (td[q]) v += in.dt_inv * ph;
+                            Ab[q * qstride + 16 * it] = inb ? v : 0.0;
+                        }
+                    }
+                    Bb[16 * it] = inb ? wq * ph : 0.0;
+                }
+            } else {
+                const int p = fp0 + pt;
+                const int lf = p / qf, gc = p - lf * qf;
+                const FaceRec<M, D>& r = frec[pt];
+                const double wq = rec_ld<GREC>(&r.w);
+                double cf[kEdRes];
+#pragma unroll
+                for (int q = 0; q < kEdRes; ++q) {
+                    cf[q] = 0.0;
+                    if (q < nres) {
+                        const int wg = wlo + q, pi = wg / (1 + D), w = wg - pi * (1 + D);
+                        const int pr = pair0 + pi, mp = pr / M, m = pr - mp * M, mm = m * M + mp;
+                        if (w == 0) cf[q] = (m == mp) ? rec_ld<GREC>(&r.tau) : 0.0;
+                        else cf[q] = rec_ld<GREC>(&r.dfh_q[mm * D + w - 1]);
+                    }
+                }
+                const double* php = dv.tphi + ((static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf + gc) * pe + bi0;
+#pragma unroll
+                for (int it = 0; it < kEdIt; ++it) {
+                    if (16 * it >= icols) break;
+                    const bool inb = live && bi0 + 16 * it < pe;
+                    const double ph = inb ? __ldg(php + 16 * it) : 0.0;
+                    if (16 * it < irows) {
+#pragma unroll
+                        for (int q = 0; q < kEdRes; ++q) {
+                            if (q >= nres) break;
+                            Ab[q * qstride + 16 * it] = inb ? cf[q] * ph : 0.0;
+                        }
+                    }
+                    Bb[16 * it] = inb ? wq * ph : 0.0;
+                }
             }
         };
         for (int g0 = 0; g0 < ngroups; g0 += nwarps * kEdSlots) {  // sub-passes when the CTA has fewer warps than tiles
@@ -273,9 +408,6 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
                 for (int a = 0; a < 2; ++a)
 #pragma unroll
                     for (int b = 0; b < 4; ++b) acc[s][a][b][0] = acc[s][a][b][1] = 0.0;
-            // zero the padding rows / columns of both buffers once per pass (the builders never write them)
-            __syncthreads();
-            for (int t = tid; t < 2 * bufd; t += nt) opbuf[t] = 0.0;
             // tile coordinates of this warp's accumulator slots (fixed over the point sweep)
             int aoff[kEdSlots], boff[kEdSlots];
 #pragma unroll
@@ -284,16 +416,21 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
                 const int w = gid / (pl.rg * pl.cg), rem = gid - w * (pl.rg * pl.cg);
                 const int rgi = rem / pl.cg, cgi = rem - rgi * pl.cg;
                 aoff[s] = gid < ngroups ? (w - wlo) * kEdKc * lda + rgi * 16 + grp + tig * lda : -1;
-                boff[s] = boff0 + (cgi * 32 + grp) * kEdLdb + tig;
+                boff[s] = boff0 + cgi * 32 + grp + tig * ldb;
             }
+            const bool cached = whi - wlo <= kEdRes;
             __syncthreads();
-            build(0, 0);
+            if (cached) build_cached(0, 0);
+            else build(0, 0);
             __syncthreads();
             for (int ch = 0; ch < nchunk; ++ch) {
                 const int buf = ch & 1;
                 // the next chunk's operands are built in the same barrier interval as this chunk's products:
                 // warps drift apart, so table loads and DMMA issue overlap across the CTA
-                if (ch + 1 < nchunk) build(ch + 1, buf ^ 1);
+                if (ch + 1 < nchunk) {
+                    if (cached) build_cached(ch + 1, buf ^ 1);
+                    else build(ch + 1, buf ^ 1);
+                }
                 const double* Ob = opbuf + buf * bufd;
 #pragma unroll
                 for (int s = 0; s < kEdSlots; ++s) {
@@ -306,7 +443,7 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
 #pragma unroll
                             for (int a = 0; a < 2; ++a) af[a] = as[kk * lda + a * 8];
 #pragma unroll
-                            for (int b = 0; b < 4; ++b) bf[b] = bs[b * 8 * kEdLdb + kk];
+                            for (int b = 0; b < 4; ++b) bf[b] = bs[kk * ldb + b * 8];
 #pragma unroll
                             for (int a = 0; a < 2; ++a)
 #pragma unroll
@@ -351,12 +488,16 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
 //   [H | G_0 .. G_{D-1}](lf b, j) = sum_gc psi_b(gc) * (c_w(gc) w_gc phis_j(gc)),  c_0 = dv_u, c_{1+dp} = dv_q[dp]
 //   F(i, lf bp)                   = sum_gc phis_i(gc) * (w_gc dfh_uh(gc) psi_bp(gc))
 // (local_ops.cpp:186-219).  psi^T and phis are the left operands, the coefficient-scaled tables the right ones.
-constexpr int kHgfW = 2;  // coefficient sets (H, G_d) resident at a time
+constexpr int kHgfW = 2;     // coefficient sets (H, G_d) resident at a time
+constexpr int kHgfRtMax = 4;  // 8-row tiles covering pf (pf <= 32)
+inline bool hgf_dmma_ok(int pf) { return pf <= 8 * kHgfRtMax; }
+// All four operands are stored k-major ([face point gc][row or column], leading dimensions = 4 mod 16): conflict-free
+// stores by consecutive lanes and conflict-free DMMA fragment loads, as in the E / D_d sweep.
 struct HgfPlan {
-    int pfp, qfp, ldp, lda, ldk, pep;
+    int pfp, qfp, ldp, lda, pep;
     __host__ __device__ size_t doubles(int D) const {
-        return static_cast<size_t>(qfp) * ldp + static_cast<size_t>(qfp) * lda + static_cast<size_t>(kHgfW) * pep * ldk +
-               static_cast<size_t>(pfp) * ldk;
+        return static_cast<size_t>(qfp) * ldp + static_cast<size_t>(qfp) * lda + static_cast<size_t>(kHgfW) * qfp * lda +
+               static_cast<size_t>(qfp) * ldp;
     }
 };
 inline __host__ __device__ HgfPlan hgf_plan(int pe, int pf, int qf) {
@@ -366,7 +507,6 @@ inline __host__ __device__ HgfPlan hgf_plan(int pe, int pf, int qf) {
     p.qfp = (qf + 3) / 4 * 4;
     p.ldp = (p.pfp + 15) / 16 * 16 + 4;
     p.lda = (p.pep + 15) / 16 * 16 + 4;
-    p.ldk = (p.qfp + 15) / 16 * 16 + 4;
     return p;
 }
 
@@ -376,113 +516,125 @@ __device__ void hgf_dmma(const DiscView& dv, const LocalOut& out, int e, const F
     // Multi-component systems: one pass per component pair (m, mp) with the pair's coefficients
     // dv_u[m M + mp], dv_q[(m M + mp) D + dp], dfh_uh[m M + mp]; rows / columns of the pair inside the blocks:
     // H, G (nfl x npe): row lf mpf + m pf + b, column mp pe + j;  F (npe x nfl): row m pe + i, column lf mpf + mp pf + bp.
+    // Tile ownership: warp <-> 8-column tile of j for H / G_d (all coefficient sets and row tiles of that column
+    // tile: psi^T fragments are shared) and <-> 8-row tile of i for F (all column tiles of bp).
     const int pe = dv.pe, pf = dv.pf, qf = dv.qf, n_lfe = dv.n_lfe;
     const int mpf = M * pf, nfl = n_lfe * mpf, npe = M * pe;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
     const int grp = lane >> 2, tig = lane & 3;
     const HgfPlan pl = hgf_plan(pe, pf, qf);
-    double* Ps = buf;                                        // psi^T: [gc][b]
-    double* Fs = Ps + pl.qfp * pl.ldp;  // phis:  [gc][i]
-    double* Bh = Fs + pl.qfp * pl.lda;  // [w][j][gc]
-    double* Bf = Bh + kHgfW * pl.pep * pl.ldk;  // [bp][gc]
+    const int ldp = pl.ldp, lda = pl.lda;
+    double* Ps = buf;                       // psi^T:                 [gc][b]
+    double* Fs = Ps + pl.qfp * ldp;         // phis:                  [gc][i]
+    double* Bh = Fs + pl.qfp * lda;         // c_w w phis:        [ww][gc][j]
+    double* Bf = Bh + kHgfW * pl.qfp * lda; // w dfh_uh psi:          [gc][bp]
     __syncthreads();
     for (int t = tid; t < static_cast<int>(pl.doubles(D)); t += nt) buf[t] = 0.0;
     __syncthreads();
     for (int t = tid; t < qf * pf; t += nt) {
         const int gc = t / pf, b = t - gc * pf;
-        Ps[gc * pl.ldp + b] = __ldg(dv.psi + b + pf * gc);
+        Ps[gc * ldp + b] = __ldg(dv.psi + b + pf * gc);
     }
-    const int rt_h = pl.pfp / 8, ct_h = pl.pep / 8;  // H/G tiles per block: rows b, columns j
-    const int ntile_f = ct_h * rt_h;                 // F tiles: rows i, columns bp
+    const int rt_h = pl.pfp / 8, ct_h = pl.pep / 8;  // 8-row tiles over b / bp, 8-column tiles over j (= row tiles over i)
     const int ksteps = pl.qfp / 4;
+    const int hw = tid >> 4, l16 = tid & 15, nhw = nt >> 4;  // builder mapping: half-warp <-> face point, lanes <-> j
     for (int lf = 0; lf < n_lfe; ++lf) {
         const double* tp = dv.tphi + (static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf * pe;
         const FaceRec<M, D>* fr = frec + lf * qf;
-        for (int t = tid; t < qf * pe; t += nt) {
-            const int gc = t / pe, j = t - gc * pe;
-            Fs[gc * pl.lda + j] = __ldg(tp + t);
-        }
+        __syncthreads();  // the previous face's tiles are done with Fs
+        for (int gc = hw; gc < qf; gc += nhw)
+            for (int j = l16; j < pe; j += 16) Fs[gc * lda + j] = __ldg(tp + static_cast<size_t>(gc) * pe + j);
         for (int pr = 0; pr < M * M; ++pr) {
             const int mp = pr / M, m = pr - mp * M, mm = m * M + mp;
             for (int w0 = 0; w0 < 1 + D; w0 += kHgfW) {  // coefficient sets [w0, w0 + nw): 0 = dv_u (H), 1 + dp = dv_q[dp] (G_dp)
                 const int nw = min(kHgfW, 1 + D - w0);
                 __syncthreads();  // Fs staged / previous tiles done with Bh, Bf
-                for (int t = tid; t < qf * pe; t += nt) {
-                    const int gc = t / pe, j = t - gc * pe;
+                for (int gc = hw; gc < qf; gc += nhw) {
                     const FaceRec<M, D>& r = fr[gc];
-                    const double wp = rec_ld<GREC>(&r.w) * Fs[gc * pl.lda + j];
-                    for (int ww = 0; ww < nw; ++ww) {
+                    const double wg = rec_ld<GREC>(&r.w);
+                    double cw[kHgfW];
+#pragma unroll
+                    for (int ww = 0; ww < kHgfW; ++ww) {
                         const int w = w0 + ww;
-                        Bh[(ww * pl.pep + j) * pl.ldk + gc] = wp * rec_ld<GREC>(w == 0 ? &r.dv_u[mm] : &r.dv_q[mm * D + w - 1]);
+                        cw[ww] = ww < nw ? wg * rec_ld<GREC>(w == 0 ? &r.dv_u[mm] : &r.dv_q[mm * D + w - 1]) : 0.0;
                     }
-                }
-                if (w0 == 0) {
-                    for (int t = tid; t < qf * pf; t += nt) {
-                        const int gc = t / pf, bp = t - gc * pf;
-                        const FaceRec<M, D>& r = fr[gc];
-                        Bf[bp * pl.ldk + gc] = rec_ld<GREC>(&r.w) * rec_ld<GREC>(&r.dfh_uh[mm]) * Ps[gc * pl.ldp + bp];
+                    for (int j = l16; j < pe; j += 16) {
+                        const double ph = Fs[gc * lda + j];
+#pragma unroll
+                        for (int ww = 0; ww < kHgfW; ++ww)
+                            if (ww < nw) Bh[(ww * pl.qfp + gc) * lda + j] = cw[ww] * ph;
+                    }
+                    if (w0 == 0) {
+                        const double cf = wg * rec_ld<GREC>(&r.dfh_uh[mm]);
+                        for (int bp = l16; bp < pf; bp += 16) Bf[gc * ldp + bp] = cf * Ps[gc * ldp + bp];
                     }
                 }
                 __syncthreads();
-                const int ntile_h = nw * rt_h * ct_h;
-                const int ntot = ntile_h + (w0 == 0 ? ntile_f : 0);
-                // two tiles per warp trip: their DMMA chains (qf / 4 dependent steps each) interleave
-                for (int t0 = 2 * warp; t0 < ntot; t0 += 2 * nwarps) {
-                    const double* as[2];
-                    const double* bs[2];
-                    int lds[2];
-                    double* dst[2];
-                    size_t o0[2], o1[2];
-                    bool ok0[2], ok1[2];
+                // ---- H / G_d tiles of this warp's column tiles ----
+                for (int ct = warp; ct < ct_h; ct += nwarps) {
+                    double c[kHgfW][kHgfRtMax][2];
 #pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        const int tile = t0 + u;
-                        ok0[u] = ok1[u] = false;
-                        as[u] = Ps; bs[u] = Bh; lds[u] = pl.ldp; dst[u] = out.H; o0[u] = o1[u] = 0;
-                        if (tile >= ntot) continue;
-                        if (tile < ntile_h) {
-                            const int ww = tile / (rt_h * ct_h), rem = tile - ww * (rt_h * ct_h);
-                            const int rt = rem / ct_h, ct = rem - rt * ct_h;
-                            as[u] = Ps + rt * 8 + grp;
-                            lds[u] = pl.ldp;
-                            bs[u] = Bh + (ww * pl.pep + ct * 8 + grp) * pl.ldk;
-                            const int b = rt * 8 + grp, w = w0 + ww, j = ct * 8 + 2 * tig;
-                            dst[u] = (w == 0 ? out.H : out.G[w - 1]) + static_cast<size_t>(e) * nfl * npe;
+                    for (int ww = 0; ww < kHgfW; ++ww)
+#pragma unroll
+                        for (int rt = 0; rt < kHgfRtMax; ++rt) c[ww][rt][0] = c[ww][rt][1] = 0.0;
+                    const double* as = Ps + grp + tig * ldp;
+                    const double* bs = Bh + ct * 8 + grp + tig * lda;
+                    for (int ks = 0; ks < ksteps; ++ks) {
+                        double af[kHgfRtMax], bf[kHgfW];
+#pragma unroll
+                        for (int rt = 0; rt < kHgfRtMax; ++rt) af[rt] = rt < rt_h ? as[4 * ks * ldp + rt * 8] : 0.0;
+#pragma unroll
+                        for (int ww = 0; ww < kHgfW; ++ww) bf[ww] = ww < nw ? bs[(ww * pl.qfp + 4 * ks) * lda] : 0.0;
+#pragma unroll
+                        for (int ww = 0; ww < kHgfW; ++ww)
+#pragma unroll
+                            for (int rt = 0; rt < kHgfRtMax; ++rt)
+                                if (ww < nw && rt < rt_h) dmma_8x8x4(c[ww][rt][0], c[ww][rt][1], af[rt], bf[ww]);
+                    }
+                    const int j = ct * 8 + 2 * tig;
+#pragma unroll
+                    for (int ww = 0; ww < kHgfW; ++ww) {
+                        if (ww >= nw) continue;
+                        const int w = w0 + ww;
+                        double* dst = (w == 0 ? out.H : out.G[w - 1]) + static_cast<size_t>(e) * nfl * npe;
+#pragma unroll
+                        for (int rt = 0; rt < kHgfRtMax; ++rt) {
+                            const int b = rt * 8 + grp;
+                            if (rt >= rt_h || b >= pf) continue;
                             const size_t row = lf * mpf + m * pf + b;
-                            o0[u] = static_cast<size_t>(mp * pe + j) * nfl + row;
-                            o1[u] = static_cast<size_t>(mp * pe + j + 1) * nfl + row;
-                            ok0[u] = b < pf && j < pe;
-                            ok1[u] = b < pf && j + 1 < pe;
-                        } else {
-                            const int tf = tile - ntile_h;
-                            const int rt = tf / rt_h, ct = tf - rt * rt_h;  // rt over i (pep / 8), ct over bp (pfp / 8)
-                            as[u] = Fs + rt * 8 + grp;
-                            lds[u] = pl.lda;
-                            bs[u] = Bf + (ct * 8 + grp) * pl.ldk;
-                            const int i = rt * 8 + grp, bp = ct * 8 + 2 * tig;
-                            dst[u] = out.F + static_cast<size_t>(e) * npe * nfl;
-                            const size_t row = m * pe + i;
-                            o0[u] = static_cast<size_t>(lf * mpf + mp * pf + bp) * npe + row;
-                            o1[u] = static_cast<size_t>(lf * mpf + mp * pf + bp + 1) * npe + row;
-                            ok0[u] = i < pe && bp < pf;
-                            ok1[u] = i < pe && bp + 1 < pf;
+                            if (j < pe) dst[static_cast<size_t>(mp * pe + j) * nfl + row] = c[ww][rt][0];
+                            if (j + 1 < pe) dst[static_cast<size_t>(mp * pe + j + 1) * nfl + row] = c[ww][rt][1];
                         }
                     }
-                    double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-                    for (int ks = 0; ks < ksteps; ++ks) {
+                }
+                // ---- F tiles of this warp's row tiles (rows i, columns bp) ----
+                if (w0 == 0) {
+                    for (int rti = warp; rti < ct_h; rti += nwarps) {
+                        double c[kHgfRtMax][2];
 #pragma unroll
-                        for (int u = 0; u < 2; ++u)
-                            dmma_8x8x4(c[u][0], c[u][1], as[u][(4 * ks + tig) * lds[u]], bs[u][4 * ks + tig]);
-                    }
+                        for (int cb = 0; cb < kHgfRtMax; ++cb) c[cb][0] = c[cb][1] = 0.0;
+                        const double* as = Fs + rti * 8 + grp + tig * lda;
+                        const double* bs = Bf + grp + tig * ldp;
+                        for (int ks = 0; ks < ksteps; ++ks) {
+                            const double af = as[4 * ks * lda];
 #pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        if (ok0[u]) dst[u][o0[u]] = c[u][0];
-                        if (ok1[u]) dst[u][o1[u]] = c[u][1];
+                            for (int cb = 0; cb < kHgfRtMax; ++cb)
+                                if (cb < rt_h) dmma_8x8x4(c[cb][0], c[cb][1], af, bs[4 * ks * ldp + cb * 8]);
+                        }
+                        const int i = rti * 8 + grp;
+                        double* dst = out.F + static_cast<size_t>(e) * npe * nfl;
+                        const size_t row = m * pe + i;
+#pragma unroll
+                        for (int cb = 0; cb < kHgfRtMax; ++cb) {
+                            const int bp = cb * 8 + 2 * tig;
+                            if (cb >= rt_h || i >= pe) continue;
+                            if (bp < pf) dst[static_cast<size_t>(lf * mpf + mp * pf + bp) * npe + row] = c[cb][0];
+                            if (bp + 1 < pf) dst[static_cast<size_t>(lf * mpf + mp * pf + bp + 1) * npe + row] = c[cb][1];
+                        }
                     }
                 }
             }
         }
-        __syncthreads();  // before the next face restages Fs
     }
 }
 
@@ -951,7 +1103,7 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
         // E / D_d on the tensor-core path when the operand chunks fit next to the point records
         size_t ed_bytes = 2 * ed_plan(dv.pe, M, D, NTD / 32).doubles(D) * sizeof(double) + 16;
         ed_bytes = std::max(ed_bytes, hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D) * sizeof(double) + 16);
-        const bool ed = want_jac && tuning().use_dmma && ed_dmma_ok(dv.pe, M, D) && all + ed_bytes <= cap;
+        const bool ed = want_jac && tuning().use_dmma && ed_dmma_ok(dv.pe, M, D) && hgf_dmma_ok(dv.pf) && all + ed_bytes <= cap;
         if (ed) kern_d<<<dv.ne, NTD, all + ed_bytes, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2 | (tuning().local_debug_skip << 4), nullptr, 0);
         else kern<<<dv.ne, 256, all, ctx->stream>>>(dv, mv, in, out, want_jac ? 1 : 0, 0, dv.qe, 0, nfp, 1, 0, nullptr, 0);
         HDGB_LAUNCH_CHECK(ctx);
@@ -959,7 +1111,7 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
     }
     // wide systems with the Jacobian on the tensor-core path: records in a global (L2) scratch, one launch
     if constexpr (M > 1) {
-        if (want_jac && tuning().use_dmma && tuning().local_global_records && ed_dmma_ok(dv.pe, M, D)) {
+        if (want_jac && tuning().use_dmma && tuning().local_global_records && ed_dmma_ok(dv.pe, M, D) && hgf_dmma_ok(dv.pf)) {
             const size_t edb = std::max(2 * ed_plan(dv.pe, M, D, 8).doubles(D), hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D)) * sizeof(double) + 32;
             const size_t rec_stride = (dv.qe * svr + nfp * sfr + 15) & ~static_cast<size_t>(15);
             if (fixed + edb <= cap) {
