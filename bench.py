@@ -332,16 +332,20 @@ def build_disc(a, ctx, world, rank, dist):
     if cfg["scaling"] == "weak":
         # every rank owns an n^3 slab of an n x n x (n*world) box
         lo, hi = (0.0, 0.0, 0.0), (1.0, 1.0, float(world))
-        coords, ev = P.box_hex_mesh(cfg["n"], cfg["n"], cfg["n"] * world, lo, hi)
-        gm = P.global_mesh("hex", coords, ev, lo=lo, hi=hi)
+
+        def build_global():
+            coords, ev = P.box_hex_mesh(cfg["n"], cfg["n"], cfg["n"] * world, lo, hi)
+            return P.global_mesh("hex", coords, ev, lo=lo, hi=hi)
         what = f"weak scaling: n x n x (n*{world}) box in z-slabs"
     else:
         # fixed global mesh (exactly the single-GPU mesh) cut into contiguous element-id slabs
-        gm = P.global_mesh_from_structured(cfg["shape"], cfg["n"], jitter=cfg["jitter"])
+        def build_global():
+            return P.global_mesh_from_structured(cfg["shape"], cfg["n"], jitter=cfg["jitter"])
         what = f"strong scaling: the fixed global mesh in {world} element-id slabs"
-    lm = P.build_my_local_mesh(gm, P.slab_partition(gm.ne, world), rank, dist if world > 1 else None)
+    # rank 0 alone materialises the global mesh and scatters the sub-domains (with their halo plans)
+    lm, nf_global = P.scatter_local_meshes(build_global, world, rank, dist if world > 1 else None)
     disc = P.make_discretization(ctx, lm, cfg["shape"], cfg["degree"], n_comp=cfg["n_comp"])
-    n_dof_global = gm.nf * disc.mpf
+    n_dof_global = nf_global * disc.mpf
     return disc, n_dof_global, what, lm
 
 

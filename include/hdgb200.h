@@ -75,7 +75,8 @@ const char* hdgb_version(void);
  *                "qelim_wn", "qelim_stages", "gemm_wn_cap", "use_blocked_gj" (blocked Gauss-Jordan inverse),
  *                "use_tile_lu" (register-tiled Gauss-Jordan, n <= 128, when the blocked one is off);
  *   assembly:    "local_dmma_min_pe", "local_global_records", "local_dmma_chunked", "assemble_budget_kb";
- *   GMRES:       "fused_cgs", "spin_sync".
+ *   GMRES:       "fused_cgs", "cgs_stream", "spin_sync";
+ *   multi-GPU:   "overlap_halo" (interior rows / elements computed while the halo exchange is in flight).
  * Returns non-zero for an unknown key.  Results do not depend on them beyond rounding. */
 int hdgb_set_tuning(const char* key, int64_t value);
 /* Caching-allocator diagnostics: device allocations / frees issued so far (no reference counterpart; the
@@ -417,6 +418,10 @@ hdgb_status hdgb_comm_set_callbacks(hdgb_ctx* ctx, int rank, int size, hdgb_halo
                                     void* user);
 void hdgb_comm_destroy(hdgb_ctx* ctx);
 hdgb_status hdgb_halo_exchange(hdgb_ctx* ctx, double* dev_vec, int width);
+/* The same exchange split in two: _begin starts it on the communicator's own stream (after everything enqueued so
+ * far), work on owned entries may follow on the context's stream, _end orders that stream after the arrival. */
+hdgb_status hdgb_halo_exchange_begin(hdgb_ctx* ctx, double* dev_vec, int width);
+hdgb_status hdgb_halo_exchange_end(hdgb_ctx* ctx);
 hdgb_status hdgb_allreduce_sum(hdgb_ctx* ctx, double* dev_buf, int n);
 int hdgb_comm_rank(const hdgb_ctx* ctx);
 int hdgb_comm_size(const hdgb_ctx* ctx);

@@ -34,6 +34,26 @@ void finish_disc(hdgb_ctx* c, hdgb_disc* d, int n_comp) {
     v.ne_owned = d->ne_owned;
     v.nf_owned = d->nf_owned;
     if (d->nf_global < 0) d->nf_global = m.nf;
+    // Domain decomposition: the leading elements whose faces are all owned, and the leading owned faces whose block
+    // row references owned faces only, need no halo data -- they run while the halo exchange is in flight
+    // (partition.py numbers them first; a caller's own numbering just gets a shorter prefix, down to none).
+    d->ne_interior = 0;
+    d->nf_interior = 0;
+    if (d->nf_owned < m.nf) {
+        std::vector<char> elem_int(m.ne, 1);
+        for (int e = 0; e < m.ne; ++e)
+            for (int l = 0; l < m.n_lfe; ++l)
+                if (m.elem_faces[static_cast<size_t>(e) * m.n_lfe + l] >= d->nf_owned) elem_int[e] = 0;
+        while (d->ne_interior < d->ne_owned && elem_int[d->ne_interior]) ++d->ne_interior;
+        auto face_int = [&](int f) {
+            for (int s = 0; s < 2; ++s) {
+                const int e = m.face_elems[2 * static_cast<size_t>(f) + s];
+                if (e >= 0 && !elem_int[e]) return false;
+            }
+            return true;
+        };
+        while (d->nf_interior < d->nf_owned && face_int(d->nf_interior)) ++d->nf_interior;
+    }
     if (!c) return;  // host-only discretisation: tables for inspection, no device state
     upload(c, d->elem_faces, m.elem_faces);
     upload(c, d->elem_side, m.elem_side);
@@ -213,6 +233,7 @@ hdgb_status hdgb_disc_set_boundary_tags(hdgb_disc* d, const int32_t* tags) {
 hdgb_status hdgb_disc_get_i32(const hdgb_disc* d, const char* name, int32_t* out, int64_t cap, int64_t* n) {
     const std::string s = name;
     const HostMesh& m = d->mesh;
+    if (s == "interior_counts") return get_vec(d, std::vector<int>{d->ne_interior, d->nf_interior}, out, cap, n);
     if (s == "element_to_face") return get_vec(d, m.elem_faces, out, cap, n);
     if (s == "element_vertices") return get_vec(d, m.elem_verts, out, cap, n);
     if (s == "face_to_elements") return get_vec(d, m.face_elems, out, cap, n);

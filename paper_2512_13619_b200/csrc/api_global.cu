@@ -16,19 +16,33 @@ namespace hdgb {
 void matvec_device(hdgb_matrix* k, const double* x, double* y) {
     // block_matvec (face_matrix.cpp:83-107) with gather_extended (:63-81) fused into the GEMV:
     // the nb neighbour slices are staged in shared memory, the block row is streamed once.
-    // Domain decomposition: the halo part of x is refreshed from its owners first.
-    if (k->ctx->comm) k->ctx->comm->halo(k->ctx, const_cast<double*>(x), k->mpf());
-    GemvArgs g;
-    g.a = k->blocks.p;
-    g.x = x;
-    g.y = y;
-    g.rows = k->mpf();
-    g.cols = k->mpf() * k->nb();
-    g.batch = k->nf;
-    g.idx = k->nbr32.p;
-    g.width = k->mpf();
-    g.comp = 1;
-    launch_team_gemv(k->ctx, g);
+    // Domain decomposition: the halo part of x is refreshed from its owners; the leading rows that reference owned
+    // faces only (nf_interior) are computed while that exchange is in flight, the interface rows after it has landed.
+    hdgb_ctx* c = k->ctx;
+    const int mpf = k->mpf(), nb = k->nb();
+    auto rows = [&](int f0, int f1) {
+        if (f1 <= f0) return;
+        GemvArgs g;
+        g.a = k->blocks.p + static_cast<size_t>(f0) * mpf * mpf * nb;
+        g.x = x;
+        g.y = y + static_cast<size_t>(f0) * mpf;
+        g.rows = mpf;
+        g.cols = mpf * nb;
+        g.batch = f1 - f0;
+        g.idx = k->nbr32.p + static_cast<size_t>(f0) * nb;
+        g.width = mpf;
+        g.comp = 1;
+        launch_team_gemv(c, g);
+    };
+    if (c->comm && tuning().overlap_halo && k->nf_interior > 0) {
+        c->comm->halo_begin(c, const_cast<double*>(x), mpf);
+        rows(0, k->nf_interior);
+        c->comm->halo_end(c);
+        rows(k->nf_interior, k->nf);
+        return;
+    }
+    if (c->comm) c->comm->halo(c, const_cast<double*>(x), mpf);
+    rows(0, k->nf);
 }
 
 void apply_base_device(hdgb_precond* p, const double* y, double* z) {
@@ -51,13 +65,29 @@ void apply_base_device(hdgb_precond* p, const double* y, double* z) {
             // solve, then the scatter-add written as an atomics-free face gather (side 0 first).
             const DiscView& v = p->disc->view;
             // domain decomposition: ghost elements are solved redundantly, so y is needed on every
-            // local face; a shared face then finds both sides' corrections locally
-            if (c->comm) c->comm->halo(c, const_cast<double*>(y), v.mpf);
-            GemvArgs g;
-            g.a = p->asm_inv.p; g.x = y; g.y = p->ze.p;
-            g.rows = v.nfl; g.cols = v.nfl; g.batch = v.ne;
-            g.idx = v.elem_faces; g.width = v.mpf; g.comp = 1;
-            launch_team_gemv(c, g);
+            // local face; a shared face then finds both sides' corrections locally.  Elements whose faces
+            // are all owned (ne_interior, numbered first) are solved while the halo exchange is in flight.
+            auto elems = [&](int e0, int e1) {
+                if (e1 <= e0) return;
+                GemvArgs g;
+                g.a = p->asm_inv.p + static_cast<size_t>(e0) * v.nfl * v.nfl;
+                g.x = y;
+                g.y = p->ze.p + static_cast<size_t>(e0) * v.nfl;
+                g.rows = v.nfl; g.cols = v.nfl; g.batch = e1 - e0;
+                g.idx = v.elem_faces + static_cast<size_t>(e0) * v.n_lfe;
+                g.width = v.mpf; g.comp = 1;
+                launch_team_gemv(c, g);
+            };
+            const int ni = p->disc->ne_interior;
+            if (c->comm && tuning().overlap_halo && ni > 0) {
+                c->comm->halo_begin(c, const_cast<double*>(y), v.mpf);
+                elems(0, ni);
+                c->comm->halo_end(c);
+                elems(ni, v.ne);
+            } else {
+                if (c->comm) c->comm->halo(c, const_cast<double*>(y), v.mpf);
+                elems(0, v.ne);
+            }
             launch_face_sum(c, p->ze.p, v.face_elems, v.face_lidx, v.nf_owned, v.mpf, v.n_lfe, z,
                             p->kind == HDGB_PC_RAS ? 1 : 2);
             break;
@@ -313,6 +343,7 @@ hdgb_matrix* assemble_global_device(hdgb_disc* d, const hdgb_ops* o) {
     k->n_lfe = v.n_lfe;
     k->nf = v.nf_owned;   // rows: owned faces (both adjacent elements are local)
     k->nf_local = v.nf;   // vectors: all local faces
+    k->nf_interior = d->nf_interior;
     const size_t row = static_cast<size_t>(v.mpf) * v.mpf * k->nb();
     k->blocks.alloc(row * k->nf);
     k->rhs.alloc(static_cast<size_t>(v.mpf) * v.nf);

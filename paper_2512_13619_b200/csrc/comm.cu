@@ -80,31 +80,66 @@ struct NcclComm : Comm {
     void* comm = nullptr;
     HaloPlan plan;
     DevBuf<double> sendbuf;
+    // the exchange runs on its own stream so that interior rows / elements overlap it (SURVEY.md 8e option (i))
+    cudaStream_t xstream = nullptr;
+    cudaEvent_t ev_packed = nullptr, ev_arrived = nullptr;
+    bool in_flight = false;
     ~NcclComm() override {
         if (comm) nccl().CommDestroy(comm);
+        if (ev_packed) cudaEventDestroy(ev_packed);
+        if (ev_arrived) cudaEventDestroy(ev_arrived);
+        if (xstream) cudaStreamDestroy(xstream);
     }
-    void halo(hdgb_ctx* c, double* vec, int width) override {
-        if (plan.nbr_rank.empty()) return;
+    void ensure_stream() {
+        if (xstream) return;
+        HDGB_CUDA(cudaStreamCreateWithFlags(&xstream, cudaStreamNonBlocking));
+        HDGB_CUDA(cudaEventCreateWithFlags(&ev_packed, cudaEventDisableTiming));
+        HDGB_CUDA(cudaEventCreateWithFlags(&ev_arrived, cudaEventDisableTiming));
+    }
+    // pack on `pack_stream`, send / receive on `xfer`
+    void exchange(hdgb_ctx* c, double* vec, int width, cudaStream_t xfer) {
         const size_t need = static_cast<size_t>(plan.total_send) * width;
         if (sendbuf.n < need) {
             HDGB_CUDA(cudaStreamSynchronize(c->stream));
+            if (xstream) HDGB_CUDA(cudaStreamSynchronize(xstream));
             sendbuf.alloc(need);
         }
         if (need) {
             pack_faces_kernel<<<ceil_div(static_cast<int64_t>(need), 256), 256, 0, c->stream>>>(vec, plan.send_ids.p, static_cast<int64_t>(need), width, sendbuf.p);
             HDGB_LAUNCH_CHECK(c);
         }
+        if (xfer != c->stream) {
+            // everything enqueued so far (the packed slices, and whatever produced the owned part of vec) precedes the transfer
+            HDGB_CUDA(cudaEventRecord(ev_packed, c->stream));
+            HDGB_CUDA(cudaStreamWaitEvent(xfer, ev_packed, 0));
+        }
         NcclApi& n = nccl();
         nccl_check(n.GroupStart(), "ncclGroupStart");
         for (size_t k = 0; k < plan.nbr_rank.size(); ++k) {
             if (plan.send_count[k])
                 nccl_check(n.Send(sendbuf.p + static_cast<size_t>(plan.send_off[k]) * width, static_cast<size_t>(plan.send_count[k]) * width,
-                                  kNcclDouble, plan.nbr_rank[k], comm, c->stream), "ncclSend");
+                                  kNcclDouble, plan.nbr_rank[k], comm, xfer), "ncclSend");
             if (plan.recv_count[k])
                 nccl_check(n.Recv(vec + static_cast<size_t>(plan.recv_off[k]) * width, static_cast<size_t>(plan.recv_count[k]) * width,
-                                  kNcclDouble, plan.nbr_rank[k], comm, c->stream), "ncclRecv");
+                                  kNcclDouble, plan.nbr_rank[k], comm, xfer), "ncclRecv");
         }
         nccl_check(n.GroupEnd(), "ncclGroupEnd");
+    }
+    void halo(hdgb_ctx* c, double* vec, int width) override {
+        if (plan.nbr_rank.empty()) return;
+        exchange(c, vec, width, c->stream);
+    }
+    void halo_begin(hdgb_ctx* c, double* vec, int width) override {
+        if (plan.nbr_rank.empty()) return;
+        ensure_stream();
+        exchange(c, vec, width, xstream);
+        HDGB_CUDA(cudaEventRecord(ev_arrived, xstream));
+        in_flight = true;
+    }
+    void halo_end(hdgb_ctx* c) override {
+        if (!in_flight) return;
+        HDGB_CUDA(cudaStreamWaitEvent(c->stream, ev_arrived, 0));
+        in_flight = false;
     }
     void allreduce(hdgb_ctx* c, double* buf, int cnt) override {
         nccl_check(nccl().AllReduce(buf, buf, static_cast<size_t>(cnt), kNcclDouble, kNcclSum, comm, c->stream), "ncclAllReduce");
@@ -201,6 +236,18 @@ hdgb_status hdgb_halo_exchange(hdgb_ctx* c, double* dev_vec, int width) {
     return guarded(c, [&] {
         if (c->comm) c->comm->halo(c, dev_vec, width);
         HDGB_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+hdgb_status hdgb_halo_exchange_begin(hdgb_ctx* c, double* dev_vec, int width) {
+    return guarded(c, [&] {
+        if (c->comm) c->comm->halo_begin(c, dev_vec, width);
+    });
+}
+
+hdgb_status hdgb_halo_exchange_end(hdgb_ctx* c) {
+    return guarded(c, [&] {
+        if (c->comm) c->comm->halo_end(c);
     });
 }
 

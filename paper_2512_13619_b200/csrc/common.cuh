@@ -42,6 +42,11 @@ struct Comm {
     virtual ~Comm() = default;
     virtual void halo(hdgb_ctx* c, double* vec, int width) = 0;
     virtual void allreduce(hdgb_ctx* c, double* buf, int n) = 0;
+    // Split exchange: halo_begin starts it (the transfer may proceed on the communicator's own stream), work that
+    // touches owned entries only may be enqueued on ctx->stream, halo_end orders ctx->stream after the arrival.
+    // Default: the blocking exchange in halo_begin.
+    virtual void halo_begin(hdgb_ctx* c, double* vec, int width) { halo(c, vec, width); }
+    virtual void halo_end(hdgb_ctx*) {}
 };
 }  // namespace hdgb
 

@@ -53,6 +53,7 @@ struct hdgb_disc {
     hdgb_dims dims{};
     hdgb::HostMesh mesh;
     int ne_owned = -1, nf_owned = -1;     // domain decomposition: owned entities come first
+    int ne_interior = 0, nf_interior = 0; // leading owned elements / faces that touch no halo face (overlap window)
     std::vector<int64_t> face_gid;        // local -> global face id (empty: identity)
     int64_t nf_global = -1;
     hdgb::MasterElement me;
@@ -109,6 +110,7 @@ struct hdgb_matrix {
     bool neighbor_valid = false;
     int m = 1, pf = 0, n_lfe = 4, nf = 0;
     int nf_local = 0;  // faces a vector spans (owned first, then halo); == nf on one GPU
+    int nf_interior = 0;  // leading rows that reference owned faces only (computed while the halo exchange is in flight)
     int mpf() const { return m * pf; }
     int nb() const { return 2 * n_lfe - 1; }
     int64_t n_dof() const { return static_cast<int64_t>(mpf()) * nf; }          // owned unknowns (rows)

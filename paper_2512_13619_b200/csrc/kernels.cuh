@@ -36,6 +36,7 @@ struct Tuning {
     int stream_packed = 1;               // small items: 16 warps, several items side by side per warp, no shuffle tree
     int stream_packed_max_cols = 32;     // ... for items with at most this many columns
     int64_t stream_packed_stage_bytes = 6144;  // ... bytes per TMA stage of a warp in packed mode
+    int overlap_halo = 1;                // domain decomposition: interior rows / elements run while the halo exchange is in flight
     int spin_sync = 1;                   // GMRES: poll an event for the per-iteration Hessenberg column instead of a blocking sync
     int fused_cgs = 0;                   // round-1 register-resident fused CGS2 pass (measured slower: 112 us vs 85 us at cfg2)
     int cgs_stream = 1;                  // CGS2 as three TMA-streamed passes over the basis (k_orth.cu) instead of four

@@ -230,7 +230,8 @@ def load_library():
         "hdgb_comm_nccl_unique_id": (i, [_vp]), "hdgb_comm_create_nccl": (i, [_vp, _vp, i, i]),
         "hdgb_comm_set_halo_plan": (i, [_vp, i, _vp, _vp, _vp, _vp, _vp]),
         "hdgb_comm_set_callbacks": (i, [_vp, i, i, _vp, _vp, _vp]), "hdgb_comm_destroy": (None, [_vp]),
-        "hdgb_halo_exchange": (i, [_vp, _vp, i]), "hdgb_allreduce_sum": (i, [_vp, _vp, i]),
+        "hdgb_halo_exchange": (i, [_vp, _vp, i]), "hdgb_halo_exchange_begin": (i, [_vp, _vp, i]),
+        "hdgb_halo_exchange_end": (i, [_vp]), "hdgb_allreduce_sum": (i, [_vp, _vp, i]),
         "hdgb_comm_rank": (i, [_vp]), "hdgb_comm_size": (i, [_vp]),
         "hdgb_device_alloc": (i, [_vp, i64, pp]), "hdgb_device_free": (None, [_vp, _vp]),
         "hdgb_copy": (i, [_vp, _vp, _vp, i64]),

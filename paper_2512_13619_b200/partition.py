@@ -144,6 +144,8 @@ class LocalMesh:
     fverts: np.ndarray
     tags: np.ndarray
     nf_global: int
+    ne_interior: int = 0         # leading owned elements all of whose faces are owned
+    nf_interior: int = 0         # leading owned faces whose block row references owned faces only
     # halo plan
     nbr_ranks: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int32))
     send_ids: list = field(default_factory=list)       # per neighbour: local ids of owned faces to send
@@ -160,6 +162,14 @@ def local_mesh(gm: GlobalMesh, part: np.ndarray, rank: int) -> LocalMesh:
     nbr_e = np.unique(gm.f2e[faces_owned_e].ravel())
     nbr_e = nbr_e[nbr_e >= 0]
     ghost_e = np.setdiff1d(nbr_e, owned_e, assume_unique=True)
+    # Overlap window of the halo exchange: an owned element is INTERIOR when this rank owns all its faces, an
+    # owned face when both adjacent elements are interior (or absent: domain boundary) -- its block row then
+    # references owned faces only.  Interior entities are numbered first (ids ascending within each group), so
+    # the library computes them while the exchange is in flight and the interface rest afterwards.
+    face_mine = part[gm.f2e[:, 0]] == rank
+    e_int = np.all(face_mine[gm.e2f[owned_e]], axis=1)
+    owned_e = np.concatenate([owned_e[e_int], owned_e[~e_int]])
+    ne_interior = int(np.count_nonzero(e_int))
     elems = np.concatenate([owned_e, ghost_e]).astype(np.int64)
     g2l_e = -np.ones(gm.ne, dtype=np.int64)
     g2l_e[elems] = np.arange(len(elems))
@@ -167,6 +177,12 @@ def local_mesh(gm: GlobalMesh, part: np.ndarray, rank: int) -> LocalMesh:
     lf = np.unique(gm.e2f[elems])
     owner = part[gm.f2e[lf, 0]]
     own = lf[owner == rank]
+    elem_interior = np.zeros(gm.ne + 1, dtype=bool)      # index -1 (no element) -> slot gm.ne
+    elem_interior[owned_e[:ne_interior]] = True
+    elem_interior[gm.ne] = True
+    f_int = np.all(elem_interior[np.where(gm.f2e[own] < 0, gm.ne, gm.f2e[own])], axis=1)
+    own = np.concatenate([own[f_int], own[~f_int]])
+    nf_interior = int(np.count_nonzero(f_int))
     halo = lf[owner != rank]
     halo_owner = part[gm.f2e[halo, 0]]
     order = np.lexsort((halo, halo_owner))
@@ -188,6 +204,7 @@ def local_mesh(gm: GlobalMesh, part: np.ndarray, rank: int) -> LocalMesh:
                    flidx=gm.flidx[faces].astype(np.int32), forient=gm.forient[faces].astype(np.int32),
                    fverts=g2l_v[gm.fverts[faces]].astype(np.int32), tags=gm.tags[faces].astype(np.int32),
                    nf_global=gm.nf)
+    lm.ne_interior, lm.nf_interior = ne_interior, nf_interior
     nbrs = np.unique(halo_owner)
     lm.needs = {int(s): halo[halo_owner == s] for s in nbrs}
     return lm
@@ -239,6 +256,23 @@ def build_my_local_mesh(gm: GlobalMesh, part: np.ndarray, rank: int, dist=None):
     return finish_halo_plan(lm, needs)
 
 
+def scatter_local_meshes(build_global, n_ranks: int, rank: int, dist):
+    """Rank 0 alone materialises the global mesh (build_global() -> GlobalMesh), cuts it into the per-rank local
+    meshes with completed halo plans and scatters them (torch.distributed object scatter, any backend); the other
+    ranks never hold more than their own sub-domain.  Returns (this rank's LocalMesh, global face count)."""
+    if dist is None or n_ranks == 1 or not dist.is_initialized():
+        gm = build_global()
+        return build_local_meshes(gm, slab_partition(gm.ne, n_ranks))[rank], gm.nf
+    box = [None]
+    if rank == 0:
+        gm = build_global()
+        lms = build_local_meshes(gm, slab_partition(gm.ne, n_ranks))
+        dist.scatter_object_list(box, lms, src=0)
+    else:
+        dist.scatter_object_list(box, None, src=0)
+    return box[0], box[0].nf_global
+
+
 def make_discretization(ctx, lm: LocalMesh, shape: str, degree: int, n_comp=1, quad_points=0):
     """hdgb_disc_create_from_tables for a local mesh."""
     L = H.load_library()
@@ -257,6 +291,7 @@ def make_discretization(ctx, lm: LocalMesh, shape: str, degree: int, n_comp=1, q
         raise H.HdgError(f"hdgb_disc_create_from_tables failed (status {st})")
     d = H.Discretization(ctx, h)
     d.ne_owned, d.nf_owned, d.local_mesh = lm.ne_owned, lm.nf_owned, lm
+    d.ne_interior, d.nf_interior = (int(v) for v in d.table("interior_counts"))  # as the library sees them
     return d
 
 

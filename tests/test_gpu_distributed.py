@@ -141,3 +141,79 @@ def test_nccl_backend_single_rank(ctx):
     finally:
         H.load_library().hdgb_comm_destroy(c2._h)
         c2.close()
+
+
+def test_overlapped_exchange_equals_blocking_exchange(ctx):
+    """Interior rows / elements computed while the halo exchange is in flight (tuning 'overlap_halo') give bit for bit
+    the operator applications of the blocking order: same kernels over sub-ranges of the same contiguous rows."""
+    shape, k = "hex", 2
+    gm = mesh(shape, (3, 3, 9))
+    lms = P.build_local_meshes(gm, P.slab_partition(gm.ne, 3))
+    assert all(lm.nf_interior > 0 and lm.ne_interior > 0 for lm in lms)
+    x = hdg.random_vector(gm.nf * 9, 11).reshape(gm.nf, -1)
+    out = {}
+    for mode in (1, 0):
+        hdg.set_tuning("overlap_halo", mode)
+        lb = Loopback(lms)
+
+        def work(r, c, lm):
+            disc = P.make_discretization(c, lm, shape, k)
+            model = hdg.make_case_model(disc, "poisson")
+            state = hdg.make_initial_state(disc, model)
+            ops = hdg.assemble_element_operators(disc, model, state)
+            K, rhs = hdg.assemble_global(disc, ops)
+            xl = np.full((len(lm.faces), disc.mpf), np.nan)
+            xl[: lm.nf_owned] = x[lm.faces[: lm.nf_owned]]
+            y = hdg.block_matvec(K, xl.ravel().copy()).reshape(len(lm.faces), -1)[: lm.nf_owned]
+            Pc = hdg.build_preconditioner("asm", K, ops, disc)
+            z = Pc.apply_base(xl.ravel().copy()).reshape(len(lm.faces), -1)[: lm.nf_owned]
+            rep = hdg.newton_solve(disc, model, state, pspec=hdg.PrecondSpec("asm"))
+            return y, z, rep.gmres_per_newton, state.uhat
+        try:
+            out[mode] = lb.run(work)
+        finally:
+            lb.close()
+            hdg.set_tuning("overlap_halo", 1)
+    for a, b in zip(out[1], out[0]):
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+        assert a[2] == b[2] and np.array_equal(a[3], b[3])
+
+
+def test_nccl_two_stream_exchange_with_self_neighbour():
+    """The NCCL exchange on its own stream (halo_begin / halo_end) exercised on ONE GPU: a 1-rank communicator whose
+    only neighbour is itself (NCCL supports send / receive to self inside a group).  Owned slices must land in
+    the halo part while work enqueued in between on the context's stream touches owned entries only."""
+    import ctypes as C
+    from paper_2512_13619_b200 import hdg as H
+    L = H.load_library()
+    c2 = hdg.Context(0)
+    try:
+        uid = (C.c_char * 128)()
+        assert L.hdgb_comm_nccl_unique_id(uid) == 0
+        c2.check(L.hdgb_comm_create_nccl(c2._h, bytes(uid.raw), 0, 1))
+        nf_owned, n_halo, width = 1000, 37, 9
+        ids = np.ascontiguousarray(np.random.default_rng(3).choice(nf_owned, n_halo, replace=False), dtype=np.int32)
+        nbr, cnt, off = (np.array([v], dtype=np.int32) for v in (0, n_halo, nf_owned))  # kept alive across the call
+        c2.check(L.hdgb_comm_set_halo_plan(c2._h, 1, nbr.ctypes.data, cnt.ctypes.data, ids.ctypes.data,
+                                           off.ctypes.data, cnt.ctypes.data))
+        vec_h = np.full((nf_owned + n_halo, width), np.nan)
+        vec_h[:nf_owned] = hdg.random_vector(nf_owned * width, 8).reshape(nf_owned, width)
+        vec = c2.alloc(vec_h.size)
+        for rounds in range(3):                    # repeated use of the stream / events / send buffer
+            c2.copy(vec, vec_h.ravel(), vec_h.size)
+            c2.check(L.hdgb_halo_exchange_begin(c2._h, vec, width))
+            c2.check(L.hdgb_halo_exchange_end(c2._h))
+            c2.synchronize()
+            back = np.empty_like(vec_h)
+            c2.copy(back.ravel(), vec, vec_h.size)
+            assert np.array_equal(back[:nf_owned], vec_h[:nf_owned])
+            assert np.array_equal(back[nf_owned:], vec_h[ids])
+            # the blocking form gives the same
+            c2.copy(vec, vec_h.ravel(), vec_h.size)
+            c2.check(L.hdgb_halo_exchange(c2._h, vec, width))
+            c2.copy(back.ravel(), vec, vec_h.size)
+            assert np.array_equal(back[nf_owned:], vec_h[ids])
+        c2.free(vec)
+    finally:
+        L.hdgb_comm_destroy(c2._h)
+        c2.close()

@@ -53,6 +53,39 @@ def test_partition_invariants(shape, nr):
             assert np.array_equal(sent_gids, recv_gids)
 
 
+@pytest.mark.parametrize("shape,dims,nr", [("quad", (8, 9), 2), ("quad", (6, 12), 3), ("hex", (3, 3, 8), 2), ("hex", (2, 3, 12), 3)])
+def test_interior_first_numbering_and_overlap_window(shape, dims, nr):
+    """The overlap window of the halo exchange: interior elements / faces are numbered first, their rows reference
+    owned faces only, and the library (host-only discretisation) finds exactly the partitioner's counts."""
+    lo, hi = ((0, 0, 0), (1, 1, 1)) if shape == "hex" else ((0, 0), (1, 1))
+    coords, ev = (P.box_hex_mesh if shape == "hex" else P.box_quad_mesh)(*dims, lo, hi)
+    gm = P.global_mesh(shape, coords, ev, lo=lo, hi=hi)
+    lms = P.build_local_meshes(gm, P.slab_partition(gm.ne, nr))
+    for lm in lms:
+        assert 0 < lm.ne_interior <= lm.ne_owned and 0 < lm.nf_interior <= lm.nf_owned
+        # interior elements touch owned faces only; the first non-interior owned element touches a halo face
+        assert np.all(lm.e2f[: lm.ne_interior] < lm.nf_owned)
+        if lm.ne_interior < lm.ne_owned:
+            assert np.all(np.any(lm.e2f[lm.ne_interior: lm.ne_owned] >= lm.nf_owned, axis=1))
+        # the block row of an interior face (all faces of both adjacent elements) stays inside the owned range
+        for f in range(lm.nf_owned):
+            row = np.concatenate([lm.e2f[e] for e in lm.f2e[f] if e >= 0])
+            assert (f < lm.nf_interior) == bool(np.all(row < lm.nf_owned)), f
+        # ids ascend inside each group (the single-domain order is kept where it can be)
+        for a, b in ((0, lm.nf_interior), (lm.nf_interior, lm.nf_owned)):
+            assert np.all(np.diff(lm.faces[a:b]) > 0)
+        for a, b in ((0, lm.ne_interior), (lm.ne_interior, lm.ne_owned)):
+            assert np.all(np.diff(lm.elems[a:b]) > 0)
+        d = P.make_discretization(None, lm, shape, 1)
+        assert (d.ne_interior, d.nf_interior) == (lm.ne_interior, lm.nf_interior)
+        d.close()
+    # one rank: everything is owned, nothing to overlap
+    one = P.build_local_meshes(gm, np.zeros(gm.ne, dtype=np.int32))[0]
+    d = P.make_discretization(None, one, shape, 1)
+    assert (d.ne_interior, d.nf_interior) == (0, 0)
+    d.close()
+
+
 def test_box_tags_match_structured_builder():
     gm = small_mesh("quad")
     d = H.Discretization.structured(None, "quad", n=4, degree=1)
@@ -121,6 +154,19 @@ def _gloo_worker(rank, world, port, ret):
         t = torch.tensor([float(lm.nf_owned), float(np.sum(vec[: lm.nf_owned, 0]))], dtype=torch.float64)
         dist.all_reduce(t)
         ok = ok and t[0].item() == gm.nf and t[1].item() == float(np.sum(np.arange(gm.nf) * 10.0))
+        # scatter_local_meshes: rank 0 alone materialises the global mesh; every rank receives the sub-domain
+        # (halo plan included) that the redundant construction gives
+        calls = []
+
+        def build_global():
+            calls.append(rank)
+            return small_mesh("hex")
+        lm2, nf_global = P.scatter_local_meshes(build_global, world, rank, dist)
+        ok = ok and calls == ([0] if rank == 0 else []) and nf_global == gm.nf
+        for name in ("elems", "faces", "e2f", "f2e", "flidx", "forient", "fverts", "tags", "nbr_ranks", "recv_off", "recv_cnt"):
+            ok = ok and np.array_equal(getattr(lm2, name), getattr(lm, name))
+        ok = ok and all(np.array_equal(a, b) for a, b in zip(lm2.send_ids, lm.send_ids))
+        ok = ok and (lm2.ne_interior, lm2.nf_interior) == (lm.ne_interior, lm.nf_interior)
         ret[rank] = ok
     finally:
         dist.destroy_process_group()
