@@ -45,12 +45,13 @@ void matvec_device(hdgb_matrix* k, const double* x, double* y) {
     rows(0, k->nf);
 }
 
-void apply_base_device(hdgb_precond* p, const double* y, double* z) {
+void apply_base_device(hdgb_precond* p, const double* y, double* z, const PolyEpi* epi) {
     hdgb_ctx* c = p->ctx;
     const int64_t n = static_cast<int64_t>(p->mpf) * p->nf;
     switch (p->kind) {
         case HDGB_PC_IDENTITY:
-            if (y != z) HDGB_CUDA(cudaMemcpyAsync(z, y, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+            if (epi) launch_poly_update(c, *epi, y, n);
+            else if (y != z) HDGB_CUDA(cudaMemcpyAsync(z, y, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
             break;
         case HDGB_PC_BJ: {
             // apply_bj (preconditioner.cpp:48-52)
@@ -58,6 +59,7 @@ void apply_base_device(hdgb_precond* p, const double* y, double* z) {
             g.a = p->bj_inv.p; g.x = y; g.y = z;
             g.rows = p->mpf; g.cols = p->mpf; g.batch = p->nf;
             launch_team_gemv(c, g);
+            if (epi) launch_poly_update(c, *epi, z, n);  // both recurrence updates in one pass over t
             break;
         }
         default: {
@@ -88,8 +90,9 @@ void apply_base_device(hdgb_precond* p, const double* y, double* z) {
                 if (c->comm) c->comm->halo(c, const_cast<double*>(y), v.mpf);
                 elems(0, v.ne);
             }
+            // the polynomial recurrence updates ride on the face sum (the value t is never stored)
             launch_face_sum(c, p->ze.p, v.face_elems, v.face_lidx, v.nf_owned, v.mpf, v.n_lfe, z,
-                            p->kind == HDGB_PC_RAS ? 1 : 2);
+                            p->kind == HDGB_PC_RAS ? 1 : 2, epi);
             break;
         }
     }
@@ -131,8 +134,50 @@ void apply_poly_op(hdgb_precond* p, const DevOp& base, hdgb_matrix* k, const dou
     }
 }
 
+// apply_poly (preconditioner.cpp:246-283) with the preconditioner's own base: identical recurrence, the vector
+// updates w += q / theta, q -= t / theta (and the pair step) applied inside the kernel that produces t.
+void apply_poly_fused(hdgb_precond* p, hdgb_matrix* k, const double* y, double* z) {
+    hdgb_ctx* c = p->ctx;
+    const int64_t n = k->n_dof();
+    const size_t ld = static_cast<size_t>(k->n_local());
+    if (p->wq.n != ld) { p->wq.alloc(ld); p->wt.alloc(ld); p->ws.alloc(ld); p->wkv.alloc(ld); }
+    double *q = p->wq.p, *t = p->wt.p, *s = p->ws.p, *kv = p->wkv.p;
+    double* w = z;
+    apply_base_device(p, y, q);
+    launch_fill(c, w, 0.0, n);
+    auto op = [&](const double* in, const PolyEpi& e) {
+        matvec_device(k, in, kv);
+        apply_base_device(p, kv, t, &e);
+        ++p->inner_ops;
+    };
+    const size_t cnt = p->ritz.size() / 2;
+    size_t i = 0;
+    while (i < cnt) {
+        const double re = p->ritz[2 * i], im = p->ritz[2 * i + 1];
+        PolyEpi e;
+        e.q = q; e.w = w; e.s = s;
+        if (im == 0.0) {
+            e.mode = PolyEpi::kReal;
+            e.a = 1.0 / re;
+            op(q, e);  // w += q / theta ; q -= op(q) / theta
+            i += 1;
+        } else {
+            const double inv = 1.0 / (re * re + im * im);
+            e.mode = PolyEpi::kMid;
+            e.a = 2.0 * re;
+            e.b = inv;
+            op(q, e);  // s = 2a q - op(q) ; w += inv s
+            e.mode = PolyEpi::kLast;
+            e.a = inv;
+            op(s, e);  // q -= inv op(s)
+            i += 2;
+        }
+    }
+}
+
 static void apply_poly_device(hdgb_precond* p, hdgb_matrix* k, const double* y, double* z) {
-    apply_poly_op(p, [p](const double* in, double* out) { apply_base_device(p, in, out); }, k, y, z);
+    if (tuning().poly_fused) apply_poly_fused(p, k, y, z);
+    else apply_poly_op(p, [p](const double* in, double* out) { apply_base_device(p, in, out); }, k, y, z);
 }
 
 void apply_precond_device(hdgb_precond* p, hdgb_matrix* k, const double* y, double* z) {

@@ -156,7 +156,7 @@ namespace {
 
 __global__ void face_sum_kernel(const double* __restrict__ ze, const int* __restrict__ face_elems,
                                 const int* __restrict__ face_lidx, int nf, int mpf, int n_lfe,
-                                double* __restrict__ z, int sides) {
+                                double* __restrict__ z, int sides, PolyEpi epi) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= static_cast<int64_t>(nf) * mpf) return;
     const int f = static_cast<int>(i / mpf);
@@ -169,7 +169,8 @@ __global__ void face_sum_kernel(const double* __restrict__ ze, const int* __rest
         const int l = face_lidx[2 * f + side];
         acc += ze[(static_cast<int64_t>(e) * n_lfe + l) * mpf + r];
     }
-    z[i] = acc;
+    if (epi.mode == PolyEpi::kNone) z[i] = acc;
+    else poly_epilogue(epi, i, acc);
 }
 
 __global__ void gather_element_trace_kernel(const double* __restrict__ v, const int* __restrict__ elem_faces,
@@ -194,10 +195,11 @@ __global__ void gather_extended_kernel(const double* __restrict__ x, const int* 
 }  // namespace
 
 void launch_face_sum(hdgb_ctx* ctx, const double* ze, const int* face_elems, const int* face_lidx,
-                     int nf, int mpf, int n_lfe, double* z, int sides) {
+                     int nf, int mpf, int n_lfe, double* z, int sides, const PolyEpi* epi) {
     const int64_t total = static_cast<int64_t>(nf) * mpf;
     if (total == 0) return;
-    face_sum_kernel<<<ceil_div(total, 256), 256, 0, ctx->stream>>>(ze, face_elems, face_lidx, nf, mpf, n_lfe, z, sides);
+    face_sum_kernel<<<ceil_div(total, 256), 256, 0, ctx->stream>>>(ze, face_elems, face_lidx, nf, mpf, n_lfe, z, sides,
+                                                                   epi ? *epi : PolyEpi());
     HDGB_LAUNCH_CHECK(ctx);
 }
 

@@ -234,6 +234,12 @@ __global__ void poly_pair_mid_kernel(double two_a, double inv, const double* __r
     }
 }
 
+__global__ void poly_update_kernel(PolyEpi epi, const double* __restrict__ t, int64_t n) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        poly_epilogue(epi, i, t[i]);
+}
+
 __global__ void check_finite_kernel(const double* __restrict__ v, int64_t n, int* flags) {
     bool bad = false;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -349,6 +355,12 @@ void launch_poly_pair_mid(hdgb_ctx* ctx, double two_a, double inv, const double*
                           double* s, double* w, int64_t n) {
     if (n <= 0) return;
     poly_pair_mid_kernel<<<stream_grid(ctx, n, 256), 256, 0, ctx->stream>>>(two_a, inv, q, t, s, w, n);
+    HDGB_LAUNCH_CHECK(ctx);
+}
+
+void launch_poly_update(hdgb_ctx* ctx, const PolyEpi& epi, const double* t, int64_t n) {
+    if (n <= 0) return;
+    poly_update_kernel<<<stream_grid(ctx, n, 256), 256, 0, ctx->stream>>>(epi, t, n);
     HDGB_LAUNCH_CHECK(ctx);
 }
 

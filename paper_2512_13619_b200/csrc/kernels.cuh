@@ -36,6 +36,7 @@ struct Tuning {
     int stream_packed = 1;               // small items: 16 warps, several items side by side per warp, no shuffle tree
     int stream_packed_max_cols = 32;     // ... for items with at most this many columns
     int64_t stream_packed_stage_bytes = 6144;  // ... bytes per TMA stage of a warp in packed mode
+    int poly_fused = 1;                  // polynomial preconditioner: recurrence updates fused into the kernel producing base(K v)
     int overlap_halo = 1;                // domain decomposition: interior rows / elements run while the halo exchange is in flight
     int spin_sync = 1;                   // GMRES: poll an event for the per-iteration Hessenberg column instead of a blocking sync
     int fused_cgs = 0;                   // round-1 register-resident fused CGS2 pass (measured slower: 112 us vs 85 us at cfg2)
@@ -58,10 +59,40 @@ struct Tuning {
 };
 Tuning& tuning();
 
+// Update step of the polynomial-preconditioner recurrence (preconditioner.cpp:259-281) applied where the value
+// t_i = (base K v)_i is produced, instead of as separate vector kernels over t:
+//   kReal : w += a q ;  q -= a t                      (real node, a = 1 / theta)
+//   kMid  : s = a q - t ;  w += b s                   (conjugate pair, first half: a = 2 Re, b = 1 / |theta|^2)
+//   kLast : q -= a t                                  (conjugate pair, second half)
+struct PolyEpi {
+    enum Mode { kNone = 0, kReal = 1, kMid = 2, kLast = 3 };
+    int mode = kNone;
+    double a = 0.0, b = 0.0;
+    double* q = nullptr;
+    double* w = nullptr;
+    double* s = nullptr;
+};
+__host__ __device__ inline void poly_epilogue(const PolyEpi& e, int64_t i, double t) {
+    if (e.mode == PolyEpi::kReal) {
+        const double qv = e.q[i];
+        e.w[i] = e.a * qv + e.w[i];
+        e.q[i] = -e.a * t + qv;
+    } else if (e.mode == PolyEpi::kMid) {
+        const double sv = e.a * e.q[i] - t;
+        e.s[i] = sv;
+        e.w[i] += e.b * sv;
+    } else {
+        e.q[i] = -e.a * t + e.q[i];
+    }
+}
+// the same update for bases that deliver t as a vector (identity, block-Jacobi, caller closures): one kernel
+void launch_poly_update(hdgb_ctx* ctx, const PolyEpi& epi, const double* t, int64_t n);
+
 // z_f[i] = ze[e0][l0][i] + ze[e1][l1][i]   (apply_asm scatter as an atomics-free face gather)
 // sides = 1 keeps only the owner's (side-0) term: the restricted (RAS) prolongation.
+// epi != nullptr: the sum feeds the polynomial update directly and z is not written.
 void launch_face_sum(hdgb_ctx* ctx, const double* ze, const int* face_elems, const int* face_lidx,
-                     int nf, int mpf, int n_lfe, double* z, int sides = 2);
+                     int nf, int mpf, int n_lfe, double* z, int sides = 2, const PolyEpi* epi = nullptr);
 // out[e][l][i] = v[elem_faces[e][l]][i]  (gather_element_trace)
 void launch_gather_element_trace(hdgb_ctx* ctx, const double* v, const int* elem_faces, int ne,
                                  int n_lfe, int mpf, double* out);

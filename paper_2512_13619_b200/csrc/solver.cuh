@@ -12,7 +12,9 @@ namespace hdgb {
 // y = K x  (block_matvec, face_matrix.cpp:83-107), device pointers.
 void matvec_device(hdgb_matrix* k, const double* x, double* y);
 // z = base(y): identity / apply_bj / apply_asm / RAS (preconditioner.cpp:285-299), device pointers.
-void apply_base_device(hdgb_precond* p, const double* y, double* z);
+// epi != nullptr: the result feeds the polynomial update (kernels.cuh PolyEpi) instead of being written to z; z is
+// then scratch of the vector length (used by the bases that deliver their result as a vector).
+void apply_base_device(hdgb_precond* p, const double* y, double* z, const PolyEpi* epi = nullptr);
 // z = P^-1 y incl. the polynomial wrapper (preconditioner.cpp:301-308).  p == nullptr: identity.
 void apply_precond_device(hdgb_precond* p, hdgb_matrix* k, const double* y, double* z);
 // build_preconditioner (newton.cpp:30-52)
@@ -50,6 +52,8 @@ std::vector<std::complex<double>> harmonic_ritz_op(hdgb_ctx* c, const DevOp& op,
                                                    int64_t n_global, bool* breakdown_out);
 // apply_poly (preconditioner.cpp:246-283) with an arbitrary base application: z = poly(base K) base y.
 void apply_poly_op(hdgb_precond* p, const DevOp& base, hdgb_matrix* k, const double* y, double* z);
+// ... with the preconditioner's own base, the recurrence updates fused into the base's last kernel
+void apply_poly_fused(hdgb_precond* p, hdgb_matrix* k, const double* y, double* z);
 // the two-sided diagonal sub-block sums of build_asm (preconditioner.cpp:59-75) straight from K-bar
 void launch_face_diag(hdgb_ctx* ctx, const DiscView& dv, const double* kbar, double* diag);
 // build_bj (preconditioner.cpp:30-46) / build_asm (:54-84) as separate entry points

@@ -178,3 +178,28 @@ def test_apply_poly_exact_inverse_with_closure_base(ctx):
     assert inner == 6
     z2, _ = hdg.apply_poly(p, K, y)   # the preconditioner's own (identity) base
     assert np.array_equal(z, z2)
+
+
+@pytest.mark.parametrize("kind", ["identity", "bj", "asm", "ras"])
+def test_fused_polynomial_epilogues_equal_the_separate_updates(ctx, kind):
+    """The recurrence updates (preconditioner.cpp:259-281) applied inside the kernel that produces base(K v) -- the ASM
+    face sum / one pass after the BJ GEMV -- against the separate vector kernels: same operations on the same
+    values, so bit-identical, for real nodes and conjugate pairs; inner operator counts unchanged."""
+    disc, model, state, ops, K, rhs = system(ctx, "burgers2d", 2, 6)
+    y = hdg.random_vector(K.n_dof, 31)
+    for spec in (hdg.PrecondSpec(kind, poly_degree=7), hdg.PrecondSpec(kind, poly_degree=6, poly_kind="chebyshev")):
+        out = {}
+        for fused in (1, 0):
+            hdg.set_tuning("poly_fused", fused)
+            try:
+                P = hdg.build_preconditioner(spec, K, ops, disc)
+                out[fused] = (P.apply(y), P.inner_ops, P.ritz)
+                if spec.poly_kind == 0:  # also with conjugate pairs among the nodes
+                    P.set_ritz([3 + 1j, 3 - 1j, 5.0, 1 + 2j, 1 - 2j])
+                    out[fused] += (P.apply(y),)
+            finally:
+                hdg.set_tuning("poly_fused", 1)
+        assert np.array_equal(out[1][2], out[0][2])
+        assert np.array_equal(out[1][0], out[0][0]) and out[1][1] == out[0][1]
+        if len(out[1]) > 3:
+            assert np.array_equal(out[1][3], out[0][3])
