@@ -1,0 +1,31 @@
+"""Small invocations of every hand-written kernel family for compute-sanitizer (memcheck / racecheck / synccheck):
+the DMMA local-assembly kernel (hex p = 3), fused q-elimination, blocked Gauss-Jordan, the bulk-TMA stream GEMV in
+plain and packed mode (forced on for small problems), the TMA-streamed CGS2 passes, the fused polynomial epilogues.
+
+  compute-sanitizer --tool racecheck python scripts/sanitize_probe.py"""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import numpy as np  # noqa: E402
+import paper_2512_13619_b200 as hdg  # noqa: E402
+
+ctx = hdg.Context(0)
+hdg.set_tuning("stream_min_elems", 0)       # route the small GEMVs through the TMA stream kernel too
+cases = [("hex", 3, 3, "poisson", hdg.PrecondSpec("asm")),
+         ("tri", 6, 4, "burgers", hdg.PrecondSpec("asm", poly_degree=4, poly_kind="chebyshev")),
+         ("quad", 6, 2, "burgers", hdg.PrecondSpec("bj", poly_degree=5))]
+for shape, n, k, case, pspec in cases:
+    disc = hdg.Discretization.structured(ctx, shape, n=n, degree=k, jitter=0.1 if shape == "tri" else 0.0)
+    model = hdg.make_case_model(disc, case)
+    state = hdg.make_initial_state(disc, model)
+    rep = hdg.newton_solve(disc, model, state, pspec=pspec)
+    assert rep.converged, (shape, rep)
+    print(shape, k, case, "newton", rep.n_newton, "gmres", rep.n_gmres_total, "launches", ctx.launch_count)
+# the streamed CGS2 passes on a basis long enough for the TMA path
+n, nvec = 1 << 16, 6
+V, _ = np.linalg.qr(hdg.random_vector(n * nvec, 1).reshape(n, nvec))
+h, w = hdg.orthogonalize(ctx, np.ascontiguousarray(V.T), hdg.random_vector(n, 2))
+assert abs(np.linalg.norm(w) - 1.0) < 1e-12 and np.max(np.abs(V.T @ w)) < 1e-12
+print("cgs ok")
+ctx.close()

@@ -107,6 +107,38 @@ def test_preconditioner_apply(ctx, ref, kind):
         assert relerr(P.apply_base(y), rc.apply_base(y)) < 1e-10
 
 
+def test_restricted_additive_schwarz_from_reference_pieces(ctx, ref):
+    """RAS is not in the reference, but every piece of it is: the inverted enriched element blocks
+    (build_asm, preconditioner.cpp:54-84), the element gather (local_ops.cpp:351-365) and the mesh's side tables.
+    The restricted prolongation -- a shared face keeps only its side-0 (owner) element's correction instead of the
+    two-sided sum of preconditioner.cpp:92-103 -- is restated here in numpy on the REFERENCE's own data, which pins
+    the device RAS apply to the compiled reference."""
+    rc, disc, model, state = make(ctx, ref, "burgers2d", 2, 6)
+    rc.perturb(11, 0.1)
+    state.u, state.uhat = rc.get("u"), rc.get("uhat")
+    rc.assemble()
+    rc.build_precond("asm")
+    ne, nf, pf = rc.ne, rc.nf, rc.pf
+    nfl = 4 * pf
+    inv = rc.get("asm_inv").reshape(ne, nfl, nfl)                     # column-major blocks: [e][col][row]
+    f2e = rc.get_i("face_to_elements").reshape(nf, 2)
+    fli = rc.get_i("face_local_index").reshape(nf, 2)
+    ops = hdg.assemble_element_operators(disc, model, state)
+    K, _ = hdg.assemble_global(disc, ops)
+    P = hdg.build_preconditioner("ras", K, ops, disc)
+    for seed in range(4):
+        y = hdg.random_vector(K.n_dof, 300 + seed)
+        ye = rc.gather_element_trace(y).reshape(ne, nfl)
+        ze = np.einsum("ecr,ec->er", inv, ye)                            # ze_e = inv_e ye_e
+        want = np.stack([ze[f2e[f, 0], fli[f, 0] * pf:(fli[f, 0] + 1) * pf] for f in range(nf)]).ravel()
+        both = want.copy().reshape(nf, pf)
+        for f in range(nf):
+            if f2e[f, 1] >= 0:
+                both[f] += ze[f2e[f, 1], fli[f, 1] * pf:(fli[f, 1] + 1) * pf]
+        assert relerr(both.ravel(), rc.apply_base(y)) < 1e-13          # the restatement reproduces the reference's ASM
+        assert relerr(P.apply_base(y), want) < 1e-10
+
+
 @pytest.mark.parametrize("kind,deg", [("bj", 6), ("asm", 10)])
 def test_polynomial_preconditioner(ctx, ref, kind, deg):
     rc, disc, model, state = make(ctx, ref, "burgers2d", 1, 8)
