@@ -75,7 +75,8 @@ const char* hdgb_version(void);
  *                "qelim_wn", "qelim_stages", "gemm_wn_cap", "use_blocked_gj" (blocked Gauss-Jordan inverse),
  *                "use_tile_lu" (register-tiled Gauss-Jordan, n <= 128, when the blocked one is off);
  *   assembly:    "local_dmma_min_pe", "local_global_records", "local_dmma_chunked", "assemble_budget_kb";
- *   GMRES:       "fused_cgs", "cgs_stream", "spin_sync", "poly_fused" (polynomial recurrence updates as epilogues);
+ *   GMRES:       "fused_cgs", "cgs_stream", "spin_sync", "poly_fused" (polynomial recurrence updates as epilogues),
+ *                "gmres_speculate" (next Arnoldi step's operator applications enqueued before the host reads the column);
  *   multi-GPU:   "overlap_halo" (interior rows / elements computed while the halo exchange is in flight).
  * Returns non-zero for an unknown key.  Results do not depend on them beyond rounding. */
 int hdgb_set_tuning(const char* key, int64_t value);

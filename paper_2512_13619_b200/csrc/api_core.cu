@@ -28,6 +28,7 @@ int hdgb_set_tuning(const char* key, int64_t value) {
     if (k == "gj_panel_cta") { hdgb::tuning().gj_panel_cta = static_cast<int>(value); return 0; }
     if (k == "use_blocked_gj") { hdgb::tuning().use_blocked_gj = static_cast<int>(value); return 0; }
     if (k == "qelim_split_rows") { hdgb::tuning().qelim_split_rows = static_cast<int>(value); return 0; }
+    if (k == "gmres_speculate") { hdgb::tuning().gmres_speculate = static_cast<int>(value); return 0; }
     if (k == "poly_fused") { hdgb::tuning().poly_fused = static_cast<int>(value); return 0; }
     if (k == "overlap_halo") { hdgb::tuning().overlap_halo = static_cast<int>(value); return 0; }
     if (k == "spin_sync") { hdgb::tuning().spin_sync = static_cast<int>(value); return 0; }

@@ -34,8 +34,12 @@ GmresWork& gmres_work(hdgb_matrix* k, int restart) {
 // the last pass already writes the normalised vector; if that difference cancels badly (w almost in span V: the
 // happy-breakdown regime) the norm is re-measured explicitly.
 // coef: 2 nvec + 2 device scalars  c | d | s0 | s1 ;  cgs: workspace of the streamed passes or nullptr.
+// between (may be null): called once the column's device-to-host copy and the normalisation are enqueued and before
+// the host waits for them -- the caller enqueues the next step's operator applications there, so the device does
+// not idle while the host reads the column and issues the next launches.
 void orthogonalize_device(hdgb_ctx* c, const double* V, int64_t ldv, int nvec, int64_t n, double* w, int orth,
-                          double* coef, double* partial, double* cgs, double* h) {
+                          double* coef, double* partial, double* cgs, double* h,
+                          const std::function<void()>* between = nullptr) {
     double* dc = coef;
     double* dd = coef + nvec;
     double* s0 = coef + 2 * nvec;
@@ -100,7 +104,12 @@ void orthogonalize_device(hdgb_ctx* c, const double* V, int64_t ldv, int nvec, i
     // travels to the host
     HDGB_CUDA(cudaMemcpyAsync(stage, coef, (2 * nvec + 1) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     launch_scale_dev(c, w, s0, 0, w, n);
-    wait();
+    if (between && host_mark(c)) {
+        (*between)();
+        host_poll(c, tuning().spin_sync != 0);
+    } else {
+        wait();
+    }
     for (int i = 0; i < nvec; ++i) h[i] = stage[i] + stage[nvec + i];
     h[nvec] = std::sqrt(stage[2 * nvec]);
 }
@@ -128,11 +137,13 @@ void gmres_device(hdgb_matrix* k, hdgb_precond* p, const double* rhs, double* x,
     if (cfg.restart < 1) throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: GMRES restart length must be >= 1");
     GmresWork& W = gmres_work(k, cfg.restart);
     gmres_core(k->ctx, k->n_dof(), k->n_local(), W, [k](const double* in, double* out) { matvec_device(k, in, out); },
-               [k, p](const double* in, double* out) { apply_precond_device(p, k, in, out); }, rhs, x, cfg, st, residual_trace);
+               [k, p](const double* in, double* out) { apply_precond_device(p, k, in, out); }, rhs, x, cfg, st, residual_trace,
+               p ? &p->inner_ops : &k->spec_dummy);
 }
 
 void gmres_core(hdgb_ctx* c, int64_t n, int64_t ld, GmresWork& W, const DevOp& matvec, const DevOp& precond,
-                const double* rhs, double* x, const hdgb_gmres_config& cfg, hdgb_gmres_stats* st, double* residual_trace) {
+                const double* rhs, double* x, const hdgb_gmres_config& cfg, hdgb_gmres_stats* st, double* residual_trace,
+                int64_t* spec_counter) {
     const int m = cfg.restart;
     if (m < 1) throw Failure(HDGB_ERR_DIMENSION_MISMATCH, "dimension mismatch: GMRES restart length must be >= 1");
     if (2 * static_cast<size_t>(m + 1) + 4 > c->pinned_doubles) throw Failure(HDGB_ERR_UNSUPPORTED, "GMRES restart length too large");
@@ -194,9 +205,17 @@ void gmres_core(hdgb_ctx* c, int64_t n, int64_t ld, GmresWork& W, const DevOp& m
         int nbasis = 1;
         int jused = 0;
         bool cycle_converged = false;
+        // Speculative pipelining (handle form, single GPU): the next step's candidate P^-1 K v_{j+1} depends only on
+        // the normalised vector the orthogonalisation leaves on the device, so it is enqueued BEFORE the host waits
+        // for this step's Hessenberg column; if the column then ends the cycle (convergence, breakdown, iteration
+        // cap) the speculative candidate is simply dropped.  spec_counter (the preconditioner's operator count) is
+        // rolled back in that case, so the reported statistics are those of the reference's control flow.
+        const bool speculate = spec_counter && tuning().gmres_speculate && !c->comm && !c->phase_timing;
+        bool have_spec = false;
+        int64_t counter_before_spec = 0;
         for (int j = 0; j < m && st->iters < cfg.max_iters; ++j) {
             double* w = V + static_cast<size_t>(j + 1) * ld;  // the candidate lands in its basis slot
-            {
+            if (!have_spec) {
                 PhaseTimer tm(c, &st->t_mv);
                 matvec(V + static_cast<size_t>(j) * ld, kv);
                 tm.stop();
@@ -204,9 +223,18 @@ void gmres_core(hdgb_ctx* c, int64_t n, int64_t ld, GmresWork& W, const DevOp& m
                 apply_prec(kv, w);
                 tp.stop();
             }
+            have_spec = false;
+            const std::function<void()> next = [&] {
+                if (j + 1 >= m || st->iters + 1 >= cfg.max_iters) return;
+                counter_before_spec = *spec_counter;
+                matvec(w, kv);
+                apply_prec(kv, w + ld);
+                have_spec = true;
+            };
             {
                 PhaseTimer to(c, &st->t_orth);
-                orthogonalize_device(c, V, ld, nbasis, n, w, cfg.orth, W.coef.p, W.partial.p, W.cgs.p, h.data());
+                orthogonalize_device(c, V, ld, nbasis, n, w, cfg.orth, W.coef.p, W.partial.p, W.cgs.p, h.data(),
+                                     speculate ? &next : nullptr);
                 to.stop();
             }
             for (int i = 0; i <= nbasis; ++i)
@@ -241,6 +269,7 @@ void gmres_core(hdgb_ctx* c, int64_t n, int64_t ld, GmresWork& W, const DevOp& m
                 break;
             }
         }
+        if (have_spec) *spec_counter = counter_before_spec;  // the cycle ended: the speculative candidate is dropped
         if (jused == 0)
             throw Failure(HDGB_ERR_NAN_DETECTED,
                           "NaN detected in gmres made no progress: the preconditioned operator annihilated the residual direction");
@@ -363,8 +392,9 @@ hdgb_status hdgb_gmres_solve_fn(hdgb_ctx* c, int64_t n, hdgb_op_fn matvec, void*
         std::unique_ptr<GmresWork> W = make_gmres_work(c, n, n, std::max(1, std::min(cf.restart, cf.max_iters)));
         run.restart = W->restart;
         hdgb_gmres_stats local;
+        // callbacks are invoked exactly as often as the reference invokes its closures: no speculation here
         gmres_core(c, n, n, *W, wrap(matvec, mv_user, "matvec"), wrap(precond, pc_user, "preconditioner"), B.dev, X.dev, run,
-                   stats ? stats : &local, residual_trace);
+                   stats ? stats : &local, residual_trace, nullptr);
         X.commit();
         HDGB_CUDA(cudaStreamSynchronize(c->stream));
     });

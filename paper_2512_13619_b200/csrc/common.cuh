@@ -88,6 +88,27 @@ inline void host_wait(hdgb_ctx* c) {
     }
     if (e != cudaSuccess) HDGB_CUDA(e);
 }
+// The same wait in two halves: host_mark() notes the point of the stream the host needs, more work may be enqueued
+// behind it, host_poll() waits for the marked point only (spinning or blocking).
+inline bool host_mark(hdgb_ctx* c) {
+    if (!c->spin_ev && cudaEventCreateWithFlags(&c->spin_ev, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        c->spin_ev = nullptr;
+        return false;
+    }
+    HDGB_CUDA(cudaEventRecord(c->spin_ev, c->stream));
+    return true;
+}
+inline void host_poll(hdgb_ctx* c, bool spin) {
+    if (!spin) {
+        HDGB_CUDA(cudaEventSynchronize(c->spin_ev));
+        return;
+    }
+    cudaError_t e;
+    while ((e = cudaEventQuery(c->spin_ev)) == cudaErrorNotReady) {
+    }
+    if (e != cudaSuccess) HDGB_CUDA(e);
+}
 }  // namespace hdgb
 
 namespace hdgb {

@@ -110,6 +110,7 @@ struct hdgb_matrix {
     bool neighbor_valid = false;
     int m = 1, pf = 0, n_lfe = 4, nf = 0;
     int nf_local = 0;  // faces a vector spans (owned first, then halo); == nf on one GPU
+    int64_t spec_dummy = 0;  // stand-in operator counter of preconditioner-free solves (speculative GMRES pipelining)
     int nf_interior = 0;  // leading rows that reference owned faces only (computed while the halo exchange is in flight)
     int mpf() const { return m * pf; }
     int nb() const { return 2 * n_lfe - 1; }

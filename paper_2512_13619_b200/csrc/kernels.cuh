@@ -36,6 +36,7 @@ struct Tuning {
     int stream_packed = 1;               // small items: 16 warps, several items side by side per warp, no shuffle tree
     int stream_packed_max_cols = 32;     // ... for items with at most this many columns
     int64_t stream_packed_stage_bytes = 6144;  // ... bytes per TMA stage of a warp in packed mode
+    int gmres_speculate = 1;             // GMRES: enqueue the next step's matvec + preconditioner before waiting for the Hessenberg column
     int poly_fused = 1;                  // polynomial preconditioner: recurrence updates fused into the kernel producing base(K v)
     int overlap_halo = 1;                // domain decomposition: interior rows / elements run while the halo exchange is in flight
     int spin_sync = 1;                   // GMRES: poll an event for the per-iteration Hessenberg column instead of a blocking sync

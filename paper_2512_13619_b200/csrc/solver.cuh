@@ -43,7 +43,7 @@ using DevOp = std::function<void(const double* in, double* out)>;
 std::unique_ptr<GmresWork> make_gmres_work(hdgb_ctx* c, int64_t n, int64_t ld, int restart);
 void gmres_core(hdgb_ctx* c, int64_t n, int64_t ld, GmresWork& W, const DevOp& matvec, const DevOp& precond,
                 const double* rhs, double* x, const hdgb_gmres_config& cfg, hdgb_gmres_stats* stats,
-                double* residual_trace);
+                double* residual_trace, int64_t* spec_counter = nullptr);
 // compute_harmonic_ritz (preconditioner.cpp:119-205) of op on n owned unknowns (ld vector length): seeded start
 // vector over n_global unknowns (face_gid maps local faces of width mpf to global ones, nullptr = identity),
 // MGS Arnoldi on the device, eigen-solve + Leja order on the host.
