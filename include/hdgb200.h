@@ -74,7 +74,7 @@ const char* hdgb_version(void);
  *   dense:       "use_dmma" (FP64 tensor-core GEMM / local blocks), "use_qelim_fused", "qelim_split_rows",
  *                "qelim_wn", "qelim_stages", "gemm_wn_cap", "use_blocked_gj" (blocked Gauss-Jordan inverse),
  *                "use_tile_lu" (register-tiled Gauss-Jordan, n <= 128, when the blocked one is off);
- *   assembly:    "local_dmma_min_pe", "local_global_records", "local_dmma_chunked", "assemble_budget_kb";
+ *   assembly:    "local_nt", "local_dmma_min_pe", "local_global_records", "local_dmma_chunked", "assemble_budget_kb";
  *   GMRES:       "fused_cgs", "cgs_stream", "spin_sync", "poly_fused" (polynomial recurrence updates as epilogues),
  *                "gmres_speculate" (next Arnoldi step's operator applications enqueued before the host reads the column);
  *   multi-GPU:   "overlap_halo" (interior rows / elements computed while the halo exchange is in flight).

@@ -123,7 +123,6 @@ constexpr int kResParts = 8;   // thread groups sharing one basis function's poi
 constexpr int kEdKc = 16;      // points per chunk
 constexpr int kEdSlotsMax = 4;  // 16 x 32 output tiles per warp: 2 for scalar systems (two CTAs per SM), 4 for wide ones (fewer passes)
 __host__ __device__ constexpr int ed_slots(int M) { return M == 1 ? 2 : kEdSlotsMax; }
-constexpr int kEdGroups = 32;  // ... of 16 warps
 
 // Operand chunks are stored POINT-major ([point in chunk][basis function], leading dimensions = 4 mod 16): the
 // builder's half-warps write 16 consecutive basis functions of one point (conflict-free stores) and both DMMA
@@ -147,11 +146,12 @@ inline __host__ __device__ EdPlan ed_plan(int pe, int M, int D, int nwarps) {
     p.lda = p.rg * 16 + 4;
     p.ldb = p.cg * 32 + 4;
     const int per_pair = (1 + D) * p.rg * p.cg;
-    int pp = kEdGroups / per_pair;
+    const int gs = nwarps * kEdSlots, rc = p.rg * p.cg;  // gs: 16 x 32 tiles the CTA's accumulator slots hold at a time
+    int pp = gs / per_pair;                               // component pairs sharing one sweep (and one weighted basis)
     if (pp < 1) pp = 1;
     if (pp > M * M) pp = M * M;
     p.pp = pp;
-    const int gs = nwarps * kEdSlots, rc = p.rg * p.cg, qp = pp * (1 + D);
+    const int qp = pp * (1 + D);
     int wsub = (gs + rc - 1) / rc + ((gs % rc) ? 1 : 0);
     if (wsub > qp) wsub = qp;
     p.wsub = wsub;
@@ -196,7 +196,8 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
     // Builder mapping (blockDim.x == 256 = 16 half-warps): half-warp <-> point of the chunk, lanes <-> basis functions
     // i0, i0 + 16, ...  A thread reads its point's coefficients once per chunk and the basis tables with 128-byte
     // half-warp loads; every operand entry the products read (incl. the zero padding) is written by exactly one thread.
-    const int bkk = tid >> 4, bi0 = tid & 15;
+    // With 512 threads two half-warps share a point: each builds every second resident matrix (cached builder only).
+    const int bkk = (tid >> 4) & 15, bi0 = tid & 15, bsub = tid >> 8, nsub = nt >> 8;
     const int irows = pl.rg * 16, icols = pl.cg * 32, ldb = pl.ldb;
     for (int pair0 = 0; pair0 < M * M; pair0 += pl.pp) {
         const int npair = min(pl.pp, M * M - pair0);
@@ -312,6 +313,7 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
             const int pt = live ? p0 + bkk : 0;
             const int nres = whi - wlo;
             const int qstride = kEdKc * lda;
+            // this thread's resident matrices: q = bsub, bsub + nsub, ... (kEdRes of them at most)
             if (vol) {
                 const int g = gv0 + pt;
                 const VolRec<M, D>& r = vrec[pt];
@@ -319,23 +321,24 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
                 double c0[kEdRes], ck[kEdRes][D];
                 bool td[kEdRes];
 #pragma unroll
-                for (int q = 0; q < kEdRes; ++q) {
-                    c0[q] = 0.0;
-                    td[q] = false;
+                for (int qi = 0; qi < kEdRes; ++qi) {
+                    const int q = bsub + nsub * qi;
+                    c0[qi] = 0.0;
+                    td[qi] = false;
 #pragma unroll
-                    for (int k = 0; k < D; ++k) ck[q][k] = 0.0;
+                    for (int k = 0; k < D; ++k) ck[qi][k] = 0.0;
                     if (q < nres) {
                         const int wg = wlo + q, pi = wg / (1 + D), w = wg - pi * (1 + D);
                         const int pr = pair0 + pi, mp = pr / M, m = pr - mp * M, mm = m * M + mp;
                         if (w == 0) {
-                            c0[q] = rec_ld<GREC>(&r.dSu[mm]);
+                            c0[qi] = rec_ld<GREC>(&r.dSu[mm]);
 #pragma unroll
-                            for (int k = 0; k < D; ++k) ck[q][k] = rec_ld<GREC>(&r.cE[mm * D + k]);
-                            td[q] = transient && m == mp;
+                            for (int k = 0; k < D; ++k) ck[qi][k] = rec_ld<GREC>(&r.cE[mm * D + k]);
+                            td[qi] = transient && m == mp;
                         } else {
-                            c0[q] = rec_ld<GREC>(&r.dSq[mm * D + w - 1]);
+                            c0[qi] = rec_ld<GREC>(&r.dSq[mm * D + w - 1]);
 #pragma unroll
-                            for (int k = 0; k < D; ++k) ck[q][k] = rec_ld<GREC>(&r.cD[((w - 1) * M * M + mm) * D + k]);
+                            for (int k = 0; k < D; ++k) ck[qi][k] = rec_ld<GREC>(&r.cD[((w - 1) * M * M + mm) * D + k]);
                         }
                     }
                 }
@@ -353,17 +356,18 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
                     for (int k = 0; k < D; ++k) dp_[k] = inb ? __ldg(dpp[k] + 16 * it) : 0.0;
                     if (16 * it < irows) {
 #pragma unroll
-                        for (int q = 0; q < kEdRes; ++q) {
+                        for (int qi = 0; qi < kEdRes; ++qi) {
+                            const int q = bsub + nsub * qi;
                             if (q >= nres) break;
                             double fs = 0.0;
 #pragma unroll
-                            for (int k = 0; k < D; ++k) fs += ck[q][k] * dp_[k];
-                            double v = -fs - c0[q] * ph;
-                            if (td[q]) v += in.dt_inv * ph;
+                            for (int k = 0; k < D; ++k) fs += ck[qi][k] * dp_[k];
+                            double v = -fs - c0[qi] * ph;
+                            if (td[qi]) v += in.dt_inv * ph;
                             Ab[q * qstride + 16 * it] = inb ? v : 0.0;
                         }
                     }
-                    Bb[16 * it] = inb ? wq * ph : 0.0;
+                    if (bsub == 0) Bb[16 * it] = inb ? wq * ph : 0.0;
                 }
             } else {
                 const int p = fp0 + pt;
@@ -372,13 +376,14 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
                 const double wq = rec_ld<GREC>(&r.w);
                 double cf[kEdRes];
 #pragma unroll
-                for (int q = 0; q < kEdRes; ++q) {
-                    cf[q] = 0.0;
+                for (int qi = 0; qi < kEdRes; ++qi) {
+                    const int q = bsub + nsub * qi;
+                    cf[qi] = 0.0;
                     if (q < nres) {
                         const int wg = wlo + q, pi = wg / (1 + D), w = wg - pi * (1 + D);
                         const int pr = pair0 + pi, mp = pr / M, m = pr - mp * M, mm = m * M + mp;
-                        if (w == 0) cf[q] = (m == mp) ? rec_ld<GREC>(&r.tau) : 0.0;
-                        else cf[q] = rec_ld<GREC>(&r.dfh_q[mm * D + w - 1]);
+                        if (w == 0) cf[qi] = (m == mp) ? rec_ld<GREC>(&r.tau) : 0.0;
+                        else cf[qi] = rec_ld<GREC>(&r.dfh_q[mm * D + w - 1]);
                     }
                 }
                 const double* php = dv.tphi + ((static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf + gc) * pe + bi0;
@@ -389,12 +394,13 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
                     const double ph = inb ? __ldg(php + 16 * it) : 0.0;
                     if (16 * it < irows) {
 #pragma unroll
-                        for (int q = 0; q < kEdRes; ++q) {
+                        for (int qi = 0; qi < kEdRes; ++qi) {
+                            const int q = bsub + nsub * qi;
                             if (q >= nres) break;
-                            Ab[q * qstride + 16 * it] = inb ? cf[q] * ph : 0.0;
+                            Ab[q * qstride + 16 * it] = inb ? cf[qi] * ph : 0.0;
                         }
                     }
-                    Bb[16 * it] = inb ? wq * ph : 0.0;
+                    if (bsub == 0) Bb[16 * it] = inb ? wq * ph : 0.0;
                 }
             }
         };
@@ -418,7 +424,7 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
                 aoff[s] = gid < ngroups ? (w - wlo) * kEdKc * lda + rgi * 16 + grp + tig * lda : -1;
                 boff[s] = boff0 + cgi * 32 + grp + tig * ldb;
             }
-            const bool cached = whi - wlo <= kEdRes;
+            const bool cached = whi - wlo <= kEdRes * nsub;  // (the launcher uses 512 threads only where this holds)
             __syncthreads();
             if (cached) build_cached(0, 0);
             else build(0, 0);
@@ -570,46 +576,35 @@ __device__ void hgf_dmma(const DiscView& dv, const LocalOut& out, int e, const F
                     }
                 }
                 __syncthreads();
-                // ---- H / G_d tiles of this warp's column tiles ----
-                for (int ct = warp; ct < ct_h; ct += nwarps) {
-                    double c[kHgfW][kHgfRtMax][2];
+                // ---- H / G_d tiles: unit = (coefficient set ww, column tile ct), all row tiles of the unit in one warp ----
+                for (int unit = warp; unit < nw * ct_h; unit += nwarps) {
+                    const int ww = unit / ct_h, ct = unit - ww * ct_h;
+                    double c[kHgfRtMax][2];
 #pragma unroll
-                    for (int ww = 0; ww < kHgfW; ++ww)
-#pragma unroll
-                        for (int rt = 0; rt < kHgfRtMax; ++rt) c[ww][rt][0] = c[ww][rt][1] = 0.0;
+                    for (int rt = 0; rt < kHgfRtMax; ++rt) c[rt][0] = c[rt][1] = 0.0;
                     const double* as = Ps + grp + tig * ldp;
-                    const double* bs = Bh + ct * 8 + grp + tig * lda;
+                    const double* bs = Bh + (ww * pl.qfp + tig) * lda + ct * 8 + grp;
                     for (int ks = 0; ks < ksteps; ++ks) {
-                        double af[kHgfRtMax], bf[kHgfW];
+                        const double bf = bs[4 * ks * lda];
 #pragma unroll
-                        for (int rt = 0; rt < kHgfRtMax; ++rt) af[rt] = rt < rt_h ? as[4 * ks * ldp + rt * 8] : 0.0;
-#pragma unroll
-                        for (int ww = 0; ww < kHgfW; ++ww) bf[ww] = ww < nw ? bs[(ww * pl.qfp + 4 * ks) * lda] : 0.0;
-#pragma unroll
-                        for (int ww = 0; ww < kHgfW; ++ww)
-#pragma unroll
-                            for (int rt = 0; rt < kHgfRtMax; ++rt)
-                                if (ww < nw && rt < rt_h) dmma_8x8x4(c[ww][rt][0], c[ww][rt][1], af[rt], bf[ww]);
+                        for (int rt = 0; rt < kHgfRtMax; ++rt)
+                            if (rt < rt_h) dmma_8x8x4(c[rt][0], c[rt][1], as[4 * ks * ldp + rt * 8], bf);
                     }
                     const int j = ct * 8 + 2 * tig;
+                    const int w = w0 + ww;
+                    double* dst = (w == 0 ? out.H : out.G[w - 1]) + static_cast<size_t>(e) * nfl * npe;
 #pragma unroll
-                    for (int ww = 0; ww < kHgfW; ++ww) {
-                        if (ww >= nw) continue;
-                        const int w = w0 + ww;
-                        double* dst = (w == 0 ? out.H : out.G[w - 1]) + static_cast<size_t>(e) * nfl * npe;
-#pragma unroll
-                        for (int rt = 0; rt < kHgfRtMax; ++rt) {
-                            const int b = rt * 8 + grp;
-                            if (rt >= rt_h || b >= pf) continue;
-                            const size_t row = lf * mpf + m * pf + b;
-                            if (j < pe) dst[static_cast<size_t>(mp * pe + j) * nfl + row] = c[ww][rt][0];
-                            if (j + 1 < pe) dst[static_cast<size_t>(mp * pe + j + 1) * nfl + row] = c[ww][rt][1];
-                        }
+                    for (int rt = 0; rt < kHgfRtMax; ++rt) {
+                        const int b = rt * 8 + grp;
+                        if (rt >= rt_h || b >= pf) continue;
+                        const size_t row = lf * mpf + m * pf + b;
+                        if (j < pe) dst[static_cast<size_t>(mp * pe + j) * nfl + row] = c[rt][0];
+                        if (j + 1 < pe) dst[static_cast<size_t>(mp * pe + j + 1) * nfl + row] = c[rt][1];
                     }
                 }
                 // ---- F tiles of this warp's row tiles (rows i, columns bp) ----
                 if (w0 == 0) {
-                    for (int rti = warp; rti < ct_h; rti += nwarps) {
+                    for (int rti = (warp + nwarps - (nw * ct_h) % nwarps) % nwarps; rti < ct_h; rti += nwarps) {
                         double c[kHgfRtMax][2];
 #pragma unroll
                         for (int cb = 0; cb < kHgfRtMax; ++cb) c[cb][0] = c[cb][1] = 0.0;
@@ -1104,6 +1099,20 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
         size_t ed_bytes = 2 * ed_plan(dv.pe, M, D, NTD / 32).doubles(D) * sizeof(double) + 16;
         ed_bytes = std::max(ed_bytes, hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D) * sizeof(double) + 16);
         const bool ed = want_jac && tuning().use_dmma && ed_dmma_ok(dv.pe, M, D) && hgf_dmma_ok(dv.pf) && all + ed_bytes <= cap;
+        // 16-warp variant (one CTA per SM): all 1 + D matrices of a scalar system in ONE point sweep
+        if constexpr (M == 1) {
+            if (ed && tuning().local_nt == 512) {
+                const EdPlan p16 = ed_plan(dv.pe, M, D, 16);
+                const size_t eb = std::max(2 * p16.doubles(D), hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D)) * sizeof(double) + 16;
+                if (p16.wsub <= 4 && all + eb <= cap) {
+                    auto kern_w = local_assemble_kernel<Model, 512, true, false>;
+                    ensure_dynamic_smem(kern_w, cap);
+                    kern_w<<<dv.ne, 512, all + eb, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2 | (tuning().local_debug_skip << 4), nullptr, 0);
+                    HDGB_LAUNCH_CHECK(ctx);
+                    return;
+                }
+            }
+        }
         if (ed) kern_d<<<dv.ne, NTD, all + ed_bytes, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2 | (tuning().local_debug_skip << 4), nullptr, 0);
         else kern<<<dv.ne, 256, all, ctx->stream>>>(dv, mv, in, out, want_jac ? 1 : 0, 0, dv.qe, 0, nfp, 1, 0, nullptr, 0);
         HDGB_LAUNCH_CHECK(ctx);
@@ -1112,8 +1121,19 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
     // wide systems with the Jacobian on the tensor-core path: records in a global (L2) scratch, one launch
     if constexpr (M > 1) {
         if (want_jac && tuning().use_dmma && tuning().local_global_records && ed_dmma_ok(dv.pe, M, D) && hgf_dmma_ok(dv.pf)) {
-            const size_t edb = std::max(2 * ed_plan(dv.pe, M, D, 8).doubles(D), hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D)) * sizeof(double) + 32;
             const size_t rec_stride = (dv.qe * svr + nfp * sfr + 15) & ~static_cast<size_t>(15);
+            // 16 warps: two component pairs share one point sweep (and one weighted-basis operand)
+            const EdPlan p16 = ed_plan(dv.pe, M, D, 16);
+            const size_t edb16 = std::max(2 * p16.doubles(D), hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D)) * sizeof(double) + 32;
+            if (tuning().local_nt == 512 && p16.wsub <= 8 && fixed + edb16 <= cap) {
+                auto kern_gw = local_assemble_kernel<Model, 512, true, true>;
+                ensure_dynamic_smem(kern_gw, cap);
+                DevBuf<char> scratch(rec_stride * static_cast<size_t>(dv.ne));
+                kern_gw<<<dv.ne, 512, fixed + edb16, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2, scratch.p, rec_stride);
+                HDGB_LAUNCH_CHECK(ctx);
+                return;
+            }
+            const size_t edb = std::max(2 * ed_plan(dv.pe, M, D, 8).doubles(D), hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D)) * sizeof(double) + 32;
             if (fixed + edb <= cap) {
                 auto kern_g = local_assemble_kernel<Model, 256, true, true>;
                 ensure_dynamic_smem(kern_g, cap);

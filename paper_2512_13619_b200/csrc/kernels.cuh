@@ -43,6 +43,9 @@ struct Tuning {
     int fused_cgs = 0;                   // round-1 register-resident fused CGS2 pass (measured slower: 112 us vs 85 us at cfg2)
     int cgs_stream = 1;                  // CGS2 as three TMA-streamed passes over the basis (k_orth.cu) instead of four
     int local_debug_skip = 0;            // measurement aid: skip phases of the local kernel (1 = E/D_d, 2 = H/G_d/F); results invalid
+    int local_nt = 256;                  // threads of the tensor-core local kernel: 256 = two 8-warp CTAs per SM (default); 512 = one 16-warp CTA, all
+                                         // 1 + D matrices (scalar) / two component pairs (wide) per point sweep -- measured slower at config 2
+                                         // (35.6 vs 33.2 ms per assembly) and equal at config 5 (0.250 vs 0.252 s at hex 16^3)
     int local_dmma_min_pe = 20;          // local blocks on the tensor-core path from this many basis functions per element
     int local_global_records = 1;        // wide systems: point records in an L2-resident scratch, one launch, E / D_d on DMMA
     int local_dmma_chunked = 0;          // E / D_d on the tensor-core path also in point-chunked sweeps (wide systems)

@@ -114,3 +114,33 @@ def test_wide_system_records_in_l2_scratch(ctx):
             hdg.set_tuning("local_global_records", 1)
     for nm in out[0]:
         assert rel(out[1][nm], out[0][nm]) <= (1e-9 if nm in ("kbar", "rbar") else 1e-12), nm
+
+
+@pytest.mark.parametrize("shape,n,k,M,case", [("hex", 3, 3, 1, "poisson"), ("quad", 4, 4, 1, "burgers"), ("hex", 2, 3, 3, "elasticity"),
+                                              ("hex", 2, 2, 5, "navier_stokes")])
+def test_sixteen_warp_local_kernel_matches_eight_warp(ctx, shape, n, k, M, case):
+    """`local_nt = 512`: one 16-warp CTA per SM, all 1 + D matrices of a scalar system (two component pairs of a wide
+    one) per point sweep, two half-warps per quadrature point in the operand builder.  Same products in the same
+    order as the default 8-warp kernel: identical raw blocks."""
+    disc = hdg.Discretization.structured(ctx, shape, n=n, degree=k, n_comp=M)
+    kw = {"mu": 0.02} if case == "navier_stokes" else {}
+    model = hdg.make_case_model(disc, case, **kw)
+    state = hdg.make_initial_state(disc, model)
+    rng = np.random.default_rng(5)
+    state.u = state.u + 0.05 * rng.standard_normal(state.u.shape)
+    state.uhat = state.uhat + 0.05 * rng.standard_normal(state.uhat.shape)
+    tkw = dict(dt=0.05, u_prev=state.u) if case == "navier_stokes" else {}
+    out = {}
+    for nt in (256, 512):
+        hdg.set_tuning("local_nt", nt)
+        try:
+            ops = hdg.assemble_element_operators(disc, model, state, keep_raw=True, **tkw)
+            names = ["e_raw", "f_raw", "h_raw", "j_raw"] + [f"d_raw{d}" for d in range(disc.dim)] + [f"g_raw{d}" for d in range(disc.dim)]
+            out[nt] = {nm: ops.get(nm) for nm in names + ["kbar", "ru"]}
+        finally:
+            hdg.set_tuning("local_nt", 256)
+    for nm in out[256]:
+        if nm == "ru":   # the residual sweep is split over nt / pe thread groups: another (fixed) summation partition
+            assert rel(out[512][nm], out[256][nm]) <= 1e-13, nm
+        else:
+            assert np.array_equal(out[512][nm], out[256][nm]), nm
