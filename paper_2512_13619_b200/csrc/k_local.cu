@@ -494,16 +494,18 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
 //   [H | G_0 .. G_{D-1}](lf b, j) = sum_gc psi_b(gc) * (c_w(gc) w_gc phis_j(gc)),  c_0 = dv_u, c_{1+dp} = dv_q[dp]
 //   F(i, lf bp)                   = sum_gc phis_i(gc) * (w_gc dfh_uh(gc) psi_bp(gc))
 // (local_ops.cpp:186-219).  psi^T and phis are the left operands, the coefficient-scaled tables the right ones.
-constexpr int kHgfW = 2;     // coefficient sets (H, G_d) resident at a time
 constexpr int kHgfRtMax = 4;  // 8-row tiles covering pf (pf <= 32)
 inline bool hgf_dmma_ok(int pf) { return pf <= 8 * kHgfRtMax; }
-// All four operands are stored k-major ([face point gc][row or column], leading dimensions = 4 mod 16): conflict-free
-// stores by consecutive lanes and conflict-free DMMA fragment loads, as in the E / D_d sweep.
+// The per-point coefficients ride on the SMALL operand: with cw_w(gc) = w_gc c_w(gc),
+//   [H | G_dp](lf b, j) = sum_gc (psi_b(gc) cw_w(gc)) * phis_j(gc),     F(i, lf bp) = sum_gc phis_i(gc) * (cf(gc) psi_bp(gc)),
+// so the trace table phis of the face (qf x pe, staged once per face) is the right operand of ALL 1 + D
+// coefficient sets and the left operand of F as it stands; per component pair only (1 + D + 1) qf x pf slabs are
+// built.  Operands are k-major ([face point][row or column], leading dimensions = 4 mod 16): conflict-free
+// stores and DMMA fragment loads, as in the E / D_d sweep.
 struct HgfPlan {
     int pfp, qfp, ldp, lda, pep;
     __host__ __device__ size_t doubles(int D) const {
-        return static_cast<size_t>(qfp) * ldp + static_cast<size_t>(qfp) * lda + static_cast<size_t>(kHgfW) * qfp * lda +
-               static_cast<size_t>(qfp) * ldp;
+        return static_cast<size_t>(qfp) * ldp * (2 + D + 1) + static_cast<size_t>(qfp) * lda;
     }
 };
 inline __host__ __device__ HgfPlan hgf_plan(int pe, int pf, int qf) {
@@ -522,18 +524,19 @@ __device__ void hgf_dmma(const DiscView& dv, const LocalOut& out, int e, const F
     // Multi-component systems: one pass per component pair (m, mp) with the pair's coefficients
     // dv_u[m M + mp], dv_q[(m M + mp) D + dp], dfh_uh[m M + mp]; rows / columns of the pair inside the blocks:
     // H, G (nfl x npe): row lf mpf + m pf + b, column mp pe + j;  F (npe x nfl): row m pe + i, column lf mpf + mp pf + bp.
-    // Tile ownership: warp <-> 8-column tile of j for H / G_d (all coefficient sets and row tiles of that column
-    // tile: psi^T fragments are shared) and <-> 8-row tile of i for F (all column tiles of bp).
+    // Tile ownership: unit = (coefficient set w, 8-column tile of j) for H / G_d -- all row tiles of the unit in one
+    // warp, sharing the phis fragments -- and 8-row tile of i for F (all column tiles of bp).
     const int pe = dv.pe, pf = dv.pf, qf = dv.qf, n_lfe = dv.n_lfe;
     const int mpf = M * pf, nfl = n_lfe * mpf, npe = M * pe;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
     const int grp = lane >> 2, tig = lane & 3;
     const HgfPlan pl = hgf_plan(pe, pf, qf);
     const int ldp = pl.ldp, lda = pl.lda;
-    double* Ps = buf;                       // psi^T:                 [gc][b]
-    double* Fs = Ps + pl.qfp * ldp;         // phis:                  [gc][i]
-    double* Bh = Fs + pl.qfp * lda;         // c_w w phis:        [ww][gc][j]
-    double* Bf = Bh + kHgfW * pl.qfp * lda; // w dfh_uh psi:          [gc][bp]
+    const int slab = pl.qfp * ldp;
+    double* Ps = buf;                 // psi^T:                    [gc][b]
+    double* Aw = Ps + slab;           // cw_w psi^T, w = 0 .. D:   [w][gc][b]
+    double* Bf = Aw + (1 + D) * slab; // cf psi:                   [gc][bp]
+    double* Fs = Bf + slab;           // phis:                     [gc][i]
     __syncthreads();
     for (int t = tid; t < static_cast<int>(pl.doubles(D)); t += nt) buf[t] = 0.0;
     __syncthreads();
@@ -543,7 +546,8 @@ __device__ void hgf_dmma(const DiscView& dv, const LocalOut& out, int e, const F
     }
     const int rt_h = pl.pfp / 8, ct_h = pl.pep / 8;  // 8-row tiles over b / bp, 8-column tiles over j (= row tiles over i)
     const int ksteps = pl.qfp / 4;
-    const int hw = tid >> 4, l16 = tid & 15, nhw = nt >> 4;  // builder mapping: half-warp <-> face point, lanes <-> j
+    const int hw = tid >> 4, l16 = tid & 15, nhw = nt >> 4;  // staging: half-warp <-> face point, lanes <-> basis function
+    const int nunit = (1 + D) * ct_h;
     for (int lf = 0; lf < n_lfe; ++lf) {
         const double* tp = dv.tphi + (static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf * pe;
         const FaceRec<M, D>* fr = frec + lf * qf;
@@ -552,81 +556,65 @@ __device__ void hgf_dmma(const DiscView& dv, const LocalOut& out, int e, const F
             for (int j = l16; j < pe; j += 16) Fs[gc * lda + j] = __ldg(tp + static_cast<size_t>(gc) * pe + j);
         for (int pr = 0; pr < M * M; ++pr) {
             const int mp = pr / M, m = pr - mp * M, mm = m * M + mp;
-            for (int w0 = 0; w0 < 1 + D; w0 += kHgfW) {  // coefficient sets [w0, w0 + nw): 0 = dv_u (H), 1 + dp = dv_q[dp] (G_dp)
-                const int nw = min(kHgfW, 1 + D - w0);
-                __syncthreads();  // Fs staged / previous tiles done with Bh, Bf
-                for (int gc = hw; gc < qf; gc += nhw) {
-                    const FaceRec<M, D>& r = fr[gc];
-                    const double wg = rec_ld<GREC>(&r.w);
-                    double cw[kHgfW];
+            if (pr > 0) __syncthreads();  // the previous pair's tiles are done with Aw, Bf
+            // the pair's slabs: (1 + D) coefficient sets for H / G_d, one for F
+            for (int t = tid; t < qf * pf; t += nt) {
+                const int gc = t / pf, b = t - gc * pf;
+                const FaceRec<M, D>& r = fr[gc];
+                const double wp = rec_ld<GREC>(&r.w) * Ps[gc * ldp + b];
+                Aw[gc * ldp + b] = wp * rec_ld<GREC>(&r.dv_u[mm]);
 #pragma unroll
-                    for (int ww = 0; ww < kHgfW; ++ww) {
-                        const int w = w0 + ww;
-                        cw[ww] = ww < nw ? wg * rec_ld<GREC>(w == 0 ? &r.dv_u[mm] : &r.dv_q[mm * D + w - 1]) : 0.0;
-                    }
-                    for (int j = l16; j < pe; j += 16) {
-                        const double ph = Fs[gc * lda + j];
+                for (int dq = 0; dq < D; ++dq) Aw[(1 + dq) * slab + gc * ldp + b] = wp * rec_ld<GREC>(&r.dv_q[mm * D + dq]);
+                Bf[gc * ldp + b] = wp * rec_ld<GREC>(&r.dfh_uh[mm]);
+            }
+            __syncthreads();  // slabs (and, for the first pair, Fs) are staged
+            // ---- H / G_d ----
+            for (int unit = warp; unit < nunit; unit += nwarps) {
+                const int w = unit / ct_h, ct = unit - w * ct_h;
+                double c[kHgfRtMax][2];
 #pragma unroll
-                        for (int ww = 0; ww < kHgfW; ++ww)
-                            if (ww < nw) Bh[(ww * pl.qfp + gc) * lda + j] = cw[ww] * ph;
-                    }
-                    if (w0 == 0) {
-                        const double cf = wg * rec_ld<GREC>(&r.dfh_uh[mm]);
-                        for (int bp = l16; bp < pf; bp += 16) Bf[gc * ldp + bp] = cf * Ps[gc * ldp + bp];
-                    }
+                for (int rt = 0; rt < kHgfRtMax; ++rt) c[rt][0] = c[rt][1] = 0.0;
+                const double* as = Aw + w * slab + grp + tig * ldp;
+                const double* bs = Fs + tig * lda + ct * 8 + grp;
+                for (int ks = 0; ks < ksteps; ++ks) {
+                    const double bf = bs[4 * ks * lda];
+#pragma unroll
+                    for (int rt = 0; rt < kHgfRtMax; ++rt)
+                        if (rt < rt_h) dmma_8x8x4(c[rt][0], c[rt][1], as[4 * ks * ldp + rt * 8], bf);
                 }
-                __syncthreads();
-                // ---- H / G_d tiles: unit = (coefficient set ww, column tile ct), all row tiles of the unit in one warp ----
-                for (int unit = warp; unit < nw * ct_h; unit += nwarps) {
-                    const int ww = unit / ct_h, ct = unit - ww * ct_h;
-                    double c[kHgfRtMax][2];
+                const int j = ct * 8 + 2 * tig;
+                double* dst = (w == 0 ? out.H : out.G[w - 1]) + static_cast<size_t>(e) * nfl * npe;
 #pragma unroll
-                    for (int rt = 0; rt < kHgfRtMax; ++rt) c[rt][0] = c[rt][1] = 0.0;
-                    const double* as = Ps + grp + tig * ldp;
-                    const double* bs = Bh + (ww * pl.qfp + tig) * lda + ct * 8 + grp;
-                    for (int ks = 0; ks < ksteps; ++ks) {
-                        const double bf = bs[4 * ks * lda];
-#pragma unroll
-                        for (int rt = 0; rt < kHgfRtMax; ++rt)
-                            if (rt < rt_h) dmma_8x8x4(c[rt][0], c[rt][1], as[4 * ks * ldp + rt * 8], bf);
-                    }
-                    const int j = ct * 8 + 2 * tig;
-                    const int w = w0 + ww;
-                    double* dst = (w == 0 ? out.H : out.G[w - 1]) + static_cast<size_t>(e) * nfl * npe;
-#pragma unroll
-                    for (int rt = 0; rt < kHgfRtMax; ++rt) {
-                        const int b = rt * 8 + grp;
-                        if (rt >= rt_h || b >= pf) continue;
-                        const size_t row = lf * mpf + m * pf + b;
-                        if (j < pe) dst[static_cast<size_t>(mp * pe + j) * nfl + row] = c[rt][0];
-                        if (j + 1 < pe) dst[static_cast<size_t>(mp * pe + j + 1) * nfl + row] = c[rt][1];
-                    }
+                for (int rt = 0; rt < kHgfRtMax; ++rt) {
+                    const int b = rt * 8 + grp;
+                    if (rt >= rt_h || b >= pf) continue;
+                    const size_t row = lf * mpf + m * pf + b;
+                    if (j < pe) dst[static_cast<size_t>(mp * pe + j) * nfl + row] = c[rt][0];
+                    if (j + 1 < pe) dst[static_cast<size_t>(mp * pe + j + 1) * nfl + row] = c[rt][1];
                 }
-                // ---- F tiles of this warp's row tiles (rows i, columns bp) ----
-                if (w0 == 0) {
-                    for (int rti = (warp + nwarps - (nw * ct_h) % nwarps) % nwarps; rti < ct_h; rti += nwarps) {
-                        double c[kHgfRtMax][2];
+            }
+            // ---- F (rows i, columns bp): the warps the H / G_d units leave idle go first ----
+            for (int rti = (warp + nwarps - nunit % nwarps) % nwarps; rti < ct_h; rti += nwarps) {
+                double c[kHgfRtMax][2];
 #pragma unroll
-                        for (int cb = 0; cb < kHgfRtMax; ++cb) c[cb][0] = c[cb][1] = 0.0;
-                        const double* as = Fs + rti * 8 + grp + tig * lda;
-                        const double* bs = Bf + grp + tig * ldp;
-                        for (int ks = 0; ks < ksteps; ++ks) {
-                            const double af = as[4 * ks * lda];
+                for (int cb = 0; cb < kHgfRtMax; ++cb) c[cb][0] = c[cb][1] = 0.0;
+                const double* as = Fs + rti * 8 + grp + tig * lda;
+                const double* bs = Bf + grp + tig * ldp;
+                for (int ks = 0; ks < ksteps; ++ks) {
+                    const double af = as[4 * ks * lda];
 #pragma unroll
-                            for (int cb = 0; cb < kHgfRtMax; ++cb)
-                                if (cb < rt_h) dmma_8x8x4(c[cb][0], c[cb][1], af, bs[4 * ks * ldp + cb * 8]);
-                        }
-                        const int i = rti * 8 + grp;
-                        double* dst = out.F + static_cast<size_t>(e) * npe * nfl;
-                        const size_t row = m * pe + i;
+                    for (int cb = 0; cb < kHgfRtMax; ++cb)
+                        if (cb < rt_h) dmma_8x8x4(c[cb][0], c[cb][1], af, bs[4 * ks * ldp + cb * 8]);
+                }
+                const int i = rti * 8 + grp;
+                double* dst = out.F + static_cast<size_t>(e) * npe * nfl;
+                const size_t row = m * pe + i;
 #pragma unroll
-                        for (int cb = 0; cb < kHgfRtMax; ++cb) {
-                            const int bp = cb * 8 + 2 * tig;
-                            if (cb >= rt_h || i >= pe) continue;
-                            if (bp < pf) dst[static_cast<size_t>(lf * mpf + mp * pf + bp) * npe + row] = c[cb][0];
-                            if (bp + 1 < pf) dst[static_cast<size_t>(lf * mpf + mp * pf + bp + 1) * npe + row] = c[cb][1];
-                        }
-                    }
+                for (int cb = 0; cb < kHgfRtMax; ++cb) {
+                    const int bp = cb * 8 + 2 * tig;
+                    if (cb >= rt_h || i >= pe) continue;
+                    if (bp < pf) dst[static_cast<size_t>(lf * mpf + mp * pf + bp) * npe + row] = c[cb][0];
+                    if (bp + 1 < pf) dst[static_cast<size_t>(lf * mpf + mp * pf + bp + 1) * npe + row] = c[cb][1];
                 }
             }
         }
