@@ -20,58 +20,150 @@ namespace {
 // ---- setup kernels ---------------------------------------------------------------------------------
 // mass(i,j) = sum_g (phi_i phi_j)(g) * (w_g detJ_g)        (local_ops.cpp:266-281)
 // bmat_d(i,j) = sum_g (w detJ phi_j)(g) * grad_d phi_i(g)   (local_ops.cpp:288-307)
-__global__ void mass_bmat_kernel(DiscView dv, double* __restrict__ mass, double* __restrict__ b0,
-                                 double* __restrict__ b1, double* __restrict__ b2) {
+// One CTA per element; the per-point weights and inverse Jacobians are staged once in shared memory and a
+// thread owns a 2 x 4 tile of (i, j) pairs, so every table value loaded serves 4 (resp. 2) entries.  The terms of
+// an entry are formed and summed exactly as in the scalar version (points ascending).
+constexpr int kMbTi = 2, kMbTj = 4;
+template <int D>
+__global__ void __launch_bounds__(256) mass_bmat_kernel(DiscView dv, double* __restrict__ mass, double* __restrict__ b0,
+                                                        double* __restrict__ b1, double* __restrict__ b2) {
+    extern __shared__ double sm_setup[];
     const int e = blockIdx.x;
-    const int pe = dv.pe, qe = dv.qe, D = dv.D;
-    for (int t = threadIdx.x; t < pe * pe; t += blockDim.x) {
-        const int j = t / pe, i = t - j * pe;
-        double am = 0.0, ab[3] = {0.0, 0.0, 0.0};
-        for (int g = 0; g < qe; ++g) {
-            const size_t gi = static_cast<size_t>(e) * qe + g;
-            const double w = dv.wq[g] * dv.elem_detjac[gi];
-            const double pi = dv.phi[i + pe * g], pj = dv.phi[j + pe * g];
-            am += (pi * pj) * w;
-            const double wpj = w * pj;
-            const double* ij = dv.elem_invjac + gi * D * D;
-            for (int d = 0; d < D; ++d) {
-                double gd = 0.0;
-                for (int r = 0; r < D; ++r) gd += dv.dphi[r][i + pe * g] * ij[r * D + d];
-                ab[d] += wpj * gd;
+    const int pe = dv.pe, qe = dv.qe;
+    double* sw = sm_setup;       // qe
+    double* sj = sw + qe;        // qe * D * D
+    for (int g = threadIdx.x; g < qe; g += blockDim.x) sw[g] = dv.wq[g] * dv.elem_detjac[static_cast<size_t>(e) * qe + g];
+    for (int t = threadIdx.x; t < qe * D * D; t += blockDim.x) sj[t] = dv.elem_invjac[static_cast<size_t>(e) * qe * D * D + t];
+    __syncthreads();
+    const int nti = (pe + kMbTi - 1) / kMbTi, ntj = (pe + kMbTj - 1) / kMbTj;
+    for (int t = threadIdx.x; t < nti * ntj; t += blockDim.x) {
+        const int tj = t / nti, ti = t - tj * nti;
+        int ii[kMbTi], jj[kMbTj];
+#pragma unroll
+        for (int a = 0; a < kMbTi; ++a) ii[a] = min(ti * kMbTi + a, pe - 1);
+#pragma unroll
+        for (int c = 0; c < kMbTj; ++c) jj[c] = min(tj * kMbTj + c, pe - 1);
+        double am[kMbTi][kMbTj], ab[kMbTi][kMbTj][D];
+#pragma unroll
+        for (int a = 0; a < kMbTi; ++a)
+#pragma unroll
+            for (int c = 0; c < kMbTj; ++c) {
+                am[a][c] = 0.0;
+#pragma unroll
+                for (int d = 0; d < D; ++d) ab[a][c][d] = 0.0;
             }
+        for (int g = 0; g < qe; ++g) {
+            const double w = sw[g];
+            const double* ij = sj + g * D * D;
+            double pi[kMbTi], gd[kMbTi][D], pj[kMbTj];
+#pragma unroll
+            for (int a = 0; a < kMbTi; ++a) {
+                pi[a] = __ldg(dv.phi + ii[a] + pe * g);
+                double dp[D];
+#pragma unroll
+                for (int r = 0; r < D; ++r) dp[r] = __ldg(dv.dphi[r] + ii[a] + pe * g);
+#pragma unroll
+                for (int d = 0; d < D; ++d) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int r = 0; r < D; ++r) s += dp[r] * ij[r * D + d];
+                    gd[a][d] = s;
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < kMbTj; ++c) pj[c] = __ldg(dv.phi + jj[c] + pe * g);
+#pragma unroll
+            for (int a = 0; a < kMbTi; ++a)
+#pragma unroll
+                for (int c = 0; c < kMbTj; ++c) {
+                    am[a][c] += (pi[a] * pj[c]) * w;
+                    const double wpj = w * pj[c];
+#pragma unroll
+                    for (int d = 0; d < D; ++d) ab[a][c][d] += wpj * gd[a][d];
+                }
         }
-        const size_t o = static_cast<size_t>(e) * pe * pe + t;
-        mass[o] = am;
-        b0[o] = ab[0];
-        b1[o] = ab[1];
-        if (D == 3) b2[o] = ab[2];
+#pragma unroll
+        for (int a = 0; a < kMbTi; ++a)
+#pragma unroll
+            for (int c = 0; c < kMbTj; ++c) {
+                const int i = ti * kMbTi + a, j = tj * kMbTj + c;
+                if (i >= pe || j >= pe) continue;
+                const size_t o = static_cast<size_t>(e) * pe * pe + static_cast<size_t>(j) * pe + i;
+                mass[o] = am[a][c];
+                b0[o] = ab[a][c][0];
+                b1[o] = ab[a][c][1];
+                if (D == 3) b2[o] = ab[a][c][D - 1];
+            }
     }
 }
 
 // cmat_d(i, (lf,b)) = - sum_gc (w psi_b)(gc) * phis_i(gc) * n_d   (local_ops.cpp:310-336)
-__global__ void cmat_kernel(DiscView dv, double* __restrict__ c0, double* __restrict__ c1, double* __restrict__ c2) {
+// Same scheme: per-face weights and normals staged in shared memory, a thread owns 2 (i) x 4 (b) entries of one
+// local face.
+template <int D>
+__global__ void __launch_bounds__(256) cmat_kernel(DiscView dv, double* __restrict__ c0, double* __restrict__ c1, double* __restrict__ c2) {
+    extern __shared__ double sm_setup[];
     const int e = blockIdx.x;
-    const int pe = dv.pe, pf = dv.pf, qf = dv.qf, D = dv.D, nfs = dv.nfs;
-    for (int t = threadIdx.x; t < pe * nfs; t += blockDim.x) {
-        const int l = t / pe, i = t - l * pe;
-        const int lf = l / pf, b = l - lf * pf;
-        const int f = dv.elem_faces[e * dv.n_lfe + lf];
-        const int side = dv.elem_side[e * dv.n_lfe + lf];
-        const int o = dv.face_orient[2 * f + side];
-        const double* tp = dv.tphi + (static_cast<size_t>(lf) * dv.n_orient + o) * qf * pe;
-        double acc[3] = {0.0, 0.0, 0.0};
+    const int pe = dv.pe, pf = dv.pf, qf = dv.qf, nfs = dv.nfs, n_lfe = dv.n_lfe;
+    double* sw = sm_setup;              // n_lfe * qf
+    double* sn = sw + n_lfe * qf;       // n_lfe * qf * D
+    __shared__ int s_orient[8];
+    if (threadIdx.x < n_lfe) {
+        const int f = dv.elem_faces[e * n_lfe + threadIdx.x];
+        s_orient[threadIdx.x] = dv.face_orient[2 * f + dv.elem_side[e * n_lfe + threadIdx.x]];
+    }
+    for (int t = threadIdx.x; t < n_lfe * qf; t += blockDim.x) {
+        const int lf = t / qf, gc = t - lf * qf;
+        const int f = dv.elem_faces[e * n_lfe + lf], side = dv.elem_side[e * n_lfe + lf];
+        sw[t] = dv.wf[gc] * dv.face_detjac[static_cast<size_t>(f) * qf + gc];
+        const double* n = dv.face_normal + ((static_cast<size_t>(f) * 2 + side) * qf + gc) * D;
+#pragma unroll
+        for (int d = 0; d < D; ++d) sn[t * D + d] = n[d];
+    }
+    __syncthreads();
+    const int nti = (pe + kMbTi - 1) / kMbTi, ntb = (pf + kMbTj - 1) / kMbTj;
+    for (int t = threadIdx.x; t < n_lfe * ntb * nti; t += blockDim.x) {
+        const int lf = t / (ntb * nti), r2 = t - lf * (ntb * nti);
+        const int tb = r2 / nti, ti = r2 - tb * nti;
+        int ii[kMbTi], bb[kMbTj];
+#pragma unroll
+        for (int a = 0; a < kMbTi; ++a) ii[a] = min(ti * kMbTi + a, pe - 1);
+#pragma unroll
+        for (int c = 0; c < kMbTj; ++c) bb[c] = min(tb * kMbTj + c, pf - 1);
+        const double* tp = dv.tphi + (static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf * pe;
+        double acc[kMbTi][kMbTj][D];
+#pragma unroll
+        for (int a = 0; a < kMbTi; ++a)
+#pragma unroll
+            for (int c = 0; c < kMbTj; ++c)
+#pragma unroll
+                for (int d = 0; d < D; ++d) acc[a][c][d] = 0.0;
         for (int gc = 0; gc < qf; ++gc) {
-            const size_t fi = static_cast<size_t>(f) * qf + gc;
-            const double w = dv.wf[gc] * dv.face_detjac[fi];
-            const double* n = dv.face_normal + ((static_cast<size_t>(f) * 2 + side) * qf + gc) * D;
-            const double pb = w * dv.psi[b + pf * gc];
-            const double ph = tp[static_cast<size_t>(gc) * pe + i];
-            for (int d = 0; d < D; ++d) acc[d] -= pb * ph * n[d];
+            const double w = sw[lf * qf + gc];
+            const double* n = sn + (lf * qf + gc) * D;
+            double ph[kMbTi], pb[kMbTj];
+#pragma unroll
+            for (int a = 0; a < kMbTi; ++a) ph[a] = __ldg(tp + static_cast<size_t>(gc) * pe + ii[a]);
+#pragma unroll
+            for (int c = 0; c < kMbTj; ++c) pb[c] = w * __ldg(dv.psi + bb[c] + pf * gc);
+#pragma unroll
+            for (int a = 0; a < kMbTi; ++a)
+#pragma unroll
+                for (int c = 0; c < kMbTj; ++c)
+#pragma unroll
+                    for (int d = 0; d < D; ++d) acc[a][c][d] -= pb[c] * ph[a] * n[d];
         }
-        const size_t off = static_cast<size_t>(e) * pe * nfs + t;
-        c0[off] = acc[0];
-        c1[off] = acc[1];
-        if (D == 3) c2[off] = acc[2];
+#pragma unroll
+        for (int a = 0; a < kMbTi; ++a)
+#pragma unroll
+            for (int c = 0; c < kMbTj; ++c) {
+                const int i = ti * kMbTi + a, b = tb * kMbTj + c;
+                if (i >= pe || b >= pf) continue;
+                const size_t off = static_cast<size_t>(e) * pe * nfs + static_cast<size_t>(lf * pf + b) * pe + i;
+                c0[off] = acc[a][c][0];
+                c1[off] = acc[a][c][1];
+                if (D == 3) c2[off] = acc[a][c][D - 1];
+            }
     }
 }
 
@@ -1173,9 +1265,19 @@ void launch_local_assemble_part2(hdgb_ctx* ctx, const DiscView& dv, const ModelV
 
 #if HDGB_LOCAL_PART == 0
 void launch_local_factors(hdgb_ctx* ctx, const DiscView& dv, double* mass, double* const bmat[3], double* const cmat[3]) {
-    mass_bmat_kernel<<<dv.ne, 128, 0, ctx->stream>>>(dv, mass, bmat[0], bmat[1], bmat[2]);
-    HDGB_LAUNCH_CHECK(ctx);
-    cmat_kernel<<<dv.ne, 128, 0, ctx->stream>>>(dv, cmat[0], cmat[1], cmat[2]);
+    const size_t sm_m = static_cast<size_t>(dv.qe) * (1 + dv.D * dv.D) * sizeof(double);
+    const size_t sm_c = static_cast<size_t>(dv.n_lfe) * dv.qf * (1 + dv.D) * sizeof(double);
+    if (dv.D == 2) {
+        ensure_dynamic_smem(mass_bmat_kernel<2>, sm_m);
+        mass_bmat_kernel<2><<<dv.ne, 256, sm_m, ctx->stream>>>(dv, mass, bmat[0], bmat[1], bmat[2]);
+        HDGB_LAUNCH_CHECK(ctx);
+        cmat_kernel<2><<<dv.ne, 256, sm_c, ctx->stream>>>(dv, cmat[0], cmat[1], cmat[2]);
+    } else {
+        ensure_dynamic_smem(mass_bmat_kernel<3>, sm_m);
+        mass_bmat_kernel<3><<<dv.ne, 256, sm_m, ctx->stream>>>(dv, mass, bmat[0], bmat[1], bmat[2]);
+        HDGB_LAUNCH_CHECK(ctx);
+        cmat_kernel<3><<<dv.ne, 256, sm_c, ctx->stream>>>(dv, cmat[0], cmat[1], cmat[2]);
+    }
     HDGB_LAUNCH_CHECK(ctx);
 }
 
