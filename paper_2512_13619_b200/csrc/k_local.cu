@@ -587,17 +587,18 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
 //   F(i, lf bp)                   = sum_gc phis_i(gc) * (w_gc dfh_uh(gc) psi_bp(gc))
 // (local_ops.cpp:186-219).  psi^T and phis are the left operands, the coefficient-scaled tables the right ones.
 constexpr int kHgfRtMax = 4;  // 8-row tiles covering pf (pf <= 32)
-inline bool hgf_dmma_ok(int pf) { return pf <= 8 * kHgfRtMax; }
-// The per-point coefficients ride on the SMALL operand: with cw_w(gc) = w_gc c_w(gc),
-//   [H | G_dp](lf b, j) = sum_gc (psi_b(gc) cw_w(gc)) * phis_j(gc),     F(i, lf bp) = sum_gc phis_i(gc) * (cf(gc) psi_bp(gc)),
-// so the trace table phis of the face (qf x pe, staged once per face) is the right operand of ALL 1 + D
-// coefficient sets and the left operand of F as it stands; per component pair only (1 + D + 1) qf x pf slabs are
-// built.  Operands are k-major ([face point][row or column], leading dimensions = 4 mod 16): conflict-free
-// stores and DMMA fragment loads, as in the E / D_d sweep.
+// The per-point coefficients are applied to the operand FRAGMENTS: with cw(gc) = w_gc c(gc),
+//   [H | G_dp](lf b, j) = sum_gc psi_b(gc) * (cw(gc) phis_j(gc)),     F(i, lf bp) = sum_gc phis_i(gc) * (cf(gc) psi_bp(gc)),
+// so per local face only the trace table phis (qf x pe) and a small table of coefficients -- M^2 (2 + D) values per
+// face point, ALL component pairs at once -- are staged; psi^T is staged once per element.  A warp owns an 8-column
+// tile of j (resp. an 8-row tile of i), keeps its phis fragments in registers and walks all (component pair,
+// coefficient set) units of the face scaling the fragment by cw on the fly: two barriers per face, none per pair.
+// Operands are k-major ([face point][row or column], leading dimensions = 4 mod 16): conflict-free DMMA fragment loads.
+constexpr int kHgfKsMax = 10;  // k-steps of 4 face points (qf <= 40)
 struct HgfPlan {
     int pfp, qfp, ldp, lda, pep;
-    __host__ __device__ size_t doubles(int D) const {
-        return static_cast<size_t>(qfp) * ldp * (2 + D + 1) + static_cast<size_t>(qfp) * lda;
+    __host__ __device__ size_t doubles(int D, int M) const {
+        return static_cast<size_t>(qfp) * ldp + static_cast<size_t>(qfp) * lda + static_cast<size_t>(M) * M * (2 + D) * qfp;
     }
 };
 inline __host__ __device__ HgfPlan hgf_plan(int pe, int pf, int qf) {
@@ -609,97 +610,108 @@ inline __host__ __device__ HgfPlan hgf_plan(int pe, int pf, int qf) {
     p.lda = (p.pep + 15) / 16 * 16 + 4;
     return p;
 }
+inline bool hgf_dmma_ok(int pf, int qf) { return pf <= 8 * kHgfRtMax && qf <= 4 * kHgfKsMax; }
 
 template <int M, int D, bool GREC>
 __device__ void hgf_dmma(const DiscView& dv, const LocalOut& out, int e, const FaceRec<M, D>* frec, const int* s_orient,
                          double* buf) {
-    // Multi-component systems: one pass per component pair (m, mp) with the pair's coefficients
-    // dv_u[m M + mp], dv_q[(m M + mp) D + dp], dfh_uh[m M + mp]; rows / columns of the pair inside the blocks:
-    // H, G (nfl x npe): row lf mpf + m pf + b, column mp pe + j;  F (npe x nfl): row m pe + i, column lf mpf + mp pf + bp.
-    // Tile ownership: unit = (coefficient set w, 8-column tile of j) for H / G_d -- all row tiles of the unit in one
-    // warp, sharing the phis fragments -- and 8-row tile of i for F (all column tiles of bp).
+    // Rows / columns of component pair (m, mp) inside the blocks: H, G (nfl x npe): row lf mpf + m pf + b, column
+    // mp pe + j;  F (npe x nfl): row m pe + i, column lf mpf + mp pf + bp.  Coefficient sets of a pair: 0 = dv_u (H),
+    // 1 + dp = dv_q[dp] (G_dp), 1 + D = dfh_uh (F).
+    constexpr int NC = 2 + D;
     const int pe = dv.pe, pf = dv.pf, qf = dv.qf, n_lfe = dv.n_lfe;
     const int mpf = M * pf, nfl = n_lfe * mpf, npe = M * pe;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
     const int grp = lane >> 2, tig = lane & 3;
     const HgfPlan pl = hgf_plan(pe, pf, qf);
-    const int ldp = pl.ldp, lda = pl.lda;
-    const int slab = pl.qfp * ldp;
-    double* Ps = buf;                 // psi^T:                    [gc][b]
-    double* Aw = Ps + slab;           // cw_w psi^T, w = 0 .. D:   [w][gc][b]
-    double* Bf = Aw + (1 + D) * slab; // cf psi:                   [gc][bp]
-    double* Fs = Bf + slab;           // phis:                     [gc][i]
+    const int ldp = pl.ldp, lda = pl.lda, qfp = pl.qfp;
+    double* Ps = buf;               // psi^T:         [gc][b]
+    double* Fs = Ps + qfp * ldp;    // phis:          [gc][i]
+    double* Cw = Fs + qfp * lda;    // coefficients:  [pair][set][gc]
     __syncthreads();
-    for (int t = tid; t < static_cast<int>(pl.doubles(D)); t += nt) buf[t] = 0.0;
+    for (int t = tid; t < static_cast<int>(pl.doubles(D, M)); t += nt) buf[t] = 0.0;
     __syncthreads();
     for (int t = tid; t < qf * pf; t += nt) {
         const int gc = t / pf, b = t - gc * pf;
         Ps[gc * ldp + b] = __ldg(dv.psi + b + pf * gc);
     }
     const int rt_h = pl.pfp / 8, ct_h = pl.pep / 8;  // 8-row tiles over b / bp, 8-column tiles over j (= row tiles over i)
-    const int ksteps = pl.qfp / 4;
+    const int ksteps = qfp / 4;
     const int hw = tid >> 4, l16 = tid & 15, nhw = nt >> 4;  // staging: half-warp <-> face point, lanes <-> basis function
-    const int nunit = (1 + D) * ct_h;
     for (int lf = 0; lf < n_lfe; ++lf) {
         const double* tp = dv.tphi + (static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf * pe;
         const FaceRec<M, D>* fr = frec + lf * qf;
-        __syncthreads();  // the previous face's tiles are done with Fs
+        __syncthreads();  // the previous face's tiles are done with Fs, Cw
         for (int gc = hw; gc < qf; gc += nhw)
             for (int j = l16; j < pe; j += 16) Fs[gc * lda + j] = __ldg(tp + static_cast<size_t>(gc) * pe + j);
-        for (int pr = 0; pr < M * M; ++pr) {
+        for (int t = tid; t < M * M * qf; t += nt) {
+            const int pr = t / qf, gc = t - pr * qf;
             const int mp = pr / M, m = pr - mp * M, mm = m * M + mp;
-            if (pr > 0) __syncthreads();  // the previous pair's tiles are done with Aw, Bf
-            // the pair's slabs: (1 + D) coefficient sets for H / G_d, one for F
-            for (int t = tid; t < qf * pf; t += nt) {
-                const int gc = t / pf, b = t - gc * pf;
-                const FaceRec<M, D>& r = fr[gc];
-                const double wp = rec_ld<GREC>(&r.w) * Ps[gc * ldp + b];
-                Aw[gc * ldp + b] = wp * rec_ld<GREC>(&r.dv_u[mm]);
+            const FaceRec<M, D>& r = fr[gc];
+            const double wg = rec_ld<GREC>(&r.w);
+            double* cw = Cw + pr * NC * qfp + gc;
+            cw[0] = wg * rec_ld<GREC>(&r.dv_u[mm]);
 #pragma unroll
-                for (int dq = 0; dq < D; ++dq) Aw[(1 + dq) * slab + gc * ldp + b] = wp * rec_ld<GREC>(&r.dv_q[mm * D + dq]);
-                Bf[gc * ldp + b] = wp * rec_ld<GREC>(&r.dfh_uh[mm]);
-            }
-            __syncthreads();  // slabs (and, for the first pair, Fs) are staged
-            // ---- H / G_d ----
-            for (int unit = warp; unit < nunit; unit += nwarps) {
-                const int w = unit / ct_h, ct = unit - w * ct_h;
-                double c[kHgfRtMax][2];
+            for (int dq = 0; dq < D; ++dq) cw[(1 + dq) * qfp] = wg * rec_ld<GREC>(&r.dv_q[mm * D + dq]);
+            cw[(1 + D) * qfp] = wg * rec_ld<GREC>(&r.dfh_uh[mm]);
+        }
+        __syncthreads();
+        // ---- H / G_d: this warp's column tiles of j ----
+        for (int ct = warp; ct < ct_h; ct += nwarps) {
+            double bf[kHgfKsMax];
 #pragma unroll
-                for (int rt = 0; rt < kHgfRtMax; ++rt) c[rt][0] = c[rt][1] = 0.0;
-                const double* as = Aw + w * slab + grp + tig * ldp;
-                const double* bs = Fs + tig * lda + ct * 8 + grp;
-                for (int ks = 0; ks < ksteps; ++ks) {
-                    const double bf = bs[4 * ks * lda];
+            for (int ks = 0; ks < kHgfKsMax; ++ks) bf[ks] = ks < ksteps ? Fs[(4 * ks + tig) * lda + ct * 8 + grp] : 0.0;
+            const int j = ct * 8 + 2 * tig;
+            for (int pr = 0; pr < M * M; ++pr) {
+                const int mp = pr / M, m = pr - mp * M;
+                for (int w = 0; w <= D; ++w) {
+                    const double* cw = Cw + (pr * NC + w) * qfp + tig;
+                    double c[kHgfRtMax][2];
 #pragma unroll
-                    for (int rt = 0; rt < kHgfRtMax; ++rt)
-                        if (rt < rt_h) dmma_8x8x4(c[rt][0], c[rt][1], as[4 * ks * ldp + rt * 8], bf);
+                    for (int rt = 0; rt < kHgfRtMax; ++rt) c[rt][0] = c[rt][1] = 0.0;
+#pragma unroll
+                    for (int ks = 0; ks < kHgfKsMax; ++ks) {
+                        if (ks >= ksteps) break;
+                        const double b = bf[ks] * cw[4 * ks];
+                        const double* as = Ps + (4 * ks + tig) * ldp + grp;
+#pragma unroll
+                        for (int rt = 0; rt < kHgfRtMax; ++rt)
+                            if (rt < rt_h) dmma_8x8x4(c[rt][0], c[rt][1], as[rt * 8], b);
+                    }
+                    double* dst = (w == 0 ? out.H : out.G[w - 1]) + static_cast<size_t>(e) * nfl * npe;
+#pragma unroll
+                    for (int rt = 0; rt < kHgfRtMax; ++rt) {
+                        const int bb = rt * 8 + grp;
+                        if (rt >= rt_h || bb >= pf) continue;
+                        const size_t row = lf * mpf + m * pf + bb;
+                        if (j < pe) dst[static_cast<size_t>(mp * pe + j) * nfl + row] = c[rt][0];
+                        if (j + 1 < pe) dst[static_cast<size_t>(mp * pe + j + 1) * nfl + row] = c[rt][1];
+                    }
                 }
-                const int j = ct * 8 + 2 * tig;
-                double* dst = (w == 0 ? out.H : out.G[w - 1]) + static_cast<size_t>(e) * nfl * npe;
-#pragma unroll
-                for (int rt = 0; rt < kHgfRtMax; ++rt) {
-                    const int b = rt * 8 + grp;
-                    if (rt >= rt_h || b >= pf) continue;
-                    const size_t row = lf * mpf + m * pf + b;
-                    if (j < pe) dst[static_cast<size_t>(mp * pe + j) * nfl + row] = c[rt][0];
-                    if (j + 1 < pe) dst[static_cast<size_t>(mp * pe + j + 1) * nfl + row] = c[rt][1];
-                }
             }
-            // ---- F (rows i, columns bp): the warps the H / G_d units leave idle go first ----
-            for (int rti = (warp + nwarps - nunit % nwarps) % nwarps; rti < ct_h; rti += nwarps) {
+        }
+        // ---- F (rows i, columns bp): this warp's row tiles of i ----
+        for (int rti = warp; rti < ct_h; rti += nwarps) {
+            double af[kHgfKsMax];
+#pragma unroll
+            for (int ks = 0; ks < kHgfKsMax; ++ks) af[ks] = ks < ksteps ? Fs[(4 * ks + tig) * lda + rti * 8 + grp] : 0.0;
+            const int i = rti * 8 + grp;
+            double* dst = out.F + static_cast<size_t>(e) * npe * nfl;
+            for (int pr = 0; pr < M * M; ++pr) {
+                const int mp = pr / M, m = pr - mp * M;
+                const double* cf = Cw + (pr * NC + 1 + D) * qfp + tig;
                 double c[kHgfRtMax][2];
 #pragma unroll
                 for (int cb = 0; cb < kHgfRtMax; ++cb) c[cb][0] = c[cb][1] = 0.0;
-                const double* as = Fs + rti * 8 + grp + tig * lda;
-                const double* bs = Bf + grp + tig * ldp;
-                for (int ks = 0; ks < ksteps; ++ks) {
-                    const double af = as[4 * ks * lda];
+#pragma unroll
+                for (int ks = 0; ks < kHgfKsMax; ++ks) {
+                    if (ks >= ksteps) break;
+                    const double cfk = cf[4 * ks];
+                    const double* bs = Ps + (4 * ks + tig) * ldp + grp;
 #pragma unroll
                     for (int cb = 0; cb < kHgfRtMax; ++cb)
-                        if (cb < rt_h) dmma_8x8x4(c[cb][0], c[cb][1], af, bs[4 * ks * ldp + cb * 8]);
+                        if (cb < rt_h) dmma_8x8x4(c[cb][0], c[cb][1], af[ks], bs[cb * 8] * cfk);
                 }
-                const int i = rti * 8 + grp;
-                double* dst = out.F + static_cast<size_t>(e) * npe * nfl;
                 const size_t row = m * pe + i;
 #pragma unroll
                 for (int cb = 0; cb < kHgfRtMax; ++cb) {
@@ -1177,13 +1189,13 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
     if (all <= budget) {
         // E / D_d on the tensor-core path when the operand chunks fit next to the point records
         size_t ed_bytes = 2 * ed_plan(dv.pe, M, D, NTD / 32).doubles(D) * sizeof(double) + 16;
-        ed_bytes = std::max(ed_bytes, hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D) * sizeof(double) + 16);
-        const bool ed = want_jac && tuning().use_dmma && ed_dmma_ok(dv.pe, M, D) && hgf_dmma_ok(dv.pf) && all + ed_bytes <= cap;
+        ed_bytes = std::max(ed_bytes, hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D, M) * sizeof(double) + 16);
+        const bool ed = want_jac && tuning().use_dmma && ed_dmma_ok(dv.pe, M, D) && hgf_dmma_ok(dv.pf, dv.qf) && all + ed_bytes <= cap;
         // 16-warp variant (one CTA per SM): all 1 + D matrices of a scalar system in ONE point sweep
         if constexpr (M == 1) {
             if (ed && tuning().local_nt == 512) {
                 const EdPlan p16 = ed_plan(dv.pe, M, D, 16);
-                const size_t eb = std::max(2 * p16.doubles(D), hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D)) * sizeof(double) + 16;
+                const size_t eb = std::max(2 * p16.doubles(D), hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D, M)) * sizeof(double) + 16;
                 if (p16.wsub <= 4 && all + eb <= cap) {
                     auto kern_w = local_assemble_kernel<Model, 512, true, false>;
                     ensure_dynamic_smem(kern_w, cap);
@@ -1200,25 +1212,25 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
     }
     // wide systems with the Jacobian on the tensor-core path: records in a global (L2) scratch, one launch
     if constexpr (M > 1) {
-        if (want_jac && tuning().use_dmma && tuning().local_global_records && ed_dmma_ok(dv.pe, M, D) && hgf_dmma_ok(dv.pf)) {
+        if (want_jac && tuning().use_dmma && tuning().local_global_records && ed_dmma_ok(dv.pe, M, D) && hgf_dmma_ok(dv.pf, dv.qf)) {
             const size_t rec_stride = (dv.qe * svr + nfp * sfr + 15) & ~static_cast<size_t>(15);
             // 16 warps: two component pairs share one point sweep (and one weighted-basis operand)
             const EdPlan p16 = ed_plan(dv.pe, M, D, 16);
-            const size_t edb16 = std::max(2 * p16.doubles(D), hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D)) * sizeof(double) + 32;
+            const size_t edb16 = std::max(2 * p16.doubles(D), hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D, M)) * sizeof(double) + 32;
             if (tuning().local_nt == 512 && p16.wsub <= 8 && fixed + edb16 <= cap) {
                 auto kern_gw = local_assemble_kernel<Model, 512, true, true>;
                 ensure_dynamic_smem(kern_gw, cap);
                 DevBuf<char> scratch(rec_stride * static_cast<size_t>(dv.ne));
-                kern_gw<<<dv.ne, 512, fixed + edb16, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2, scratch.p, rec_stride);
+                kern_gw<<<dv.ne, 512, fixed + edb16, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2 | (tuning().local_debug_skip << 4), scratch.p, rec_stride);
                 HDGB_LAUNCH_CHECK(ctx);
                 return;
             }
-            const size_t edb = std::max(2 * ed_plan(dv.pe, M, D, 8).doubles(D), hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D)) * sizeof(double) + 32;
+            const size_t edb = std::max(2 * ed_plan(dv.pe, M, D, 8).doubles(D), hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D, M)) * sizeof(double) + 32;
             if (fixed + edb <= cap) {
                 auto kern_g = local_assemble_kernel<Model, 256, true, true>;
                 ensure_dynamic_smem(kern_g, cap);
                 DevBuf<char> scratch(rec_stride * static_cast<size_t>(dv.ne));
-                kern_g<<<dv.ne, 256, fixed + edb, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2, scratch.p, rec_stride);
+                kern_g<<<dv.ne, 256, fixed + edb, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2 | (tuning().local_debug_skip << 4), scratch.p, rec_stride);
                 HDGB_LAUNCH_CHECK(ctx);
                 return;
             }
