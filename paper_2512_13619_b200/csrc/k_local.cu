@@ -271,6 +271,10 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
     constexpr int kEdSlots = ed_slots(M);
     constexpr int kEdRes = (M == 1) ? 2 : 4;  // resident matrices whose coefficient rows the cached builder keeps in registers
     constexpr int kEdIt = 4;                  // strips of 16 basis functions covering the padded columns (pe <= 64)
+    // Table loads of the next chunk issued before the current chunk's products, operands finished after them: pays
+    // where the registers are there (one CTA per SM, 255 registers: config 5 local kernel 37.0 -> 35.5 ms at hex 12^3);
+    // at two CTAs per SM (128 registers) the 16 prefetched values spill and the kernel loses (17.2 -> 19.0 ms at config 2).
+    constexpr bool kSplitBuild = GREC;
     const int pe = dv.pe, qf = dv.qf, npe = M * pe;
     const int qe = gv1 - gv0, nfp = fp1 - fp0;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
@@ -395,7 +399,40 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
         // The same builder with everything hoisted for the common shapes (the resident matrices of a sub-pass fit
         // kEdRes coefficient rows in registers: scalar systems with pe in 49..64, wide systems one pair per pass):
         // coefficient rows read once per chunk, the basis-function strips unrolled with constant offsets.
-        auto build_cached = [&](int ch, int buf) {
+        // Stage 1 of the cached builder: only the table loads of chunk ch (this thread's point, its strips of 16 basis
+        // functions) -- issued BEFORE the products of the current chunk so that their L2 latency is covered by the
+        // warp's own DMMA chain; stage 2 (coefficient rows from the records, FMAs, shared-memory stores) runs after it.
+        auto load_tables = [&](int ch, double (&tb)[kEdIt][1 + D]) {
+            const bool vol = ch < nchunk_v;
+            const int p0 = vol ? ch * kEdKc : (ch - nchunk_v) * kEdKc;
+            const int np = min(kEdKc, (vol ? qe : nfp) - p0);
+            const bool live = bkk < np;
+            const int pt = live ? p0 + bkk : 0;
+            if (vol) {
+                const int g = gv0 + pt;
+                const double* php = dv.phi + static_cast<size_t>(pe) * g + bi0;
+                const double* dpp[D];
+#pragma unroll
+                for (int k = 0; k < D; ++k) dpp[k] = dv.dphi[k] + static_cast<size_t>(pe) * g + bi0;
+#pragma unroll
+                for (int it = 0; it < kEdIt; ++it) {
+                    const bool inb = live && 16 * it < icols && bi0 + 16 * it < pe;  // outside: exact zero padding
+                    tb[it][0] = inb ? __ldg(php + 16 * it) : 0.0;
+#pragma unroll
+                    for (int k = 0; k < D; ++k) tb[it][1 + k] = inb ? __ldg(dpp[k] + 16 * it) : 0.0;
+                }
+            } else {
+                const int p = fp0 + pt;
+                const int lf = p / qf, gc = p - lf * qf;
+                const double* php = dv.tphi + ((static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf + gc) * pe + bi0;
+#pragma unroll
+                for (int it = 0; it < kEdIt; ++it) {
+                    const bool inb = live && 16 * it < icols && bi0 + 16 * it < pe;
+                    tb[it][0] = inb ? __ldg(php + 16 * it) : 0.0;
+                }
+            }
+        };
+        auto build_cached = [&](int ch, int buf, const double (&tb)[kEdIt][1 + D]) {
             double* Ab = opbuf + buf * bufd + bkk * lda + bi0;       // this thread's entry of resident matrix 0, strip 0
             double* Bb = opbuf + buf * bufd + boff0 + bkk * ldb + bi0;
             const bool vol = ch < nchunk_v;
@@ -407,7 +444,6 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
             const int qstride = kEdKc * lda;
             // this thread's resident matrices: q = bsub, bsub + nsub, ... (kEdRes of them at most)
             if (vol) {
-                const int g = gv0 + pt;
                 const VolRec<M, D>& r = vrec[pt];
                 const double wq = rec_ld<GREC>(&r.w);
                 double c0[kEdRes], ck[kEdRes][D];
@@ -434,18 +470,19 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
                         }
                     }
                 }
-                const double* php = dv.phi + static_cast<size_t>(pe) * g + bi0;
+                const double* php = dv.phi + static_cast<size_t>(pe) * (gv0 + pt) + bi0;
                 const double* dpp[D];
 #pragma unroll
-                for (int k = 0; k < D; ++k) dpp[k] = dv.dphi[k] + static_cast<size_t>(pe) * g + bi0;
+                for (int k = 0; k < D; ++k) dpp[k] = dv.dphi[k] + static_cast<size_t>(pe) * (gv0 + pt) + bi0;
 #pragma unroll
                 for (int it = 0; it < kEdIt; ++it) {
                     if (16 * it >= icols) break;
-                    const bool inb = live && bi0 + 16 * it < pe;  // outside: exact zero padding
-                    const double ph = inb ? __ldg(php + 16 * it) : 0.0;
+                    const bool inb = live && bi0 + 16 * it < pe;
+                    // prefetched by load_tables (split build) or loaded here, strip by strip
+                    const double ph = kSplitBuild ? tb[it][0] : (inb ? __ldg(php + 16 * it) : 0.0);
                     double dp_[D];
 #pragma unroll
-                    for (int k = 0; k < D; ++k) dp_[k] = inb ? __ldg(dpp[k] + 16 * it) : 0.0;
+                    for (int k = 0; k < D; ++k) dp_[k] = kSplitBuild ? tb[it][1 + k] : (inb ? __ldg(dpp[k] + 16 * it) : 0.0);
                     if (16 * it < irows) {
 #pragma unroll
                         for (int qi = 0; qi < kEdRes; ++qi) {
@@ -462,8 +499,6 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
                     if (bsub == 0) Bb[16 * it] = inb ? wq * ph : 0.0;
                 }
             } else {
-                const int p = fp0 + pt;
-                const int lf = p / qf, gc = p - lf * qf;
                 const FaceRec<M, D>& r = frec[pt];
                 const double wq = rec_ld<GREC>(&r.w);
                 double cf[kEdRes];
@@ -478,12 +513,14 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
                         else cf[qi] = rec_ld<GREC>(&r.dfh_q[mm * D + w - 1]);
                     }
                 }
+                const int pf_ = fp0 + pt;
+                const int lf = pf_ / qf, gc = pf_ - lf * qf;
                 const double* php = dv.tphi + ((static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf + gc) * pe + bi0;
 #pragma unroll
                 for (int it = 0; it < kEdIt; ++it) {
                     if (16 * it >= icols) break;
                     const bool inb = live && bi0 + 16 * it < pe;
-                    const double ph = inb ? __ldg(php + 16 * it) : 0.0;
+                    const double ph = kSplitBuild ? tb[it][0] : (inb ? __ldg(php + 16 * it) : 0.0);
                     if (16 * it < irows) {
 #pragma unroll
                         for (int qi = 0; qi < kEdRes; ++qi) {
@@ -517,17 +554,26 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
                 boff[s] = boff0 + cgi * 32 + grp + tig * ldb;
             }
             const bool cached = whi - wlo <= kEdRes * nsub;  // (the launcher uses 512 threads only where this holds)
+            double tb[kEdIt][1 + D];  // prefetched table values of the next chunk (cached builder)
             __syncthreads();
-            if (cached) build_cached(0, 0);
-            else build(0, 0);
+            if (cached) {
+                if (kSplitBuild) load_tables(0, tb);
+                build_cached(0, 0, tb);
+            } else {
+                build(0, 0);
+            }
             __syncthreads();
             for (int ch = 0; ch < nchunk; ++ch) {
                 const int buf = ch & 1;
                 // the next chunk's operands are built in the same barrier interval as this chunk's products:
                 // warps drift apart, so table loads and DMMA issue overlap across the CTA
                 if (ch + 1 < nchunk) {
-                    if (cached) build_cached(ch + 1, buf ^ 1);
-                    else build(ch + 1, buf ^ 1);
+                    if (cached) {
+                        if (kSplitBuild) load_tables(ch + 1, tb);
+                        else build_cached(ch + 1, buf ^ 1, tb);
+                    } else {
+                        build(ch + 1, buf ^ 1);
+                    }
                 }
                 const double* Ob = opbuf + buf * bufd;
 #pragma unroll
@@ -549,6 +595,8 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
                         }
                     }
                 }
+                // stage 2 of the cached builder: the tables requested before the products have arrived by now
+                if (kSplitBuild && cached && ch + 1 < nchunk) build_cached(ch + 1, buf ^ 1, tb);
                 __syncthreads();
             }
             // ---- write this pass's blocks ----
