@@ -773,8 +773,10 @@ __device__ void hgf_dmma(const DiscView& dv, const LocalOut& out, int e, const F
     }
 }
 
-template <class Model, int NT, bool ED, bool GREC>
-__global__ void __launch_bounds__(NT, (!GREC && Model::M == 1 && NT <= 256) ? 2 : 1) local_assemble_kernel(DiscView dv, ModelView mv, LocalIn in, LocalOut out,
+// RES: residual-only specialisation (assemble_residual: once per Newton step and per line-search trial).  Without the
+// Jacobian code the kernel needs half the registers, so four CTAs per SM cover each other's load latency.
+template <class Model, int NT, bool ED, bool GREC, bool RES = false>
+__global__ void __launch_bounds__(NT, RES ? (Model::M == 1 ? 4 : 2) : ((!GREC && Model::M == 1 && NT <= 256) ? 2 : 1)) local_assemble_kernel(DiscView dv, ModelView mv, LocalIn in, LocalOut out,
                                                             int want_jac, int gv0, int gv1, int fp0, int fp1, int first,
                                                             int ed_dmma_on, char* rec_scratch, size_t rec_stride) {
     // GREC: the point records of wide systems do not fit shared memory; they are staged per element in a
@@ -870,7 +872,7 @@ __global__ void __launch_bounds__(NT, (!GREC && Model::M == 1 && NT <= 256) ? 2 
                 r.Fr[m * D + rr] = sfl;
             }
         }
-        if (want_jac) {
+        if (!RES && want_jac) {
             double dFu[M * D * M], dFq[M * D * M * D];
             model.dflux_du(ug, qg, x, dFu);
             model.dflux_dq(ug, qg, x, dFq);
@@ -925,40 +927,52 @@ __global__ void __launch_bounds__(NT, (!GREC && Model::M == 1 && NT <= 256) ? 2 
             for (int d = 0; d < D; ++d) fn += Fl[m * D + d] * n[d];
             r.fhat[m] = fn + tau * (ug[m] - uh[m]);
         }
-        double dFu[M * D * M], dFq[M * D * M * D];
-        if (want_jac || tag != 0) {
-            model.dflux_du(uh, qg, x, dFu);
-            model.dflux_dq(uh, qg, x, dFq);
+        if constexpr (RES) {
+            // residual only: the face contribution needs fhat (interior faces) or the boundary value, no derivatives
+            if (tag == 0) {
+                for (int m = 0; m < M; ++m) r.val[m] = r.fhat[m];
+            } else {
+                BFlux<M, D> b;
+                const double* gD = mv.dirichlet_q ? mv.dirichlet_q + fi * M : nullptr;
+                model.boundary(tag, ug, qg, uh, n, x, gD, b);
+                for (int m = 0; m < M; ++m) r.val[m] = b.val[m];
+            }
         } else {
-            for (int k = 0; k < M * D * M; ++k) dFu[k] = 0.0;
-            for (int k = 0; k < M * D * M * D; ++k) dFq[k] = 0.0;
-        }
-        // derivatives of the numerical flux (local_ops.cpp:186-189)
-        for (int m = 0; m < M; ++m)
-            for (int mp = 0; mp < M; ++mp) {
-                double su = 0.0;
-                for (int d = 0; d < D; ++d) su += dFu[(m * D + d) * M + mp] * n[d];
-                r.dfh_uh[m * M + mp] = su - ((m == mp) ? tau : 0.0);
-                for (int dp = 0; dp < D; ++dp) {
-                    double sq = 0.0;
-                    for (int d = 0; d < D; ++d) sq += dFq[((m * D + d) * M + mp) * D + dp] * n[d];
-                    r.dfh_q[(m * M + mp) * D + dp] = sq;
+            double dFu[M * D * M], dFq[M * D * M * D];
+            if (want_jac || tag != 0) {
+                model.dflux_du(uh, qg, x, dFu);
+                model.dflux_dq(uh, qg, x, dFq);
+            } else {
+                for (int k = 0; k < M * D * M; ++k) dFu[k] = 0.0;
+                for (int k = 0; k < M * D * M * D; ++k) dFq[k] = 0.0;
+            }
+            // derivatives of the numerical flux (local_ops.cpp:186-189)
+            for (int m = 0; m < M; ++m)
+                for (int mp = 0; mp < M; ++mp) {
+                    double su = 0.0;
+                    for (int d = 0; d < D; ++d) su += dFu[(m * D + d) * M + mp] * n[d];
+                    r.dfh_uh[m * M + mp] = su - ((m == mp) ? tau : 0.0);
+                    for (int dp = 0; dp < D; ++dp) {
+                        double sq = 0.0;
+                        for (int d = 0; d < D; ++d) sq += dFq[((m * D + d) * M + mp) * D + dp] * n[d];
+                        r.dfh_q[(m * M + mp) * D + dp] = sq;
+                    }
                 }
+            if (tag == 0) {
+                for (int m = 0; m < M; ++m) r.val[m] = r.fhat[m];
+                for (int k = 0; k < M * M; ++k) {
+                    r.dv_u[k] = ((k / M) == (k % M)) ? tau : 0.0;
+                    r.dv_uh[k] = r.dfh_uh[k];
+                }
+                for (int k = 0; k < M * M * D; ++k) r.dv_q[k] = r.dfh_q[k];
+            } else {
+                BFlux<M, D> b;
+                const double* gD = mv.dirichlet_q ? mv.dirichlet_q + fi * M : nullptr;
+                model.boundary(tag, ug, qg, uh, n, x, gD, b);
+                for (int m = 0; m < M; ++m) r.val[m] = b.val[m];
+                for (int k = 0; k < M * M; ++k) { r.dv_u[k] = b.d_u[k]; r.dv_uh[k] = b.d_uh[k]; }
+                for (int k = 0; k < M * M * D; ++k) r.dv_q[k] = b.d_q[k];
             }
-        if (tag == 0) {
-            for (int m = 0; m < M; ++m) r.val[m] = r.fhat[m];
-            for (int k = 0; k < M * M; ++k) {
-                r.dv_u[k] = ((k / M) == (k % M)) ? tau : 0.0;
-                r.dv_uh[k] = r.dfh_uh[k];
-            }
-            for (int k = 0; k < M * M * D; ++k) r.dv_q[k] = r.dfh_q[k];
-        } else {
-            BFlux<M, D> b;
-            const double* gD = mv.dirichlet_q ? mv.dirichlet_q + fi * M : nullptr;
-            model.boundary(tag, ug, qg, uh, n, x, gD, b);
-            for (int m = 0; m < M; ++m) r.val[m] = b.val[m];
-            for (int k = 0; k < M * M; ++k) { r.dv_u[k] = b.d_u[k]; r.dv_uh[k] = b.d_uh[k]; }
-            for (int k = 0; k < M * M * D; ++k) r.dv_q[k] = b.d_q[k];
         }
     }
     __syncthreads();
@@ -1022,7 +1036,7 @@ __global__ void __launch_bounds__(NT, (!GREC && Model::M == 1 && NT <= 256) ? 2 
             *o = first ? -acc[m] : *o - acc[m];
         }
     }
-    if (!want_jac) return;
+    if (RES || !want_jac) return;
 
     // ---- phase 2b: E and D_d.  A thread owns a TI x TJ tile of scalar-basis pairs (i, j); per point it
     // forms the i-side values once and rank-1 updates the tile.  Component columns mp are swept one
@@ -1229,9 +1243,11 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
     if (fixed + std::max(svr, sfr) > budget)
         throw Failure(HDGB_ERR_UNSUPPORTED, "local assembly: element state exceeds shared memory");
     auto kern = local_assemble_kernel<Model, 256, false, false>;
+    auto kern_r = local_assemble_kernel<Model, 256, false, false, true>;  // residual only
     constexpr int NTD = 256;  // tensor-core mode: 8 warps, two CTAs per SM for scalar systems (their phases overlap)
     auto kern_d = local_assemble_kernel<Model, NTD, true, false>;
     ensure_dynamic_smem(kern, cap);
+    ensure_dynamic_smem(kern_r, cap);
     ensure_dynamic_smem(kern_d, cap);
     const size_t all = fixed + dv.qe * svr + nfp * sfr;
     if (all <= budget) {
@@ -1254,7 +1270,8 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
             }
         }
         if (ed) kern_d<<<dv.ne, NTD, all + ed_bytes, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2 | (tuning().local_debug_skip << 4), nullptr, 0);
-        else kern<<<dv.ne, 256, all, ctx->stream>>>(dv, mv, in, out, want_jac ? 1 : 0, 0, dv.qe, 0, nfp, 1, 0, nullptr, 0);
+        else if (!want_jac) kern_r<<<dv.ne, 256, all, ctx->stream>>>(dv, mv, in, out, 0, 0, dv.qe, 0, nfp, 1, 0, nullptr, 0);
+        else kern<<<dv.ne, 256, all, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 0, nullptr, 0);
         HDGB_LAUNCH_CHECK(ctx);
         return;
     }
@@ -1299,7 +1316,8 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
         const int g1 = std::min(dv.qe, g0 + vc);
         const size_t sm_b = fixed + (g1 - g0) * svr + ed_bytes;
         if (edf) kern_d<<<dv.ne, NTD, sm_b, ctx->stream>>>(dv, mv, in, out, 1, g0, g1, 0, 0, first, 1, nullptr, 0);
-        else kern<<<dv.ne, 256, sm_b, ctx->stream>>>(dv, mv, in, out, want_jac ? 1 : 0, g0, g1, 0, 0, first, 0, nullptr, 0);
+        else if (!want_jac) kern_r<<<dv.ne, 256, sm_b, ctx->stream>>>(dv, mv, in, out, 0, g0, g1, 0, 0, first, 0, nullptr, 0);
+        else kern<<<dv.ne, 256, sm_b, ctx->stream>>>(dv, mv, in, out, 1, g0, g1, 0, 0, first, 0, nullptr, 0);
         HDGB_LAUNCH_CHECK(ctx);
         first = 0;
     }
@@ -1307,7 +1325,8 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
         const int p1 = std::min(nfp, p0 + fc);
         const size_t sm_b = fixed + (p1 - p0) * sfr + ed_bytes;
         if (edf) kern_d<<<dv.ne, NTD, sm_b, ctx->stream>>>(dv, mv, in, out, 1, 0, 0, p0, p1, first, 1, nullptr, 0);
-        else kern<<<dv.ne, 256, sm_b, ctx->stream>>>(dv, mv, in, out, want_jac ? 1 : 0, 0, 0, p0, p1, first, 0, nullptr, 0);
+        else if (!want_jac) kern_r<<<dv.ne, 256, sm_b, ctx->stream>>>(dv, mv, in, out, 0, 0, 0, p0, p1, first, 0, nullptr, 0);
+        else kern<<<dv.ne, 256, sm_b, ctx->stream>>>(dv, mv, in, out, 1, 0, 0, p0, p1, first, 0, nullptr, 0);
         HDGB_LAUNCH_CHECK(ctx);
         first = 0;
     }

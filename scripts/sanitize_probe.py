@@ -13,15 +13,26 @@ import paper_2512_13619_b200 as hdg  # noqa: E402
 ctx = hdg.Context(0)
 hdg.set_tuning("stream_min_elems", 0)       # route the small GEMVs through the TMA stream kernel too
 cases = [("hex", 3, 3, "poisson", hdg.PrecondSpec("asm")),
+         ("hex", 2, 3, "navier_stokes", hdg.PrecondSpec("bj")),       # wide system: records through the L2 scratch, split operand build
+         ("hex", 2, 3, "elasticity", hdg.PrecondSpec("asm")),
          ("tri", 6, 4, "burgers", hdg.PrecondSpec("asm", poly_degree=4, poly_kind="chebyshev")),
          ("quad", 6, 2, "burgers", hdg.PrecondSpec("bj", poly_degree=5))]
 for shape, n, k, case, pspec in cases:
-    disc = hdg.Discretization.structured(ctx, shape, n=n, degree=k, jitter=0.1 if shape == "tri" else 0.0)
-    model = hdg.make_case_model(disc, case)
+    ncomp = {"navier_stokes": 5, "elasticity": 3}.get(case, 1)
+    disc = hdg.Discretization.structured(ctx, shape, n=n, degree=k, n_comp=ncomp, jitter=0.1 if shape == "tri" else 0.0)
+    model = hdg.make_case_model(disc, case, **({"mu": 0.02} if case == "navier_stokes" else {}))
     state = hdg.make_initial_state(disc, model)
-    rep = hdg.newton_solve(disc, model, state, pspec=pspec)
+    tkw = dict(dt=0.05, u_prev=state.u) if case == "navier_stokes" else {}
+    rep = hdg.newton_solve(disc, model, state, pspec=pspec, **tkw)
     assert rep.converged, (shape, rep)
     print(shape, k, case, "newton", rep.n_newton, "gmres", rep.n_gmres_total, "launches", ctx.launch_count)
+# the 16-warp variant of the local kernel
+hdg.set_tuning("local_nt", 512)
+disc = hdg.Discretization.structured(ctx, "hex", n=2, degree=3)
+model = hdg.make_case_model(disc, "poisson")
+ops = hdg.assemble_element_operators(disc, model, hdg.make_initial_state(disc, model))
+hdg.set_tuning("local_nt", 256)
+print("16-warp local kernel ok")
 # the streamed CGS2 passes on a basis long enough for the TMA path
 n, nvec = 1 << 16, 6
 V, _ = np.linalg.qr(hdg.random_vector(n * nvec, 1).reshape(n, nvec))
