@@ -89,7 +89,7 @@ def parse():
     ap.add_argument("--precond", default=None, choices=["bj", "asm", "ras"])
     ap.add_argument("--cpu-cells", dest="cpu_n", type=int, default=None,
                     help="cells per direction of the bounded CPU sample (default: sized to the time budget)")
-    ap.add_argument("--cpu-budget-s", type=float, default=240.0, help="--impl reference: wall-clock budget of the whole run")
+    ap.add_argument("--cpu-budget-s", type=float, default=400.0, help="--impl reference: wall-clock budget of the whole run")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--transport", default="auto", choices=["auto", "nccl", "host"])
     a = ap.parse_args()
