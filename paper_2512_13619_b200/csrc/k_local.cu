@@ -1256,7 +1256,7 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
         ed_bytes = std::max(ed_bytes, hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D, M) * sizeof(double) + 16);
         const bool ed = want_jac && tuning().use_dmma && ed_dmma_ok(dv.pe, M, D) && hgf_dmma_ok(dv.pf, dv.qf) && all + ed_bytes <= cap;
         // 16-warp variant (one CTA per SM): all 1 + D matrices of a scalar system in ONE point sweep
-        if constexpr (M == 1) {
+        if constexpr (M == 1 && D == 3) {  // (instantiated for the 3D models only: build time)
             if (ed && tuning().local_nt == 512) {
                 const EdPlan p16 = ed_plan(dv.pe, M, D, 16);
                 const size_t eb = std::max(2 * p16.doubles(D), hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D, M)) * sizeof(double) + 16;
@@ -1282,13 +1282,15 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
             // 16 warps: two component pairs share one point sweep (and one weighted-basis operand)
             const EdPlan p16 = ed_plan(dv.pe, M, D, 16);
             const size_t edb16 = std::max(2 * p16.doubles(D), hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D, M)) * sizeof(double) + 32;
-            if (tuning().local_nt == 512 && p16.wsub <= 8 && fixed + edb16 <= cap) {
-                auto kern_gw = local_assemble_kernel<Model, 512, true, true>;
-                ensure_dynamic_smem(kern_gw, cap);
-                DevBuf<char> scratch(rec_stride * static_cast<size_t>(dv.ne));
-                kern_gw<<<dv.ne, 512, fixed + edb16, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2 | (tuning().local_debug_skip << 4), scratch.p, rec_stride);
-                HDGB_LAUNCH_CHECK(ctx);
-                return;
+            if constexpr (D == 3) {
+                if (tuning().local_nt == 512 && p16.wsub <= 8 && fixed + edb16 <= cap) {
+                    auto kern_gw = local_assemble_kernel<Model, 512, true, true>;
+                    ensure_dynamic_smem(kern_gw, cap);
+                    DevBuf<char> scratch(rec_stride * static_cast<size_t>(dv.ne));
+                    kern_gw<<<dv.ne, 512, fixed + edb16, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2 | (tuning().local_debug_skip << 4), scratch.p, rec_stride);
+                    HDGB_LAUNCH_CHECK(ctx);
+                    return;
+                }
             }
             const size_t edb = std::max(2 * ed_plan(dv.pe, M, D, 8).doubles(D), hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D, M)) * sizeof(double) + 32;
             if (fixed + edb <= cap) {
