@@ -274,3 +274,179 @@ def test_non_finite_state_is_reported(ctx):                      # local_ops.cpp
     state.uhat = uh
     with pytest.raises(hdg.NonFiniteState, match="trace"):
         hdg.assemble_residual(disc, model, state)
+
+
+# ---- test_dense_batch.cpp -------------------------------------------------------------------------------------------
+def test_lu_invert_pivoting_handles_zero_diagonal(ctx):          # LuInvertBatch.PivotingHandlesZeroDiagonal
+    a = np.zeros((1, 2, 2))
+    a[0, 1, 0] = 1.0   # [b][c][r]: entry (r = 0, c = 1)
+    a[0, 0, 1] = 1.0
+    inv = hdg.lu_invert_batch(ctx, a.ravel(), 2, 1).reshape(1, 2, 2)
+    assert inv[0, 1, 0] == 1.0 and inv[0, 0, 1] == 1.0 and inv[0, 0, 0] == 0.0 and inv[0, 1, 1] == 0.0
+
+
+def test_lu_invert_identity_diagonal_and_singular_index(ctx):    # LuInvertBatch.IdentityBlocks / DiagonalBlock / SingularBlockNamesIndex
+    n, batch = 3, 4
+    eye = np.tile(np.eye(n).ravel(), batch)
+    assert np.array_equal(hdg.lu_invert_batch(ctx, eye, n, batch), eye)
+    d = np.diag([2.0, 4.0, 8.0]).ravel()
+    assert np.array_equal(hdg.lu_invert_batch(ctx, d, n, 1), np.diag([0.5, 0.25, 0.125]).ravel())
+    a = np.zeros((3, 2, 2))
+    a[0] = a[2] = np.eye(2)          # block 1 stays all-zero
+    with pytest.raises(hdg.SingularBlock) as ei:
+        hdg.lu_invert_batch(ctx, a.ravel(), 2, 3)
+    assert ei.value.index == 1
+
+
+def test_gemv_accumulate_twice_doubles_and_matches_gemm_column(ctx):  # GemvStridedBatch.AccumulateTwiceDoubles / BitIdenticalToGemmSingleColumn
+    rows, cols, batch = 6, 4, 7
+    a = hdg.random_vector(rows * cols * batch, 51)
+    x = hdg.random_vector(cols * batch, 52)
+    y = hdg.gemv_strided_batch(ctx, a, rows, cols, batch, x)
+    y2 = hdg.gemv_strided_batch(ctx, a, rows, cols, batch, x, y=y.copy(), accumulate=True)
+    assert np.array_equal(y2, 2.0 * y)
+    c = hdg.gemm_batch(ctx, a, rows, cols, batch, x, cols, 1, batch)
+    assert np.max(np.abs(c - y)) <= 1e-15 * max(1.0, np.max(np.abs(y)))
+
+
+def test_gemm_identity_transpose_broadcast_and_mismatch(ctx):    # GemmBatch.IdentityTimesB / TransposeA / BroadcastMatchesLoopOracle / DimensionMismatch
+    n, k, batch = 5, 3, 4
+    b = hdg.random_vector(n * k * batch, 7)
+    eye = np.eye(n).ravel()
+    assert np.array_equal(hdg.gemm_batch(ctx, eye, n, n, 1, b, n, k, batch), b)   # broadcast A = I
+    a = hdg.random_vector(n * k * batch, 8)                                         # A_b: n x k, used transposed
+    c = hdg.gemm_batch(ctx, a, n, k, batch, b, n, k, batch, transpose_a=True).reshape(batch, k, k)
+    A = a.reshape(batch, k, n)   # column-major n x k -> [b][col][row]
+    B = b.reshape(batch, k, n)
+    want = np.einsum("bir,bjr->bji", A, B)   # (A^T B)[i, j] stored [b][j][i]
+    assert np.max(np.abs(c - want)) <= 1e-14
+    with pytest.raises(hdg.DimensionMismatch):
+        hdg.gemm_batch(ctx, a, n, k, batch, b, n, k, batch)       # inner dimensions k vs n
+
+
+# ---- test_face_matrix.cpp ------------------------------------------------------------------------------------------
+def quad_case(ctx, k, n, case="poisson2d"):
+    disc = hdg.Discretization.structured(ctx, "quad", n=n, degree=k)
+    model = hdg.make_case_model(disc, case)
+    state = hdg.make_initial_state(disc, model)
+    ops = hdg.assemble_element_operators(disc, model, state)
+    K, rhs = hdg.assemble_global(disc, ops)
+    return disc, model, state, ops, K, rhs
+
+
+def test_gather_extended_scatter_transpose_counts_multiplicity(ctx):  # GatherExtended.ScatterTransposeCountsMultiplicity
+    disc, model, state, ops, K, rhs = quad_case(ctx, 1, 3)
+    mpf, nb = K.block_dim, K.nb
+    gathered = hdg.gather_extended(K, np.ones(K.n_dof)).reshape(K.nf, nb, mpf)
+    nbr = K.neighbor.reshape(K.nf, nb)
+    counts = np.zeros((K.nf, mpf))
+    for f in range(K.nf):
+        for s in range(nb):
+            if nbr[f, s] >= 0:
+                counts[nbr[f, s]] += gathered[f, s]
+    boundary = disc.table("face_to_elements").reshape(K.nf, 2)[:, 1] < 0
+    assert np.all(counts[boundary] == 4.0) and np.all(counts[~boundary] == 7.0)
+
+
+def test_assemble_global_structure_properties(ctx):              # AssembleGlobal.NeighborStructureSymmetric / PoissonTraceOperatorSymmetricDefinite / SelfBlocksInvertible
+    disc, model, state, ops, K, rhs = quad_case(ctx, 2, 3)
+    nbr = K.neighbor.reshape(K.nf, K.nb)
+    for f in range(K.nf):
+        assert nbr[f, 0] == f
+        for g in nbr[f, 1:]:
+            if g >= 0:
+                assert f in nbr[g]                                  # g lists f back
+    # symmetric and (after a sign flip) definite on the flux-continuity rows = interior faces; Dirichlet faces carry
+    # the one-sided constraint row uhat = u_D (test_face_matrix.cpp:87-121)
+    A = K.to_dense()
+    bd = K.block_dim
+    interior = np.flatnonzero(disc.table("face_to_elements").reshape(K.nf, 2)[:, 1] >= 0)
+    keep = (interior[:, None] * bd + np.arange(bd)[None, :]).ravel()
+    sub = -A[np.ix_(keep, keep)]
+    assert np.max(np.abs(sub - sub.T)) <= 1e-12 * max(1.0, np.max(np.abs(sub)))
+    np.linalg.cholesky(0.5 * (sub + sub.T))                         # raises if not positive definite
+    blocks = K.blocks.reshape(K.nf, K.nb, bd, bd)
+    assert all(abs(np.linalg.det(blocks[f, 0])) > 1e-12 for f in range(K.nf))
+
+
+def test_block_matvec_identity_self_blocks_and_linearity(ctx):   # BlockMatvec.IdentitySelfBlocks / Linear
+    disc, model, state, ops, K, rhs = quad_case(ctx, 1, 3)
+    bd, nb = K.block_dim, K.nb
+    blocks = np.zeros((K.nf, nb * bd, bd))
+    blocks[:, :bd, :] = np.eye(bd)
+    I = hdg.FaceBlockMatrix.from_host(ctx, 1, disc.pf, disc.n_lfe, K.nf, K.neighbor, blocks.ravel())
+    x = hdg.random_vector(K.n_dof, 4)
+    assert np.array_equal(hdg.block_matvec(I, x), x)
+    y = hdg.random_vector(K.n_dof, 5)
+    lhs = hdg.block_matvec(K, 2.0 * x - 3.0 * y)
+    rhs2 = 2.0 * hdg.block_matvec(K, x) - 3.0 * hdg.block_matvec(K, y)
+    assert np.max(np.abs(lhs - rhs2)) <= 1e-12 * max(1.0, np.max(np.abs(rhs2)))
+
+
+def test_reversed_face_gives_mirrored_coefficients(ctx):         # Orientation.ReversedFaceGivesMirroredCoefficients
+    from paper_2512_13619_b200 import partition as P
+    k, n = 2, 2
+    coords, ev = P.box_quad_mesh(n, n)
+    gm = P.global_mesh("quad", coords, ev, lo=(0, 0), hi=(1, 1))
+
+    def solve(flip):
+        lm = P.build_local_meshes(gm, np.zeros(gm.ne, dtype=np.int32))[0]
+        target = int(np.flatnonzero(lm.f2e[:, 1] >= 0)[0])
+        if flip:   # reverse the canonical direction of the first interior face: end vertices swapped, both sides' flags toggled
+            lm.fverts[target] = lm.fverts[target][::-1]
+            lm.forient[target] = 1 - lm.forient[target]
+        disc = P.make_discretization(ctx, lm, "quad", k)
+        model = hdg.make_case_model(disc, "poisson2d")
+        state = hdg.State(disc)
+        K, rhs = hdg.assemble_global(disc, hdg.assemble_element_operators(disc, model, state))
+        return np.linalg.solve(K.to_dense(), rhs).reshape(K.nf, -1), target
+    ub, target = solve(False)
+    uf, _ = solve(True)
+    for f in range(ub.shape[0]):
+        want = uf[f, ::-1] if f == target else uf[f]
+        assert np.max(np.abs(ub[f] - want)) <= 1e-11
+
+
+# ---- test_precond.cpp (structure / property tests) --------------------------------------------------------------------
+def test_build_asm_shared_face_diagonal_sums_and_one_element_exact_solve(ctx):  # BuildAsm.SharedFaceDiagonalSums / ApplyAsm.OneElementIsExactSolve
+    disc, model, state, ops, K, rhs = quad_case(ctx, 1, 1)           # one element: ASM block = K-bar, apply = exact solve
+    P1 = hdg.build_asm(ops, disc, K)
+    y = hdg.random_vector(K.n_dof, 9)
+    z = hdg.apply_asm(P1, y)
+    assert np.max(np.abs(K.to_dense() @ z - y)) <= 1e-10 * max(1.0, np.max(np.abs(y)))
+    # 2 x 2 mesh: the enriched diagonal sub-block of an interior face is the sum of both elements' sub-blocks = K_ff
+    disc, model, state, ops, K, rhs = quad_case(ctx, 1, 2)
+    P2 = hdg.build_asm(ops, disc, K)
+    nfl, pf = disc.nfl, disc.pf
+    pbar = np.linalg.inv(P2.get("asm_inv").reshape(disc.ne, nfl, nfl))   # [e][c][r] of the inverse's inverse
+    kbar = ops.get("kbar").reshape(disc.ne, nfl, nfl)
+    e2f = disc.table("element_to_face").reshape(disc.ne, -1)
+    f2e = disc.table("face_to_elements").reshape(disc.nf, 2)
+    fli = disc.table("face_local_index").reshape(disc.nf, 2)
+    for f in np.flatnonzero(f2e[:, 1] >= 0):
+        (e0, e1), (l0, l1) = f2e[f], fli[f]
+        s = kbar[e0, l0 * pf:(l0 + 1) * pf, l0 * pf:(l0 + 1) * pf] + kbar[e1, l1 * pf:(l1 + 1) * pf, l1 * pf:(l1 + 1) * pf]
+        for e, l in ((e0, l0), (e1, l1)):
+            assert np.max(np.abs(pbar[e, l * pf:(l + 1) * pf, l * pf:(l + 1) * pf] - s)) <= 1e-9 * max(1.0, np.max(np.abs(s)))
+    assert e2f.shape[1] == 4
+
+
+def test_preconditioner_applications_are_linear(ctx):            # ApplyPreconditioners.Linearity
+    disc, model, state, ops, K, rhs = quad_case(ctx, 2, 3, "burgers2d")
+    x, y = hdg.random_vector(K.n_dof, 31), hdg.random_vector(K.n_dof, 32)
+    for spec in (hdg.PrecondSpec("bj"), hdg.PrecondSpec("asm"), hdg.PrecondSpec("asm", poly_degree=4)):
+        Pc = hdg.build_preconditioner(spec, K, ops, disc)
+        lhs = Pc.apply(2.0 * x - 3.0 * y)
+        rhs2 = 2.0 * Pc.apply(x) - 3.0 * Pc.apply(y)
+        assert np.max(np.abs(lhs - rhs2)) <= 1e-10 * max(1.0, np.max(np.abs(rhs2)))
+
+
+def test_asm_needs_fewer_iterations_than_bj(ctx):                # PrecondEffectiveness.AsmNeedsFewerIterationsThanBj
+    disc, model, state, ops, K, rhs = quad_case(ctx, 2, 8, "burgers2d")
+    its = {}
+    for kind in ("bj", "asm"):
+        Pc = hdg.build_preconditioner(kind, K, ops, disc)
+        x, st = hdg.gmres_solve(K, Pc, rhs, cfg=hdg.GmresConfig(tol=1e-8))
+        assert st.converged
+        its[kind] = st.iters
+    assert its["asm"] < its["bj"]
