@@ -3,6 +3,8 @@
 // optional fused norm, scaling by a device-resident scalar, and the polynomial recurrence updates.
 // All reductions are two-stage with a fixed combination order => bit-reproducible run to run.
 // Roofline: HBM.  multi_dot / multi_axpy stream 8*n*(nvec+1) (+8n write) bytes.
+#include <cstdint>
+
 #include "kernels.cuh"
 
 namespace hdgb {
@@ -20,26 +22,53 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // Stage 1: partial[j * nblocks + blockIdx.x] = sum over this CTA's chunk of V_j .* w
+// VEC2: 128-bit loads (a thread owns pairs of consecutive entries; needs even n, even ldv and 16-byte aligned
+// pointers -- the launcher checks); otherwise 64-bit loads with the same chunking.
+template <bool VEC2>
 __global__ void __launch_bounds__(kDotThreads) multi_dot_partial_kernel(
     const double* __restrict__ V, int64_t ldv, int nvec, const double* __restrict__ w, int64_t n,
     double* __restrict__ partial, int nblocks) {
     extern __shared__ double red[];  // [nwarps][nvec]
     const int64_t base = static_cast<int64_t>(blockIdx.x) * kDotChunk;
     double wr[kDotPerThread];
-    int64_t idx[kDotPerThread];
+    int64_t idx[kDotPerThread];  // VEC2: idx[2 p] is the (even) index of pair p
 #pragma unroll
     for (int k = 0; k < kDotPerThread; ++k) {
-        idx[k] = base + k * kDotThreads + threadIdx.x;
-        wr[k] = idx[k] < n ? w[idx[k]] : 0.0;
-        if (idx[k] >= n) idx[k] = n - 1;  // safe address; contribution is multiplied by 0
+        if constexpr (VEC2) idx[k] = base + 2 * ((k >> 1) * kDotThreads + threadIdx.x) + (k & 1);
+        else idx[k] = base + k * kDotThreads + threadIdx.x;
+    }
+    if constexpr (VEC2) {
+#pragma unroll
+        for (int p = 0; p < kDotPerThread / 2; ++p) {
+            const bool in = idx[2 * p] < n;  // n even: the pair is inside or outside as a whole
+            if (!in) idx[2 * p] = n - 2;     // safe address; contribution is multiplied by 0
+            const double2 v = *reinterpret_cast<const double2*>(w + idx[2 * p]);
+            wr[2 * p] = in ? v.x : 0.0;
+            wr[2 * p + 1] = in ? v.y : 0.0;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kDotPerThread; ++k) {
+            wr[k] = idx[k] < n ? w[idx[k]] : 0.0;
+            if (idx[k] >= n) idx[k] = n - 1;  // safe address; contribution is multiplied by 0
+        }
     }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int nwarps = kDotThreads / 32;
     for (int j = 0; j < nvec; ++j) {
         const double* vj = V + static_cast<int64_t>(j) * ldv;
         double vals[kDotPerThread];
+        if constexpr (VEC2) {
 #pragma unroll
-        for (int k = 0; k < kDotPerThread; ++k) vals[k] = __ldg(vj + idx[k]);
+            for (int p = 0; p < kDotPerThread / 2; ++p) {
+                const double2 v = __ldg(reinterpret_cast<const double2*>(vj + idx[2 * p]));
+                vals[2 * p] = v.x;
+                vals[2 * p + 1] = v.y;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < kDotPerThread; ++k) vals[k] = __ldg(vj + idx[k]);
+        }
         double acc = 0.0;
 #pragma unroll
         for (int k = 0; k < kDotPerThread; ++k) acc = fma(vals[k], wr[k], acc);
@@ -76,7 +105,9 @@ __global__ void __launch_bounds__(128) reduce_partials_kernel(const double* __re
 constexpr int kAxpyThreads = 256;
 constexpr int kAxpyPerThread = 4;
 
-// w[i] += sign * sum_j c[j] V_j[i]; optional partial sums of w_new^2.
+// w[i] += sign * sum_j c[j] V_j[i]; optional partial sums of w_new^2.  VEC2: 128-bit loads / stores (even n, even ldv,
+// 16-byte aligned pointers).
+template <bool VEC2>
 __global__ void __launch_bounds__(kAxpyThreads) multi_axpy_kernel(
     const double* __restrict__ V, int64_t ldv, int nvec, const double* __restrict__ c, double sign,
     double* __restrict__ w, int64_t n, double* __restrict__ norm_partial) {
@@ -89,24 +120,60 @@ __global__ void __launch_bounds__(kAxpyThreads) multi_axpy_kernel(
     bool ok[kAxpyPerThread];
 #pragma unroll
     for (int k = 0; k < kAxpyPerThread; ++k) {
-        idx[k] = base + k * kAxpyThreads + threadIdx.x;
+        if constexpr (VEC2) idx[k] = base + 2 * ((k >> 1) * kAxpyThreads + threadIdx.x) + (k & 1);
+        else idx[k] = base + k * kAxpyThreads + threadIdx.x;
         ok[k] = idx[k] < n;
-        if (!ok[k]) idx[k] = n - 1;
-        acc[k] = w[idx[k]];
     }
-#pragma unroll 4
-    for (int j = 0; j < nvec; ++j) {
-        const double* vj = V + static_cast<int64_t>(j) * ldv;
-        const double cj = cs[j];
+    if constexpr (VEC2) {
 #pragma unroll
-        for (int k = 0; k < kAxpyPerThread; ++k) acc[k] = fma(cj, __ldg(vj + idx[k]), acc[k]);
+        for (int p = 0; p < kAxpyPerThread / 2; ++p) {
+            if (!ok[2 * p]) idx[2 * p] = n - 2;  // n even: pairs are inside or outside as a whole
+            const double2 v = *reinterpret_cast<const double2*>(w + idx[2 * p]);
+            acc[2 * p] = v.x;
+            acc[2 * p + 1] = v.y;
+        }
+#pragma unroll 4
+        for (int j = 0; j < nvec; ++j) {
+            const double* vj = V + static_cast<int64_t>(j) * ldv;
+            const double cj = cs[j];
+#pragma unroll
+            for (int p = 0; p < kAxpyPerThread / 2; ++p) {
+                const double2 v = __ldg(reinterpret_cast<const double2*>(vj + idx[2 * p]));
+                acc[2 * p] = fma(cj, v.x, acc[2 * p]);
+                acc[2 * p + 1] = fma(cj, v.y, acc[2 * p + 1]);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kAxpyPerThread; ++k) {
+            if (!ok[k]) idx[k] = n - 1;
+            acc[k] = w[idx[k]];
+        }
+#pragma unroll 4
+        for (int j = 0; j < nvec; ++j) {
+            const double* vj = V + static_cast<int64_t>(j) * ldv;
+            const double cj = cs[j];
+#pragma unroll
+            for (int k = 0; k < kAxpyPerThread; ++k) acc[k] = fma(cj, __ldg(vj + idx[k]), acc[k]);
+        }
     }
     double sq = 0.0;
+    if constexpr (VEC2) {
 #pragma unroll
-    for (int k = 0; k < kAxpyPerThread; ++k) {
-        if (ok[k]) {
-            w[idx[k]] = acc[k];
-            sq = fma(acc[k], acc[k], sq);
+        for (int p = 0; p < kAxpyPerThread / 2; ++p) {
+            if (ok[2 * p]) {
+                *reinterpret_cast<double2*>(w + idx[2 * p]) = make_double2(acc[2 * p], acc[2 * p + 1]);
+                sq = fma(acc[2 * p], acc[2 * p], sq);
+                sq = fma(acc[2 * p + 1], acc[2 * p + 1], sq);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kAxpyPerThread; ++k) {
+            if (ok[k]) {
+                w[idx[k]] = acc[k];
+                sq = fma(acc[k], acc[k], sq);
+            }
         }
     }
     if (norm_partial != nullptr) {
@@ -281,8 +348,11 @@ void launch_multi_dot(hdgb_ctx* ctx, const double* V, int64_t ldv, int nvec, con
     for (int j0 = 0; j0 < nvec; j0 += kGroup) {
         const int nv = nvec - j0 < kGroup ? nvec - j0 : kGroup;
         const size_t smem = static_cast<size_t>(kDotThreads / 32) * nv * sizeof(double);
-        multi_dot_partial_kernel<<<nblocks, kDotThreads, smem, ctx->stream>>>(V + static_cast<int64_t>(j0) * ldv, ldv, nv, w, n, partial,
-                                                                             nblocks);
+        const double* vg = V + static_cast<int64_t>(j0) * ldv;
+        // 128-bit loads when every row start is 16-byte aligned and entries pair up
+        const bool vec2 = n % 2 == 0 && ldv % 2 == 0 && n >= 2 && (reinterpret_cast<uintptr_t>(vg) | reinterpret_cast<uintptr_t>(w)) % 16 == 0;
+        if (vec2) multi_dot_partial_kernel<true><<<nblocks, kDotThreads, smem, ctx->stream>>>(vg, ldv, nv, w, n, partial, nblocks);
+        else multi_dot_partial_kernel<false><<<nblocks, kDotThreads, smem, ctx->stream>>>(vg, ldv, nv, w, n, partial, nblocks);
         HDGB_LAUNCH_CHECK(ctx);
         const bool last = j0 + nv == nvec;
         reduce_partials_kernel<<<nv, 128, 0, ctx->stream>>>(partial, nblocks, out + j0, (sqrt_last && last) ? nv - 1 : -1);
@@ -301,8 +371,10 @@ void launch_multi_axpy(hdgb_ctx* ctx, const double* V, int64_t ldv, int nvec, co
         const int nv = nvec - j0 < kGroup ? nvec - j0 : kGroup;
         const bool last = j0 + nv >= nvec;
         const size_t smem = (static_cast<size_t>(nv) + 8) * sizeof(double);
-        multi_axpy_kernel<<<nblocks, kAxpyThreads, smem, ctx->stream>>>(V + static_cast<int64_t>(j0) * ldv, ldv, nv, c + j0, sign, w, n,
-                                                                        (norm2_out && last) ? partial : nullptr);
+        const double* vg = V + static_cast<int64_t>(j0) * ldv;
+        const bool vec2 = n % 2 == 0 && ldv % 2 == 0 && n >= 2 && (reinterpret_cast<uintptr_t>(vg) | reinterpret_cast<uintptr_t>(w)) % 16 == 0;
+        if (vec2) multi_axpy_kernel<true><<<nblocks, kAxpyThreads, smem, ctx->stream>>>(vg, ldv, nv, c + j0, sign, w, n, (norm2_out && last) ? partial : nullptr);
+        else multi_axpy_kernel<false><<<nblocks, kAxpyThreads, smem, ctx->stream>>>(vg, ldv, nv, c + j0, sign, w, n, (norm2_out && last) ? partial : nullptr);
         HDGB_LAUNCH_CHECK(ctx);
         j0 += nv;
     } while (j0 < nvec);
