@@ -71,7 +71,7 @@ def test_config3_triangles_p4_burgers_polynomial_preconditioners(ctx):
     assert relerr(Pc.apply(y), oc.apply_precond(y)) < 1e-8
 
 
-@pytest.mark.parametrize("nr", [2, 4])
+@pytest.mark.parametrize("nr", [2, 4, 8])
 def test_config4_tets_p2_elasticity_asm_partitioned(ctx, nr):
     """configs[3]: 3D linear elasticity, tetrahedra, p = 2 (3-component blocks), additive Schwarz,
     partitioned across ranks -- must reproduce the single-domain run."""
@@ -109,11 +109,12 @@ def test_config4_tets_p2_elasticity_asm_partitioned(ctx, nr):
         assert np.max(np.abs(uh[: lm.nf_owned] - uh1[lm.faces[: lm.nf_owned]])) < 1e-7 * max(1.0, np.max(np.abs(uh1)))
 
 
-def test_config5_hex_navier_stokes_bj_partitioned(ctx):
+@pytest.mark.parametrize("dims,nr", [((2, 2, 2), 2), ((2, 2, 8), 8)])
+def test_config5_hex_navier_stokes_bj_partitioned(ctx, dims, nr):
     """configs[4]: 3D compressible Navier-Stokes, hex, 5-component blocks, Newton-GMRES with block-Jacobi,
-    one backward-Euler step, partitioned over 2 ranks vs single domain."""
+    one backward-Euler step, partitioned over 2 / 8 ranks (BASELINE: strong scaling 1/2/4/8) vs single domain."""
     lo, hi = (0, 0, 0), (1, 1, 1)
-    coords, ev = P.box_hex_mesh(2, 2, 2, lo, hi)
+    coords, ev = P.box_hex_mesh(*dims, lo, hi)
     gm = P.global_mesh("hex", coords, ev, lo=lo, hi=hi)
     pspec, gcfg, dt = hdg.PrecondSpec("bj"), hdg.GmresConfig(tol=1e-8), 0.02
     one = P.build_local_meshes(gm, np.zeros(gm.ne, dtype=np.int32))[0]
@@ -123,7 +124,7 @@ def test_config5_hex_navier_stokes_bj_partitioned(ctx):
     rep1 = hdg.newton_solve(disc, model, state, gcfg=gcfg, pspec=pspec, dt=dt, u_prev=state.u)
     assert rep1.converged
     uh1 = state.uhat.reshape(gm.nf, -1)
-    lms = P.build_local_meshes(gm, P.slab_partition(gm.ne, 2))
+    lms = P.build_local_meshes(gm, P.slab_partition(gm.ne, nr))
     lb = Loopback(lms)
 
     def work(r, c, lm):
