@@ -79,6 +79,31 @@ void finish_disc(hdgb_ctx* c, hdgb_disc* d, int n_comp) {
     v.phi = d->phi.p;
     for (int k = 0; k < 3; ++k) v.dphi[k] = d->dphi[k].p;
     v.psi = d->psi.p; v.tphi = d->tphi.p; v.wq = d->wq.p; v.wf = d->wf.p;
+    v.es_vol = nullptr;
+    v.es_face = nullptr;
+    if (me.pe == 64) {
+        // padded table images for the streamed E / D_d sweep of the local kernel (k_local.cu: ed_stream)
+        constexpr int kPts = 8, kLd = 68;
+        const int qe = static_cast<int>(me.elem_wts.size());
+        const int nsv = (qe + kPts - 1) / kPts, nt = 1 + m.dim;
+        std::vector<double> ev(static_cast<size_t>(nsv) * nt * kPts * kLd, 0.0);
+        for (int s = 0; s < nsv; ++s)
+            for (int k = 0; k < nt; ++k)
+                for (int p = 0; p < kPts; ++p) {
+                    const int g = std::min(s * kPts + p, qe - 1);
+                    const std::vector<double>& tab = k == 0 ? me.phi : me.dphi[k - 1];
+                    std::copy(tab.begin() + static_cast<size_t>(me.pe) * g, tab.begin() + static_cast<size_t>(me.pe) * (g + 1),
+                              ev.begin() + ((static_cast<size_t>(s) * nt + k) * kPts + p) * kLd);
+                }
+        const size_t rows = me.tphi.size() / me.pe;
+        std::vector<double> ef(rows * kLd, 0.0);
+        for (size_t r = 0; r < rows; ++r)
+            std::copy(me.tphi.begin() + r * me.pe, me.tphi.begin() + (r + 1) * me.pe, ef.begin() + r * kLd);
+        upload(c, d->es_vol, ev);
+        upload(c, d->es_face, ef);
+        v.es_vol = d->es_vol.p;
+        v.es_face = d->es_face.p;
+    }
     v.elem_detjac = d->elem_detjac.p; v.elem_invjac = d->elem_invjac.p; v.elem_coords = d->elem_coords.p;
     v.face_detjac = d->face_detjac.p; v.face_coords = d->face_coords.p; v.face_normal = d->face_normal.p;
 

@@ -27,6 +27,9 @@ struct DiscView {
     const double* dphi[3];   // pe x qe
     const double* psi;       // pf x qf
     const double* tphi;      // [((lf*n_orient+o)*qf + gc)*pe + i]
+    const double* es_vol;    // pe = 64 only (else null): ring-stage images of phi, dphi_r for the streamed E / D_d sweep,
+                             // [stage of 8 points][table][point][68]; points past qe repeat the last one
+    const double* es_face;   // pe = 64 only: tphi rows padded to 68 doubles, [((lf*n_orient+o)*qf + gc)*68 + i]
     const double* wq;        // qe
     const double* wf;        // qf
     const double* elem_detjac;
@@ -60,7 +63,7 @@ struct hdgb_disc {
     hdgb::HostGeom geom;
     // device tables
     hdgb::DevBuf<int> elem_faces, elem_side, face_elems, face_lidx, face_orient, bnd_tag;
-    hdgb::DevBuf<double> phi, dphi[3], psi, tphi, wq, wf;
+    hdgb::DevBuf<double> phi, dphi[3], psi, tphi, wq, wf, es_vol, es_face;
     hdgb::DevBuf<double> elem_detjac, elem_invjac, elem_coords, face_detjac, face_coords, face_normal;
     hdgb::DevBuf<double> mass, mass_inv, bmat[3], cmat[3], minv_b[3], minv_c[3];
     hdgb::DiscView view{};

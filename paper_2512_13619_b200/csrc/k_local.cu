@@ -12,6 +12,7 @@
 // Roofline: FP64 pipe; per-element traffic is one write of the raw blocks.
 #include "kernels_local.cuh"
 #include "models.cuh"
+#include "tma.cuh"
 
 namespace hdgb {
 
@@ -629,6 +630,166 @@ __device__ void ed_dmma(const DiscView& dv, const LocalIn& in, const LocalOut& o
     }
 }
 
+// ---- E and D_d of scalar systems with pe = 64: table ring + fragment-built operands ---------------------------
+// The chunked builder above spends its time in dependent latency: table loads from L2 -> FMAs -> shared-memory
+// stores -> CTA barrier -> fragment loads, once per 16 points.  For the hot shape (hex p = 3, M = 1)
+// the sweep is restructured so that no operand is ever built in shared memory and no CTA barrier is taken:
+//   * the basis tables of 8 points (phi, dphi_r rows of pe = 64 doubles, contiguous in global memory) are streamed by
+//     bulk-TMA row copies into a 3-stage shared-memory ring ([table][point][68]: k-major, leading dimension = 4 mod 16,
+//     conflict-free for both fragment loads); warp 0's lanes issue one row copy each, full / empty mbarriers per stage;
+//   * warp w owns the 8 rows i = 8 w .. 8 w + 7 of TWO of the 1 + D matrices over all 64 columns (16 accumulator
+//     tiles = the 128-register budget of two CTAs per SM); two sub-passes over the point list cover E, D_0 | D_1, D_2;
+//   * per k-step of 4 points a lane reads ITS (row, point) entry of the 1 + D tables, forms the left fragment
+//     a_w = -w_pt (c0_w phi + sum_r ck_w[r] dphi_r) of both resident matrices in registers from its point's
+//     record (4 distinct records per warp: broadcast loads) and multiplies with the raw phi rows as right operand.
+// Dead points of a partial stage copy a valid row (finite values) and get weight zero.  Same contraction as ed_dmma
+// with the quadrature weight on the left operand instead of the right one: equal to rounding.
+constexpr int kEsPts = 8;      // points per ring stage (two k-steps)
+constexpr int kEsStages = 3;
+constexpr int kEsLd = 68;      // 64 rows + 4
+constexpr int kEsPe = 64;
+inline __host__ __device__ size_t ed_stream_doubles(int D) { return static_cast<size_t>(kEsStages) * (1 + D) * kEsPts * kEsLd; }
+inline bool ed_stream_ok(const DiscView& dv, int M) { return M == 1 && dv.D == 3 && dv.pe == kEsPe && dv.es_vol && tuning().local_ed_stream; }
+
+template <int D>
+__device__ void ed_stream(const DiscView& dv, const LocalIn& in, const LocalOut& out, int e, const VolRec<1, D>* vrec,
+                          const FaceRec<1, D>* frec, const int* s_orient, double* ring, uint64_t* bars) {
+    constexpr int NQ = 2;                       // resident matrices per sub-pass
+    constexpr int NSP = (1 + D + NQ - 1) / NQ;  // sub-passes
+    constexpr int NCT = kEsPe / 8;              // column tiles
+    constexpr int stage_d = (1 + D) * kEsPts * kEsLd;
+        const int qe = dv.qe, qf = dv.qf, nfp = dv.n_lfe * qf;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int grp = lane >> 2, tig = lane & 3;
+    const int nsv = (qe + kEsPts - 1) / kEsPts, nsf = (nfp + kEsPts - 1) / kEsPts, nst = nsv + nsf;
+    const int total = NSP * nst;
+    uint64_t* full = bars;
+    uint64_t* empty = bars + kEsStages;
+    const double dtv = in.dt_inv > 0.0 ? in.dt_inv : 0.0;
+
+    // producer side (lane 0 of warp 0): stage s of a sub-pass into ring slot `slot`.  The padded stage images of the
+    // volume tables (DiscView::es_vol, one contiguous block per stage) and the padded trace-table rows (es_face)
+    // are prepared once per discretisation, so a stage is ONE bulk copy (volume) or one per local face it touches.
+    auto issue = [&](int s, int slot) {
+        if (lane != 0) return;
+        double* dst = ring + slot * stage_d;
+        if (s < nsv) {
+            mbar_expect_tx(full + slot, stage_d * sizeof(double));
+            tma_bulk_g2s(dst, dv.es_vol + static_cast<size_t>(s) * stage_d, stage_d * sizeof(double), full + slot);
+        } else {
+            constexpr uint32_t rb = kEsLd * sizeof(double);
+            mbar_expect_tx(full + slot, kEsPts * rb);
+            const int p0 = (s - nsv) * kEsPts;
+            int p = p0;
+            while (p < p0 + kEsPts) {
+                const int pc = min(p, nfp - 1);  // dead points of the last stage: the last row again (finite values)
+                const int lf = pc / qf, gc = pc - lf * qf;
+                const int run = p < nfp ? min(min(p0 + kEsPts, nfp), (lf + 1) * qf) - p : 1;
+                const double* src = dv.es_face + ((static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf + gc) * kEsLd;
+                tma_bulk_g2s(dst + (p - p0) * kEsLd, src, run * rb, full + slot);
+                p += run;
+            }
+        }
+    };
+    if (warp == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        for (int it = 0; it < kEsStages - 1 && it < total; ++it) issue(it % nst, it);
+    }
+
+    double acc[NQ][NCT][2];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+#pragma unroll
+        for (int b = 0; b < NCT; ++b) acc[q][b][0] = acc[q][b][1] = 0.0;
+
+    const int rowoff = 8 * warp + grp;  // this lane's row of the left fragments
+    int slot = 0, par = 0;              // ring slot and parity of the stage being consumed
+    int it = 0;
+#pragma unroll
+    for (int sp = 0; sp < NSP; ++sp) {
+        const int w0 = sp * NQ;  // resident matrices w0, w0 + 1 (0 = E, 1 + d = D_d)
+        for (int s = 0; s < nst; ++s, ++it) {
+            if (warp == 0) {
+                const int nx = it + kEsStages - 1;
+                if (nx < total) {
+                    int nslot = slot + kEsStages - 1;
+                    if (nslot >= kEsStages) nslot -= kEsStages;
+                    // the slot was last used by stage it - 1: wait until every warp released it
+                    if (it >= 1) mbar_wait(empty + nslot, ((it - 1) / kEsStages) & 1);
+                    issue(nx % nst, nslot);
+                }
+            }
+            mbar_wait(full + slot, par);
+            const double* St = ring + slot * stage_d;
+            const bool vol = s < nsv;
+            const int p0 = vol ? s * kEsPts : (s - nsv) * kEsPts;
+            const int npts = vol ? qe : nfp;
+#pragma unroll
+            for (int ks = 0; ks < kEsPts / 4; ++ks) {
+                const int p = 4 * ks + tig;
+                const bool live = p0 + p < npts;
+                const int pt = live ? p0 + p : npts - 1;
+                double a[NQ];
+                if (vol) {
+                    const VolRec<1, D>& r = vrec[pt];
+                    const double nw = live ? -r.w : 0.0;
+                    const double t0 = St[p * kEsLd + rowoff];
+                    double tk[D];
+#pragma unroll
+                    for (int k = 0; k < D; ++k) tk[k] = St[((1 + k) * kEsPts + p) * kEsLd + rowoff];
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q) {
+                        const int w = w0 + q;
+                        if (w > D) { a[q] = 0.0; continue; }
+                        double c0;
+                        const double* ck;
+                        if (w == 0) { c0 = r.dSu[0] - dtv; ck = r.cE; }
+                        else { c0 = r.dSq[w - 1]; ck = r.cD + (w - 1) * D; }
+                        double v = c0 * t0;
+#pragma unroll
+                        for (int k = 0; k < D; ++k) v = fma(ck[k], tk[k], v);
+                        a[q] = nw * v;
+                    }
+                } else {
+                    const FaceRec<1, D>& r = frec[pt];
+                    const double wq = live ? r.w : 0.0;
+                    const double t0 = wq * St[p * kEsLd + rowoff];
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q) {
+                        const int w = w0 + q;
+                        a[q] = w > D ? 0.0 : (w == 0 ? r.tau : r.dfh_q[w - 1]) * t0;
+                    }
+                }
+                const double* bs = St + p * kEsLd + grp;
+#pragma unroll
+                for (int b = 0; b < NCT; ++b) {
+                    const double bf = bs[8 * b];
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q)
+                        if (w0 + q <= D) dmma_8x8x4(acc[q][b][0], acc[q][b][1], a[q], bf);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + slot);
+            if (++slot == kEsStages) { slot = 0; par ^= 1; }
+        }
+        // ---- this sub-pass's blocks ----
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const int w = w0 + q;
+            if (w > D) continue;
+            double* dst = (w == 0 ? out.E : out.Dm[w - 1]) + static_cast<size_t>(e) * kEsPe * kEsPe + rowoff;
+#pragma unroll
+            for (int b = 0; b < NCT; ++b)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    dst[static_cast<size_t>(8 * b + 2 * tig + h) * kEsPe] = acc[q][b][h];
+                    acc[q][b][h] = 0.0;
+                }
+        }
+    }
+}
+
 // ---- H, G_d and F of scalar systems (M = 1) on the tensor-core path ------------------------------------------
 // Per local face lf (K = the qf face points):
 //   [H | G_0 .. G_{D-1}](lf b, j) = sum_gc psi_b(gc) * (c_w(gc) w_gc phis_j(gc)),  c_0 = dv_u, c_{1+dp} = dv_q[dp]
@@ -815,6 +976,16 @@ __global__ void __launch_bounds__(NT, RES ? (Model::M == 1 ? 4 : 2) : ((!GREC &&
         opbuf_base = sm + ((reinterpret_cast<const char*>(frec + (fp1 - fp0)) - reinterpret_cast<const char*>(sm) + 15) / 16) * 2;
     }
     __shared__ int s_face[8], s_side[8], s_orient[8], s_tag[8];
+    __shared__ uint64_t s_bars[2 * kEsStages];  // full / empty mbarriers of ed_stream's table ring
+    if constexpr (ED && M == 1 && D == 3 && !GREC && NT == 256) {
+        if (tid == 0) {
+            for (int i = 0; i < kEsStages; ++i) {
+                mbar_init(s_bars + i, 1);
+                mbar_init(s_bars + kEsStages + i, NT / 32);
+            }
+            mbar_fence_init();
+        }
+    }
 
     const Model model(mv);
     const bool transient = in.dt_inv > 0.0;
@@ -1042,11 +1213,19 @@ __global__ void __launch_bounds__(NT, RES ? (Model::M == 1 ? 4 : 2) : ((!GREC &&
     // forms the i-side values once and rank-1 updates the tile.  Component columns mp are swept one
     // at a time so that the accumulators (M (1 + D) per pair) stay in registers for wide systems ----
     const int dbg_skip = ed_dmma_on >> 4;  // measurement aid (hdgb_set_tuning "local_debug_skip"): 1 = E/D_d, 2 = H/G_d/F
-    ed_dmma_on &= 15;
+    const bool ed_streamed = ed_dmma_on & 8;  // launcher: pe = 64 scalar system, all points in this launch
+    ed_dmma_on &= 7;
     if (ED && ed_dmma_on && !(dbg_skip & 1)) {
         // operand chunks live behind the point records (16-byte aligned)
         double* opbuf = opbuf_base;
-        ed_dmma<M, D, GREC>(dv, in, out, e, vrec, frec, s_orient, opbuf, gv0, gv1, fp0, fp1, first);
+        bool streamed = false;
+        if constexpr (M == 1 && D == 3 && !GREC && NT == 256) {
+            if (ed_streamed) {  // table ring + fragment-built operands
+                ed_stream<D>(dv, in, out, e, vrec, frec, s_orient, opbuf, s_bars);
+                streamed = true;
+            }
+        }
+        if (!streamed) ed_dmma<M, D, GREC>(dv, in, out, e, vrec, frec, s_orient, opbuf, gv0, gv1, fp0, fp1, first);
     } else if (!(dbg_skip & 1)) {
         constexpr int TI = (M == 1) ? 2 : 1, TJ = (M == 1) ? 4 : 1;
         constexpr int Q = M * (1 + D);  // per row component m: E then D_0..D_{D-1}
@@ -1267,6 +1446,14 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
                     HDGB_LAUNCH_CHECK(ctx);
                     return;
                 }
+            }
+        }
+        if (ed && ed_stream_ok(dv, M)) {
+            const size_t es_bytes = std::max(ed_stream_doubles(D), hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D, M)) * sizeof(double) + 16;
+            if (all + es_bytes <= cap) {
+                kern_d<<<dv.ne, NTD, all + es_bytes, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2 | 8 | (tuning().local_debug_skip << 4), nullptr, 0);
+                HDGB_LAUNCH_CHECK(ctx);
+                return;
             }
         }
         if (ed) kern_d<<<dv.ne, NTD, all + ed_bytes, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2 | (tuning().local_debug_skip << 4), nullptr, 0);

@@ -131,6 +131,7 @@ def test_sixteen_warp_local_kernel_matches_eight_warp(ctx, shape, n, k, M, case)
     state.uhat = state.uhat + 0.05 * rng.standard_normal(state.uhat.shape)
     tkw = dict(dt=0.05, u_prev=state.u) if case == "navier_stokes" else {}
     out = {}
+    hdg.set_tuning("local_ed_stream", 0)   # both sides on the chunked operand builder (the streamed sweep is 8-warp only)
     for nt in (256, 512):
         hdg.set_tuning("local_nt", nt)
         try:
@@ -139,8 +140,42 @@ def test_sixteen_warp_local_kernel_matches_eight_warp(ctx, shape, n, k, M, case)
             out[nt] = {nm: ops.get(nm) for nm in names + ["kbar", "ru"]}
         finally:
             hdg.set_tuning("local_nt", 256)
+            hdg.set_tuning("local_ed_stream", 1)
     for nm in out[256]:
         if nm == "ru":   # the residual sweep is split over nt / pe thread groups: another (fixed) summation partition
             assert rel(out[512][nm], out[256][nm]) <= 1e-13, nm
         else:
             assert np.array_equal(out[512][nm], out[256][nm]), nm
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,n,case,transient", [("hex", 3, "poisson", False), ("hex", 2, "burgers", True),
+                                                    ("hex", 2, "reaction", True)])
+def test_streamed_ed_sweep_matches_chunked_builder(ctx, shape, n, case, transient):
+    """`local_ed_stream` (default on for scalar systems with 64 basis functions per element: hex p = 3): E and
+    D_d from the bulk-TMA table ring with fragment-built left operands against the chunked shared-memory operand
+    builder and against the scalar (no tensor core) sweep.  Same contraction, the quadrature weight on the other
+    operand: equal to rounding.  Jittered meshes, perturbed states, with and without the backward-Euler mass term."""
+    disc = hdg.Discretization.structured(ctx, shape, n=n, degree=3, jitter=0.15, seed=3)
+    assert disc.pe == 64
+    model = hdg.make_case_model(disc, case)
+    state = hdg.make_initial_state(disc, model)
+    rng = np.random.default_rng(11)
+    state.u = state.u + 0.1 * rng.standard_normal(state.u.shape)
+    state.uhat = state.uhat + 0.1 * rng.standard_normal(state.uhat.shape)
+    tkw = dict(dt=0.05, u_prev=state.u + 0.01) if transient else {}
+    names = ["e_raw"] + [f"d_raw{d}" for d in range(disc.dim)] + ["f_raw", "h_raw", "j_raw", "kbar", "ru"]
+    out = {}
+    for tag, stream, dmma in (("stream", 1, 1), ("chunked", 0, 1), ("scalar", 0, 0)):
+        hdg.set_tuning("local_ed_stream", stream)
+        hdg.set_tuning("use_dmma", dmma)
+        try:
+            ops = hdg.assemble_element_operators(disc, model, state, keep_raw=True, **tkw)
+            out[tag] = {nm: ops.get(nm) for nm in names}
+        finally:
+            hdg.set_tuning("local_ed_stream", 1)
+            hdg.set_tuning("use_dmma", 1)
+    for nm in names:
+        assert np.all(np.isfinite(out["stream"][nm])), nm
+        assert rel(out["stream"][nm], out["chunked"][nm]) <= 1e-13, nm
+        assert rel(out["stream"][nm], out["scalar"][nm]) <= 1e-12, nm
