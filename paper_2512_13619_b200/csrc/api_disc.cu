@@ -96,7 +96,7 @@ void finish_disc(hdgb_ctx* c, hdgb_disc* d, int n_comp) {
                               ev.begin() + ((static_cast<size_t>(s) * nt + k) * kPts + p) * kLd);
                 }
         const size_t rows = me.tphi.size() / me.pe;
-        std::vector<double> ef(rows * kLd, 0.0);
+        std::vector<double> ef((rows + 8) * kLd, 0.0);  // + 8 zero rows: a face stage copies up to 4 ceil(qf / 4) rows
         for (size_t r = 0; r < rows; ++r)
             std::copy(me.tphi.begin() + r * me.pe, me.tphi.begin() + (r + 1) * me.pe, ef.begin() + r * kLd);
         upload(c, d->es_vol, ev);

@@ -649,11 +649,11 @@ constexpr int kEsStages = 3;
 constexpr int kEsLd = 68;      // 64 rows + 4
 constexpr int kEsPe = 64;
 inline __host__ __device__ size_t ed_stream_doubles(int D) { return static_cast<size_t>(kEsStages) * (1 + D) * kEsPts * kEsLd; }
-inline bool ed_stream_ok(const DiscView& dv, int M) { return M == 1 && dv.D == 3 && dv.pe == kEsPe && dv.es_vol && tuning().local_ed_stream; }
+inline bool ed_stream_ok(const DiscView& dv, int M) { return M == 1 && dv.D == 3 && dv.pe == kEsPe && dv.es_vol && (tuning().local_ed_stream & 3); }
 
 template <int D>
 __device__ void ed_stream(const DiscView& dv, const LocalIn& in, const LocalOut& out, int e, const VolRec<1, D>* vrec,
-                          const FaceRec<1, D>* frec, const int* s_orient, double* ring, uint64_t* bars) {
+                          const FaceRec<1, D>* frec, const int* s_orient, double* ring, uint64_t* bars, bool do_ed, bool do_hgf) {
     constexpr int NQ = 2;                       // resident matrices per sub-pass
     constexpr int NSP = (1 + D + NQ - 1) / NQ;  // sub-passes
     constexpr int NCT = kEsPe / 8;              // column tiles
@@ -662,7 +662,9 @@ __device__ void ed_stream(const DiscView& dv, const LocalIn& in, const LocalOut&
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int grp = lane >> 2, tig = lane & 3;
     const int nsv = (qe + kEsPts - 1) / kEsPts, nsf = (nfp + kEsPts - 1) / kEsPts, nst = nsv + nsf;
-    const int total = NSP * nst;
+    const int n_ed = do_ed ? NSP * nst : 0;            // E / D_d stages, then one stage per local face (H, G_d, F, J)
+    const int hks = (qf + 3) / 4;                      // k-steps of a face stage
+    const int total = n_ed + (do_hgf ? dv.n_lfe : 0);
     uint64_t* full = bars;
     uint64_t* empty = bars + kEsStages;
     const double dtv = in.dt_inv > 0.0 ? in.dt_inv : 0.0;
@@ -670,9 +672,17 @@ __device__ void ed_stream(const DiscView& dv, const LocalIn& in, const LocalOut&
     // producer side (lane 0 of warp 0): stage s of a sub-pass into ring slot `slot`.  The padded stage images of the
     // volume tables (DiscView::es_vol, one contiguous block per stage) and the padded trace-table rows (es_face)
     // are prepared once per discretisation, so a stage is ONE bulk copy (volume) or one per local face it touches.
-    auto issue = [&](int s, int slot) {
+    auto issue = [&](int gi, int slot) {
         if (lane != 0) return;
         double* dst = ring + slot * stage_d;
+        if (gi >= n_ed) {  // face stage: all points of local face gi - n_ed (rows past qf: the table's next rows, weight zero)
+            const int lf = gi - n_ed;
+            const uint32_t bytes = 4 * hks * kEsLd * sizeof(double);
+            mbar_expect_tx(full + slot, bytes);
+            tma_bulk_g2s(dst, dv.es_face + (static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf * kEsLd, bytes, full + slot);
+            return;
+        }
+        const int s = gi % nst;
         if (s < nsv) {
             mbar_expect_tx(full + slot, stage_d * sizeof(double));
             tma_bulk_g2s(dst, dv.es_vol + static_cast<size_t>(s) * stage_d, stage_d * sizeof(double), full + slot);
@@ -691,9 +701,10 @@ __device__ void ed_stream(const DiscView& dv, const LocalIn& in, const LocalOut&
             }
         }
     };
+    __syncthreads();  // earlier users of the ring's shared memory (generic proxy) are done
     if (warp == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        for (int it = 0; it < kEsStages - 1 && it < total; ++it) issue(it % nst, it);
+        for (int it = 0; it < kEsStages - 1 && it < total; ++it) issue(it, it);
     }
 
     double acc[NQ][NCT][2];
@@ -705,20 +716,23 @@ __device__ void ed_stream(const DiscView& dv, const LocalIn& in, const LocalOut&
     const int rowoff = 8 * warp + grp;  // this lane's row of the left fragments
     int slot = 0, par = 0;              // ring slot and parity of the stage being consumed
     int it = 0;
+    // warp 0 keeps the ring kEsStages - 1 stages ahead of its own position
+    auto produce = [&]() {
+        if (warp != 0) return;
+        const int nx = it + kEsStages - 1;
+        if (nx < total) {
+            int nslot = slot + kEsStages - 1;
+            if (nslot >= kEsStages) nslot -= kEsStages;
+            // the slot was last used by stage it - 1: wait until every warp released it
+            if (it >= 1) mbar_wait(empty + nslot, ((it - 1) / kEsStages) & 1);
+            issue(nx, nslot);
+        }
+    };
 #pragma unroll
-    for (int sp = 0; sp < NSP; ++sp) {
+    for (int sp = 0; sp < (do_ed ? NSP : 0); ++sp) {
         const int w0 = sp * NQ;  // resident matrices w0, w0 + 1 (0 = E, 1 + d = D_d)
         for (int s = 0; s < nst; ++s, ++it) {
-            if (warp == 0) {
-                const int nx = it + kEsStages - 1;
-                if (nx < total) {
-                    int nslot = slot + kEsStages - 1;
-                    if (nslot >= kEsStages) nslot -= kEsStages;
-                    // the slot was last used by stage it - 1: wait until every warp released it
-                    if (it >= 1) mbar_wait(empty + nslot, ((it - 1) / kEsStages) & 1);
-                    issue(nx % nst, nslot);
-                }
-            }
+            produce();
             mbar_wait(full + slot, par);
             const double* St = ring + slot * stage_d;
             const bool vol = s < nsv;
@@ -769,8 +783,7 @@ __device__ void ed_stream(const DiscView& dv, const LocalIn& in, const LocalOut&
                         if (w0 + q <= D) dmma_8x8x4(acc[q][b][0], acc[q][b][1], a[q], bf);
                 }
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(empty + slot);
+            ring_release(empty + slot, lane);
             if (++slot == kEsStages) { slot = 0; par ^= 1; }
         }
         // ---- this sub-pass's blocks ----
@@ -786,6 +799,91 @@ __device__ void ed_stream(const DiscView& dv, const LocalIn& in, const LocalOut&
                     dst[static_cast<size_t>(8 * b + 2 * tig + h) * kEsPe] = acc[q][b][h];
                     acc[q][b][h] = 0.0;
                 }
+        }
+    }
+    if (!do_hgf) return;
+    // ---- H, G_d, F and J, one ring stage per local face (local_ops.cpp:186-219) ----
+    //   [H | G_d](lf b, j) = sum_gc psi_b(gc) (cw(gc) phis_j(gc)),   F(i, lf bp) = sum_gc phis_i(gc) (cf(gc) psi_bp(gc)),
+    //   J(lf b, lf bp)     = sum_gc psi_b(gc) (cj(gc) psi_bp(gc)).
+    // psi (pf = 16 rows, the same for every face and element) lives in registers: lane (grp, tig) holds psi_{8 t + grp}(4 ks + tig),
+    // which is both the left fragment of H / G_d / J and the right fragment of F / J.  The warp owns columns j (rows i)
+    // 8 w .. 8 w + 7: ONE shared-memory load per k-step serves all products; coefficients come from the face records.
+    constexpr int KS = 8;  // k-steps of a face stage (qf <= 32), RT = 2 row tiles of psi (pf = 16)
+    const int pf = dv.pf, nfl = dv.n_lfe * pf;
+    double psr[2][KS];
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+            const int gc = 4 * ks + tig, b = 8 * t + grp;
+            psr[t][ks] = (gc < qf && b < pf) ? __ldg(dv.psi + b + pf * gc) : 0.0;
+        }
+    for (int lf = 0; lf < dv.n_lfe; ++lf, ++it) {
+        produce();
+        mbar_wait(full + slot, par);
+        const double* St = ring + slot * stage_d + rowoff;
+        const FaceRec<1, D>* fr = frec + lf * qf;
+        const bool jw = warp == lf;  // J of this face: one warp
+        double hg[1 + D][2][2], fa[2][2], ja[2][2][2];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+#pragma unroll
+            for (int w = 0; w <= D; ++w) hg[w][t][0] = hg[w][t][1] = 0.0;
+            fa[t][0] = fa[t][1] = 0.0;
+            ja[t][0][0] = ja[t][0][1] = ja[t][1][0] = ja[t][1][1] = 0.0;
+        }
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+            if (ks >= hks) break;
+            const int gc = 4 * ks + tig;
+            const bool live = gc < qf;
+            const FaceRec<1, D>& r = fr[live ? gc : qf - 1];
+            const double wg = live ? r.w : 0.0;
+            const double ph = St[gc * kEsLd];
+#pragma unroll
+            for (int w = 0; w <= D; ++w) {
+                const double b = (wg * (w == 0 ? r.dv_u[0] : r.dv_q[w - 1])) * ph;
+#pragma unroll
+                for (int t = 0; t < 2; ++t) dmma_8x8x4(hg[w][t][0], hg[w][t][1], psr[t][ks], b);
+            }
+            const double cf = wg * r.dfh_uh[0];
+#pragma unroll
+            for (int t = 0; t < 2; ++t) dmma_8x8x4(fa[t][0], fa[t][1], ph, psr[t][ks] * cf);
+            if (jw) {
+                const double cj = wg * r.dv_uh[0];
+#pragma unroll
+                for (int t = 0; t < 2; ++t)
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) dmma_8x8x4(ja[t][c][0], ja[t][c][1], psr[t][ks], psr[c][ks] * cj);
+            }
+        }
+            ring_release(empty + slot, lane);
+            if (++slot == kEsStages) { slot = 0; par ^= 1; }
+        // ---- this face's blocks ----
+        const int j0 = 8 * warp + 2 * tig;
+#pragma unroll
+        for (int w = 0; w <= D; ++w) {
+            double* dst = (w == 0 ? out.H : out.G[w - 1]) + static_cast<size_t>(e) * nfl * kEsPe + lf * pf + grp;
+#pragma unroll
+            for (int t = 0; t < 2; ++t)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) dst[static_cast<size_t>(j0 + h) * nfl + 8 * t] = hg[w][t][h];
+        }
+        {
+            double* dst = out.F + static_cast<size_t>(e) * kEsPe * nfl + rowoff;
+#pragma unroll
+            for (int t = 0; t < 2; ++t)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) dst[static_cast<size_t>(lf * pf + 8 * t + 2 * tig + h) * kEsPe] = fa[t][h];
+        }
+        if (jw) {
+            double* dst = out.J + static_cast<size_t>(e) * nfl * nfl + lf * pf + grp;
+#pragma unroll
+            for (int t = 0; t < 2; ++t)
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) dst[static_cast<size_t>(lf * pf + 8 * c + 2 * tig + h) * nfl + 8 * t] = ja[t][c][h];
         }
     }
 }
@@ -1212,20 +1310,33 @@ __global__ void __launch_bounds__(NT, RES ? (Model::M == 1 ? 4 : 2) : ((!GREC &&
     // ---- phase 2b: E and D_d.  A thread owns a TI x TJ tile of scalar-basis pairs (i, j); per point it
     // forms the i-side values once and rank-1 updates the tile.  Component columns mp are swept one
     // at a time so that the accumulators (M (1 + D) per pair) stay in registers for wide systems ----
-    const int dbg_skip = ed_dmma_on >> 4;  // measurement aid (hdgb_set_tuning "local_debug_skip"): 1 = E/D_d, 2 = H/G_d/F
-    const bool ed_streamed = ed_dmma_on & 8;  // launcher: pe = 64 scalar system, all points in this launch
+    int dbg_skip = (ed_dmma_on >> 4) & 7;  // measurement aid (hdgb_set_tuning "local_debug_skip"): 1 = E/D_d, 2 = H/G_d/F
+    // launcher: pe = 64 scalar system, all points in this launch; bit 3: E / D_d streamed, bit 7: H / G_d / F / J streamed
+    const bool ed_streamed = ed_dmma_on & 8, hgf_streamed = ed_dmma_on & 128;
     ed_dmma_on &= 7;
+    bool hgf_done = false, j_done = false;
+    if constexpr (ED && M == 1 && D == 3 && !GREC && NT == 256) {
+        if (ed_streamed || hgf_streamed) {
+            // table ring + fragment-built operands: E, D_d, then H, G_d, F, J -- one barrier-free pipeline.  J's entries
+            // outside the per-face diagonal blocks are zero.
+            const bool hs = hgf_streamed && ed_dmma_on == 2 && pf == 16 && qf <= 32 && 4 * ((qf + 3) / 4) <= (1 + D) * kEsPts;
+            if (hs && !(dbg_skip & 2)) {
+                for (int t = tid; t < nfl * nfl; t += nt) {
+                    const int c = t / nfl, r = t - c * nfl;
+                    if (c / pf != r / pf) out.J[static_cast<size_t>(e) * nfl * nfl + t] = 0.0;
+                }
+            }
+            if (!ed_streamed && !(dbg_skip & 1))
+                ed_dmma<M, D, GREC>(dv, in, out, e, vrec, frec, s_orient, opbuf_base, gv0, gv1, fp0, fp1, first);
+            ed_stream<D>(dv, in, out, e, vrec, frec, s_orient, opbuf_base, s_bars, ed_streamed && !(dbg_skip & 1), hs && !(dbg_skip & 2));
+            if (hs) hgf_done = j_done = true;
+            dbg_skip |= 1;
+        }
+    }
     if (ED && ed_dmma_on && !(dbg_skip & 1)) {
         // operand chunks live behind the point records (16-byte aligned)
         double* opbuf = opbuf_base;
-        bool streamed = false;
-        if constexpr (M == 1 && D == 3 && !GREC && NT == 256) {
-            if (ed_streamed) {  // table ring + fragment-built operands
-                ed_stream<D>(dv, in, out, e, vrec, frec, s_orient, opbuf, s_bars);
-                streamed = true;
-            }
-        }
-        if (!streamed) ed_dmma<M, D, GREC>(dv, in, out, e, vrec, frec, s_orient, opbuf, gv0, gv1, fp0, fp1, first);
+        ed_dmma<M, D, GREC>(dv, in, out, e, vrec, frec, s_orient, opbuf, gv0, gv1, fp0, fp1, first);
     } else if (!(dbg_skip & 1)) {
         constexpr int TI = (M == 1) ? 2 : 1, TJ = (M == 1) ? 4 : 1;
         constexpr int Q = M * (1 + D);  // per row component m: E then D_0..D_{D-1}
@@ -1322,9 +1433,9 @@ __global__ void __launch_bounds__(NT, RES ? (Model::M == 1 ? 4 : 2) : ((!GREC &&
             }
         }
     }
-    bool hgf_done = false;
     if constexpr (ED) {
-        if (ed_dmma_on == 2 && (dbg_skip & 2)) hgf_done = true;
+        if (hgf_done) {
+        } else if (ed_dmma_on == 2 && (dbg_skip & 2)) hgf_done = true;
         else if (ed_dmma_on == 2) {  // all face points in this launch, every output entry written exactly once
             double* opbuf = opbuf_base;
             hgf_dmma<M, D, GREC>(dv, out, e, frec, s_orient, opbuf);
@@ -1384,6 +1495,7 @@ __global__ void __launch_bounds__(NT, RES ? (Model::M == 1 ? 4 : 2) : ((!GREC &&
     }
     // ---- J: block diagonal over local faces; rows (lf, m, b), columns (lf, mp, bp); the other
     // entries of the nfl x nfl block are zero ----
+    if (j_done) return;
     if (first)
         for (int t = tid; t < nfl * nfl; t += nt) out.J[static_cast<size_t>(e) * nfl * nfl + t] = 0.0;
     __syncthreads();
@@ -1451,7 +1563,7 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
         if (ed && ed_stream_ok(dv, M)) {
             const size_t es_bytes = std::max(ed_stream_doubles(D), hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D, M)) * sizeof(double) + 16;
             if (all + es_bytes <= cap) {
-                kern_d<<<dv.ne, NTD, all + es_bytes, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2 | 8 | (tuning().local_debug_skip << 4), nullptr, 0);
+                kern_d<<<dv.ne, NTD, all + es_bytes, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2 | ((tuning().local_ed_stream & 1) ? 8 : 0) | ((tuning().local_ed_stream & 2) ? 128 : 0) | ((tuning().local_debug_skip & 7) << 4), nullptr, 0);
                 HDGB_LAUNCH_CHECK(ctx);
                 return;
             }

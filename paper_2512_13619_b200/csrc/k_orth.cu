@@ -169,8 +169,7 @@ __global__ void __launch_bounds__(kThreads, 1) cgs_pass_kernel(OrthArgs a) {
                 }
                 if constexpr (kUpdate) consumer_sync();  // wsm is rewritten by the next tile's update
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(empty + s);  // this warp is done with stage s
+            ring_release(empty + s, lane);  // this warp is done with stage s (reads completed: see tma.cuh)
         }
         // ---- per-CTA partials ----
         const int grid = gridDim.x;

@@ -140,9 +140,9 @@ __global__ void __launch_bounds__(kMaxThreads, 1) stream_gemv_kernel(GemvArgs g,
             elems = cnt * item_elems;
         }
         const uint32_t bytes = static_cast<uint32_t>(elems * sizeof(double));
-        // The stage is re-armed by lane 0 after __syncwarp(): every lane's reads of it have returned
-        // (their values fed FMAs).  Write-after-read across proxies needs no proxy fence -- the same
-        // ordering TMA producer/consumer pipelines rely on when a consumer releases a stage.
+        // The stage is re-armed by lane 0 after a cross-proxy fence + __syncwarp() (the call sites): every lane's reads
+        // of it have completed.  That FMAs consumed the loaded values is NOT enough -- ptxas may schedule the copy
+        // behind the ISSUE of the last loads and ahead of their consumers (tma.cuh: ring_release).
         mbar_expect_tx(my_full + s, bytes);
         if (bytes) tma_bulk_g2s(my_stage + static_cast<size_t>(s) * p.stage_elems, src, bytes, my_full + s);
     };
@@ -296,6 +296,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) stream_gemv_kernel(GemvArgs g,
                 const int nc = min(p.cpc, cols - c0);
                 mbar_wait(my_full + rs, rph);
                 accumulate<V, RT>(my_stage + static_cast<size_t>(rs) * p.stage_elems, xs + c0, rows, nc, rl, cg, CG, acc);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
                 if (lane == 0 && n + SW < my_chunks) issue(n + SW, rs);
                 if (++rs == SW) { rs = 0; rph ^= 1u; }
@@ -373,6 +374,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) stream_gemv_kernel(GemvArgs g,
                     reduce_store(acc, item0 + it);
                 }
             }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0 && n + SW < my_chunks) issue(n + SW, rs);
             if (++rs == SW) { rs = 0; rph ^= 1u; }

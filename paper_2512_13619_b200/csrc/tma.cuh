@@ -16,6 +16,17 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Consumer release of a TMA ring stage.  The stage's shared-memory reads must have COMPLETED before the arrive becomes
+// visible to the producer, whose refill writes the stage through the async proxy.  An instruction that merely consumes
+// the loaded registers (FMA, mma.sync) does not pin that order: ptxas is free to schedule the arrive ahead of those
+// consumers, right behind the ISSUE of the loads (seen in SASS: SYNCS.ARRIVE between the last LDS batch and its DMMAs),
+// and a refill from L2 can then land while loads are still queued -- observed as one corrupted 8 x 8 tile in ~3e5
+// elements.  The cross-proxy fence orders this thread's prior generic-proxy accesses before later async-proxy writes.
+__device__ __forceinline__ void ring_release(uint64_t* empty_bar, int lane) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty_bar);
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n"

@@ -112,3 +112,30 @@ def test_full_size_solve(ctx, cid):
     # idempotence: the solution is a fixed point of the solver
     rep2 = hdg.newton_solve(disc, model, state, pspec=pspec, **tkw)
     assert rep2.converged and rep2.n_newton == 0 and rep2.n_gmres_total == 0
+
+
+def test_full_size_assembly_bitwise_reproducible(ctx):
+    """Config 2 at full size, repeated: the condensed operators and the Newton / GMRES trace must not depend on timing.
+    (The local kernel's TMA table ring once released a stage while shared-memory loads of it were still queued --
+    tma.cuh: ring_release -- which corrupted one 8 x 8 tile in ~3e5 elements, only at this scale: 21 952 CTAs, two per SM.)"""
+    import hashlib
+    cfg = FULL[2]
+    disc, model, state = setup(ctx, cfg)
+    rng = np.random.default_rng(1)
+    state.u = state.u + 0.1 * rng.standard_normal(state.u.shape)
+    state.uhat = state.uhat + 0.1 * rng.standard_normal(state.uhat.shape)
+    digests = set()
+    for _ in range(16):
+        ops = hdg.assemble_element_operators(disc, model, state)
+        digests.add(hashlib.sha1(ops.get("kbar").tobytes()).hexdigest())
+        del ops
+    assert len(digests) == 1
+    disc, model, state = setup(ctx, cfg)
+    u0, uh0 = state.u, state.uhat
+    traces = set()
+    for _ in range(3):
+        state.set("u", u0)
+        state.set("uhat", uh0)
+        rep = hdg.newton_solve(disc, model, state, hdg.NewtonConfig(), hdg.GmresConfig(), hdg.PrecondSpec(cfg["precond"]))
+        traces.add((rep.n_gmres_total, tuple(rep.residual_history)))
+    assert len(traces) == 1
