@@ -36,6 +36,7 @@ int hdgb_set_tuning(const char* key, int64_t value) {
     if (k == "fused_cgs") { hdgb::tuning().fused_cgs = static_cast<int>(value); return 0; }
     if (k == "local_debug_skip") { hdgb::tuning().local_debug_skip = static_cast<int>(value); return 0; }
     if (k == "local_nt") { hdgb::tuning().local_nt = static_cast<int>(value); return 0; }
+    if (k == "local_nt_wide") { hdgb::tuning().local_nt_wide = static_cast<int>(value); return 0; }
     if (k == "local_ed_stream") { hdgb::tuning().local_ed_stream = static_cast<int>(value); return 0; }
     if (k == "local_dmma_min_pe") { hdgb::tuning().local_dmma_min_pe = static_cast<int>(value); return 0; }
     if (k == "local_global_records") { hdgb::tuning().local_global_records = static_cast<int>(value); return 0; }

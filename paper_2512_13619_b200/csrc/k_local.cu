@@ -888,6 +888,204 @@ __device__ void ed_stream(const DiscView& dv, const LocalIn& in, const LocalOut&
     }
 }
 
+// ---- E and D_d of WIDE systems (M > 1, pe = 64: hex p = 3) through the same table ring ------------------------------
+// One component pair (m, mp) per sweep of the point list, all 1 + D blocks of the pair resident (warp w: rows 8 w ..
+// 8 w + 7 of four 64 x 64 blocks = 32 accumulator tiles; one CTA per SM, 255 registers).  The table ring keeps flowing
+// across the M^2 sweeps.  The pair's coefficient rows -- 4 (1 + D) values per volume point, 1 + D per face point, scattered
+// over the point records in the global (L2) scratch -- are gathered into a shared-memory table [point][18] by all
+// threads, double-buffered: the loads of pair n + 1 are issued before the sweep of pair n and stored after it, so one
+// CTA barrier per pair is the only synchronisation besides the ring's mbarriers.
+constexpr int kEwLd = 18;  // coefficient row: 16 values + the weight + 1 (rows 144 bytes apart: 16-byte aligned, conflict-free 128-bit loads)
+inline __host__ __device__ size_t ed_wide_doubles(int D, int qe, int nfp) {
+    return ed_stream_doubles(D) + 2 * static_cast<size_t>(qe + nfp) * kEwLd;
+}
+
+template <int M, int D, int NW>
+__device__ void ed_stream_wide(const DiscView& dv, const LocalIn& in, const LocalOut& out, int e, const VolRec<M, D>* vrec,
+                               const FaceRec<M, D>* frec, const int* s_orient, double* ring, uint64_t* bars) {
+    static_assert(D == 3, "coefficient rows are laid out for 1 + D = 4 blocks");
+    constexpr int NQ = 1 + D;
+    constexpr int NH = NW / 8;           // column parts: 8 warps own all 64 columns of their rows, 16 warps half of them
+    constexpr int NCT = kEsPe / 8 / NH;  // column tiles per warp
+    constexpr int stage_d = (1 + D) * kEsPts * kEsLd;
+    constexpr int NPAIR = M * M;
+    constexpr int NCV = 4 * NQ + 1;  // table entries per volume point and pair: 4 (1 + D) coefficients + the quadrature weight
+    constexpr int NCF = NQ + 1;      // per face point: 1 + D coefficients + the weight
+    const int qe = dv.qe, qf = dv.qf, nfp = dv.n_lfe * qf, npe = M * kEsPe;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    const int grp = lane >> 2, tig = lane & 3;
+    const int nsv = (qe + kEsPts - 1) / kEsPts, nsf = (nfp + kEsPts - 1) / kEsPts, nst = nsv + nsf;
+    const int total = NPAIR * nst;
+    const int npt = qe + nfp;
+    uint64_t* full = bars;
+    uint64_t* empty = bars + kEsStages;
+    const double dtv = in.dt_inv > 0.0 ? in.dt_inv : 0.0;
+    double* cb = ring + kEsStages * stage_d;  // [2][npt][kEwLd]
+
+    auto issue = [&](int gi, int slot) {
+        if (lane != 0) return;
+        double* dst = ring + slot * stage_d;
+        const int s = gi % nst;
+        if (s < nsv) {
+            mbar_expect_tx(full + slot, stage_d * sizeof(double));
+            tma_bulk_g2s(dst, dv.es_vol + static_cast<size_t>(s) * stage_d, stage_d * sizeof(double), full + slot);
+        } else {
+            constexpr uint32_t rb = kEsLd * sizeof(double);
+            mbar_expect_tx(full + slot, kEsPts * rb);
+            const int p0 = (s - nsv) * kEsPts;
+            int p = p0;
+            while (p < p0 + kEsPts) {
+                const int pc = min(p, nfp - 1);
+                const int lf = pc / qf, gc = pc - lf * qf;
+                const int run = p < nfp ? min(min(p0 + kEsPts, nfp), (lf + 1) * qf) - p : 1;
+                const double* src = dv.es_face + ((static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf + gc) * kEsLd;
+                tma_bulk_g2s(dst + (p - p0) * kEsLd, src, run * rb, full + slot);
+                p += run;
+            }
+        }
+    };
+    // coefficient gather of pair pr: this thread's items (item = (point, coefficient index)); loads first, stores later
+    constexpr int kItems = 12 / NH;  // (8 warps) ceil((125 * 17 + 150 * 5) / 256) for the default rule; more points: extra trips
+    const int nitem = qe * NCV + nfp * NCF;
+    auto coef_ptr = [&](int pr, int item) -> const double* {
+        const int mp = pr / M, m = pr - mp * M, mm = m * M + mp;
+        if (item < qe * NCV) {
+            const int pt = item / NCV, c = item - pt * NCV, w = c >> 2, k = c & 3;
+            const VolRec<M, D>& r = vrec[pt];
+            if (c == NCV - 1) return &r.w;
+            if (w == 0) return k == 0 ? &r.dSu[mm] : &r.cE[mm * D + k - 1];
+            return k == 0 ? &r.dSq[mm * D + w - 1] : &r.cD[((w - 1) * M * M + mm) * D + k - 1];
+        }
+        const int f = item - qe * NCV, pt = f / NCF, w = f - pt * NCF;
+        const FaceRec<M, D>& r = frec[pt];
+        if (w == NQ) return &r.w;
+        return w == 0 ? &r.tau : &r.dfh_q[mm * D + w - 1];
+    };
+    auto coef_slot = [&](int item) -> int {
+        if (item < qe * NCV) { const int pt = item / NCV; return pt * kEwLd + (item - pt * NCV); }
+        const int f = item - qe * NCV, pt = f / NCF;
+        return (qe + pt) * kEwLd + (f - pt * NCF);
+    };
+    auto gather_direct = [&](int pr, double* dstb) {  // first pair, and the tail items beyond kItems trips
+        for (int item = tid; item < nitem; item += nt) dstb[coef_slot(item)] = __ldcg(coef_ptr(pr, item));
+    };
+
+    __syncthreads();  // earlier users of this shared memory (generic proxy) are done
+    if (warp == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        for (int it = 0; it < kEsStages - 1 && it < total; ++it) issue(it, it);
+    }
+    gather_direct(0, cb);
+    __syncthreads();
+
+    const int rowoff = 8 * (warp & 7) + grp;
+    const int col0 = (warp >> 3) * NCT * 8;  // first column of this warp's tiles
+    int slot = 0, par = 0, it = 0;
+    auto produce = [&]() {
+        if (warp != 0) return;
+        const int nx = it + kEsStages - 1;
+        if (nx < total) {
+            int nslot = slot + kEsStages - 1;
+            if (nslot >= kEsStages) nslot -= kEsStages;
+            if (it >= 1) mbar_wait(empty + nslot, ((it - 1) / kEsStages) & 1);
+            issue(nx, nslot);
+        }
+    };
+    for (int pr = 0; pr < NPAIR; ++pr) {
+        const int mp = pr / M, m = pr - mp * M;
+        const double* cbp = cb + static_cast<size_t>(pr & 1) * npt * kEwLd;
+        double* cbn = cb + static_cast<size_t>((pr + 1) & 1) * npt * kEwLd;
+        const double dte = (m == mp) ? dtv : 0.0;
+        // next pair's coefficients: loads in flight during this pair's sweep
+        double cst[kItems];
+        const bool more = pr + 1 < NPAIR;
+#pragma unroll
+        for (int j = 0; j < kItems; ++j) {
+            const int item = tid + j * nt;
+            cst[j] = (more && item < nitem) ? __ldcg(coef_ptr(pr + 1, item)) : 0.0;
+        }
+        double acc[NQ][NCT][2];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+#pragma unroll
+            for (int b = 0; b < NCT; ++b) acc[q][b][0] = acc[q][b][1] = 0.0;
+        for (int s = 0; s < nst; ++s, ++it) {
+            produce();
+            mbar_wait(full + slot, par);
+            const double* St = ring + slot * stage_d;
+            const bool vol = s < nsv;
+            const int p0 = vol ? s * kEsPts : (s - nsv) * kEsPts;
+            const int npts = vol ? qe : nfp;
+            // left fragments of both k-steps first (their loads and FMA chains overlap), then the products
+            double a[kEsPts / 4][NQ];
+#pragma unroll
+            for (int ks = 0; ks < kEsPts / 4; ++ks) {
+                const int p = 4 * ks + tig;
+                const bool live = p0 + p < npts;
+                const int pt = live ? p0 + p : npts - 1;
+                if (vol) {
+                    const double2* cr = reinterpret_cast<const double2*>(cbp + pt * kEwLd);
+                    const double nw = live ? -cbp[pt * kEwLd + NCV - 1] : 0.0;
+                    const double t0 = St[p * kEsLd + rowoff];
+                    double tk[D];
+#pragma unroll
+                    for (int k = 0; k < D; ++k) tk[k] = St[((1 + k) * kEsPts + p) * kEsLd + rowoff];
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q) {
+                        const double2 c01 = cr[2 * q], c23 = cr[2 * q + 1];
+                        double v = (q == 0 ? c01.x - dte : c01.x) * t0;
+                        v = fma(c01.y, tk[0], v);
+                        v = fma(c23.x, tk[1], v);
+                        v = fma(c23.y, tk[2], v);
+                        a[ks][q] = nw * v;
+                    }
+                } else {
+                    const double2* cr = reinterpret_cast<const double2*>(cbp + (qe + pt) * kEwLd);
+                    const double wq = live ? cbp[(qe + pt) * kEwLd + NQ] : 0.0;
+                    const double t0 = wq * St[p * kEsLd + rowoff];
+                    const double2 c01 = cr[0], c23 = cr[1];
+                    a[ks][0] = (m == mp ? c01.x : 0.0) * t0;
+                    a[ks][1] = c01.y * t0;
+                    a[ks][2] = c23.x * t0;
+                    a[ks][3] = c23.y * t0;
+                }
+            }
+#pragma unroll
+            for (int ks = 0; ks < kEsPts / 4; ++ks) {
+                const double* bs = St + (4 * ks + tig) * kEsLd + col0 + grp;
+#pragma unroll
+                for (int b = 0; b < NCT; ++b) {
+                    const double bf = bs[8 * b];
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q) dmma_8x8x4(acc[q][b][0], acc[q][b][1], a[ks][q], bf);
+                }
+            }
+            ring_release(empty + slot, lane);
+            if (++slot == kEsStages) { slot = 0; par ^= 1; }
+        }
+        // ---- this pair's blocks: rows (m, i), columns (mp, j) ----
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            double* dst = (q == 0 ? out.E : out.Dm[q - 1]) + static_cast<size_t>(e) * npe * npe +
+                          static_cast<size_t>(mp * kEsPe) * npe + m * kEsPe + rowoff;
+#pragma unroll
+            for (int b = 0; b < NCT; ++b)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) dst[static_cast<size_t>(col0 + 8 * b + 2 * tig + h) * npe] = acc[q][b][h];
+        }
+        // next pair's coefficient table (the other buffer: its last readers passed the previous barrier)
+        if (more) {
+#pragma unroll
+            for (int j = 0; j < kItems; ++j) {
+                const int item = tid + j * nt;
+                if (item < nitem) cbn[coef_slot(item)] = cst[j];
+            }
+            for (int item = tid + kItems * nt; item < nitem; item += nt) cbn[coef_slot(item)] = __ldcg(coef_ptr(pr + 1, item));
+        }
+        __syncthreads();
+    }
+}
+
 // ---- H, G_d and F of scalar systems (M = 1) on the tensor-core path ------------------------------------------
 // Per local face lf (K = the qf face points):
 //   [H | G_0 .. G_{D-1}](lf b, j) = sum_gc psi_b(gc) * (c_w(gc) w_gc phis_j(gc)),  c_0 = dv_u, c_{1+dp} = dv_q[dp]
@@ -1075,7 +1273,7 @@ __global__ void __launch_bounds__(NT, RES ? (Model::M == 1 ? 4 : 2) : ((!GREC &&
     }
     __shared__ int s_face[8], s_side[8], s_orient[8], s_tag[8];
     __shared__ uint64_t s_bars[2 * kEsStages];  // full / empty mbarriers of ed_stream's table ring
-    if constexpr (ED && M == 1 && D == 3 && !GREC && NT == 256) {
+    if constexpr (ED && D == 3 && ((NT == 256 && (M == 1) != GREC) || (NT == 512 && M > 1 && GREC))) {
         if (tid == 0) {
             for (int i = 0; i < kEsStages; ++i) {
                 mbar_init(s_bars + i, 1);
@@ -1333,6 +1531,12 @@ __global__ void __launch_bounds__(NT, RES ? (Model::M == 1 ? 4 : 2) : ((!GREC &&
             dbg_skip |= 1;
         }
     }
+    if constexpr (ED && GREC && M > 1 && D == 3 && (NT == 256 || NT == 512)) {
+        if (ed_streamed && !(dbg_skip & 1)) {  // wide system, pe = 64: one streamed sweep per component pair
+            ed_stream_wide<M, D, NT / 32>(dv, in, out, e, vrec, frec, s_orient, opbuf_base, s_bars);
+            dbg_skip |= 1;
+        }
+    }
     if (ED && ed_dmma_on && !(dbg_skip & 1)) {
         // operand chunks live behind the point records (16-byte aligned)
         double* opbuf = opbuf_base;
@@ -1582,6 +1786,18 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
             const EdPlan p16 = ed_plan(dv.pe, M, D, 16);
             const size_t edb16 = std::max(2 * p16.doubles(D), hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D, M)) * sizeof(double) + 32;
             if constexpr (D == 3) {
+                const bool wide_stream = dv.pe == kEsPe && dv.es_vol && (tuning().local_ed_stream & 1);
+                const size_t edw16 = std::max(ed_wide_doubles(D, dv.qe, nfp), hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D, M)) * sizeof(double) + 32;
+                // streamed sweep with 16 warps (each warp half the columns): measured slower than 8 warps (config 5 at 12^3: 32.8 vs 31.4 ms -- the
+                // left fragments are formed twice), kept behind local_nt_wide = 512
+                if (wide_stream && tuning().local_nt_wide == 512 && fixed + edw16 <= cap) {
+                    auto kern_gw = local_assemble_kernel<Model, 512, true, true>;
+                    ensure_dynamic_smem(kern_gw, cap);
+                    DevBuf<char> scratch(rec_stride * static_cast<size_t>(dv.ne));
+                    kern_gw<<<dv.ne, 512, fixed + edw16, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2 | 8 | ((tuning().local_debug_skip & 7) << 4), scratch.p, rec_stride);
+                    HDGB_LAUNCH_CHECK(ctx);
+                    return;
+                }
                 if (tuning().local_nt == 512 && p16.wsub <= 8 && fixed + edb16 <= cap) {
                     auto kern_gw = local_assemble_kernel<Model, 512, true, true>;
                     ensure_dynamic_smem(kern_gw, cap);
@@ -1591,12 +1807,17 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
                     return;
                 }
             }
-            const size_t edb = std::max(2 * ed_plan(dv.pe, M, D, 8).doubles(D), hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D, M)) * sizeof(double) + 32;
+            size_t edb = std::max(2 * ed_plan(dv.pe, M, D, 8).doubles(D), hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D, M)) * sizeof(double) + 32;
+            int stream_flag = 0;
+            if (D == 3 && dv.pe == kEsPe && dv.es_vol && (tuning().local_ed_stream & 1)) {
+                const size_t edw = std::max(ed_wide_doubles(D, dv.qe, nfp), hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D, M)) * sizeof(double) + 32;
+                if (fixed + edw <= cap) { edb = edw; stream_flag = 8; }
+            }
             if (fixed + edb <= cap) {
                 auto kern_g = local_assemble_kernel<Model, 256, true, true>;
                 ensure_dynamic_smem(kern_g, cap);
                 DevBuf<char> scratch(rec_stride * static_cast<size_t>(dv.ne));
-                kern_g<<<dv.ne, 256, fixed + edb, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2 | (tuning().local_debug_skip << 4), scratch.p, rec_stride);
+                kern_g<<<dv.ne, 256, fixed + edb, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2 | stream_flag | ((tuning().local_debug_skip & 7) << 4), scratch.p, rec_stride);
                 HDGB_LAUNCH_CHECK(ctx);
                 return;
             }

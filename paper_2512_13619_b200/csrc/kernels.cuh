@@ -46,6 +46,7 @@ struct Tuning {
     int local_nt = 256;                  // threads of the tensor-core local kernel: 256 = two 8-warp CTAs per SM (default); 512 = one 16-warp CTA, all
                                          // 1 + D matrices (scalar) / two component pairs (wide) per point sweep -- measured slower at config 2
                                          // (35.6 vs 33.2 ms per assembly) and equal at config 5 (0.250 vs 0.252 s at hex 16^3)
+    int local_nt_wide = 256;             // threads of the streamed local kernel of wide systems (M > 1, pe = 64): 512 = 16 warps, 256 = 8 warps
     int local_ed_stream = 3;             // scalar systems with 64 basis functions per element: E / D_d from a bulk-TMA table ring with fragment-built operands (no operand build phase, no CTA barrier in the point sweep)
     int local_dmma_min_pe = 20;          // local blocks on the tensor-core path from this many basis functions per element
     int local_global_records = 1;        // wide systems: point records in an L2-resident scratch, one launch, E / D_d on DMMA

@@ -12,6 +12,8 @@ else:
     model = hdg.make_case_model(disc, "poisson")
 state = hdg.make_initial_state(disc, model)
 kw = dict(dt=0.01, u_prev=state.u) if cfgn == 5 else {}
+if len(sys.argv) > 2:
+    hdg.set_tuning("local_nt_wide", int(sys.argv[2]))
 for skip in (0, 1, 2, 3):
     hdg.set_tuning("local_debug_skip", skip)
     ops = hdg.assemble_element_operators(disc, model, state, **kw)

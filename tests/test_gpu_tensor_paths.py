@@ -131,16 +131,16 @@ def test_sixteen_warp_local_kernel_matches_eight_warp(ctx, shape, n, k, M, case)
     state.uhat = state.uhat + 0.05 * rng.standard_normal(state.uhat.shape)
     tkw = dict(dt=0.05, u_prev=state.u) if case == "navier_stokes" else {}
     out = {}
-    hdg.set_tuning("local_ed_stream", 0)   # both sides on the chunked operand builder (the streamed sweep is 8-warp only)
-    for nt in (256, 512):
-        hdg.set_tuning("local_nt", nt)
-        try:
+    try:
+        hdg.set_tuning("local_ed_stream", 0)   # both sides on the chunked operand builder
+        for nt in (256, 512):
+            hdg.set_tuning("local_nt", nt)
             ops = hdg.assemble_element_operators(disc, model, state, keep_raw=True, **tkw)
             names = ["e_raw", "f_raw", "h_raw", "j_raw"] + [f"d_raw{d}" for d in range(disc.dim)] + [f"g_raw{d}" for d in range(disc.dim)]
             out[nt] = {nm: ops.get(nm) for nm in names + ["kbar", "ru"]}
-        finally:
-            hdg.set_tuning("local_nt", 256)
-            hdg.set_tuning("local_ed_stream", 1)
+    finally:
+        hdg.set_tuning("local_nt", 256)
+        hdg.set_tuning("local_ed_stream", 3)
     for nm in out[256]:
         if nm == "ru":   # the residual sweep is split over nt / pe thread groups: another (fixed) summation partition
             assert rel(out[512][nm], out[256][nm]) <= 1e-13, nm
@@ -166,14 +166,47 @@ def test_streamed_ed_sweep_matches_chunked_builder(ctx, shape, n, case, transien
     tkw = dict(dt=0.05, u_prev=state.u + 0.01) if transient else {}
     names = ["e_raw"] + [f"d_raw{d}" for d in range(disc.dim)] + ["f_raw", "h_raw", "j_raw", "kbar", "ru"]
     out = {}
-    for tag, stream, dmma in (("stream", 1, 1), ("chunked", 0, 1), ("scalar", 0, 0)):
+    for tag, stream, dmma in (("stream", 3, 1), ("chunked", 0, 1), ("scalar", 0, 0)):
         hdg.set_tuning("local_ed_stream", stream)
         hdg.set_tuning("use_dmma", dmma)
         try:
             ops = hdg.assemble_element_operators(disc, model, state, keep_raw=True, **tkw)
             out[tag] = {nm: ops.get(nm) for nm in names}
         finally:
-            hdg.set_tuning("local_ed_stream", 1)
+            hdg.set_tuning("local_ed_stream", 3)
+            hdg.set_tuning("use_dmma", 1)
+    for nm in names:
+        assert np.all(np.isfinite(out["stream"][nm])), nm
+        assert rel(out["stream"][nm], out["chunked"][nm]) <= 1e-13, nm
+        assert rel(out["stream"][nm], out["scalar"][nm]) <= 1e-12, nm
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case,M,nt", [("navier_stokes", 5, 512), ("navier_stokes", 5, 256), ("elasticity", 3, 512)])
+def test_streamed_wide_sweep_matches_chunked_builder(ctx, case, M, nt):
+    """Wide systems on hexahedra of degree 3 (config 5's shape): E / D_d one streamed sweep per component pair (table
+    ring, coefficient rows gathered into shared memory, 16 or 8 warps) against the chunked operand builder and the
+    scalar sweep; backward-Euler mass term on the diagonal pairs."""
+    disc = hdg.Discretization.structured(ctx, "hex", n=2, degree=3, n_comp=M, jitter=0.1, seed=4)
+    kw = {"mu": 0.02} if case == "navier_stokes" else {}
+    model = hdg.make_case_model(disc, case, **kw)
+    state = hdg.make_initial_state(disc, model)
+    rng = np.random.default_rng(12)
+    state.u = state.u + 0.02 * rng.standard_normal(state.u.shape)
+    state.uhat = state.uhat + 0.02 * rng.standard_normal(state.uhat.shape)
+    tkw = dict(dt=0.05, u_prev=state.u + 0.01)
+    names = ["e_raw"] + [f"d_raw{d}" for d in range(3)] + ["f_raw", "h_raw", "j_raw", "kbar", "ru"]
+    out = {}
+    for tag, stream, dmma in (("stream", 3, 1), ("chunked", 0, 1), ("scalar", 0, 0)):
+        hdg.set_tuning("local_ed_stream", stream)
+        hdg.set_tuning("local_nt_wide", nt)
+        hdg.set_tuning("use_dmma", dmma)
+        try:
+            ops = hdg.assemble_element_operators(disc, model, state, keep_raw=True, **tkw)
+            out[tag] = {nm: ops.get(nm) for nm in names}
+        finally:
+            hdg.set_tuning("local_ed_stream", 3)
+            hdg.set_tuning("local_nt_wide", 256)
             hdg.set_tuning("use_dmma", 1)
     for nm in names:
         assert np.all(np.isfinite(out["stream"][nm])), nm
