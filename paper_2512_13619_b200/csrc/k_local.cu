@@ -653,7 +653,7 @@ inline bool ed_stream_ok(const DiscView& dv, int M) { return M == 1 && dv.D == 3
 
 template <int D>
 __device__ void ed_stream(const DiscView& dv, const LocalIn& in, const LocalOut& out, int e, const VolRec<1, D>* vrec,
-                          const FaceRec<1, D>* frec, const int* s_orient, double* ring, uint64_t* bars, bool do_ed, bool do_hgf) {
+                          const FaceRec<1, D>* frec, const int* s_orient, double* ring, uint64_t* bars, bool do_ed, bool do_hgf, bool split_copies) {
     constexpr int NQ = 2;                       // resident matrices per sub-pass
     constexpr int NSP = (1 + D + NQ - 1) / NQ;  // sub-passes
     constexpr int NCT = kEsPe / 8;              // column tiles
@@ -679,13 +679,23 @@ __device__ void ed_stream(const DiscView& dv, const LocalIn& in, const LocalOut&
             const int lf = gi - n_ed;
             const uint32_t bytes = 4 * hks * kEsLd * sizeof(double);
             mbar_expect_tx(full + slot, bytes);
-            tma_bulk_g2s(dst, dv.es_face + (static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf * kEsLd, bytes, full + slot);
+            const double* src = dv.es_face + (static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf * kEsLd;
+            if (split_copies) {  // (measurement / sanitizer aid: copies of 4 rows)
+                for (int r = 0; r < 4 * hks; r += 4) tma_bulk_g2s(dst + r * kEsLd, src + r * kEsLd, 4 * kEsLd * sizeof(double), full + slot);
+            } else {
+                tma_bulk_g2s(dst, src, bytes, full + slot);
+            }
             return;
         }
         const int s = gi % nst;
         if (s < nsv) {
             mbar_expect_tx(full + slot, stage_d * sizeof(double));
-            tma_bulk_g2s(dst, dv.es_vol + static_cast<size_t>(s) * stage_d, stage_d * sizeof(double), full + slot);
+            const double* src = dv.es_vol + static_cast<size_t>(s) * stage_d;
+            if (split_copies) {
+                for (int r = 0; r < (1 + D) * kEsPts; r += 4) tma_bulk_g2s(dst + r * kEsLd, src + r * kEsLd, 4 * kEsLd * sizeof(double), full + slot);
+            } else {
+                tma_bulk_g2s(dst, src, stage_d * sizeof(double), full + slot);
+            }
         } else {
             constexpr uint32_t rb = kEsLd * sizeof(double);
             mbar_expect_tx(full + slot, kEsPts * rb);
@@ -783,7 +793,7 @@ __device__ void ed_stream(const DiscView& dv, const LocalIn& in, const LocalOut&
                         if (w0 + q <= D) dmma_8x8x4(acc[q][b][0], acc[q][b][1], a[q], bf);
                 }
             }
-            ring_release(empty + slot, lane);
+            ring_release_all(empty + slot);
             if (++slot == kEsStages) { slot = 0; par ^= 1; }
         }
         // ---- this sub-pass's blocks ----
@@ -857,7 +867,7 @@ __device__ void ed_stream(const DiscView& dv, const LocalIn& in, const LocalOut&
                     for (int c = 0; c < 2; ++c) dmma_8x8x4(ja[t][c][0], ja[t][c][1], psr[t][ks], psr[c][ks] * cj);
             }
         }
-            ring_release(empty + slot, lane);
+            ring_release_all(empty + slot);
             if (++slot == kEsStages) { slot = 0; par ^= 1; }
         // ---- this face's blocks ----
         const int j0 = 8 * warp + 2 * tig;
@@ -1060,7 +1070,7 @@ __device__ void ed_stream_wide(const DiscView& dv, const LocalIn& in, const Loca
                     for (int q = 0; q < NQ; ++q) dmma_8x8x4(acc[q][b][0], acc[q][b][1], a[ks][q], bf);
                 }
             }
-            ring_release(empty + slot, lane);
+            ring_release_all(empty + slot);
             if (++slot == kEsStages) { slot = 0; par ^= 1; }
         }
         // ---- this pair's blocks: rows (m, i), columns (mp, j) ----
@@ -1277,7 +1287,7 @@ __global__ void __launch_bounds__(NT, RES ? (Model::M == 1 ? 4 : 2) : ((!GREC &&
         if (tid == 0) {
             for (int i = 0; i < kEsStages; ++i) {
                 mbar_init(s_bars + i, 1);
-                mbar_init(s_bars + kEsStages + i, NT / 32);
+                mbar_init(s_bars + kEsStages + i, NT);  // every thread releases a stage for itself (tma.cuh: ring_release_all)
             }
             mbar_fence_init();
         }
@@ -1510,7 +1520,7 @@ __global__ void __launch_bounds__(NT, RES ? (Model::M == 1 ? 4 : 2) : ((!GREC &&
     // at a time so that the accumulators (M (1 + D) per pair) stay in registers for wide systems ----
     int dbg_skip = (ed_dmma_on >> 4) & 7;  // measurement aid (hdgb_set_tuning "local_debug_skip"): 1 = E/D_d, 2 = H/G_d/F
     // launcher: pe = 64 scalar system, all points in this launch; bit 3: E / D_d streamed, bit 7: H / G_d / F / J streamed
-    const bool ed_streamed = ed_dmma_on & 8, hgf_streamed = ed_dmma_on & 128;
+    const bool ed_streamed = ed_dmma_on & 8, hgf_streamed = ed_dmma_on & 128, split_copies = ed_dmma_on & 256;
     ed_dmma_on &= 7;
     bool hgf_done = false, j_done = false;
     if constexpr (ED && M == 1 && D == 3 && !GREC && NT == 256) {
@@ -1526,7 +1536,7 @@ __global__ void __launch_bounds__(NT, RES ? (Model::M == 1 ? 4 : 2) : ((!GREC &&
             }
             if (!ed_streamed && !(dbg_skip & 1))
                 ed_dmma<M, D, GREC>(dv, in, out, e, vrec, frec, s_orient, opbuf_base, gv0, gv1, fp0, fp1, first);
-            ed_stream<D>(dv, in, out, e, vrec, frec, s_orient, opbuf_base, s_bars, ed_streamed && !(dbg_skip & 1), hs && !(dbg_skip & 2));
+            ed_stream<D>(dv, in, out, e, vrec, frec, s_orient, opbuf_base, s_bars, ed_streamed && !(dbg_skip & 1), hs && !(dbg_skip & 2), split_copies);
             if (hs) hgf_done = j_done = true;
             dbg_skip |= 1;
         }
@@ -1767,7 +1777,7 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
         if (ed && ed_stream_ok(dv, M)) {
             const size_t es_bytes = std::max(ed_stream_doubles(D), hgf_plan(dv.pe, dv.pf, dv.qf).doubles(D, M)) * sizeof(double) + 16;
             if (all + es_bytes <= cap) {
-                kern_d<<<dv.ne, NTD, all + es_bytes, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2 | ((tuning().local_ed_stream & 1) ? 8 : 0) | ((tuning().local_ed_stream & 2) ? 128 : 0) | ((tuning().local_debug_skip & 7) << 4), nullptr, 0);
+                kern_d<<<dv.ne, NTD, all + es_bytes, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2 | ((tuning().local_ed_stream & 1) ? 8 : 0) | ((tuning().local_ed_stream & 2) ? 128 : 0) | ((tuning().local_ed_stream & 4) ? 256 : 0) | ((tuning().local_debug_skip & 7) << 4), nullptr, 0);
                 HDGB_LAUNCH_CHECK(ctx);
                 return;
             }

@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(kThreads, 1) cgs_pass_kernel(OrthArgs a) {
     if (tid == 0) {
         for (int s = 0; s < a.stages; ++s) {
             mbar_init(full + s, 1);
-            mbar_init(empty + s, kWarps);
+            mbar_init(empty + s, kWarps * 32);  // every consumer thread releases a stage for itself (tma.cuh)
         }
         mbar_fence_init();
     }
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(kThreads, 1) cgs_pass_kernel(OrthArgs a) {
                 }
                 if constexpr (kUpdate) consumer_sync();  // wsm is rewritten by the next tile's update
             }
-            ring_release(empty + s, lane);  // this warp is done with stage s (reads completed: see tma.cuh)
+            ring_release_all(empty + s);  // this thread is done with stage s (reads completed: see tma.cuh)
         }
         // ---- per-CTA partials ----
         const int grid = gridDim.x;

@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) stream_gemv_kernel(GemvArgs g,
         const uint32_t bytes = static_cast<uint32_t>(elems * sizeof(double));
         // The stage is re-armed by lane 0 after a cross-proxy fence + __syncwarp() (the call sites): every lane's reads
         // of it have completed.  That FMAs consumed the loaded values is NOT enough -- ptxas may schedule the copy
-        // behind the ISSUE of the last loads and ahead of their consumers (tma.cuh: ring_release).
+        // behind the ISSUE of the last loads and ahead of their consumers (tma.cuh: ring_release_all).
         mbar_expect_tx(my_full + s, bytes);
         if (bytes) tma_bulk_g2s(my_stage + static_cast<size_t>(s) * p.stage_elems, src, bytes, my_full + s);
     };

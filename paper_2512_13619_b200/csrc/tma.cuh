@@ -22,10 +22,13 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // consumers, right behind the ISSUE of the loads (seen in SASS: SYNCS.ARRIVE between the last LDS batch and its DMMAs),
 // and a refill from L2 can then land while loads are still queued -- observed as one corrupted 8 x 8 tile in ~3e5
 // elements.  The cross-proxy fence orders this thread's prior generic-proxy accesses before later async-proxy writes.
-__device__ __forceinline__ void ring_release(uint64_t* empty_bar, int lane) {
+// Every reading thread releases for itself (the empty barrier counts threads, not warps): no reliance on __syncwarp()
+// to extend lane 0's release to the other lanes' reads -- compute-sanitizer's racecheck does not accept that extension
+// (it reported the lanes 1..31 of every consumer warp against the refill), costs nothing measurable, and is the form
+// racecheck verifies clean.
+__device__ __forceinline__ void ring_release_all(uint64_t* empty_bar) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty_bar);
+    mbar_arrive(empty_bar);
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(

@@ -33,6 +33,18 @@ model = hdg.make_case_model(disc, "poisson")
 ops = hdg.assemble_element_operators(disc, model, hdg.make_initial_state(disc, model))
 hdg.set_tuning("local_nt", 256)
 print("16-warp local kernel ok")
+# the chunked shared-memory operand builder (the streamed table-ring pipeline is the default for hex p = 3) and the 16-warp streamed sweep of wide systems
+for stream, ntw in ((0, 256), (1, 256), (2, 256), (3, 512)):
+    hdg.set_tuning("local_ed_stream", stream)
+    hdg.set_tuning("local_nt_wide", ntw)
+    for case, ncomp in (("poisson", 1), ("navier_stokes", 5)):
+        disc = hdg.Discretization.structured(ctx, "hex", n=2, degree=3, n_comp=ncomp)
+        model = hdg.make_case_model(disc, case, **({"mu": 0.02} if case == "navier_stokes" else {}))
+        st = hdg.make_initial_state(disc, model)
+        ops = hdg.assemble_element_operators(disc, model, st, **(dict(dt=0.05, u_prev=st.u) if ncomp > 1 else {}))
+hdg.set_tuning("local_ed_stream", 3)
+hdg.set_tuning("local_nt_wide", 256)
+print("local kernel variants ok")
 # the streamed CGS2 passes on a basis long enough for the TMA path
 n, nvec = 1 << 16, 6
 V, _ = np.linalg.qr(hdg.random_vector(n * nvec, 1).reshape(n, nvec))

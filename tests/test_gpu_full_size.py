@@ -117,7 +117,7 @@ def test_full_size_solve(ctx, cid):
 def test_full_size_assembly_bitwise_reproducible(ctx):
     """Config 2 at full size, repeated: the condensed operators and the Newton / GMRES trace must not depend on timing.
     (The local kernel's TMA table ring once released a stage while shared-memory loads of it were still queued --
-    tma.cuh: ring_release -- which corrupted one 8 x 8 tile in ~3e5 elements, only at this scale: 21 952 CTAs, two per SM.)"""
+    tma.cuh: ring_release_all -- which corrupted one 8 x 8 tile in ~3e5 elements, only at this scale: 21 952 CTAs, two per SM.)"""
     import hashlib
     cfg = FULL[2]
     disc, model, state = setup(ctx, cfg)
