@@ -45,7 +45,7 @@ __global__ void gj_prepare_kernel(int n, const double* __restrict__ a, double* _
     for (int64_t t = threadIdx.x; t < nn; t += blockDim.x) {
         const double v = A[t];
         m = fmax(m, fabs(v));  // fmax drops NaNs like the reference's std::max scan
-        if (X != A) X[t] = v;
+        if (x0 && X != A) X[t] = v;
     }
     __shared__ double red[32];
 #pragma unroll
@@ -251,7 +251,10 @@ template <int RT>
 __global__ void __launch_bounds__(128) gj_panel_reg_kernel(int n, int j0, int64_t batch, const double* __restrict__ old,
                                                            double* __restrict__ nw, const double* __restrict__ amax,
                                                            int* __restrict__ piv, int* __restrict__ src, int* flags,
-                                                           int64_t b_base) {
+                                                           int64_t b_base, int* __restrict__ dstmap, int* __restrict__ cmscratch) {
+    // dstmap != nullptr: LAST panel -- all pivots are known after it, so lane 0 also forms the final column permutation
+    // (column j of the work matrix is column dstmap[j] of the inverse), this kernel writes its panel columns straight to
+    // their final places in nw (= the destination) and the last update does the same: no separate permutation pass.
     __shared__ double s_scr[4][2][NB];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t b = static_cast<int64_t>(blockIdx.x) * 4 + warp;
@@ -341,6 +344,40 @@ __global__ void __launch_bounds__(128) gj_panel_reg_kernel(int n, int j0, int64_
         }
     }
     if (bad && lane == 0) atomicMin(flags, static_cast<int>(b_base + b));
+    if (dstmap) {
+        int* dm = dstmap + b * n;
+        // cmap = identity pushed through the interchanges in reverse order; dm[cmap[j]] = j
+        __shared__ int s_cm[4][128], s_pv[4][128];
+        for (int j = lane; j < n; j += 32) {
+            s_cm[warp][j] = j;
+            s_pv[warp][j] = piv[b * n + j];
+        }
+        __syncwarp();
+        if (lane == 0) {
+            // (serial, in shared memory as in gj_colperm_kernel; the pivots were staged by all lanes above)
+            for (int k = n - 1; k >= 0; --k) {
+                const int p = s_pv[warp][k];
+                const int t = s_cm[warp][k];
+                s_cm[warp][k] = s_cm[warp][p];
+                s_cm[warp][p] = t;
+            }
+        }
+        __syncwarp();
+        for (int j = lane; j < n; j += 32) dm[s_cm[warp][j]] = j;
+        __syncwarp();
+        double* Wf = nw + b * nn;
+#pragma unroll
+        for (int c = 0; c < NB; ++c) {
+            if (c >= nbk) continue;
+            double* wc = Wf + static_cast<int64_t>(dm[j0 + c]) * n;
+#pragma unroll
+            for (int t = 0; t < RT; ++t) {
+                const int r = lane + 32 * t;
+                if (r < n) wc[r] = a[t][c];
+            }
+        }
+        return;
+    }
     double* W = nw + b * nn + static_cast<int64_t>(j0) * n;
 #pragma unroll
     for (int c = 0; c < NB; ++c)
@@ -356,7 +393,9 @@ __global__ void __launch_bounds__(128) gj_panel_reg_kernel(int n, int j0, int64_
 // that several are resident per SM and their load -> multiply -> store phases overlap.
 template <int WM>
 __global__ void __launch_bounds__(WM * 32, (WM <= 2) ? 6 : 4) gj_update_kernel(int n, int j0, const double* __restrict__ old,
-                                                                               double* __restrict__ nw, const int* __restrict__ src) {
+                                                                               double* __restrict__ nw, const int* __restrict__ src,
+                                                                               const int* __restrict__ dstmap) {
+    // dstmap != nullptr (last panel): column c of the work matrix is read / written at column dstmap[c] of nw (= the inverse)
     constexpr int BM = 32 * WM, BN = 32, NT = WM * 32;
     constexpr int LDA = BM + 4;
     __shared__ __align__(16) double As[NB * LDA];  // panel rows of this tile: As[kk][row]
@@ -368,6 +407,7 @@ __global__ void __launch_bounds__(WM * 32, (WM <= 2) ? 6 : 4) gj_update_kernel(i
     const double* O = old + b * nn;
     double* W = nw + b * nn;
     const int* S = src + b * n;
+    const int* DM = dstmap ? dstmap + b * n : nullptr;
     const int nbk = min(NB, n - j0);
     const int ncol = n - nbk;  // non-panel columns, index c' -> column c' (< j0) or c' + nbk
     const int row0 = blockIdx.x * BM, cp0 = blockIdx.y * BN;
@@ -398,7 +438,7 @@ __global__ void __launch_bounds__(WM * 32, (WM <= 2) ? 6 : 4) gj_update_kernel(i
         double v[NB];
 #pragma unroll
         for (int kk = 0; kk < NB; ++kk)
-            v[kk] = (kk < nbk && r < n) ? __ldg(W + static_cast<int64_t>(j0 + kk) * n + r) : 0.0;
+            v[kk] = (kk < nbk && r < n) ? __ldg(W + static_cast<int64_t>(DM ? DM[j0 + kk] : j0 + kk) * n + r) : 0.0;
 #pragma unroll
         for (int kk = 0; kk < NB; ++kk) As[kk * LDA + tid] = v[kk];
     }
@@ -440,7 +480,7 @@ __global__ void __launch_bounds__(WM * 32, (WM <= 2) ? 6 : 4) gj_update_kernel(i
             const int cp = cp0 + j * 8 + 2 * tig + h;
             if (cp >= ncol) continue;
             const int c = cp < j0 ? cp : cp + nbk;
-            double* wc = W + static_cast<int64_t>(c) * n;
+            double* wc = W + static_cast<int64_t>(DM ? DM[c] : c) * n;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int r = row0 + wm * 32 + i * 8 + grp;
@@ -701,15 +741,22 @@ void launch_gj_invert_batch(hdgb_ctx* ctx, int n, int64_t batch, const double* a
     DevBuf<double> tmp(static_cast<size_t>(nn) * batch);
     DevBuf<double> amax(static_cast<size_t>(batch));
     DevBuf<int> piv(static_cast<size_t>(batch) * n), src(static_cast<size_t>(batch) * n);
+    // n <= 128 (E-bar, additive-Schwarz blocks): the first panel reads the input directly (the prepass
+    // only scans for max|A|) and the last panel + update write the inverse's columns at their final places -- no copy
+    // pass, no permutation pass.  The ping-pong then ends in inv: x[steps & 1] = inv, the step before it reads tmp.
+    // In place (a == inv: the additive-Schwarz and block-Jacobi builds) this works when the number of panels is even: the
+    // first panel then reads a = inv and writes tmp, and inv is only overwritten from the second panel on.
+    const bool direct = (a != inv || steps % 2 == 0) && n <= 128 && tuning().gj_direct;
+    DevBuf<int> dstmap(direct ? 2 * static_cast<size_t>(batch) * n : 0);
     // ping-pong so that the last panel leaves the result in tmp and the column permutation writes inv
     double* x[2];
-    x[0] = (steps % 2 == 0) ? tmp.p : inv;
-    x[1] = (steps % 2 == 0) ? inv : tmp.p;
+    x[0] = ((steps % 2 == 0) != direct) ? tmp.p : inv;
+    x[1] = ((steps % 2 == 0) != direct) ? inv : tmp.p;
     int64_t done = 0;
     while (done < batch) {  // gridDim.x / z limits
         const int64_t nbt = (batch - done) < 65535 ? (batch - done) : 65535;
         const int64_t off = done * nn;
-        gj_prepare_kernel<<<static_cast<unsigned>(nbt), 256, 0, ctx->stream>>>(n, a + off, x[0] + off, amax.p + done);
+        gj_prepare_kernel<<<static_cast<unsigned>(nbt), 256, 0, ctx->stream>>>(n, a + off, direct ? nullptr : x[0] + off, amax.p + done);
         HDGB_LAUNCH_CHECK(ctx);
         const int ldp = n | 1;
         const size_t per_warp = static_cast<size_t>(NB) * ldp * sizeof(double);
@@ -720,18 +767,19 @@ void launch_gj_invert_batch(hdgb_ctx* ctx, int n, int64_t batch, const double* a
         ensure_dynamic_smem(gj_panel_kernel, psm);
         for (int s = 0; s < steps; ++s) {
             const int j0 = s * NB;
-            const double* old = x[s & 1] + off;
+            const double* old = (direct && s == 0 ? a : x[s & 1]) + off;
             double* nw = x[(s + 1) & 1] + off;
+            int* dm = (direct && s == steps - 1) ? dstmap.p + done * n : nullptr;
             if (n <= 128) {
                 const int rt = ceil_div(n, 32);
                 const unsigned pg = static_cast<unsigned>(ceil_div(nbt, 4));
                 int* pp = piv.p + done * n;
                 int* sp = src.p + done * n;
                 switch (rt) {
-                    case 1: gj_panel_reg_kernel<1><<<pg, 128, 0, ctx->stream>>>(n, j0, nbt, old, nw, amax.p + done, pp, sp, flags, done); break;
-                    case 2: gj_panel_reg_kernel<2><<<pg, 128, 0, ctx->stream>>>(n, j0, nbt, old, nw, amax.p + done, pp, sp, flags, done); break;
-                    case 3: gj_panel_reg_kernel<3><<<pg, 128, 0, ctx->stream>>>(n, j0, nbt, old, nw, amax.p + done, pp, sp, flags, done); break;
-                    default: gj_panel_reg_kernel<4><<<pg, 128, 0, ctx->stream>>>(n, j0, nbt, old, nw, amax.p + done, pp, sp, flags, done); break;
+                    case 1: gj_panel_reg_kernel<1><<<pg, 128, 0, ctx->stream>>>(n, j0, nbt, old, nw, amax.p + done, pp, sp, flags, done, dm, dm ? dstmap.p + (batch + done) * n : nullptr); break;
+                    case 2: gj_panel_reg_kernel<2><<<pg, 128, 0, ctx->stream>>>(n, j0, nbt, old, nw, amax.p + done, pp, sp, flags, done, dm, dm ? dstmap.p + (batch + done) * n : nullptr); break;
+                    case 3: gj_panel_reg_kernel<3><<<pg, 128, 0, ctx->stream>>>(n, j0, nbt, old, nw, amax.p + done, pp, sp, flags, done, dm, dm ? dstmap.p + (batch + done) * n : nullptr); break;
+                    default: gj_panel_reg_kernel<4><<<pg, 128, 0, ctx->stream>>>(n, j0, nbt, old, nw, amax.p + done, pp, sp, flags, done, dm, dm ? dstmap.p + (batch + done) * n : nullptr); break;
                 }
             } else if (tuning().gj_panel_cta) {
                 const size_t csm = per_warp;  // one panel per CTA
@@ -750,16 +798,18 @@ void launch_gj_invert_batch(hdgb_ctx* ctx, int n, int64_t batch, const double* a
                 dim3 grid(ceil_div(n, 32 * wm), ceil_div(ncol, 32), static_cast<unsigned>(nbt));
                 const int* sp = src.p + done * n;
                 switch (wm) {
-                    case 1: gj_update_kernel<1><<<grid, 32, 0, ctx->stream>>>(n, j0, old, nw, sp); break;
-                    case 2: gj_update_kernel<2><<<grid, 64, 0, ctx->stream>>>(n, j0, old, nw, sp); break;
-                    case 3: gj_update_kernel<3><<<grid, 96, 0, ctx->stream>>>(n, j0, old, nw, sp); break;
-                    default: gj_update_kernel<4><<<grid, 128, 0, ctx->stream>>>(n, j0, old, nw, sp); break;
+                    case 1: gj_update_kernel<1><<<grid, 32, 0, ctx->stream>>>(n, j0, old, nw, sp, dm); break;
+                    case 2: gj_update_kernel<2><<<grid, 64, 0, ctx->stream>>>(n, j0, old, nw, sp, dm); break;
+                    case 3: gj_update_kernel<3><<<grid, 96, 0, ctx->stream>>>(n, j0, old, nw, sp, dm); break;
+                    default: gj_update_kernel<4><<<grid, 128, 0, ctx->stream>>>(n, j0, old, nw, sp, dm); break;
                 }
                 HDGB_LAUNCH_CHECK(ctx);
             }
         }
-        gj_colperm_kernel<<<static_cast<unsigned>(nbt), 256, 2 * n * sizeof(int), ctx->stream>>>(n, tmp.p + off, inv + off, piv.p + done * n);
-        HDGB_LAUNCH_CHECK(ctx);
+        if (!direct) {
+            gj_colperm_kernel<<<static_cast<unsigned>(nbt), 256, 2 * n * sizeof(int), ctx->stream>>>(n, tmp.p + off, inv + off, piv.p + done * n);
+            HDGB_LAUNCH_CHECK(ctx);
+        }
         done += nbt;
     }
 }

@@ -8,18 +8,20 @@ import paper_2512_13619_b200 as hdg
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["gj", "gj-cta", "gj-smem", "tile", "smem"])
+@pytest.fixture(params=["gj", "gj-copy", "gj-cta", "gj-smem", "tile", "smem"])
 def lu_kernel(request):
     """gj: blocked Gauss-Jordan with DMMA rank-16 updates (the default for n > 24; gj-cta: its panel of large
     blocks factored by a 4-warp CTA instead of one warp); tile: register-tiled Gauss-Jordan (n <= 128); smem: one
     block per CTA in shared memory / the global-memory fallback."""
     hdg.set_tuning("use_blocked_gj", 1 if request.param.startswith("gj") else 0)
     hdg.set_tuning("gj_panel_cta", 1 if request.param == "gj-cta" else 0)
+    hdg.set_tuning("gj_direct", 0 if request.param == "gj-copy" else 1)   # gj-copy: copy prepass + separate column-permutation pass
     hdg.set_tuning("gj_smem", 1 if request.param == "gj-smem" else 0)   # single kernel, block in shared memory (n <= 128)
     hdg.set_tuning("use_tile_lu", 1 if request.param == "tile" else 0)
     yield request.param
     hdg.set_tuning("use_blocked_gj", 1)
     hdg.set_tuning("gj_panel_cta", 0)
+    hdg.set_tuning("gj_direct", 1)
     hdg.set_tuning("gj_smem", 0)
     hdg.set_tuning("use_tile_lu", 1)
 
@@ -106,3 +108,22 @@ def test_gemm_batch_and_broadcast(ctx, gemm_kernel, m, k, n, batch):
     assert np.max(np.abs(got - np.einsum("bmk,bnk->bnm", at, b))) <= tol
     with pytest.raises(hdg.DimensionMismatch):
         hdg.gemm_batch(ctx, a.ravel(), m, k, batch, b.ravel(), k + 1, n, batch)
+
+
+@pytest.mark.parametrize("n,batch", [(16, 30), (40, 50), (64, 33), (96, 21), (128, 5)])
+def test_blocked_gj_direct_placement_is_bitwise_the_copy_form(ctx, n, batch):
+    """`gj_direct` (default, out-of-place inverses with n <= 128): the first panel reads the input and the last panel and
+    update write the inverse's columns at their final places.  Same arithmetic as the form with a copy prepass and a
+    separate column-permutation pass: identical bits, including blocks whose pivoting permutes every row."""
+    rng = np.random.default_rng(100 + n)
+    a = rng.standard_normal((batch, n, n))
+    a[1] = np.eye(n)[rng.permutation(n)] * rng.uniform(0.5, 2.0, n)[None, :]
+    flat = np.transpose(a, (0, 2, 1)).ravel()
+    out = {}
+    for flag in (1, 0):
+        hdg.set_tuning("gj_direct", flag)
+        try:
+            out[flag] = hdg.lu_invert_batch(ctx, flat, n, batch)
+        finally:
+            hdg.set_tuning("gj_direct", 1)
+    assert np.array_equal(out[0], out[1])
