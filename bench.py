@@ -91,6 +91,7 @@ def parse():
                     help="cells per direction of the bounded CPU sample (default: sized to the time budget)")
     ap.add_argument("--cpu-budget-s", type=float, default=400.0, help="--impl reference: wall-clock budget of the whole run")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tune", default="", help="A/B aid: hdgb_set_tuning knobs, e.g. gj_direct=0,stream_evict_first=0 (echoed in the JSON line)")
     ap.add_argument("--transport", default="auto", choices=["auto", "nccl", "host"])
     a = ap.parse_args()
     cfg = dict(CONFIGS[a.config])
@@ -381,6 +382,9 @@ def run_ours(a):
             dist.init_process_group("gloo")
 
     ctx = hdg.Context(device)
+    for kv in filter(None, a.tune.split(",")):
+        k, v = kv.split("=")
+        hdg.set_tuning(k, float(v))
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)  # so torch.cuda.Event sees the launching stream
 
@@ -546,6 +550,7 @@ def run_ours(a):
             "l2_policy": "inputs larger than L2 (K = %.2f GB, preconditioner blocks = %.2f GB vs 126 MB L2)" %
                          (8e-9 * nf * mpf * mpf * nb, bytes_pc * 1e-9) if big else
                          "operator fits L2 (K = %.1f MB): kernel timings are L2-resident, launch-latency bound" % (8e-6 * nf * mpf * mpf * nb),
+            **({"tuning": a.tune} if a.tune else {}),
             "timing_order": "kernel-level measurements (~3 s of GPU work: the B200 power ramp after idle, profiles/r02_power_trace.txt) "
                             "-> W warm-up solves -> K timed device-resident solves -> K timed end-to-end solves",
             "e2e": {"value": n_dof_global * a.steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

@@ -53,6 +53,7 @@ struct StreamPlan {
     int ipw;              // packed mode (> 0): items a warp multiplies side by side, one (item, row group) per lane
     int xstride;          // doubles between the x slices of consecutive items of a chunk (cols, or cols + 1 in packed mode with odd cols)
     float inv_cols, inv_width, inv_nslots;  // reciprocals for the gather's index arithmetic
+    int evict_first;      // bulk copies of the matrix carry an L2 evict-first hint (the gathered vector stays cached)
 };
 
 template <int V>
@@ -121,6 +122,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) stream_gemv_kernel(GemvArgs g,
     const int64_t w0 = u0 + warp;  // first unit of this warp; its unit t is w0 + t * kWarps
 
     // chunk n of this warp into ring stage s
+    const uint64_t l2pol = p.evict_first ? l2_policy_evict_first() : 0;
     auto issue = [&](int n, int s) {
         const double* src;
         int64_t elems;
@@ -144,7 +146,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1) stream_gemv_kernel(GemvArgs g,
         // of it have completed.  That FMAs consumed the loaded values is NOT enough -- ptxas may schedule the copy
         // behind the ISSUE of the last loads and ahead of their consumers (tma.cuh: ring_release_all).
         mbar_expect_tx(my_full + s, bytes);
-        if (bytes) tma_bulk_g2s(my_stage + static_cast<size_t>(s) * p.stage_elems, src, bytes, my_full + s);
+        if (bytes) {
+            if (p.evict_first) tma_bulk_g2s_hint(my_stage + static_cast<size_t>(s) * p.stage_elems, src, bytes, my_full + s, l2pol);
+            else tma_bulk_g2s(my_stage + static_cast<size_t>(s) * p.stage_elems, src, bytes, my_full + s);
+        }
     };
     if (lane == 0)
         for (int n = 0; n < SW && n < my_chunks; ++n) issue(n, n);
@@ -426,6 +431,9 @@ bool launch_stream_gemv(hdgb_ctx* ctx, const GemvArgs& g) {
     const int kWarps = packed ? 16 : 8;
     p.warps = kWarps;
     p.ipw = packed ? 32 / RL : 0;
+    // (measured: config 2 matvec 235 -> 222 us, ASM apply 269 -> 257 us; neutral at config 4; the packed mode of tiny blocks
+    // loses 3-7 % with the hint at config 3, so it is left out there)
+    p.evict_first = tuning().stream_evict_first && p.ipw == 0;
     const size_t kWarpBudget = kSmemBudget / kWarps;  // stage(s) + x buffer + index buffer of one warp
     // per-warp shared memory: one or more stages + the x slice(s) + the index row(s)
     const size_t per_item = static_cast<size_t>(item_elems + 2 * (cols + 1)) * sizeof(double) + 3 * static_cast<size_t>(nslots) * sizeof(int) + 8;
