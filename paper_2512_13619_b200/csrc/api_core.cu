@@ -24,6 +24,8 @@ int hdgb_set_tuning(const char* key, int64_t value) {
     const std::string k = key ? key : "";
     if (k == "use_stream") { hdgb::tuning().use_stream = static_cast<int>(value); return 0; }
     if (k == "stream_min_elems") { hdgb::tuning().stream_min_elems = value; return 0; }
+    if (k == "cgs_evict_first") { hdgb::tuning().cgs_evict_first = static_cast<int>(value); return 0; }
+    if (k == "stream_persist_mb") { hdgb::tuning().stream_persist_mb = static_cast<int>(value); return 0; }
     if (k == "stream_evict_first") { hdgb::tuning().stream_evict_first = static_cast<int>(value); return 0; }
     if (k == "gj_direct") { hdgb::tuning().gj_direct = static_cast<int>(value); return 0; }
     if (k == "gj_smem") { hdgb::tuning().gj_smem = static_cast<int>(value); return 0; }

@@ -55,6 +55,7 @@ struct OrthArgs {
     double* partial;      // [n_out][grid]
     unsigned* counter;    // ticket of the last-CTA reduction (zero on entry, zeroed again on exit)
     int stages;
+    int evict_first;      // basis columns copied with an L2 evict-first hint (w and the newest vectors stay cached between passes)
 };
 
 // MODE 0: out[0..nvec) = V^T w
@@ -102,6 +103,7 @@ __global__ void __launch_bounds__(kThreads, 1) cgs_pass_kernel(OrthArgs a) {
 
     if (warp == kWarps) {
         // ---- producer warp: one bulk copy per column (w last) into the stage, as soon as the consumers freed it ----
+        const uint64_t l2pol = a.evict_first ? l2_policy_evict_first() : 0;
         for (int it = 0; it < my_tiles; ++it) {
             const int s = it % a.stages, use = it / a.stages;
             if (use > 0) mbar_wait(empty + s, static_cast<uint32_t>((use - 1) & 1));
@@ -113,7 +115,8 @@ __global__ void __launch_bounds__(kThreads, 1) cgs_pass_kernel(OrthArgs a) {
             __syncwarp();
             for (int j = lane; j < ncol; j += 32) {
                 const double* src = j < nvec ? a.V + static_cast<int64_t>(j) * a.ldv + row0 : a.w + row0;
-                tma_bulk_g2s(dst + static_cast<size_t>(j) * kRows, src, bytes, full + s);
+                if (a.evict_first && j < nvec) tma_bulk_g2s_hint(dst + static_cast<size_t>(j) * kRows, src, bytes, full + s, l2pol);
+                else tma_bulk_g2s(dst + static_cast<size_t>(j) * kRows, src, bytes, full + s);
             }
         }
     } else {
@@ -230,6 +233,7 @@ void launch_mode(hdgb_ctx* ctx, const OrthArgs& a0) {
     const int64_t per = (ntiles + grid - 1) / grid;
     if (stages > per) stages = static_cast<int>(per < 1 ? 1 : per);
     a.stages = stages;
+    a.evict_first = tuning().cgs_evict_first;
     const size_t smem = stages * col_bytes + (kRows + kOrthMaxVec + 2 + kWarps) * sizeof(double) + 2 * kMaxStages * sizeof(uint64_t);
     auto kern = cgs_pass_kernel<MODE>;
     ensure_dynamic_smem(kern, smem);
@@ -261,6 +265,7 @@ void launch_cgs_pass(hdgb_ctx* ctx, int mode, const double* V, int64_t ldv, int 
     a.partial = work + 2;
     a.counter = reinterpret_cast<unsigned*>(work);
     a.stages = 2;
+    a.evict_first = 0;
     switch (mode) {
         case 0: launch_mode<0>(ctx, a); break;
         case 1: launch_mode<1>(ctx, a); break;

@@ -53,6 +53,7 @@ struct StreamPlan {
     int ipw;              // packed mode (> 0): items a warp multiplies side by side, one (item, row group) per lane
     int xstride;          // doubles between the x slices of consecutive items of a chunk (cols, or cols + 1 in packed mode with odd cols)
     float inv_cols, inv_width, inv_nslots;  // reciprocals for the gather's index arithmetic
+    int64_t persist_bytes; // leading bytes of the matrix copied with an evict-last hint (0: none)
     int evict_first;      // bulk copies of the matrix carry an L2 evict-first hint (the gathered vector stays cached)
 };
 
@@ -123,6 +124,12 @@ __global__ void __launch_bounds__(kMaxThreads, 1) stream_gemv_kernel(GemvArgs g,
 
     // chunk n of this warp into ring stage s
     const uint64_t l2pol = p.evict_first ? l2_policy_evict_first() : 0;
+    // (stream_persist_mb, off: the leading part of the matrix copied with an evict-last hint so that it survives in the L2 from
+    // one application to the next -- measured slower at config 2 with 24 / 32 / 48 MB per matrix: matvec 221 -> 225-229 us,
+    // ASM apply 255 -> 262-270 us)
+    uint64_t l2keep = 0;
+    if (p.persist_bytes > 0) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(l2keep));
+    const double* keep_end = g.a + p.persist_bytes / static_cast<int64_t>(sizeof(double));
     auto issue = [&](int n, int s) {
         const double* src;
         int64_t elems;
@@ -147,7 +154,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) stream_gemv_kernel(GemvArgs g,
         // behind the ISSUE of the last loads and ahead of their consumers (tma.cuh: ring_release_all).
         mbar_expect_tx(my_full + s, bytes);
         if (bytes) {
-            if (p.evict_first) tma_bulk_g2s_hint(my_stage + static_cast<size_t>(s) * p.stage_elems, src, bytes, my_full + s, l2pol);
+            if (p.evict_first) tma_bulk_g2s_hint(my_stage + static_cast<size_t>(s) * p.stage_elems, src, bytes, my_full + s, (p.persist_bytes > 0 && src < keep_end) ? l2keep : l2pol);
             else tma_bulk_g2s(my_stage + static_cast<size_t>(s) * p.stage_elems, src, bytes, my_full + s);
         }
     };
@@ -434,6 +441,7 @@ bool launch_stream_gemv(hdgb_ctx* ctx, const GemvArgs& g) {
     // (measured: config 2 matvec 235 -> 222 us, ASM apply 269 -> 257 us; neutral at config 4; the packed mode of tiny blocks
     // loses 3-7 % with the hint at config 3, so it is left out there)
     p.evict_first = tuning().stream_evict_first && p.ipw == 0;
+    p.persist_bytes = p.evict_first ? static_cast<int64_t>(tuning().stream_persist_mb) << 20 : 0;
     const size_t kWarpBudget = kSmemBudget / kWarps;  // stage(s) + x buffer + index buffer of one warp
     // per-warp shared memory: one or more stages + the x slice(s) + the index row(s)
     const size_t per_item = static_cast<size_t>(item_elems + 2 * (cols + 1)) * sizeof(double) + 3 * static_cast<size_t>(nslots) * sizeof(int) + 8;

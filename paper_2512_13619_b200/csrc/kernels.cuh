@@ -57,6 +57,8 @@ struct Tuning {
     int qelim_wn = 1;                    // 32-column tiles per CTA of the fused q-elimination product
     int use_qelim_fused = 1;             // q-elimination as two fused stacked products per component instead of 4 D
     int use_dmma = 1;                    // batched GEMMs on the FP64 tensor-core path (k_gemm_dmma.cu)
+    int cgs_evict_first = 0;             // CGS2 passes: Krylov basis copies with an L2 evict-first hint
+    int stream_persist_mb = 0;           // stream GEMV: leading MB of every streamed matrix copied with an L2 evict-last hint (experiment)
     int stream_evict_first = 1;          // stream GEMV: matrix copies carry an L2 evict-first hint, so the gathered vector is not pushed out of the L2
     int gj_direct = 1;                   // out-of-place inverses with n <= 128: first panel reads the input, last panel / update write the permuted columns (no copy pass, no permutation pass)
     int gj_smem = 0;                     // n <= 128: blocked Gauss-Jordan in ONE kernel, block resident in shared memory (measured 2-3x slower: latency bound)
