@@ -149,14 +149,17 @@ def test_sixteen_warp_local_kernel_matches_eight_warp(ctx, shape, n, k, M, case)
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("shape,n,case,transient", [("hex", 3, "poisson", False), ("hex", 2, "burgers", True),
-                                                    ("hex", 2, "reaction", True)])
-def test_streamed_ed_sweep_matches_chunked_builder(ctx, shape, n, case, transient):
+@pytest.mark.parametrize("shape,n,case,transient,qp", [("hex", 3, "poisson", False, 0), ("hex", 2, "burgers", True, 0),
+                                                       ("hex", 2, "reaction", True, 0), ("hex", 2, "burgers", False, 4),
+                                                       ("hex", 2, "burgers", True, 6)])
+def test_streamed_ed_sweep_matches_chunked_builder(ctx, shape, n, case, transient, qp):
     """`local_ed_stream` (default on for scalar systems with 64 basis functions per element: hex p = 3): E and
     D_d from the bulk-TMA table ring with fragment-built left operands against the chunked shared-memory operand
     builder and against the scalar (no tensor core) sweep.  Same contraction, the quadrature weight on the other
     operand: equal to rounding.  Jittered meshes, perturbed states, with and without the backward-Euler mass term."""
-    disc = hdg.Discretization.structured(ctx, shape, n=n, degree=3, jitter=0.15, seed=3)
+    # qp: quadrature points per direction (0 = default k + 2 = 5).  4: partial ring stages everywhere (64 volume, 16 face points
+    # per face); 6: 216 volume points and 36 > 32 face points per face -- H / G_d / F / J fall back to the staged face kernel
+    disc = hdg.Discretization.structured(ctx, shape, n=n, degree=3, jitter=0.15, seed=3, quad_points=qp)
     assert disc.pe == 64
     model = hdg.make_case_model(disc, case)
     state = hdg.make_initial_state(disc, model)
