@@ -911,8 +911,8 @@ inline __host__ __device__ size_t ed_wide_doubles(int D, int qe, int nfp) {
 }
 
 template <int M, int D, int NW>
-__device__ void ed_stream_wide(const DiscView& dv, const LocalIn& in, const LocalOut& out, int e, const VolRec<M, D>* vrec,
-                               const FaceRec<M, D>* frec, const int* s_orient, double* ring, uint64_t* bars) {
+__device__ bool ed_stream_wide(const DiscView& dv, const LocalIn& in, const LocalOut& out, int e, const VolRec<M, D>* vrec,
+                               const FaceRec<M, D>* frec, const int* s_orient, double* ring, uint64_t* bars, bool do_hgf) {
     static_assert(D == 3, "coefficient rows are laid out for 1 + D = 4 blocks");
     constexpr int NQ = 1 + D;
     constexpr int NH = NW / 8;           // column parts: 8 warps own all 64 columns of their rows, 16 warps half of them
@@ -925,7 +925,14 @@ __device__ void ed_stream_wide(const DiscView& dv, const LocalIn& in, const Loca
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
     const int grp = lane >> 2, tig = lane & 3;
     const int nsv = (qe + kEsPts - 1) / kEsPts, nsf = (nfp + kEsPts - 1) / kEsPts, nst = nsv + nsf;
-    const int total = NPAIR * nst;
+    // after the M^2 sweeps: one ring stage per local face for H, G_d, F, J of all pairs (8-warp form only)
+    constexpr int NCH = 6;                      // face coefficient sets per pair: dv_u, dv_q[0..2], dfh_uh, dv_uh (weight folded in)
+    const int hks = (qf + 3) / 4;               // k-steps of a face stage
+    const int pf = dv.pf, mpf = M * pf, nfl = dv.n_lfe * mpf;
+    const int nith = 4 * hks * NPAIR * NCH;     // entries of a face's coefficient table [point][pair][set]
+    const bool hgf = do_hgf && NW == 8 && pf == 16 && qf <= 32 && 2 * nith <= 2 * (qe + nfp) * kEwLd;
+    const int n_ed = NPAIR * nst;
+    const int total = n_ed + (hgf ? dv.n_lfe : 0);
     const int npt = qe + nfp;
     uint64_t* full = bars;
     uint64_t* empty = bars + kEsStages;
@@ -935,6 +942,13 @@ __device__ void ed_stream_wide(const DiscView& dv, const LocalIn& in, const Loca
     auto issue = [&](int gi, int slot) {
         if (lane != 0) return;
         double* dst = ring + slot * stage_d;
+        if (gi >= n_ed) {  // face stage: all points of local face gi - n_ed
+            const int lf = gi - n_ed;
+            const uint32_t bytes = 4 * hks * kEsLd * sizeof(double);
+            mbar_expect_tx(full + slot, bytes);
+            tma_bulk_g2s(dst, dv.es_face + (static_cast<size_t>(lf) * dv.n_orient + s_orient[lf]) * qf * kEsLd, bytes, full + slot);
+            return;
+        }
         const int s = gi % nst;
         if (s < nsv) {
             mbar_expect_tx(full + slot, stage_d * sizeof(double));
@@ -1094,6 +1108,122 @@ __device__ void ed_stream_wide(const DiscView& dv, const LocalIn& in, const Loca
         }
         __syncthreads();
     }
+    if (!hgf) return false;
+    // ---- H, G_d, F, J of all component pairs, one ring stage per local face ----
+    // [H | G_d](lf m b, mp j) = sum_gc psi_b(gc) (cw(gc) phis_j(gc)),  F(m i, lf mp bp) = sum_gc phis_i(gc) (cf(gc) psi_bp(gc)),
+    // J(lf m b, lf mp bp) = sum_gc psi_b(gc) (cj(gc) psi_bp(gc)).  psi lives in registers (left fragment of H / G_d / J, right
+    // fragment of F / J), the face's trace-table fragments are read once from the ring and serve all M^2 pairs, the pairs'
+    // weighted coefficients come from a shared-memory table gathered per face from the record scratch (double-buffered).
+    constexpr int KS = 8;
+    constexpr int kItemsH = 17;  // ceil(28 * 25 * 6 / 256) for M = 5 and the default rule; more: extra trips
+    double* hb = cb;             // [2][nith]
+    auto hcoef = [&](int lf, int item) -> double {
+        const int gc = item / (NPAIR * NCH), rem = item - gc * (NPAIR * NCH);
+        const int pr = rem / NCH, c = rem - pr * NCH;
+        if (gc >= qf) return 0.0;
+        const int mp = pr / M, m = pr - mp * M, mm = m * M + mp;
+        const FaceRec<M, D>& r = frec[lf * qf + gc];
+        const double* v = c == 0 ? &r.dv_u[mm] : (c <= D ? &r.dv_q[mm * D + c - 1] : (c == 1 + D ? &r.dfh_uh[mm] : &r.dv_uh[mm]));
+        return __ldcg(&r.w) * __ldcg(v);
+    };
+    for (int item = tid; item < nith; item += nt) hb[item] = hcoef(0, item);
+    double psr[2][KS];
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+            const int gc = 4 * ks + tig, bb = 8 * t + grp;
+            psr[t][ks] = (gc < qf && bb < pf) ? __ldg(dv.psi + bb + pf * gc) : 0.0;
+        }
+    __syncthreads();
+    for (int lf = 0; lf < dv.n_lfe; ++lf, ++it) {
+        const double* hbp = hb + static_cast<size_t>(lf & 1) * nith;
+        double* hbn = hb + static_cast<size_t>((lf + 1) & 1) * nith;
+        const bool more = lf + 1 < dv.n_lfe;
+        double hst[kItemsH];
+#pragma unroll
+        for (int j = 0; j < kItemsH; ++j) {
+            const int item = tid + j * nt;
+            hst[j] = (more && item < nith) ? hcoef(lf + 1, item) : 0.0;
+        }
+        produce();
+        mbar_wait(full + slot, par);
+        const double* St = ring + slot * stage_d + rowoff;
+        double ph[KS];
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) ph[ks] = ks < hks ? St[(4 * ks + tig) * kEsLd] : 0.0;
+        ring_release_all(empty + slot);  // the fragments are in registers
+        if (++slot == kEsStages) { slot = 0; par ^= 1; }
+        const int j0 = 8 * warp + 2 * tig;
+        for (int pr = 0; pr < NPAIR; ++pr) {
+            const int mp = pr / M, m = pr - mp * M;
+            const bool jw = (pr & 7) == warp;  // J block of this (face, pair): one warp
+            double hg[1 + D][2][2], fa[2][2], ja[2][2][2];
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+#pragma unroll
+                for (int w = 0; w <= D; ++w) hg[w][t][0] = hg[w][t][1] = 0.0;
+                fa[t][0] = fa[t][1] = 0.0;
+                ja[t][0][0] = ja[t][0][1] = ja[t][1][0] = ja[t][1][1] = 0.0;
+            }
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) {
+                if (ks >= hks) break;
+                const double2* cr = reinterpret_cast<const double2*>(hbp + (static_cast<size_t>(4 * ks + tig) * NPAIR + pr) * NCH);
+                const double2 c01 = cr[0], c23 = cr[1], c45 = cr[2];
+                const double cwv[1 + D] = {c01.x, c01.y, c23.x, c23.y};
+#pragma unroll
+                for (int w = 0; w <= D; ++w) {
+                    const double bq = cwv[w] * ph[ks];
+#pragma unroll
+                    for (int t = 0; t < 2; ++t) dmma_8x8x4(hg[w][t][0], hg[w][t][1], psr[t][ks], bq);
+                }
+#pragma unroll
+                for (int t = 0; t < 2; ++t) dmma_8x8x4(fa[t][0], fa[t][1], ph[ks], psr[t][ks] * c45.x);
+                if (jw) {
+#pragma unroll
+                    for (int t = 0; t < 2; ++t)
+#pragma unroll
+                        for (int c = 0; c < 2; ++c) dmma_8x8x4(ja[t][c][0], ja[t][c][1], psr[t][ks], psr[c][ks] * c45.y);
+                }
+            }
+#pragma unroll
+            for (int w = 0; w <= D; ++w) {
+                double* dst = (w == 0 ? out.H : out.G[w - 1]) + static_cast<size_t>(e) * nfl * npe +
+                              static_cast<size_t>(mp * kEsPe + j0) * nfl + lf * mpf + m * pf + grp;
+#pragma unroll
+                for (int t = 0; t < 2; ++t)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) dst[static_cast<size_t>(h) * nfl + 8 * t] = hg[w][t][h];
+            }
+            {
+                double* dst = out.F + static_cast<size_t>(e) * npe * nfl + static_cast<size_t>(lf * mpf + mp * pf) * npe + m * kEsPe + rowoff;
+#pragma unroll
+                for (int t = 0; t < 2; ++t)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) dst[static_cast<size_t>(8 * t + 2 * tig + h) * npe] = fa[t][h];
+            }
+            if (jw) {
+                double* dst = out.J + static_cast<size_t>(e) * nfl * nfl + static_cast<size_t>(lf * mpf + mp * pf) * nfl + lf * mpf + m * pf + grp;
+#pragma unroll
+                for (int t = 0; t < 2; ++t)
+#pragma unroll
+                    for (int c = 0; c < 2; ++c)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) dst[static_cast<size_t>(8 * c + 2 * tig + h) * nfl + 8 * t] = ja[t][c][h];
+            }
+        }
+        if (more) {
+#pragma unroll
+            for (int j = 0; j < kItemsH; ++j) {
+                const int item = tid + j * nt;
+                if (item < nith) hbn[item] = hst[j];
+            }
+            for (int item = tid + kItemsH * nt; item < nith; item += nt) hbn[item] = hcoef(lf + 1, item);
+        }
+        __syncthreads();
+    }
+    return true;
 }
 
 // ---- H, G_d and F of scalar systems (M = 1) on the tensor-core path ------------------------------------------
@@ -1542,8 +1672,16 @@ __global__ void __launch_bounds__(NT, RES ? (Model::M == 1 ? 4 : 2) : ((!GREC &&
         }
     }
     if constexpr (ED && GREC && M > 1 && D == 3 && (NT == 256 || NT == 512)) {
-        if (ed_streamed && !(dbg_skip & 1)) {  // wide system, pe = 64: one streamed sweep per component pair
-            ed_stream_wide<M, D, NT / 32>(dv, in, out, e, vrec, frec, s_orient, opbuf_base, s_bars);
+        if (ed_streamed && !(dbg_skip & 1)) {  // wide system, pe = 64: one streamed sweep per component pair, then the face blocks
+            const bool want_hgf = hgf_streamed && ed_dmma_on == 2 && !(dbg_skip & 2);
+            if (want_hgf && NT == 256 && pf == 16 && qf <= 32) {
+                // J outside the per-face diagonal blocks is zero (the face stages write the blocks themselves)
+                for (int t = tid; t < nfl * nfl; t += nt) {
+                    const int c = t / nfl, r = t - c * nfl;
+                    if (c / mpf != r / mpf) out.J[static_cast<size_t>(e) * nfl * nfl + t] = 0.0;
+                }
+            }
+            if (ed_stream_wide<M, D, NT / 32>(dv, in, out, e, vrec, frec, s_orient, opbuf_base, s_bars, want_hgf)) hgf_done = j_done = true;
             dbg_skip |= 1;
         }
     }
@@ -1827,7 +1965,7 @@ void launch_assemble_t(hdgb_ctx* ctx, const DiscView& dv, const ModelView& mv, c
                 auto kern_g = local_assemble_kernel<Model, 256, true, true>;
                 ensure_dynamic_smem(kern_g, cap);
                 DevBuf<char> scratch(rec_stride * static_cast<size_t>(dv.ne));
-                kern_g<<<dv.ne, 256, fixed + edb, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2 | stream_flag | ((tuning().local_debug_skip & 7) << 4), scratch.p, rec_stride);
+                kern_g<<<dv.ne, 256, fixed + edb, ctx->stream>>>(dv, mv, in, out, 1, 0, dv.qe, 0, nfp, 1, 2 | stream_flag | ((stream_flag && (tuning().local_ed_stream & 2)) ? 128 : 0) | ((tuning().local_debug_skip & 7) << 4), scratch.p, rec_stride);
                 HDGB_LAUNCH_CHECK(ctx);
                 return;
             }
