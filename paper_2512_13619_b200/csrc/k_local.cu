@@ -24,7 +24,7 @@ namespace {
 // One CTA per element; the per-point weights and inverse Jacobians are staged once in shared memory and a
 // thread owns a 2 x 4 tile of (i, j) pairs, so every table value loaded serves 4 (resp. 2) entries.  The terms of
 // an entry are formed and summed exactly as in the scalar version (points ascending).
-constexpr int kMbTi = 2, kMbTj = 4;
+[[maybe_unused]] constexpr int kMbTi = 2, kMbTj = 4;
 template <int D>
 __global__ void __launch_bounds__(256) mass_bmat_kernel(DiscView dv, double* __restrict__ mass, double* __restrict__ b0,
                                                         double* __restrict__ b1, double* __restrict__ b2) {
@@ -1390,7 +1390,7 @@ __global__ void __launch_bounds__(NT, RES ? (Model::M == 1 ? 4 : 2) : ((!GREC &&
     const int e = blockIdx.x;
     const int pe = dv.pe, pf = dv.pf, qe = dv.qe, qf = dv.qf, n_lfe = dv.n_lfe;
     const int npe = M * pe, mpf = M * pf, nfl = n_lfe * mpf;
-    const int nfp = n_lfe * qf;
+    [[maybe_unused]] const int nfp = n_lfe * qf;
     const int tid = threadIdx.x, nt = blockDim.x;
 
     double* us = sm;                  // npe
