@@ -70,13 +70,18 @@ void hdgb_ctx_reset_launch_count(hdgb_ctx* ctx);
 const char* hdgb_version(void);
 /* Process-wide kernel-selection knobs for A/B measurements and tests (defaults in csrc/kernels.cuh):
  *   GEMV:        "use_stream" (TMA stream kernel for large GEMVs), "stream_min_elems", "stream_packed" (several
- *                small items per warp pass), "stream_packed_max_cols", "stream_packed_stage_bytes";
+ *                small items per warp pass), "stream_packed_max_cols", "stream_packed_stage_bytes",
+ *                "stream_evict_first" (L2 evict-first hint on the matrix stream), "stream_persist_mb" (experiment, off);
  *   dense:       "use_dmma" (FP64 tensor-core GEMM / local blocks), "use_qelim_fused", "qelim_split_rows",
  *                "qelim_wn", "qelim_stages", "gemm_wn_cap", "use_blocked_gj" (blocked Gauss-Jordan inverse),
+ *                "gj_direct" (no copy / permutation passes, n <= 128), "gj_smem", "gj_panel_cta",
  *                "use_tile_lu" (register-tiled Gauss-Jordan, n <= 128, when the blocked one is off);
- *   assembly:    "local_nt", "local_dmma_min_pe", "local_global_records", "local_dmma_chunked", "assemble_budget_kb";
- *   GMRES:       "fused_cgs", "cgs_stream", "spin_sync", "poly_fused" (polynomial recurrence updates as epilogues),
- *                "gmres_speculate" (next Arnoldi step's operator applications enqueued before the host reads the column);
+ *   assembly:    "local_ed_stream" (hex p = 3: bit 0 = E / D_d, bit 1 = H / G_d / F / J through the bulk-TMA table ring,
+ *                bit 2 = stage copies split in 4-row pieces), "local_nt", "local_nt_wide", "local_dmma_min_pe",
+ *                "local_global_records", "local_dmma_chunked", "local_debug_skip" (measurement: phases left out),
+ *                "assemble_budget_kb";
+ *   GMRES:       "fused_cgs", "cgs_stream", "cgs_evict_first", "spin_sync", "poly_fused" (polynomial recurrence updates as
+ *                epilogues), "gmres_speculate" (next Arnoldi step's operator applications enqueued before the host reads the column);
  *   multi-GPU:   "overlap_halo" (interior rows / elements computed while the halo exchange is in flight).
  * Returns non-zero for an unknown key.  Results do not depend on them beyond rounding. */
 int hdgb_set_tuning(const char* key, int64_t value);
