@@ -47,6 +47,7 @@ int hdgb_set_tuning(const char* key, int64_t value) {
     if (k == "local_dmma_chunked") { hdgb::tuning().local_dmma_chunked = static_cast<int>(value); return 0; }
     if (k == "qelim_stages") { hdgb::tuning().qelim_stages = static_cast<int>(value); return 0; }
     if (k == "gemm_wn_cap") { hdgb::tuning().gemm_wn_cap = static_cast<int>(value < 1 ? 1 : value); return 0; }
+    if (k == "schur_fused") { hdgb::tuning().schur_fused = static_cast<int>(value); return 0; }
     if (k == "qelim_wn") { hdgb::tuning().qelim_wn = static_cast<int>(value); return 0; }
     if (k == "use_qelim_fused") { hdgb::tuning().use_qelim_fused = static_cast<int>(value); return 0; }
     if (k == "use_dmma") { hdgb::tuning().use_dmma = static_cast<int>(value); return 0; }

@@ -685,13 +685,19 @@ hdgb_ops* assemble_element_operators_device(hdgb_disc* d, const hdgb_model* m, h
         if (bad >= 0)
             throw Failure(HDGB_ERR_SINGULAR_LOCAL_SOLVE, "singular local solve in element " + std::to_string(e0 + bad), e0 + bad);
         // K-bar = J-bar - H-bar (E-bar^-1 F-bar)   (local_ops.cpp:408-411)
-        launch_gemm_batch(c, npe, nfl, npe, o->ebar_inv.p + sEE * e0, sEE, false, lo.F, sEF, wT.p, sEF, cnt, 1.0, 0.0);
-        if (tuning().use_dmma && nfl * nfl > 256) {
-            // K-bar = 1 * J-bar - H-bar T: the J-bar term is read in the epilogue, no copy of J-bar into K-bar first
-            launch_gemm_dmma(c, nfl, nfl, npe, lo.H, sEF, wT.p, sEF, o->kbar.p + sFF * e0, sFF, cnt, -1.0, 1.0, 0, 0, lo.J);
+        const bool schur_dmma = tuning().use_dmma && nfl * nfl > 256;
+        if (schur_dmma && tuning().schur_fused &&
+            launch_schur_fused(c, npe, nfl, o->ebar_inv.p + sEE * e0, sEE, lo.F, lo.H, sEF, lo.J, o->kbar.p + sFF * e0, sFF, cnt)) {
+            // one kernel: T = E-bar^-1 F-bar stays in shared memory, J-bar is read in the epilogue
         } else {
-            HDGB_CUDA(cudaMemcpyAsync(o->kbar.p + sFF * e0, lo.J, sFF * cnt * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-            launch_gemm_batch(c, nfl, nfl, npe, lo.H, sEF, false, wT.p, sEF, o->kbar.p + sFF * e0, sFF, cnt, -1.0, 1.0);
+            launch_gemm_batch(c, npe, nfl, npe, o->ebar_inv.p + sEE * e0, sEE, false, lo.F, sEF, wT.p, sEF, cnt, 1.0, 0.0);
+            if (schur_dmma) {
+                // K-bar = 1 * J-bar - H-bar T: the J-bar term is read in the epilogue, no copy of J-bar into K-bar first
+                launch_gemm_dmma(c, nfl, nfl, npe, lo.H, sEF, wT.p, sEF, o->kbar.p + sFF * e0, sFF, cnt, -1.0, 1.0, 0, 0, lo.J);
+            } else {
+                HDGB_CUDA(cudaMemcpyAsync(o->kbar.p + sFF * e0, lo.J, sFF * cnt * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+                launch_gemm_batch(c, nfl, nfl, npe, lo.H, sEF, false, wT.p, sEF, o->kbar.p + sFF * e0, sFF, cnt, -1.0, 1.0);
+            }
         }
         // r-bar = r_uhat - H-bar (E-bar^-1 r_u)   (local_ops.cpp:413-418)
         GemvArgs g1;

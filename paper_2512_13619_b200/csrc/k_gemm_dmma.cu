@@ -186,6 +186,172 @@ void launch_wmwn(hdgb_ctx* ctx, const GemmArgs& g, int64_t batch, bool vec) {
     }
 }
 
+// ---- fused Schur complement --------------------------------------------------------------------------------
+// K-bar = J-bar - H-bar (E-bar^-1 F-bar)   (local_ops.cpp:408-411) as ONE kernel: a CTA owns 32 columns of one
+// element's K-bar.  Sweep 1 forms the 32 columns of T = E-bar^-1 F-bar from E-bar^-1 streamed in k-chunks of 16
+// (the same two-stage cp.async ring as gemm_dmma_kernel) against the F-bar columns resident in shared memory;
+// the accumulators are stored over the F-bar columns in right-operand layout, and sweep 2 streams H-bar through
+// the same ring against that T.  T never goes to HBM (2 x 8 npe nfl bytes per element less traffic, one launch
+// instead of two, the first H-bar chunk in flight while T is written).  WM = ceil(nfl / 32) warps; the warps whose
+// 32 rows lie beyond npe only help loading in sweep 1.
+struct SchurArgs {
+    int npe, nfl;
+    const double* einv;
+    int64_t s_ee;
+    const double* f;
+    const double* h;
+    int64_t s_ef;
+    const double* j;
+    double* k;
+    int64_t s_ff;
+};
+
+template <int WM, bool VEC>
+__global__ void __launch_bounds__(WM * 32) schur_fused_kernel(SchurArgs g) {
+    constexpr int BM = 32 * WM, BN = 32, NT = WM * 32;
+    constexpr int LDA = BM + 4;  // = 4 (mod 16)
+    extern __shared__ __align__(16) double smem[];
+    const int npe = g.npe, nfl = g.nfl;
+    const int kp = (npe + KC - 1) / KC * KC;
+    const int ldt = kp + 4;  // = 4 (mod 16)
+    double* As = smem;                 // [2][KC][LDA]
+    double* Ts = smem + 2 * KC * LDA;  // [BN][ldt]: F-bar columns, then T columns
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int grp = lane >> 2, tig = lane & 3;
+    const int64_t item = blockIdx.y;
+    const double* Einv = g.einv + item * g.s_ee;
+    const double* F = g.f + item * g.s_ef;
+    const double* H = g.h + item * g.s_ef;
+    const double* J = g.j + item * g.s_ff;
+    double* K = g.k + item * g.s_ff;
+    const int col0 = blockIdx.x * BN;
+    constexpr int W = VEC ? 2 : 1;
+
+    // columns k0 .. k0 + KC - 1 of the column-major (m x npe) matrix A into ring stage s (rows >= m, columns >= npe: zero)
+    auto load_stage = [&](int s, const double* A, int m, int k0) {
+        double* as = As + s * KC * LDA;
+        for (int t = tid; t < KC * (BM / W); t += NT) {
+            const int p = t / (BM / W), i = (t - p * (BM / W)) * W;
+            const int gp = k0 + p;
+            const bool ok = i < m && gp < npe;
+            cp_async_zfill<VEC>(smem_addr(as + p * LDA + i), ok ? A + static_cast<int64_t>(gp) * m + i : A, ok);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+
+    double acc[4][4][2];
+    auto clear = [&]() {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    };
+    // acc += A[rows of this warp, :] * Ts over all k-chunks; stage 0 of the ring already holds chunk 0
+    auto sweep = [&](const double* A, int m, bool active) {
+        const int nk = kp / KC;
+        for (int c = 0; c < nk; ++c) {
+            const int s = c & 1;
+            if (c + 1 < nk) {
+                load_stage(s ^ 1, A, m, (c + 1) * KC);
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
+            } else {
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+            }
+            __syncthreads();
+            if (active) {
+                const double* as = As + s * KC * LDA + warp * 32 + grp;
+                const double* bs = Ts + grp * ldt + c * KC;
+#pragma unroll
+                for (int kk = 0; kk < KC; kk += 4) {
+                    double af[4], bf[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) af[i] = as[(kk + tig) * LDA + i * 8];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) bf[j] = bs[j * 8 * ldt + kk + tig];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+                }
+            }
+            __syncthreads();
+        }
+    };
+
+    // F-bar columns col0 .. col0 + 31 (rows >= npe and columns >= nfl: zero) ride in the first commit group
+    for (int t = tid; t < BN * (kp / W); t += NT) {
+        const int j = t / (kp / W), p = (t - j * (kp / W)) * W;
+        const bool ok = col0 + j < nfl && p < npe;
+        cp_async_zfill<VEC>(smem_addr(Ts + j * ldt + p), ok ? F + static_cast<int64_t>(col0 + j) * npe + p : F, ok);
+    }
+    load_stage(0, Einv, npe, 0);
+    clear();
+    const bool act1 = warp * 32 < npe;
+    sweep(Einv, npe, act1);
+    // every warp is past its last read of the F-bar columns (trailing barrier of the sweep): start H-bar, store T
+    load_stage(0, H, nfl, 0);
+    if (act1) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int r = warp * 32 + i * 8 + grp;
+            if (r < kp) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    Ts[(j * 8 + 2 * tig) * ldt + r] = acc[i][j][0];
+                    Ts[(j * 8 + 2 * tig + 1) * ldt + r] = acc[i][j][1];
+                }
+            }
+        }
+    }
+    clear();
+    sweep(H, nfl, true);  // its first barrier orders the T stores before the first fragment load
+
+    // K-bar = J-bar - acc: the J-bar entries of a column group are loaded as one batch before the stores
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        double old[2][4];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int gj = col0 + j * 8 + 2 * tig + h;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int gi = warp * 32 + i * 8 + grp;
+                old[h][i] = (gj < nfl && gi < nfl) ? J[static_cast<int64_t>(gj) * nfl + gi] : 0.0;
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int gj = col0 + j * 8 + 2 * tig + h;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int gi = warp * 32 + i * 8 + grp;
+                if (gj < nfl && gi < nfl) K[static_cast<int64_t>(gj) * nfl + gi] = old[h][i] - acc[i][j][h];
+            }
+        }
+    }
+}
+
+template <int WM>
+void launch_schur_wm(hdgb_ctx* ctx, const SchurArgs& g, int64_t batch, bool vec) {
+    const int kp = ceil_div(g.npe, KC) * KC;
+    const size_t smem = (2 * KC * (32 * WM + 4) + 32 * static_cast<size_t>(kp + 4)) * sizeof(double);
+    auto kv = schur_fused_kernel<WM, true>;
+    auto ks = schur_fused_kernel<WM, false>;
+    ensure_dynamic_smem(kv, smem);
+    ensure_dynamic_smem(ks, smem);
+    int64_t done = 0;
+    while (done < batch) {  // gridDim.y limit
+        const int64_t nb = (batch - done) < 65535 ? (batch - done) : 65535;
+        SchurArgs h = g;
+        h.einv += done * g.s_ee; h.f += done * g.s_ef; h.h += done * g.s_ef; h.j += done * g.s_ff; h.k += done * g.s_ff;
+        dim3 grid(ceil_div(g.nfl, 32), static_cast<unsigned>(nb));
+        if (vec) kv<<<grid, WM * 32, smem, ctx->stream>>>(h);
+        else ks<<<grid, WM * 32, smem, ctx->stream>>>(h);
+        HDGB_LAUNCH_CHECK(ctx);
+        done += nb;
+    }
+}
+
 template <int WM>
 void launch_wm(hdgb_ctx* ctx, const GemmArgs& g, int64_t batch, bool vec, int wn) {
     switch (wn) {
@@ -363,6 +529,24 @@ void launch_gemm_dmma(hdgb_ctx* ctx, int m, int n, int k, const double* a, int64
         case 3: launch_wm<3>(ctx, g, batch, vec, wn); break;
         default: launch_wm<4>(ctx, g, batch, vec, wn); break;
     }
+}
+
+// Returns false when the element sizes are outside the fused kernel's range (caller runs the two products).
+bool launch_schur_fused(hdgb_ctx* ctx, int npe, int nfl, const double* einv, int64_t s_ee, const double* f, const double* h,
+                        int64_t s_ef, const double* j, double* k, int64_t s_ff, int64_t batch) {
+    if (npe <= 0 || nfl <= 0 || nfl > 128 || ceil_div(npe, 32) > ceil_div(nfl, 32)) return false;
+    if (batch <= 0) return true;
+    SchurArgs g{npe, nfl, einv, s_ee, f, h, s_ef, j, k, s_ff};
+    const bool vec = (npe % 2 == 0) && (nfl % 2 == 0) && (s_ee % 2 == 0) && (s_ef % 2 == 0) &&
+                     (reinterpret_cast<uintptr_t>(einv) % 16 == 0) && (reinterpret_cast<uintptr_t>(f) % 16 == 0) &&
+                     (reinterpret_cast<uintptr_t>(h) % 16 == 0);
+    switch (ceil_div(nfl, 32)) {
+        case 1: launch_schur_wm<1>(ctx, g, batch, vec); break;
+        case 2: launch_schur_wm<2>(ctx, g, batch, vec); break;
+        case 3: launch_schur_wm<3>(ctx, g, batch, vec); break;
+        default: launch_schur_wm<4>(ctx, g, batch, vec); break;
+    }
+    return true;
 }
 
 }  // namespace hdgb

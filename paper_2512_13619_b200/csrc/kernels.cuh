@@ -54,6 +54,7 @@ struct Tuning {
     int qelim_stages = 2;                // cp.async ring depth of the fused q-elimination product (2 or 3)
     int qelim_split_rows = 1;            // fused q-elimination: one product per output block instead of stacked row blocks
     int gemm_wn_cap = 4;                 // 32-column tiles per CTA of the generic DMMA GEMM (1..4)
+    int schur_fused = 1;                 // Schur complement as one kernel with E-bar^-1 F-bar kept in shared memory (nfl <= 128)
     int qelim_wn = 1;                    // 32-column tiles per CTA of the fused q-elimination product
     int use_qelim_fused = 1;             // q-elimination as two fused stacked products per component instead of 4 D
     int use_dmma = 1;                    // batched GEMMs on the FP64 tensor-core path (k_gemm_dmma.cu)
@@ -168,6 +169,10 @@ void launch_gemm_dmma(hdgb_ctx* ctx, int m, int n, int k, const double* a, int64
 bool launch_qelim_fused(hdgb_ctx* ctx, int m0, int m1, int n, int k, int nterm, const double* const a0[3], int64_t a0_stride,
                         const double* const a1[3], int64_t a1_stride, const double* const b[3], int64_t b_stride, double* c0,
                         int64_t c0_stride, double* c1, int64_t c1_stride, int64_t batch, int c_colw = 0, int c_colstride = 0);
+
+// Fused Schur complement K = J - H (E^-1 F), T = E^-1 F kept in shared memory (k_gemm_dmma.cu); false = shape not supported.
+bool launch_schur_fused(hdgb_ctx* ctx, int npe, int nfl, const double* einv, int64_t s_ee, const double* f, const double* h,
+                        int64_t s_ef, const double* j, double* k, int64_t s_ff, int64_t batch);
 
 // ---- shared host helpers (api_core.cu) ------------------------------------------------------------
 void reset_flags(hdgb_ctx* c);

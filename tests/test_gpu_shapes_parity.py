@@ -164,3 +164,31 @@ def test_point_chunked_assembly_matches_single_sweep(ctx, shape, case, k, n, nco
         assert relerr(out[8][nm], out[216][nm]) < (1e-11 if nm in ("kbar", "rbar") else 1e-13), nm
     for a, b in zip(out[8]["res"][:2], out[216]["res"][:2]):
         assert relerr(a, b) < 1e-13
+
+
+@pytest.mark.parametrize("shape,case,k,n,ncomp", [
+    ("hex", "poisson", 3, 3, 1),      # config 2's element: npe 64, nfl 96 (three warps, 16-byte copies)
+    ("hex", "burgers", 2, 3, 1),      # npe 27 (odd: 8-byte copies, k padded to 32), nfl 54
+    ("hex", "elasticity", 1, 3, 3),   # npe 24, nfl 72
+    ("tet", "elasticity", 2, 2, 3),   # config 4's element: npe 30, nfl 72
+    ("tet", "poisson", 3, 2, 1),      # npe 20, nfl 40
+    ("quad", "elasticity", 3, 4, 2),  # npe 32, nfl 32
+    ("hex", "elasticity", 2, 2, 3)])  # nfl 162 > 128: the fused kernel declines, two products
+def test_schur_fused_matches_two_products(ctx, shape, case, k, n, ncomp):
+    """K-bar = J-bar - H-bar (E-bar^-1 F-bar) (local_ops.cpp:408-411): the one-kernel form with T in shared memory
+    against the two batched products (rounding-level agreement), and against the tier-B oracle."""
+    disc, model, state, oc = setup(ctx, shape, n, k, case, n_comp=ncomp, jitter=0.1)
+    perturb(disc, state, oc)
+    got = {}
+    try:
+        for flag in (0, 1):
+            hdg.set_tuning("schur_fused", flag)
+            ops = hdg.assemble_element_operators(disc, model, state, keep_raw=True)
+            got[flag] = {nm: ops.get(nm).copy() for nm in ("kbar", "ebar_inv", "fbar", "hbar", "rbar")}
+    finally:
+        hdg.set_tuning("schur_fused", 1)
+    for nm in ("ebar_inv", "fbar", "hbar", "rbar"):
+        assert np.array_equal(got[0][nm], got[1][nm]), nm
+    assert relerr(got[1]["kbar"], got[0]["kbar"]) < 1e-12
+    oc.assemble()
+    assert relerr(got[1]["kbar"], oc.get("kbar")) < 1e-9
