@@ -1,6 +1,6 @@
 """Small invocations of every hand-written kernel family for compute-sanitizer (memcheck / racecheck / synccheck):
 the DMMA local-assembly kernel (hex p = 3), fused q-elimination, blocked Gauss-Jordan, the bulk-TMA stream GEMV in
-plain and packed mode (forced on for small problems), the TMA-streamed CGS2 passes, the fused polynomial epilogues.
+plain and packed mode (forced on for small problems), the TMA-streamed CGS2 passes, the fused polynomial epilogues, the one-kernel Schur complement.
 
   compute-sanitizer --tool racecheck python scripts/sanitize_probe.py"""
 import sys
@@ -45,6 +45,12 @@ for stream, ntw in ((0, 256), (1, 256), (2, 256), (3, 512)):
 hdg.set_tuning("local_ed_stream", 3)
 hdg.set_tuning("local_nt_wide", 256)
 print("local kernel variants ok")
+# the one-kernel Schur complement over its warp counts and both copy widths (npe odd: 8-byte cp.async, k padded)
+for shape, k, case, ncomp in (("hex", 2, "poisson", 1), ("tet", 2, "elasticity", 3), ("quad", 3, "elasticity", 2), ("tet", 3, "poisson", 1)):
+    disc = hdg.Discretization.structured(ctx, shape, n=2, degree=k, n_comp=ncomp)
+    model = hdg.make_case_model(disc, case)
+    ops = hdg.assemble_element_operators(disc, model, hdg.make_initial_state(disc, model))
+print("fused Schur variants ok")
 # the streamed CGS2 passes on a basis long enough for the TMA path
 n, nvec = 1 << 16, 6
 V, _ = np.linalg.qr(hdg.random_vector(n * nvec, 1).reshape(n, nvec))
