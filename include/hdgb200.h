@@ -73,7 +73,7 @@ const char* hdgb_version(void);
  *                small items per warp pass), "stream_packed_max_cols", "stream_packed_stage_bytes",
  *                "stream_evict_first" (L2 evict-first hint on the matrix stream), "stream_persist_mb" (experiment, off);
  *   dense:       "use_dmma" (FP64 tensor-core GEMM / local blocks), "use_qelim_fused", "qelim_split_rows",
- *                "qelim_wn", "qelim_stages", "gemm_wn_cap", "schur_fused" (one-kernel Schur complement), "use_blocked_gj" (blocked Gauss-Jordan inverse),
+ *                "qelim_wn", "qelim_stages", "gemm_wm_cap", "gemm_wn_cap", "schur_fused" (one-kernel Schur complement), "use_blocked_gj" (blocked Gauss-Jordan inverse),
  *                "gj_direct" (no copy / permutation passes, n <= 128), "gj_smem", "gj_panel_cta",
  *                "use_tile_lu" (register-tiled Gauss-Jordan, n <= 128, when the blocked one is off);
  *   assembly:    "local_ed_stream" (hex p = 3: bit 0 = E / D_d, bit 1 = H / G_d / F / J through the bulk-TMA table ring,

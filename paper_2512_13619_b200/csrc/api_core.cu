@@ -46,6 +46,7 @@ int hdgb_set_tuning(const char* key, int64_t value) {
     if (k == "local_global_records") { hdgb::tuning().local_global_records = static_cast<int>(value); return 0; }
     if (k == "local_dmma_chunked") { hdgb::tuning().local_dmma_chunked = static_cast<int>(value); return 0; }
     if (k == "qelim_stages") { hdgb::tuning().qelim_stages = static_cast<int>(value); return 0; }
+    if (k == "gemm_wm_cap") { hdgb::tuning().gemm_wm_cap = static_cast<int>(value < 1 ? 1 : (value > 4 ? 4 : value)); return 0; }
     if (k == "gemm_wn_cap") { hdgb::tuning().gemm_wn_cap = static_cast<int>(value < 1 ? 1 : value); return 0; }
     if (k == "schur_fused") { hdgb::tuning().schur_fused = static_cast<int>(value); return 0; }
     if (k == "qelim_wn") { hdgb::tuning().qelim_wn = static_cast<int>(value); return 0; }

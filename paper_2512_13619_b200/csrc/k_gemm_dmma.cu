@@ -520,6 +520,7 @@ void launch_gemm_dmma(hdgb_ctx* ctx, int m, int n, int k, const double* a, int64
     if (wm > 4) wm = 4;
     if (wn > 4) wn = 4;
     if (wn > tuning().gemm_wn_cap) wn = tuning().gemm_wn_cap;  // narrow CTAs: more of them resident per SM
+    if (wm > tuning().gemm_wm_cap) wm = tuning().gemm_wm_cap;
     // keep CTAs at <= 12 warps: a 4 x 4 arrangement would leave one CTA per SM
     if (wm * wn > 12) { if (wn > 3) wn = 3; }
     if (wm * wn > 12) wm = 3;

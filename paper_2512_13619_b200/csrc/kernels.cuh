@@ -53,7 +53,11 @@ struct Tuning {
     int local_dmma_chunked = 0;          // E / D_d on the tensor-core path also in point-chunked sweeps (wide systems)
     int qelim_stages = 2;                // cp.async ring depth of the fused q-elimination product (2 or 3)
     int qelim_split_rows = 1;            // fused q-elimination: one product per output block instead of stacked row blocks
-    int gemm_wn_cap = 4;                 // 32-column tiles per CTA of the generic DMMA GEMM (1..4)
+    // generic DMMA GEMM: CTAs of at most 2 x 1 warp tiles (64 x 32 outputs).  Small CTAs, four or more resident per SM, overlap
+    // each other's barrier-separated load / multiply phases: config-5 assembly at hex 12^3 99.5 ms with 4 x 3 tiles (one
+    // 12-warp CTA per SM at 122 registers), 93.8 with 4 x 1, 93.2 with 2 x 1 (profiles/r02_s3_gemm_tile_ab.txt)
+    int gemm_wm_cap = 2;                 // 32-row tiles per CTA of the generic DMMA GEMM (1..4)
+    int gemm_wn_cap = 1;                 // 32-column tiles per CTA of the generic DMMA GEMM (1..4)
     int schur_fused = 1;                 // Schur complement as one kernel with E-bar^-1 F-bar kept in shared memory (nfl <= 128)
     int qelim_wn = 1;                    // 32-column tiles per CTA of the fused q-elimination product
     int use_qelim_fused = 1;             // q-elimination as two fused stacked products per component instead of 4 D
