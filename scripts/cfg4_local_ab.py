@@ -16,8 +16,9 @@ state = hdg.make_initial_state(disc, model)
 print("ne", disc.ne, "pe", disc.pe, "pf", disc.pf, "qe", disc.qe, "qf", disc.qf, "npe", disc.npe, "nfl", disc.nfl, flush=True)
 ref = None
 for rep in range(2):
-    for min_pe in (20, 8):
+    for min_pe, budget in ((20, 216), (8, 216), (8, 96), (8, 48), (20, 96), (20, 48)):
         hdg.set_tuning("local_dmma_min_pe", min_pe)
+        hdg.set_tuning("assemble_budget_kb", budget)
         ts = []
         for _ in range(4):
             t0 = time.perf_counter()
@@ -26,10 +27,11 @@ for rep in range(2):
             kb = ops.get("kbar") if _ == 3 and rep == 0 else None
             del ops
         if kb is not None:
-            if ref is None:
+            if ref is None or budget == 216 and min_pe == 20:
                 ref = kb
             else:
                 print("   kbar vs scalar kernel: max rel diff", np.max(np.abs(kb - ref)) / np.max(np.abs(ref)))
-        print(f"local_dmma_min_pe={min_pe} assemble_element_operators min {min(ts[1:]) * 1e3:.2f} ms  (all: {[round(t * 1e3, 2) for t in ts]})", flush=True)
+        print(f"local_dmma_min_pe={min_pe} assemble_budget_kb={budget} assemble_element_operators min {min(ts[1:]) * 1e3:.2f} ms  (all: {[round(t * 1e3, 2) for t in ts]})", flush=True)
 hdg.set_tuning("local_dmma_min_pe", 20)
+hdg.set_tuning("assemble_budget_kb", 216)
 ctx.close()
